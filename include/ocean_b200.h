@@ -32,6 +32,12 @@ extern "C" {
 
 #define OCN_ABI_VERSION 1
 
+#if defined(__GNUC__)
+#define OCN_API __attribute__((visibility("default")))
+#else
+#define OCN_API
+#endif
+
 /* ---- status codes (core.hpp:21-35 error types; main.cpp:303-320 exits) ---- */
 #define OCN_OK 0
 #define OCN_ERR_CONFIG 2  /* ConfigError  */
@@ -200,169 +206,185 @@ typedef struct ocn_mesh ocn_mesh;
 typedef struct ocn_zone ocn_zone;
 
 /* ================================ context ================================ */
-int ocn_abi_version(void);
-int ocn_ctx_create(int device, ocn_ctx** out);
-int ocn_ctx_destroy(ocn_ctx* ctx);
+OCN_API int ocn_abi_version(void);
+OCN_API int ocn_ctx_create(int device, ocn_ctx** out);
+OCN_API int ocn_ctx_destroy(ocn_ctx* ctx);
 /* Last error message of this context (or the global one when ctx == NULL). */
-const char* ocn_last_error(const ocn_ctx* ctx);
-int ocn_ctx_synchronize(ocn_ctx* ctx);
+OCN_API const char* ocn_last_error(const ocn_ctx* ctx);
+OCN_API int ocn_ctx_synchronize(ocn_ctx* ctx);
 /* The cudaStream_t all work of this context is enqueued on. */
-void* ocn_ctx_stream(ocn_ctx* ctx);
+OCN_API void* ocn_ctx_stream(ocn_ctx* ctx);
 /* Number of kernels this library has launched on the context (graph launches
  * count every kernel node). Used by bench.py for "gpu_launches". */
-uint64_t ocn_ctx_kernel_launches(const ocn_ctx* ctx);
+OCN_API uint64_t ocn_ctx_kernel_launches(const ocn_ctx* ctx);
+
+/* Per-stage device timing with CUDA events on the context stream (used by
+ * bench.py for the roofline of the dominant kernels). Categories: */
+#define OCN_PROF_EVOLVE 0   /* k_evolve (time evolution h~, G)          */
+#define OCN_PROF_ROWS 1     /* k_rows (coefficients + row FFT)          */
+#define OCN_PROF_COLS 2     /* k_cols (column FFT + sign + Re/Im split) */
+#define OCN_PROF_HYDRO 3    /* whole ocn_hydro_aggregate pipeline        */
+#define OCN_PROF_MASK 4     /* compute_mask (+ apply)                    */
+#define OCN_PROF_FDM 5      /* FdmZone::step stencil                     */
+#define OCN_PROF_SPECTRAL 6 /* whole spectral step (evolve+rows+cols)    */
+#define OCN_PROF_COUNT 8
+OCN_API int ocn_ctx_profile(ocn_ctx* ctx, int enable);
+/* Synchronizes, then returns the accumulated milliseconds and launch count of
+ * a category since the last reset. */
+OCN_API int ocn_ctx_profile_read(ocn_ctx* ctx, int category, double* total_ms, uint64_t* count);
+OCN_API int ocn_ctx_profile_reset(ocn_ctx* ctx);
 
 /* ============================ spectrum scalars =========================== */
 /* Scalar spectrum model, spectra.cpp:10-130. Same __host__ __device__ code
  * as the device kernels; exposed for the C++ drop-in of spectra.hpp:37-79. */
-int ocn_spectrum_validate(const ocn_spectrum_params* p);
-double ocn_alpha(const ocn_spectrum_params* p);
-double ocn_peak_omega(const ocn_spectrum_params* p);
-double ocn_standard_peak_omega(const ocn_spectrum_params* p);
-double ocn_dispersion(double k, double g);
-int ocn_jonswap(double omega, const ocn_spectrum_params* p, double* out);
-double ocn_beta_s(double r_omega);
-double ocn_directional_kernel(double beta, double theta);
-double ocn_donelan_banner(double omega, double theta, double omega_p);
-double ocn_swell_spread(double omega, double theta, double omega_p, double xi);
-double ocn_q_dbxi_approx(double r_omega);
-double ocn_q_dbxi_quadrature(double r_omega, double xi, int panels);
-double ocn_directional(double omega, double theta, const ocn_spectrum_params* p);
-double ocn_h0_variance(double kx, double kz, double k, double omega, double tile_length,
+OCN_API int ocn_spectrum_validate(const ocn_spectrum_params* p);
+OCN_API double ocn_alpha(const ocn_spectrum_params* p);
+OCN_API double ocn_peak_omega(const ocn_spectrum_params* p);
+OCN_API double ocn_standard_peak_omega(const ocn_spectrum_params* p);
+OCN_API double ocn_dispersion(double k, double g);
+OCN_API int ocn_jonswap(double omega, const ocn_spectrum_params* p, double* out);
+OCN_API double ocn_beta_s(double r_omega);
+OCN_API double ocn_directional_kernel(double beta, double theta);
+OCN_API double ocn_donelan_banner(double omega, double theta, double omega_p);
+OCN_API double ocn_swell_spread(double omega, double theta, double omega_p, double xi);
+OCN_API double ocn_q_dbxi_approx(double r_omega);
+OCN_API double ocn_q_dbxi_quadrature(double r_omega, double xi, int panels);
+OCN_API double ocn_directional(double omega, double theta, const ocn_spectrum_params* p);
+OCN_API double ocn_h0_variance(double kx, double kz, double k, double omega, double tile_length,
                        const ocn_spectrum_params* p);
-double ocn_damping_factor(double speed, double d0, double d_max, double v_max);
-double ocn_attenuation(double k, double y);
-int ocn_log_distribution(double y, double y_min, double* out);
-int ocn_exp_interp(double a, double f_a, double b, double f_b, double x, double* out);
-int ocn_slice_depths(const ocn_slice_config* cfg, double* host_depths);
+OCN_API double ocn_damping_factor(double speed, double d0, double d_max, double v_max);
+OCN_API double ocn_attenuation(double k, double y);
+OCN_API int ocn_log_distribution(double y, double y_min, double* out);
+OCN_API int ocn_exp_interp(double a, double f_a, double b, double f_b, double x, double* out);
+OCN_API int ocn_slice_depths(const ocn_slice_config* cfg, double* host_depths);
 
 /* ============================ cascades (K1) ============================== */
 /* generate_h0 (spectra.cpp:132-179) for `count` grids of one resolution, run
  * as one sm_100a kernel (fp64 spectrum, bit-exact Philox and band mask).
  * CascadeSet (surface.cpp:22-37) is count = lengths.size() with bands from
  * the cutoffs; generate_h0 alone is count = 1. */
-int ocn_cascades_create(ocn_ctx* ctx, int resolution, int count, const double* host_lengths,
+OCN_API int ocn_cascades_create(ocn_ctx* ctx, int resolution, int count, const double* host_lengths,
                         const double* host_band_min, const double* host_band_max,
                         const uint32_t* host_cascade_index, const ocn_spectrum_params* params,
                         ocn_cascades** out);
-int ocn_cascades_destroy(ocn_cascades* c);
-int ocn_cascades_info(const ocn_cascades* c, int* resolution, int* count);
+OCN_API int ocn_cascades_destroy(ocn_cascades* c);
+OCN_API int ocn_cascades_info(const ocn_cascades* c, int* resolution, int* count);
 /* WaveGrid accessors (spectra.hpp:95-104): h0 / h0_conj_neg as interleaved
  * complex (2*N*N doubles), in_band (N*N bytes), waves (4*N*N doubles:
  * kx, kz, k, omega per mode). Any pointer may be NULL. */
-int ocn_cascades_download(ocn_cascades* c, int grid, double* host_h0, double* host_h0cn,
+OCN_API int ocn_cascades_download(ocn_cascades* c, int grid, double* host_h0, double* host_h0cn,
                           uint8_t* host_in_band, double* host_waves);
 
 /* =========================== surface maps (K2+K4) ========================= */
 /* SurfaceMaps (surface.hpp:65-80): 8 fp32 fields per cascade, device-resident. */
-int ocn_maps_create(ocn_cascades* c, ocn_maps** out);
-int ocn_maps_destroy(ocn_maps* m);
+OCN_API int ocn_maps_create(ocn_cascades* c, ocn_maps** out);
+OCN_API int ocn_maps_destroy(ocn_maps* m);
 /* generate_maps (surface.cpp:70-103), (async). Same pairing as
  * surface.cpp:77-80; each pair is one C2C inverse FFT of X + iY. */
-int ocn_surface_generate(ocn_maps* m, double t, double choppiness);
-int ocn_maps_time(const ocn_maps* m, double* t);
-int ocn_maps_download(ocn_maps* m, int cascade, int field, double* host_out);
-int ocn_maps_download_f32(ocn_maps* m, int cascade, int field, float* host_out);
-int ocn_maps_device_field(ocn_maps* m, int cascade, int field, const float** dev_out);
+OCN_API int ocn_surface_generate(ocn_maps* m, double t, double choppiness);
+OCN_API int ocn_maps_time(const ocn_maps* m, double* t);
+OCN_API int ocn_maps_download(ocn_maps* m, int cascade, int field, double* host_out);
+OCN_API int ocn_maps_download_f32(ocn_maps* m, int cascade, int field, float* host_out);
+OCN_API int ocn_maps_device_field(ocn_maps* m, int cascade, int field, const float** dev_out);
 
 /* ========================= velocity slices (K3+K4) ======================== */
-int ocn_slices_create(ocn_cascades* c, const ocn_slice_config* cfg, ocn_slices** out);
-int ocn_slices_destroy(ocn_slices* s);
+OCN_API int ocn_slices_create(ocn_cascades* c, const ocn_slice_config* cfg, ocn_slices** out);
+OCN_API int ocn_slices_destroy(ocn_slices* s);
 /* build_slices (velocity.cpp:104-179), (async). (vx, vz) packed per depth,
  * vy packed across adjacent depths, zero partner for an odd count. */
-int ocn_velocity_build(ocn_slices* s, double t);
-int ocn_slices_depths(const ocn_slices* s, int* count, double* host_depths);
+OCN_API int ocn_velocity_build(ocn_slices* s, double t);
+OCN_API int ocn_slices_depths(const ocn_slices* s, int* count, double* host_depths);
 /* component: 0 = vx, 1 = vy, 2 = vz */
-int ocn_slices_download(ocn_slices* s, int depth, int cascade, int component, double* host_out);
+OCN_API int ocn_slices_download(ocn_slices* s, int depth, int cascade, int component, double* host_out);
 
 /* Fused per-frame spectral step: maps and (optional) slices at time t in one
  * enqueued graph (async). Equivalent to ocn_surface_generate + ocn_velocity_build. */
-int ocn_spectral_step(ocn_maps* m, ocn_slices* s, double t, double choppiness);
+OCN_API int ocn_spectral_step(ocn_maps* m, ocn_slices* s, double t, double choppiness);
 
 /* ============================= standalone FFT ============================= */
 /* ifft2_centered (fft.cpp:69-77) and ifft2_hermitian_pair (fft.cpp:79-101) on
  * host fp64 interleaved complex buffers (2*N*N doubles); device math is fp32. */
-int ocn_ifft2_centered(ocn_ctx* ctx, int n, const double* host_in, double* host_out);
-int ocn_ifft2_pair(ocn_ctx* ctx, int n, const double* host_x, const double* host_y,
+OCN_API int ocn_ifft2_centered(ocn_ctx* ctx, int n, const double* host_in, double* host_out);
+OCN_API int ocn_ifft2_pair(ocn_ctx* ctx, int n, const double* host_x, const double* host_y,
                    double* host_re, double* host_im);
 
 /* ============================ batched samplers ============================ */
 /* SurfaceMaps::sample (surface.cpp:125-129): out[i] = sum_c bilinear(field_c, x_i). */
-int ocn_maps_sample(ocn_maps* m, int field, int64_t n, const double* xz, double* out);
+OCN_API int ocn_maps_sample(ocn_maps* m, int field, int64_t n, const double* xz, double* out);
 /* SurfaceMaps::sample_displacement (surface.cpp:131-139): out = (dx, h, dz) per point. */
-int ocn_sample_displacement(ocn_maps* m, int64_t n, const double* xz, double* out);
+OCN_API int ocn_sample_displacement(ocn_maps* m, int64_t n, const double* xz, double* out);
 /* height_at (surface.cpp:141-151), Algorithm 1 with 4 rounds. */
-int ocn_height_at(ocn_maps* m, int64_t n, const double* xz, double* out);
+OCN_API int ocn_height_at(ocn_maps* m, int64_t n, const double* xz, double* out);
 /* height_at_tolerance (surface.cpp:153-169). */
-int ocn_height_at_tolerance(ocn_maps* m, int64_t n, const double* xz, double tol,
+OCN_API int ocn_height_at_tolerance(ocn_maps* m, int64_t n, const double* xz, double tol,
                             int max_iters, double* out, int32_t* iterations);
 /* North-star item 3 (no reference function): at each query
  * point x, the composed displaced surface after Algorithm 1:
  * out[10*i + 0..9] = (X - x)_x, h, (X - x)_z, normal(3), jacobian,
  *                    sum DxDx, sum DzDx, sum DzDz.
  * normal ∝ (-Hx, 1, -Hz), J = (1 - DxDx)(1 - DzDz) - DzDx^2 (SURVEY sign convention). */
-int ocn_surface_assemble(ocn_maps* m, int64_t n, const double* xz, double* out);
+OCN_API int ocn_surface_assemble(ocn_maps* m, int64_t n, const double* xz, double* out);
 /* VelocitySlices::sample_slice (velocity.cpp:203-211), out = 3 per point. */
-int ocn_sample_slice(ocn_slices* s, int depth, int64_t n, const double* xz, double* out);
+OCN_API int ocn_sample_slice(ocn_slices* s, int depth, int64_t n, const double* xz, double* out);
 /* velocity_at (velocity.cpp:213-265). xzy = (x, z, y) per point; out = 3 per point.
  * clamp != 0 clamps y into [y_min, y_max] first (sim.cpp:39-42). */
-int ocn_velocity_at(ocn_slices* s, int64_t n, const double* xzy, int interp, int clamp,
+OCN_API int ocn_velocity_at(ocn_slices* s, int64_t n, const double* xzy, int interp, int clamp,
                     double* out);
 
 /* ============================== hydro (K5-K8) ============================== */
 /* A validated, outward-oriented TriMesh (mesh.cpp:48-116 is load-time host
  * code in the C++ layer); normals / areas per triangle as the reference computes. */
-int ocn_mesh_create(ocn_ctx* ctx, int n_vertices, const double* host_vertices, int n_triangles,
+OCN_API int ocn_mesh_create(ocn_ctx* ctx, int n_vertices, const double* host_vertices, int n_triangles,
                     const int32_t* host_triangles, const double* host_normals,
                     const double* host_areas, double volume, ocn_mesh** out);
-int ocn_mesh_destroy(ocn_mesh* mesh);
+OCN_API int ocn_mesh_destroy(ocn_mesh* mesh);
 /* aggregate (hydro.cpp:253-306) incl. classify_clip (hydro.cpp:63-215).
  * host_vertex_depth may be NULL (depths from the fluid's maps + zones); when
  * given, it replaces the surface sampler (signed depth per vertex, e.g. from a
  * user sampler). report may be NULL: the evaluation then stays asynchronous
  * and the report is fetched with ocn_hydro_report_get. */
-int ocn_hydro_aggregate(ocn_mesh* mesh, const ocn_pose* pose, const ocn_fluid* fluid,
+OCN_API int ocn_hydro_aggregate(ocn_mesh* mesh, const ocn_pose* pose, const ocn_fluid* fluid,
                         const double* host_vertex_depth, ocn_hydro_report* report);
-int ocn_hydro_report_get(ocn_mesh* mesh, ocn_hydro_report* report);
+OCN_API int ocn_hydro_report_get(ocn_mesh* mesh, ocn_hydro_report* report);
 /* Per-vertex world positions (3 doubles) and signed depths of the last evaluation. */
-int ocn_hydro_vertices(ocn_mesh* mesh, double* host_world, double* host_depth);
+OCN_API int ocn_hydro_vertices(ocn_mesh* mesh, double* host_world, double* host_depth);
 /* TriangleStates of the last evaluation in parent order (ClipResult::states). */
-int ocn_hydro_states(ocn_mesh* mesh, int capacity, ocn_triangle_state* host_states, int* count);
+OCN_API int ocn_hydro_states(ocn_mesh* mesh, int capacity, ocn_triangle_state* host_states, int* count);
 /* Waterline loops of the last evaluation: loop_offsets has n_loops + 1 entries;
  * points are xyz triples (closed loops repeat their first point, hydro.cpp:208-209). */
-int ocn_hydro_waterline(ocn_mesh* mesh, int* n_loops, int* n_points, int32_t* host_loop_offsets,
+OCN_API int ocn_hydro_waterline(ocn_mesh* mesh, int* n_loops, int* n_points, int32_t* host_loop_offsets,
                         double* host_points);
 
 /* ============================ FDM zone (K9-K10) ============================ */
-int ocn_zone_create(ocn_ctx* ctx, const ocn_fdm_config* cfg, double body_size, double body_x,
+OCN_API int ocn_zone_create(ocn_ctx* ctx, const ocn_fdm_config* cfg, double body_size, double body_x,
                     double body_z, double dt, ocn_zone** out);
-int ocn_zone_destroy(ocn_zone* z);
-int ocn_zone_get_state(const ocn_zone* z, ocn_zone_state* out);
+OCN_API int ocn_zone_destroy(ocn_zone* z);
+OCN_API int ocn_zone_get_state(const ocn_zone* z, ocn_zone_state* out);
 /* FdmZone::update_stability (interactive.cpp:54-65). */
-int ocn_zone_update_stability(ocn_zone* z, double body_speed, double dt);
+OCN_API int ocn_zone_update_stability(ocn_zone* z, double body_speed, double dt);
 /* FdmZone::step (interactive.cpp:67-111), (async). */
-int ocn_zone_step(ocn_zone* z, double dt, double body_x, double body_z);
+OCN_API int ocn_zone_step(ocn_zone* z, double dt, double body_x, double body_z);
 /* FdmZone::apply_mask (interactive.cpp:113-118) for an explicit cell list. */
-int ocn_zone_apply_cells(ocn_zone* z, int n, const int32_t* host_ij, const double* host_h);
+OCN_API int ocn_zone_apply_cells(ocn_zone* z, int n, const int32_t* host_ij, const double* host_h);
 /* compute_mask (interactive.cpp:146-195) against explicit host loops
  * (loop_offsets: n_loops + 1 entries, points xyz). apply != 0 also performs
  * apply_mask. The cell list is kept on the device; n_cells returns its size. */
-int ocn_zone_compute_mask(ocn_zone* z, int n_loops, const int32_t* host_loop_offsets,
+OCN_API int ocn_zone_compute_mask(ocn_zone* z, int n_loops, const int32_t* host_loop_offsets,
                           const double* host_points, double body_yaw, double body_x,
                           double body_z, double body_speed, const ocn_mask_frame* frame,
                           const ocn_mask_params* params, int apply, int* n_cells);
 /* compute_mask + apply_mask from the device-resident waterline and submerged
  * volume of mesh's last ocn_hydro_aggregate (sim.cpp:86-109), (async). */
-int ocn_zone_mask_from_hydro(ocn_zone* z, ocn_mesh* mesh, double body_yaw, double body_x,
+OCN_API int ocn_zone_mask_from_hydro(ocn_zone* z, ocn_mesh* mesh, double body_yaw, double body_x,
                              double body_z, double body_speed, const ocn_mask_frame* frame,
                              const ocn_mask_params* params);
 /* Cells of the last mask in row-major order (MaskCell, interactive.hpp:56-59). */
-int ocn_zone_mask_download(ocn_zone* z, int capacity, int32_t* host_ij, double* host_h,
+OCN_API int ocn_zone_mask_download(ocn_zone* z, int capacity, int32_t* host_ij, double* host_h,
                            int* n_cells);
 /* FdmZone::sample (interactive.cpp:120-129). */
-int ocn_zone_sample(ocn_zone* z, int64_t n, const double* xz, double* out);
-int ocn_zone_download(ocn_zone* z, double* host_curr, double* host_prev);
-int ocn_zone_upload(ocn_zone* z, const double* host_curr, const double* host_prev);
+OCN_API int ocn_zone_sample(ocn_zone* z, int64_t n, const double* xz, double* out);
+OCN_API int ocn_zone_download(ocn_zone* z, double* host_curr, double* host_prev);
+OCN_API int ocn_zone_upload(ocn_zone* z, const double* host_curr, const double* host_prev);
 
 #ifdef __cplusplus
 }

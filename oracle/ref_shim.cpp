@@ -607,3 +607,102 @@ int ref_normalization_study(int samples, uint64_t seed, double* out4) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// CPU baseline driver: one Simulation-like frame of the reference hot path
+// (sim.cpp:59-109 minus the rigid integrator), stage by stage, timed with
+// steady_clock. depth_sample <= slices.count builds only that many depth
+// slices (bench.py scales build_slices linearly to the configured count).
+#include <chrono>
+
+namespace {
+struct RefBench {
+  CascadeSet cascades;
+  SliceConfig slices;
+  TriMesh mesh;
+  FdmZone zone;
+  BodyPose pose;
+  Vec3 wind;
+  double time = 0.0;
+};
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+}  // namespace
+
+extern "C" void* ref_bench_create(int n, int C, const double* lengths, const double* cutoffs,
+                                  const ocn_spectrum_params* p, const ocn_slice_config* sc,
+                                  int nv, const double* verts, int nt, const int32_t* tris,
+                                  const ocn_pose* pose, const ocn_fdm_config* fc, double body_size,
+                                  double dt, const double* wind, int* status) {
+  RefBench* b = nullptr;
+  *status = guard([&] {
+    b = new RefBench{CascadeSet(to_cascades(n, C, lengths, cutoffs), to_params(p)), to_slices(sc),
+                     mesh_from(nv, verts, nt, tris),
+                     FdmZone([&] {
+                       FdmConfig f;
+                       f.grid_size = fc->grid_size;
+                       f.margin = fc->margin;
+                       f.delta_min = fc->delta_min;
+                       f.delta_max = fc->delta_max;
+                       f.delta_rate_limit = fc->delta_rate_limit;
+                       f.damping = {fc->d0, fc->d_max, fc->v_max};
+                       return f;
+                     }(), body_size, {pose->position[0], pose->position[2]}, dt),
+                     to_pose(pose), {wind[0], wind[1], wind[2]}};
+  });
+  return b;
+}
+
+extern "C" void ref_bench_destroy(void* b) { delete static_cast<RefBench*>(b); }
+
+// stage seconds: [0] generate_maps, [1] build_slices(depth_sample), [2] aggregate,
+// [3] update_stability + compute_mask, [4] apply_mask + FdmZone::step
+extern "C" int ref_bench_frame(void* bp, double dt, int depth_sample, double* stage) {
+  return guard([&] {
+    RefBench& b = *static_cast<RefBench*>(bp);
+    double t_next = b.time + dt;
+    double t0 = now_s();
+    SurfaceMaps maps = generate_maps(b.cascades, t_next, {});
+    double t1 = now_s();
+    SliceConfig sc = b.slices;
+    // the first depth_sample depths of the configured distribution
+    VelocitySlices vs = build_slices(b.cascades, t_next, [&] {
+      SliceConfig s2 = sc;
+      s2.count = depth_sample;
+      return s2;
+    }());
+    double t2 = now_s();
+    FluidQuery fluid;
+    fluid.surface_height = [&](Vec2 x) { return height_at(maps, x); };
+    fluid.water_velocity = [&](Vec2 x, double y) {
+      double yc = std::clamp(y, vs.y_min(), vs.y_max());
+      return velocity_at(vs, x, yc, DepthInterp::Exponential);
+    };
+    fluid.wind = b.wind;
+    HydroReport rep = aggregate(b.mesh, b.pose, fluid, {});
+    double t3 = now_s();
+    double speed = b.pose.linear_velocity.norm();
+    b.zone.update_stability(speed, dt);
+    Vec3 ext = b.mesh.bbox_max() - b.mesh.bbox_min();
+    MaskFrame frame;
+    frame.half_beam = ext.x;
+    frame.z_min = b.mesh.bbox_min().z;
+    frame.z_max = b.mesh.bbox_max().z;
+    frame.mesh_height = b.mesh.height();
+    frame.volume_ratio = rep.submerged_volume / b.mesh.volume();
+    auto cells = compute_mask(b.zone, rep.waterline, b.pose.yaw(), b.pose.position.xz(), speed,
+                              frame, {});
+    double t4 = now_s();
+    b.zone.apply_mask(cells);
+    b.pose.position += b.pose.linear_velocity * dt;
+    b.zone.step(dt, b.pose.position.xz());
+    double t5 = now_s();
+    b.time = t_next;
+    stage[0] = t1 - t0;
+    stage[1] = t2 - t1;
+    stage[2] = t3 - t2;
+    stage[3] = t4 - t3;
+    stage[4] = t5 - t4;
+  });
+}

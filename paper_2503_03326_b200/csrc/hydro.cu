@@ -1,0 +1,784 @@
+// hydro.cu — fluid-to-solid forces on a triangle hull (K5-K8), sm_100a.
+//
+// Reference path replaced: classify_clip (hydro.cpp:63-215), submerged_volume
+// (:217-223), center_of_immersion (:225-238), buoyancy (:240), drag (:242-251),
+// aggregate (:253-306) with the Simulation samplers (sim.cpp:39-51, 74-83).
+//
+// Pipeline (one stream, no host round trip until the report is read):
+//   k_vertices   world transform + Algorithm-1 height (+ other zones) -> depth
+//   k_classify   per triangle: 0 / 1 / 3 states, 0 / 1 waterline segment
+//   scan         order-preserving offsets (parent order, hydro.cpp:151-163)
+//   k_emit       TriangleStates and crossing segments at their offsets
+//   k_forces     per state: prism volume, immersion moment, drag (velocity_at
+//                at the centroid), dry area / moment -> fixed-tree block sums
+//   k_finalize   fixed-order reduction of the block sums, clamps, buoyancy,
+//                application points, composed force / torque (sim.cpp:114-122)
+//   k_chain      waterline chaining with the reference's visiting order
+//                (hydro.cpp:165-213): start at the lowest unused segment,
+//                enter through its first edge, last-writer crossing points.
+// All reductions are fixed trees over a fixed state->thread mapping, so the
+// report is bit-identical run to run.
+#include <cstring>
+
+#include "hydro_internal.cuh"
+#include "samplers.cuh"
+
+namespace ocn {
+namespace {
+
+__device__ __forceinline__ double3 d3(double x, double y, double z) { return make_double3(x, y, z); }
+__device__ __forceinline__ double3 operator+(double3 a, double3 b) { return d3(a.x + b.x, a.y + b.y, a.z + b.z); }
+__device__ __forceinline__ double3 operator-(double3 a, double3 b) { return d3(a.x - b.x, a.y - b.y, a.z - b.z); }
+__device__ __forceinline__ double3 operator*(double3 a, double s) { return d3(a.x * s, a.y * s, a.z * s); }
+__device__ __forceinline__ double3 cross3(double3 a, double3 b) {
+  return d3(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
+}
+__device__ __forceinline__ double dot3(double3 a, double3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ double norm3(double3 a) { return sqrt(a.x * a.x + a.y * a.y + a.z * a.z); }
+__device__ __forceinline__ double3 ld3(const double* p) { return d3(p[0], p[1], p[2]); }
+__device__ __forceinline__ void st3(double* p, double3 v) { p[0] = v.x, p[1] = v.y, p[2] = v.z; }
+
+// Quat::rotate (core.hpp:164-169)
+__device__ __forceinline__ double3 qrot(const PoseDev& P, double3 v) {
+  const double3 u = d3(P.q[1], P.q[2], P.q[3]);
+  const double3 t = cross3(u, v) * 2.0;
+  return (v + t * P.q[0]) + cross3(u, t);
+}
+
+// ---------------------------------------------------------------- K5: vertices
+__global__ void __launch_bounds__(128) k_vertices(int nv, const double* __restrict__ verts,
+                                                  PoseDev P, SurfView surf, int have_surf,
+                                                  ZoneList zones, const double* override_depth,
+                                                  double* wpos, double* depth) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += gridDim.x * blockDim.x) {
+    const double3 b = ld3(verts + 3 * i);
+    const double3 w = d3(P.p[0], P.p[1], P.p[2]) + qrot(P, b - d3(P.com[0], P.com[1], P.com[2]));
+    st3(wpos + 3 * i, w);
+    double d;
+    if (override_depth) {
+      d = override_depth[i];
+    } else {
+      double h = have_surf ? height_at_dev(surf, w.x, w.z) : 0.0;
+      for (int z = 0; z < zones.count; ++z) h += zone_sample(zones.z[z], w.x, w.z);
+      d = w.y - h;
+    }
+    depth[i] = d;
+  }
+}
+
+// ---------------------------------------------------------------- K7: classify
+// counts.x = states emitted (0 degenerate, 1 whole, 3 split), counts.y = segment
+__global__ void __launch_bounds__(256) k_classify(int nt, const int3* __restrict__ tris,
+                                                  const double* __restrict__ areas,
+                                                  const double* __restrict__ depth, int2* counts) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
+    int2 c = make_int2(0, 0);
+    if (areas[t] > 0.0) {
+      const int3 v = tris[t];
+      const int above = (depth[v.x] >= 0.0) + (depth[v.y] >= 0.0) + (depth[v.z] >= 0.0);
+      if (above == 0 || above == 3) {
+        c.x = 1;
+      } else {
+        c.x = 3;
+        c.y = 1;  // keys (a,b) != (a,c) since a, b, c are distinct in a validated mesh
+      }
+    }
+    counts[t] = c;
+  }
+}
+
+// ---------------------------------------------------------------- scan (int2)
+constexpr int kScanBlock = 1024;
+
+__device__ __forceinline__ int2 add2(int2 a, int2 b) { return make_int2(a.x + b.x, a.y + b.y); }
+
+__device__ int2 block_exclusive_scan(int2 v, int2* sh, int2* total) {
+  // Hillis-Steele in shared memory (blockDim = kScanBlock)
+  const int t = threadIdx.x;
+  sh[t] = v;
+  __syncthreads();
+  for (int off = 1; off < blockDim.x; off <<= 1) {
+    int2 a = t >= off ? sh[t - off] : make_int2(0, 0);
+    __syncthreads();
+    sh[t] = add2(sh[t], a);
+    __syncthreads();
+  }
+  int2 incl = sh[t];
+  *total = sh[blockDim.x - 1];
+  __syncthreads();
+  return make_int2(incl.x - v.x, incl.y - v.y);
+}
+
+__global__ void __launch_bounds__(kScanBlock) k_scan_local(int n, const int2* in, int2* out,
+                                                           int2* block_sums) {
+  __shared__ int2 sh[kScanBlock];
+  const int i = blockIdx.x * kScanBlock + threadIdx.x;
+  int2 v = i < n ? in[i] : make_int2(0, 0);
+  int2 tot;
+  int2 ex = block_exclusive_scan(v, sh, &tot);
+  if (i < n) out[i] = ex;
+  if (threadIdx.x == 0) block_sums[blockIdx.x] = tot;
+}
+
+// scans the block sums sequentially in one block (count <= a few hundred)
+__global__ void k_scan_blocks(int nb, int2* block_sums, int2* total) {
+  if (threadIdx.x == 0) {
+    int2 acc = make_int2(0, 0);
+    for (int b = 0; b < nb; ++b) {
+      int2 v = block_sums[b];
+      block_sums[b] = acc;
+      acc = add2(acc, v);
+    }
+    *total = acc;
+  }
+}
+
+__global__ void k_scan_add(int n, int2* out, const int2* block_sums) {
+  const int i = blockIdx.x * kScanBlock + threadIdx.x;
+  if (i < n) out[i] = add2(out[i], block_sums[blockIdx.x]);
+}
+
+// ---------------------------------------------------------------- K7: emit
+__device__ __forceinline__ void emit_state(StateDev* s, int parent, int status, double3 a, double3 b,
+                                           double3 c, double da, double db, double dc, double3 n) {
+  StateDev r;
+  r.parent = parent;
+  r.status = status;
+  r.area = 0.5 * norm3(cross3(b - a, c - a));
+  // (a + b + c) / 3 as the reference divides (hydro.cpp:47)
+  r.centroid = d3(((a.x + b.x) + c.x) / 3.0, ((a.y + b.y) + c.y) / 3.0, ((a.z + b.z) + c.z) / 3.0);
+  r.depth = (da + db + dc) / 3.0;
+  r.normal = n;
+  *s = r;
+}
+
+__global__ void __launch_bounds__(256) k_emit(int nt, const int3* __restrict__ tris,
+                                              const double* __restrict__ normals,
+                                              const double* __restrict__ wpos,
+                                              const double* __restrict__ depth, PoseDev P,
+                                              const int2* __restrict__ counts,
+                                              const int2* __restrict__ offsets, StateDev* states,
+                                              SegDev* segs) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
+    const int2 c = counts[t];
+    if (c.x == 0) continue;
+    const int2 off = offsets[t];
+    const int3 v = tris[t];
+    const double3 n = qrot(P, ld3(normals + 3 * t));
+    const double d0 = depth[v.x], d1 = depth[v.y], d2 = depth[v.z];
+    if (c.x == 1) {
+      const int status = d0 >= 0.0 ? 1 : 0;  // all above -> Dry (1), all below -> Submerged (0)
+      emit_state(states + off.x, t, status, ld3(wpos + 3 * v.x), ld3(wpos + 3 * v.y),
+                 ld3(wpos + 3 * v.z), d0, d1, d2, n);
+      continue;
+    }
+    const bool ab0 = d0 >= 0.0, ab1 = d1 >= 0.0, ab2 = d2 >= 0.0;
+    const int above = ab0 + ab1 + ab2;
+    int a, b, cc;
+    bool odd_above;
+    if (above == 1) {
+      odd_above = true;
+      if (ab0) a = v.x, b = v.y, cc = v.z;
+      else if (ab1) a = v.y, b = v.z, cc = v.x;
+      else a = v.z, b = v.x, cc = v.y;
+    } else {
+      odd_above = false;
+      if (!ab0) a = v.x, b = v.y, cc = v.z;
+      else if (!ab1) a = v.y, b = v.z, cc = v.x;
+      else a = v.z, b = v.x, cc = v.y;
+    }
+    const double da = depth[a], db = depth[b], dc = depth[cc];
+    const double alpha_ab = da / (da - db);
+    const double alpha_ac = da / (da - dc);
+    const double3 wa = ld3(wpos + 3 * a), wb = ld3(wpos + 3 * b), wc = ld3(wpos + 3 * cc);
+    const double3 pab = wa + (wb - wa) * alpha_ab;
+    const double3 pac = wa + (wc - wa) * alpha_ac;
+    const int odd_status = odd_above ? 1 : 0, rest = odd_above ? 0 : 1;
+    emit_state(states + off.x, t, odd_status, wa, pab, pac, da, 0.0, 0.0, n);
+    emit_state(states + off.x + 1, t, rest, pab, wb, wc, 0.0, db, dc, n);
+    emit_state(states + off.x + 2, t, rest, pab, wc, pac, 0.0, dc, 0.0, n);
+    SegDev s;
+    s.ka = make_int2(min(a, b), max(a, b));
+    s.kb = make_int2(min(a, cc), max(a, cc));
+    s.pa = pab;
+    s.pb = pac;
+    segs[off.y] = s;
+  }
+}
+
+// ---------------------------------------------------------------- K6 + K8: forces
+// Per-state terms accumulated per thread over a fixed strided set of states,
+// then a fixed shared-memory tree. Slots (all fp64):
+//  0 v_w   1 cw   2..4 moment   5..7 F_w/rho   8..10 F_a   11 dry area
+//  12..14 dry moment   15 submerged area   16 nonfinite count
+constexpr int kTerms = 17;
+constexpr int kForceThreads = 256;
+
+__device__ __forceinline__ double3 drag_dev(const StateDev& s, double3 medium, double rho,
+                                            double cd, const PoseDev& P) {
+  const double3 pos = d3(P.p[0], P.p[1], P.p[2]);
+  const double3 vpt = d3(P.v[0], P.v[1], P.v[2]) + cross3(d3(P.w[0], P.w[1], P.w[2]), s.centroid - pos);
+  const double3 vrel = vpt - medium;
+  const double speed = norm3(vrel);
+  if (speed < 1e-12 || s.area <= 0.0) return d3(0, 0, 0);
+  const double facing = dot3(s.normal, d3(vrel.x / speed, vrel.y / speed, vrel.z / speed));
+  if (facing <= 0.0) return d3(0, 0, 0);
+  const double a_perp = s.area * facing;
+  return vrel * (-(0.5 * cd * rho * a_perp * speed));
+}
+
+__global__ void __launch_bounds__(kForceThreads) k_forces(const StateDev* __restrict__ states,
+                                                          const int2* total, PoseDev P,
+                                                          SliceView vel, int have_vel, int clamp,
+                                                          FluidDev F, double* block_out,
+                                                          int* domain_err) {
+  __shared__ double sh[kTerms][kForceThreads];
+  const int ns = total->x;
+  double acc[kTerms];
+#pragma unroll
+  for (int k = 0; k < kTerms; ++k) acc[k] = 0.0;
+  const int stride = gridDim.x * blockDim.x;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ns; i += stride) {
+    const StateDev s = states[i];
+    if (s.status == 0) {
+      const double w = s.area * s.depth * s.normal.y;
+      acc[0] += w;
+      acc[1] += w;
+      acc[2] += s.centroid.x * w;
+      acc[3] += (s.centroid.y - 0.5 * s.depth) * w;
+      acc[4] += s.centroid.z * w;
+      double3 med = d3(0, 0, 0);
+      if (have_vel) {
+        double v[3];
+        if (!velocity_at_dev(vel, s.centroid.x, s.centroid.z, s.centroid.y, OCN_INTERP_EXPONENTIAL,
+                             clamp, v))
+          atomicOr(domain_err, 1);
+        med = d3(v[0], v[1], v[2]);
+      }
+      const double3 f = drag_dev(s, med, 1.0, F.cd_water, P);  // rho_w applied at finalize
+      acc[5] += f.x, acc[6] += f.y, acc[7] += f.z;
+      acc[15] += s.area;
+    } else {
+      const double3 f = drag_dev(s, d3(F.wind[0], F.wind[1], F.wind[2]), F.air_density, F.cd_air, P);
+      acc[8] += f.x, acc[9] += f.y, acc[10] += f.z;
+      acc[11] += s.area;
+      acc[12] += s.centroid.x * s.area;
+      acc[13] += s.centroid.y * s.area;
+      acc[14] += s.centroid.z * s.area;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kTerms - 1; ++k) sh[k][threadIdx.x] = acc[k];
+  sh[kTerms - 1][threadIdx.x] = 0.0;
+  __syncthreads();
+  for (int off = kForceThreads / 2; off > 0; off >>= 1) {
+    if (threadIdx.x < off)
+      for (int k = 0; k < kTerms; ++k) sh[k][threadIdx.x] += sh[k][threadIdx.x + off];
+    __syncthreads();
+  }
+  if (threadIdx.x < kTerms) block_out[blockIdx.x * kTerms + threadIdx.x] = sh[threadIdx.x][0];
+}
+
+__device__ __forceinline__ double density_at_dev(const FluidDev& F, double y) {
+  const int n = F.n_profile;
+  const double* p = F.profile;
+  if (n == 0) return F.water_density;
+  if (y <= p[0]) return p[1];
+  if (y >= p[2 * (n - 1)]) return p[2 * (n - 1) + 1];
+  for (int i = 1; i < n; ++i)
+    if (y <= p[2 * i]) {
+      const double y0 = p[2 * (i - 1)], r0 = p[2 * (i - 1) + 1], y1 = p[2 * i], r1 = p[2 * i + 1];
+      const double u = (y - y0) / (y1 - y0);
+      return (1.0 - u) * r0 + u * r1;
+    }
+  return F.water_density;
+}
+
+__device__ __forceinline__ bool finite3(double3 v) {
+  return isfinite(v.x) && isfinite(v.y) && isfinite(v.z);
+}
+
+// one block: fixed-order tree over the block partials, then the report
+__global__ void __launch_bounds__(256) k_finalize(int nblocks, const double* block_out, PoseDev P,
+                                                  FluidDev F, double mesh_volume, const int2* total,
+                                                  int degenerate, ReportDev* rep) {
+  __shared__ double sh[kTerms][256];
+  for (int k = 0; k < kTerms; ++k) {
+    double a = 0.0;
+    for (int b = threadIdx.x; b < nblocks; b += 256) a += block_out[b * kTerms + k];
+    sh[k][threadIdx.x] = a;
+  }
+  __syncthreads();
+  for (int off = 128; off > 0; off >>= 1) {
+    if (threadIdx.x < off)
+      for (int k = 0; k < kTerms; ++k) sh[k][threadIdx.x] += sh[k][threadIdx.x + off];
+    __syncthreads();
+  }
+  if (threadIdx.x != 0) return;
+  ocn_hydro_report r;
+  memset(&r, 0, sizeof(r));
+  double vw = sh[0][0];
+  if (vw < 0.0) {
+    vw = 0.0;
+    r.volume_clamped = 1;
+  } else if (vw > mesh_volume) {
+    vw = mesh_volume;
+    r.volume_clamped = 1;
+  }
+  r.submerged_volume = vw;
+  const double cw = sh[1][0];
+  const double3 pos = d3(P.p[0], P.p[1], P.p[2]);
+  double3 coi = d3(0, 0, 0);
+  r.has_center_of_immersion = cw > 1e-12;
+  if (r.has_center_of_immersion) coi = d3(sh[2][0] / cw, sh[3][0] / cw, sh[4][0] / cw);
+  double rho_w = F.water_density;
+  if (F.n_profile > 0 && r.has_center_of_immersion) rho_w = density_at_dev(F, coi.y);
+  const double3 fw = d3(sh[5][0] * rho_w, sh[6][0] * rho_w, sh[7][0] * rho_w);
+  const double3 fa = d3(sh[8][0], sh[9][0], sh[10][0]);
+  double3 fb = d3(0, 0, 0), wc = pos;
+  if (r.has_center_of_immersion) {
+    fb = d3(0.0 * -(vw * rho_w), -kGravity * -(vw * rho_w), 0.0 * -(vw * rho_w));  // hydro.cpp:240, 290
+    wc = coi;
+  }
+  const double dry = sh[11][0];
+  const double3 ac = dry > 1e-12 ? d3(sh[12][0] / dry, sh[13][0] / dry, sh[14][0] / dry) : pos;
+  double3 Ft = d3(0, 0, 0), T = d3(0, 0, 0);
+  if (r.has_center_of_immersion) {
+    Ft = Ft + fb;
+    T = T + cross3(wc - pos, fb);
+    Ft = Ft + fw;
+    T = T + cross3(wc - pos, fw);
+  }
+  Ft = Ft + fa;
+  T = T + cross3(ac - pos, fa);
+  st3(r.center_of_immersion, coi);
+  st3(r.buoyancy_force, fb);
+  st3(r.water_drag, fw);
+  st3(r.air_drag, fa);
+  st3(r.water_center, wc);
+  st3(r.air_center, ac);
+  r.submerged_area = sh[15][0];
+  r.dry_area = dry;
+  st3(r.force, Ft);
+  st3(r.torque, T);
+  r.state_count = total->x;
+  r.degenerate_skipped = degenerate;
+  r.nonfinite = !(isfinite(vw) && finite3(coi) && finite3(fw) && finite3(fa) && finite3(Ft) &&
+                  finite3(T) && finite3(ac));
+  rep->r = r;
+}
+
+// ---------------------------------------------------------------- waterline chaining
+__device__ __forceinline__ unsigned long long key64(int2 k) {
+  return ((unsigned long long)(unsigned)k.x << 32) | (unsigned)k.y;
+}
+__device__ __forceinline__ unsigned hash64(unsigned long long k) {
+  k ^= k >> 33;
+  k *= 0xff51afd7ed558ccdULL;
+  k ^= k >> 33;
+  k *= 0xc4ceb9fe1a85ec53ULL;
+  k ^= k >> 33;
+  return (unsigned)k;
+}
+
+// Inserts every (segment, side) under its edge key; a key on a closed mesh
+// has exactly two entries (the two triangles sharing the crossed edge).
+__global__ void k_chain_hash(const SegDev* segs, const int2* total, int hcap,
+                             unsigned long long* hkeys, int* hvals, int* err) {
+  const int nseg = total->y;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < 2 * nseg; e += gridDim.x * blockDim.x) {
+    const int s = e >> 1, side = e & 1;
+    const int2 k = side ? segs[s].kb : segs[s].ka;
+    const unsigned long long key = key64(k) + 1ull;
+    unsigned h = hash64(key) & (hcap - 1);
+    for (int probe = 0; probe < hcap; ++probe) {
+      const unsigned long long prev = atomicCAS(&hkeys[h], 0ull, key);
+      if (prev == 0ull || prev == key) {
+        // two value slots per key; order fixed below by segment index
+        const int slot = atomicAdd(&hvals[3 * h + 2], 1);
+        if (slot < 2) hvals[3 * h + slot] = e;
+        else atomicOr(err, 2);  // > 2 segments on one edge (non-manifold)
+        break;
+      }
+      h = (h + 1) & (hcap - 1);
+    }
+  }
+}
+
+// partner[e] = the other (segment, side) with the same key, or -1
+__global__ void k_chain_partner(const SegDev* segs, const int2* total, int hcap,
+                                const unsigned long long* hkeys, const int* hvals, int* partner) {
+  const int nseg = total->y;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < 2 * nseg; e += gridDim.x * blockDim.x) {
+    const int s = e >> 1, side = e & 1;
+    const int2 k = side ? segs[s].kb : segs[s].ka;
+    const unsigned long long key = key64(k) + 1ull;
+    unsigned h = hash64(key) & (hcap - 1);
+    int p = -1;
+    for (int probe = 0; probe < hcap; ++probe) {
+      if (hkeys[h] == key) {
+        const int cnt = min(hvals[3 * h + 2], 2);
+        for (int q = 0; q < cnt; ++q)
+          if (hvals[3 * h + q] != e) p = hvals[3 * h + q];
+        break;
+      }
+      h = (h + 1) & (hcap - 1);
+    }
+    partner[e] = p;
+  }
+}
+
+// Sequential walk with the reference's visiting order (hydro.cpp:167-213) in
+// shared memory. Emits point references e = 2*segment + side: the crossing
+// point of that key as stored by the larger segment (std::map last writer).
+constexpr int kChainSmem = 12288;  // segments held in shared memory
+
+__global__ void __launch_bounds__(256) k_chain_walk(const int2* total, const int* partner_g,
+                                                    unsigned char* used_g, int* loop_off,
+                                                    int* point_ref, int* counts_out) {
+  extern __shared__ int sm_chain[];
+  const int nseg = total->y;
+  const bool in_smem = nseg <= kChainSmem;
+  const int* partner = in_smem ? sm_chain : partner_g;
+  unsigned char* used =
+      in_smem ? reinterpret_cast<unsigned char*>(sm_chain + 2 * kChainSmem) : used_g;
+  if (in_smem)
+    for (int e = threadIdx.x; e < 2 * nseg; e += blockDim.x) sm_chain[e] = partner_g[e];
+  for (int s = threadIdx.x; s < nseg; s += blockDim.x) used[s] = 0;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  int nl = 0, np = 0;
+  loop_off[0] = 0;
+  auto canon = [&](int e) {
+    const int p = partner[e];
+    return (p >= 0 && (p >> 1) > (e >> 1)) ? p : e;
+  };
+  for (int start = 0; start < nseg; ++start) {
+    if (used[start]) continue;
+    int lp = 0, seg = start, entry = 0;
+    bool closed = false;
+    const int first = 2 * start;  // first_entry = start's first key
+    for (;;) {
+      used[seg] = 1;
+      point_ref[np + lp++] = canon(2 * seg + entry);
+      const int ex = 2 * seg + (1 - entry);
+      const int p = partner[ex];
+      if (p == first) {
+        closed = true;
+        break;
+      }
+      if (p < 0 || used[p >> 1]) {
+        point_ref[np + lp++] = canon(ex);
+        break;
+      }
+      seg = p >> 1;
+      entry = p & 1;
+    }
+    if (lp >= 3) {
+      if (closed) point_ref[np + lp] = point_ref[np], ++lp;
+      np += lp;
+      loop_off[++nl] = np;
+    }
+  }
+  counts_out[0] = nl;
+  counts_out[1] = np;
+}
+
+__global__ void k_chain_points(const SegDev* segs, const int* counts, const int* point_ref,
+                               double* points) {
+  const int np = counts[1];
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < np; q += gridDim.x * blockDim.x) {
+    const int e = point_ref[q];
+    const SegDev& s = segs[e >> 1];
+    const double3 p = (e & 1) ? s.pb : s.pa;
+    st3(points + 3 * q, p);
+  }
+}
+
+__global__ void k_report_loops(ReportDev* rep, const int* counts) {
+  rep->r.waterline_loops = counts[0];
+  rep->r.waterline_points = counts[1];
+}
+
+int grid_of(ocn_ctx* ctx, int n, int threads) {
+  int b = (n + threads - 1) / threads;
+  int cap = ctx->sm_count * 8;
+  return b < 1 ? 1 : (b > cap ? cap : b);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- host pipeline
+void hydro_evaluate(ocn_mesh* m, const ocn_pose* pose, const ocn_fluid* fluid,
+                    const double* host_depth) {
+  ocn_ctx* ctx = m->ctx;
+  DeviceScope ds(ctx);
+  cudaStream_t st = ctx->stream;
+  PoseDev P;
+  for (int k = 0; k < 3; ++k) {
+    P.p[k] = pose->position[k];
+    P.v[k] = pose->linear_velocity[k];
+    P.w[k] = pose->angular_velocity[k];
+    P.com[k] = pose->com_body[k];
+  }
+  for (int k = 0; k < 4; ++k) P.q[k] = pose->orientation[k];
+  ocn_maps* maps = fluid ? (ocn_maps*)fluid->maps : nullptr;
+  ocn_slices* slices = fluid ? (ocn_slices*)fluid->slices : nullptr;
+  // maps == NULL: still water (FluidQuery::still_water, hydro.cpp:25-30) plus any zones
+  SurfView sv{};
+  if (maps) sv = make_surf_view(maps);
+  SliceView vv{};
+  if (slices) vv = make_slice_view(slices);
+  ZoneList zl{};
+  if (fluid && fluid->n_zones) {
+    OCN_REQUIRE(fluid->n_zones <= kMaxZones, "too many zones (%d)", fluid->n_zones);
+    zl.count = fluid->n_zones;
+    for (int z = 0; z < zl.count; ++z) zl.z[z] = zone_view((ocn_zone*)fluid->zones[z]);
+  }
+  FluidDev F{};
+  if (fluid) {
+    for (int k = 0; k < 3; ++k) F.wind[k] = fluid->wind[k];
+    F.water_density = fluid->water_density;
+    F.air_density = fluid->air_density;
+    F.cd_water = fluid->cd_water;
+    F.cd_air = fluid->cd_air;
+    F.n_profile = fluid->n_profile;
+    if (fluid->n_profile > 0) {
+      m->d_profile.ensure(2 * (size_t)fluid->n_profile);
+      OCN_CUDA(cudaMemcpyAsync(m->d_profile.p, fluid->host_profile,
+                               2 * (size_t)fluid->n_profile * sizeof(double),
+                               cudaMemcpyHostToDevice, st));
+      F.profile = m->d_profile.p;
+    }
+  } else {
+    F.water_density = 1025.0;
+    F.air_density = 1.204;
+    F.cd_water = F.cd_air = 1.0;
+  }
+  const int nv = m->nv, nt = m->nt;
+  const double* d_override = nullptr;
+  if (host_depth) {
+    OCN_CUDA(cudaMemcpyAsync(m->override_depth.p, host_depth, nv * sizeof(double),
+                             cudaMemcpyHostToDevice, st));
+    d_override = m->override_depth.p;
+  }
+  ProfWindow pw(ctx, OCN_PROF_HYDRO);
+  OCN_CUDA(cudaMemsetAsync(m->flags.p, 0, 4 * sizeof(int), st));
+  k_vertices<<<grid_of(ctx, nv, 128), 128, 0, st>>>(nv, m->verts.p, P, sv, maps != nullptr, zl,
+                                                   d_override, m->wpos.p, m->depth.p);
+  OCN_LAUNCHED(ctx);
+  k_classify<<<grid_of(ctx, nt, 256), 256, 0, st>>>(nt, m->tris.p, m->areas.p, m->depth.p,
+                                                   m->counts.p);
+  OCN_LAUNCHED(ctx);
+  const int nb = (nt + kScanBlock - 1) / kScanBlock;
+  k_scan_local<<<nb, kScanBlock, 0, st>>>(nt, m->counts.p, m->offsets.p, m->block_sums.p);
+  OCN_LAUNCHED(ctx);
+  k_scan_blocks<<<1, 32, 0, st>>>(nb, m->block_sums.p, m->total.p);
+  OCN_LAUNCHED(ctx);
+  k_scan_add<<<nb, kScanBlock, 0, st>>>(nt, m->offsets.p, m->block_sums.p);
+  OCN_LAUNCHED(ctx);
+  k_emit<<<grid_of(ctx, nt, 256), 256, 0, st>>>(nt, m->tris.p, m->normals.p, m->wpos.p, m->depth.p,
+                                               P, m->counts.p, m->offsets.p, m->states.p,
+                                               m->segs.p);
+  OCN_LAUNCHED(ctx);
+  const int fblocks = ctx->sm_count * 2;
+  k_forces<<<fblocks, kForceThreads, 0, st>>>(m->states.p, m->total.p, P, vv, slices != nullptr,
+                                             fluid ? fluid->velocity_clamp : 1, F,
+                                             m->block_out.p, m->flags.p);
+  OCN_LAUNCHED(ctx);
+  k_finalize<<<1, 256, 0, st>>>(fblocks, m->block_out.p, P, F, m->volume, m->total.p,
+                                m->degenerate, m->report.p);
+  OCN_LAUNCHED(ctx);
+  // waterline
+  OCN_CUDA(cudaMemsetAsync(m->hkeys.p, 0, m->hkeys.bytes(), st));
+  OCN_CUDA(cudaMemsetAsync(m->hvals.p, 0, m->hvals.bytes(), st));
+  k_chain_hash<<<grid_of(ctx, 2 * nt, 256), 256, 0, st>>>(m->segs.p, m->total.p, m->hcap,
+                                                          m->hkeys.p, m->hvals.p, m->flags.p + 1);
+  OCN_LAUNCHED(ctx);
+  k_chain_partner<<<grid_of(ctx, 2 * nt, 256), 256, 0, st>>>(m->segs.p, m->total.p, m->hcap,
+                                                             m->hkeys.p, m->hvals.p, m->partner.p);
+  OCN_LAUNCHED(ctx);
+  const size_t chain_smem = 2 * kChainSmem * sizeof(int) + kChainSmem;
+  static bool attr = false;
+  if (!attr) {
+    OCN_CUDA(cudaFuncSetAttribute(k_chain_walk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)chain_smem));
+    attr = true;
+  }
+  k_chain_walk<<<1, 256, chain_smem, st>>>(m->total.p, m->partner.p, m->used.p, m->loop_off.p,
+                                           m->point_ref.p, m->loop_counts.p);
+  OCN_LAUNCHED(ctx);
+  k_chain_points<<<grid_of(ctx, nt, 256), 256, 0, st>>>(m->segs.p, m->loop_counts.p,
+                                                        m->point_ref.p, m->loop_points.p);
+  OCN_LAUNCHED(ctx);
+  k_report_loops<<<1, 1, 0, st>>>(m->report.p, m->loop_counts.p);
+  OCN_LAUNCHED(ctx);
+  m->evaluated = true;
+}
+
+void hydro_check_flags(ocn_mesh* m) {
+  int flags[4];
+  OCN_CUDA(cudaMemcpy(flags, m->flags.p, sizeof(flags), cudaMemcpyDeviceToHost));
+  if (flags[0]) fail(OCN_ERR_DOMAIN, "velocity_at: depth outside [y_min, y_max]");
+  if (flags[1]) fail(OCN_ERR_MESH, "waterline: an edge is shared by more than two triangles");
+}
+
+}  // namespace ocn
+
+using namespace ocn;
+
+extern "C" {
+
+int ocn_mesh_create(ocn_ctx* ctx, int nv, const double* verts, int nt, const int32_t* tris,
+                    const double* normals, const double* areas, double volume, ocn_mesh** out) {
+  return api_call(ctx, [&] {
+    OCN_REQUIRE(ctx && out && verts && tris && normals && areas, "null argument");
+    if (nv <= 0 || nt <= 0) fail(OCN_ERR_MESH, "empty mesh");
+    DeviceScope ds(ctx);
+    auto m = std::make_unique<ocn_mesh>();
+    m->ctx = ctx;
+    m->nv = nv;
+    m->nt = nt;
+    m->volume = volume;
+    for (int t = 0; t < nt; ++t) {
+      for (int k = 0; k < 3; ++k)
+        if (tris[3 * t + k] < 0 || tris[3 * t + k] >= nv)
+          fail(OCN_ERR_MESH, "mesh: face references a missing vertex");
+      if (areas[t] <= 0.0) ++m->degenerate;
+    }
+    m->verts.alloc(3 * (size_t)nv);
+    m->tris.alloc(nt);
+    m->normals.alloc(3 * (size_t)nt);
+    m->areas.alloc(nt);
+    OCN_CUDA(cudaMemcpy(m->verts.p, verts, 3 * (size_t)nv * sizeof(double), cudaMemcpyHostToDevice));
+    OCN_CUDA(cudaMemcpy(m->tris.p, tris, (size_t)nt * sizeof(int3), cudaMemcpyHostToDevice));
+    OCN_CUDA(cudaMemcpy(m->normals.p, normals, 3 * (size_t)nt * sizeof(double), cudaMemcpyHostToDevice));
+    OCN_CUDA(cudaMemcpy(m->areas.p, areas, (size_t)nt * sizeof(double), cudaMemcpyHostToDevice));
+    m->wpos.alloc(3 * (size_t)nv);
+    m->depth.alloc(nv);
+    m->override_depth.alloc(nv);
+    m->counts.alloc(nt);
+    m->offsets.alloc(nt);
+    m->block_sums.alloc((nt + kScanBlock - 1) / kScanBlock + 1);
+    m->total.alloc(1);
+    m->states.alloc(3 * (size_t)nt);
+    m->segs.alloc(nt);
+    m->block_out.alloc((size_t)ctx->sm_count * 2 * kTerms);
+    m->report.alloc(1);
+    m->flags.alloc(4);
+    int hcap = 1;
+    while (hcap < 4 * nt) hcap <<= 1;
+    m->hcap = hcap;
+    m->hkeys.alloc(hcap);
+    m->hvals.alloc(3 * (size_t)hcap);
+    m->partner.alloc(2 * (size_t)nt);
+    m->used.alloc(nt);
+    m->loop_off.alloc((size_t)nt + 2);
+    m->point_ref.alloc(2 * (size_t)nt + 2);
+    m->loop_points.alloc(3 * (2 * (size_t)nt + 2));
+    m->loop_counts.alloc(2);
+    OCN_CUDA(cudaMemset(m->total.p, 0, sizeof(int2)));
+    OCN_CUDA(cudaMemset(m->loop_counts.p, 0, 2 * sizeof(int)));
+    ctx_retain(ctx);
+    *out = m.release();
+  });
+}
+
+int ocn_mesh_destroy(ocn_mesh* m) {
+  if (!m) return OCN_OK;
+  ocn_ctx* ctx = m->ctx;
+  {
+    DeviceScope ds(ctx);
+    cudaStreamSynchronize(ctx->stream);
+    delete m;
+  }
+  ctx_release(ctx);
+  return OCN_OK;
+}
+
+int ocn_hydro_aggregate(ocn_mesh* m, const ocn_pose* pose, const ocn_fluid* fluid,
+                        const double* host_depth, ocn_hydro_report* report) {
+  return api_call(m ? m->ctx : nullptr, [&] {
+    OCN_REQUIRE(m && pose, "null argument");
+    hydro_evaluate(m, pose, fluid, host_depth);
+    if (report) {
+      ReportDev r;
+      OCN_CUDA(cudaMemcpyAsync(&r, m->report.p, sizeof(r), cudaMemcpyDeviceToHost, m->ctx->stream));
+      OCN_CUDA(cudaStreamSynchronize(m->ctx->stream));
+      hydro_check_flags(m);
+      *report = r.r;
+    }
+  });
+}
+
+int ocn_hydro_report_get(ocn_mesh* m, ocn_hydro_report* report) {
+  return api_call(m ? m->ctx : nullptr, [&] {
+    OCN_REQUIRE(m && report, "null argument");
+    OCN_REQUIRE(m->evaluated, "no hydro evaluation yet");
+    DeviceScope ds(m->ctx);
+    ReportDev r;
+    OCN_CUDA(cudaMemcpyAsync(&r, m->report.p, sizeof(r), cudaMemcpyDeviceToHost, m->ctx->stream));
+    OCN_CUDA(cudaStreamSynchronize(m->ctx->stream));
+    hydro_check_flags(m);
+    *report = r.r;
+  });
+}
+
+int ocn_hydro_vertices(ocn_mesh* m, double* world, double* depth) {
+  return api_call(m ? m->ctx : nullptr, [&] {
+    OCN_REQUIRE(m && m->evaluated, "no hydro evaluation yet");
+    DeviceScope ds(m->ctx);
+    OCN_CUDA(cudaStreamSynchronize(m->ctx->stream));
+    if (world)
+      OCN_CUDA(cudaMemcpy(world, m->wpos.p, 3 * (size_t)m->nv * sizeof(double), cudaMemcpyDeviceToHost));
+    if (depth)
+      OCN_CUDA(cudaMemcpy(depth, m->depth.p, (size_t)m->nv * sizeof(double), cudaMemcpyDeviceToHost));
+  });
+}
+
+int ocn_hydro_states(ocn_mesh* m, int capacity, ocn_triangle_state* out, int* count) {
+  return api_call(m ? m->ctx : nullptr, [&] {
+    OCN_REQUIRE(m && m->evaluated, "no hydro evaluation yet");
+    DeviceScope ds(m->ctx);
+    OCN_CUDA(cudaStreamSynchronize(m->ctx->stream));
+    int2 tot;
+    OCN_CUDA(cudaMemcpy(&tot, m->total.p, sizeof(tot), cudaMemcpyDeviceToHost));
+    if (count) *count = tot.x;
+    if (out && capacity > 0) {
+      int n = std::min(capacity, tot.x);
+      std::vector<StateDev> tmp(n);
+      OCN_CUDA(cudaMemcpy(tmp.data(), m->states.p, n * sizeof(StateDev), cudaMemcpyDeviceToHost));
+      for (int i = 0; i < n; ++i) {
+        out[i].parent = tmp[i].parent;
+        out[i].status = tmp[i].status;
+        out[i].area = tmp[i].area;
+        out[i].centroid[0] = tmp[i].centroid.x;
+        out[i].centroid[1] = tmp[i].centroid.y;
+        out[i].centroid[2] = tmp[i].centroid.z;
+        out[i].depth = tmp[i].depth;
+        out[i].normal[0] = tmp[i].normal.x;
+        out[i].normal[1] = tmp[i].normal.y;
+        out[i].normal[2] = tmp[i].normal.z;
+      }
+    }
+  });
+}
+
+int ocn_hydro_waterline(ocn_mesh* m, int* n_loops, int* n_points, int32_t* offsets, double* points) {
+  return api_call(m ? m->ctx : nullptr, [&] {
+    OCN_REQUIRE(m && m->evaluated, "no hydro evaluation yet");
+    DeviceScope ds(m->ctx);
+    OCN_CUDA(cudaStreamSynchronize(m->ctx->stream));
+    int cnt[2];
+    OCN_CUDA(cudaMemcpy(cnt, m->loop_counts.p, sizeof(cnt), cudaMemcpyDeviceToHost));
+    if (n_loops) *n_loops = cnt[0];
+    if (n_points) *n_points = cnt[1];
+    if (offsets)
+      OCN_CUDA(cudaMemcpy(offsets, m->loop_off.p, (cnt[0] + 1) * sizeof(int), cudaMemcpyDeviceToHost));
+    if (points && cnt[1] > 0)
+      OCN_CUDA(cudaMemcpy(points, m->loop_points.p, 3 * (size_t)cnt[1] * sizeof(double),
+                          cudaMemcpyDeviceToHost));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,121 @@
+// objects.cuh — the opaque handle types behind the C-ABI, and the API guard.
+#pragma once
+
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "common.cuh"
+
+namespace ocn {
+
+constexpr int kMaxCascades = 16;
+
+// One packed C2C transform of the spectral step (X + iY of one field pair).
+enum XformKind : int {
+  kSurfHDx = 0,     // (H, Dx)        surface.cpp:77
+  kSurfDzDxDx = 1,  // (Dz, DxDx)     surface.cpp:78
+  kSurfDzDxDzDz = 2,// (DzDx, DzDz)   surface.cpp:79
+  kSurfHxHz = 3,    // (Hx, Hz)       surface.cpp:80
+  kVelXZ = 4,       // (vx_d, vz_d)   velocity.cpp:156-161
+  kVelYPair = 5,    // (vy_d, vy_d+1) velocity.cpp:163-167
+  kVelYSingle = 6,  // (vy_d, 0)      velocity.cpp:168-172
+};
+
+struct XformDesc {
+  int cascade;
+  int kind;
+  float y0, y1;   // slice depths for the velocity kinds
+  float* out_re;  // fp32 plane [N][N] receiving Re
+  float* out_im;  // fp32 plane receiving Im (nullptr: dropped)
+};
+
+struct SpectralPlan {
+  DevBuf<XformDesc> desc;
+  std::vector<XformDesc> host_desc;
+  std::vector<int> first;  // per cascade: first transform index
+  std::vector<int> count;  // per cascade: number of transforms
+  bool need_surface = false, need_velocity = false;
+};
+
+}  // namespace ocn
+
+struct ocn_cascades {
+  ocn_ctx* ctx = nullptr;
+  int refs = 1;  // owner + every maps / slices built on it (freed at zero)
+  int n = 0, count = 0;
+  std::vector<double> lengths, band_min, band_max;
+  std::vector<uint32_t> cascade_index;
+  ocn_spectrum_params params{};
+  ocn::DevBuf<double2> h0_f64;  // [C][N][N] fp64 amplitudes (API download)
+  ocn::DevBuf<float2> h0;       // [C][N][N] fp32 hot-path table
+  ocn::DevBuf<uint8_t> in_band; // [C][N][N]
+  ocn::DevBuf<float2> twiddle;  // per-N inter-pass twiddles (fft_core.cuh)
+  ocn::DevBuf<float4> spec;     // [C][N][N] evolved (h~, G) at the current frame
+  ocn::DevBuf<float2> scratch;  // row-pass intermediates of one transform group
+  int group = 1;                // transforms per group
+  std::map<std::pair<const void*, const void*>, std::unique_ptr<ocn::SpectralPlan>> plans;
+};
+
+struct ocn_maps {
+  ocn_cascades* cas = nullptr;
+  double time = 0.0;
+  double choppiness = 1.0;
+  ocn::DevBuf<float> fields;  // [C][8][N][N]
+  float* field(int c, int f) { return fields.p + ((size_t)c * 8 + f) * (size_t)cas->n * cas->n; }
+};
+
+struct ocn_slices {
+  ocn_cascades* cas = nullptr;
+  ocn_slice_config cfg{};
+  std::vector<double> depths;
+  double time = 0.0;
+  ocn::DevBuf<double> d_depths;
+  ocn::DevBuf<float> fields;  // [D][C][3][N][N]
+  float* field(int d, int c, int comp) {
+    size_t nn = (size_t)cas->n * cas->n;
+    return fields.p + (((size_t)d * cas->count + c) * 3 + comp) * nn;
+  }
+};
+
+namespace ocn {
+
+// Per-thread fallback error slot for calls without a context.
+std::string& global_error();
+
+template <typename F>
+int api_call(ocn_ctx* ctx, F&& f) {
+  try {
+    f();
+    return OCN_OK;
+  } catch (const Error& e) {
+    if (ctx) ctx->last_error = e.what();
+    global_error() = e.what();
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    if (ctx) ctx->last_error = "out of host memory";
+    global_error() = "out of host memory";
+    return OCN_ERR_CUDA;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->last_error = e.what();
+    global_error() = e.what();
+    return OCN_ERR_ARG;
+  }
+}
+
+#define OCN_REQUIRE(cond, ...)                         \
+  do {                                                 \
+    if (!(cond)) ::ocn::fail(OCN_ERR_ARG, __VA_ARGS__); \
+  } while (0)
+
+void ctx_retain(ocn_ctx* ctx);
+void ctx_release(ocn_ctx* ctx);
+
+// Spectral engine (spectral.cu)
+void spectral_step(ocn_cascades* cas, ocn_maps* maps, ocn_slices* slices, double t,
+                   double choppiness);
+
+}  // namespace ocn

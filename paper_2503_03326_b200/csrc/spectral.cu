@@ -1,0 +1,1085 @@
+// spectral.cu — K1 (spectrum init), time evolution, and the fused
+// coefficient + batched packed 2D inverse FFT (K2 + K3 + K4) on sm_100a.
+//
+// Reference path replaced: generate_h0 (spectra.cpp:132-179), CascadeSet
+// (surface.cpp:22-37), assemble_coefficients + generate_maps
+// (surface.cpp:39-103), build_slices (velocity.cpp:104-179),
+// ifft2_centered / ifft2_hermitian_pair (fft.cpp:39-101).
+//
+// Per frame and cascade:
+//   k_evolve     : h~(k,t) = h0 e^{iwt} + conj(h0(-k)) e^{-iwt} and
+//                  G(k,t) = h0 e^{iwt} - conj(h0(-k)) e^{-iwt}  (fp64 phase,
+//                  reduced mod 2pi before the fp32 sincos) -> spec[c] (L2)
+//   k_rows<N>    : per (row, transform of the group): the packed coefficient
+//                  X + iY = spec * multiplier(k) generated in registers (no
+//                  coefficient arrays in HBM), then the row FFT -> scratch
+//   k_cols<N>    : column FFT of scratch, (-1)^(i+j), Re -> field X,
+//                  Im -> field Y (fp32 maps / slices, row-major [i][j])
+// The group size keeps scratch (group * N^2 * 8 B) L2-resident at N = 1024.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "fft_core.cuh"
+#include "objects.cuh"
+#include "spectrum_math.cuh"
+
+namespace ocn {
+
+std::string& global_error() {
+  static thread_local std::string e;
+  return e;
+}
+
+// Handles keep their context (and maps / slices their cascades) alive, so
+// destruction order from garbage-collected front ends never matters.
+void ctx_retain(ocn_ctx* ctx) { ctx->refs.fetch_add(1); }
+void ctx_release(ocn_ctx* ctx) {
+  if (!ctx || ctx->refs.fetch_sub(1) != 1) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+static void cascades_release(ocn_cascades* c) {
+  if (!c || --c->refs != 0) return;
+  ocn_ctx* ctx = c->ctx;
+  {
+    DeviceScope ds(ctx);
+    cudaStreamSynchronize(ctx->stream);
+    delete c;
+  }
+  ctx_release(ctx);
+}
+
+namespace {
+
+constexpr int kThreads = 256;
+
+template <int N>
+struct Launch {
+  using PL = fft::Plan<N>;
+  static constexpr int T = PL::T;
+  static constexpr int THREADS = T > kThreads ? T : kThreads;
+  static constexpr int PER_CTA = THREADS / T;  // transforms per CTA
+  // per-transform shared stride: >= SMEM and == 4 (mod 16) float2 so that
+  // neighbouring transforms start 8 banks apart
+  static constexpr int STRIDE = PL::SMEM + ((4 - (PL::SMEM % 16)) + 16) % 16;
+  static constexpr size_t SMEM_BYTES = (PL::P > 1) ? (size_t)PER_CTA * STRIDE * sizeof(float2) : 0;
+};
+
+// ------------------------------------------------------------------ K1
+struct InitArgs {
+  int n, count;
+  double dk[kMaxCascades];
+  double length[kMaxCascades];
+  double band_min[kMaxCascades], band_max[kMaxCascades];
+  uint32_t cindex[kMaxCascades];
+  ocn_spectrum_params p;
+  double2* h0_f64;
+  float2* h0;
+  uint8_t* in_band;
+};
+
+// generate_h0, spectra.cpp:150-169, one thread per mode (fp64, bit-exact
+// Philox and band mask).
+__global__ void __launch_bounds__(256) k_spectrum_init(const InitArgs a) {
+  const size_t nn = (size_t)a.n * a.n;
+  const size_t total = nn * a.count;
+  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    const int c = (int)(idx / nn);
+    const size_t q = idx - (size_t)c * nn;
+    const int i = (int)(q / a.n), j = (int)(q - (size_t)i * a.n);
+    const double dk = a.dk[c];
+    const double kx = dk * (i - a.n / 2);
+    const double kz = dk * (j - a.n / 2);
+    const double k = sm::hypot_ref(kx, kz);
+    const double omega = sqrt(a.p.gravity * k);
+    const bool banded = k > 0.0 && k >= a.band_min[c] && k < a.band_max[c];
+    double hr = 0.0, hi = 0.0;
+    if (banded) {
+      double gr, gi;
+      sm::gaussian_complex(a.p.rng_seed, a.cindex[c], (uint32_t)i, (uint32_t)j, &gr, &gi);
+      const double amp = sqrt(sm::h0_variance(kx, kz, k, omega, a.length[c], a.p));
+      hr = gr * amp;
+      hi = gi * amp;
+    }
+    a.h0_f64[idx] = make_double2(hr, hi);
+    a.h0[idx] = make_float2((float)hr, (float)hi);
+    a.in_band[idx] = banded ? 1 : 0;
+  }
+}
+
+// WaveGrid accessors: h0_conj_neg (spectra.cpp:171-177) and wave vectors.
+__global__ void k_grid_extras(int n, double dk, double g, const double2* h0, double2* h0cn,
+                              double4* waves) {
+  const size_t nn = (size_t)n * n;
+  for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < nn;
+       q += (size_t)gridDim.x * blockDim.x) {
+    const int i = (int)(q / n), j = (int)(q % n);
+    if (h0cn) {
+      const int ni = i == 0 ? 0 : n - i, nj = j == 0 ? 0 : n - j;
+      const double2 v = h0[(size_t)ni * n + nj];
+      h0cn[q] = make_double2(v.x, -v.y);
+    }
+    if (waves) {
+      const double kx = dk * (i - n / 2), kz = dk * (j - n / 2);
+      const double k = sm::hypot_ref(kx, kz);
+      waves[q] = make_double4(kx, kz, k, sqrt(g * k));
+    }
+  }
+}
+
+// ------------------------------------------------------------------ evolve
+// h~ and G (surface.cpp:49-50; velocity.cpp:16-20) at time t, one cascade.
+__global__ void __launch_bounds__(256) k_evolve(int n, double dk, double g, double t,
+                                                const float2* __restrict__ h0, float4* spec) {
+  const int nn = n * n;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nn; q += gridDim.x * blockDim.x) {
+    const int i = q / n, j = q - i * n;
+    const int ni = i == 0 ? 0 : n - i, nj = j == 0 ? 0 : n - j;
+    const float2 a = __ldg(h0 + q);
+    const float2 m = __ldg(h0 + ni * n + nj);
+    const float2 b = make_float2(m.x, -m.y);  // conj(h0(-k))
+    const double kx = dk * (i - n / 2), kz = dk * (j - n / 2);
+    const double omega = sqrt(g * sqrt(kx * kx + kz * kz));
+    double ph = omega * t;
+    ph -= 6.283185307179586476925 * rint(ph * 0.15915494309189533577);
+    float s, c;
+    sincosf((float)ph, &s, &c);
+    // A = a e^{i ph}, B = b e^{-i ph}
+    const float ar = a.x * c - a.y * s, ai = a.x * s + a.y * c;
+    const float br = b.x * c + b.y * s, bi = b.y * c - b.x * s;
+    spec[q] = make_float4(ar + br, ai + bi, ar - br, ai - bi);
+  }
+}
+
+// ------------------------------------------------------------------ rows
+struct RowArgs {
+  int items;  // N * G
+  int G;
+  const XformDesc* desc;  // group descriptors (spectral mode)
+  const float4* spec;     // cascade's (h~, G) table
+  float dk, gravity, chop;
+  const float2* src;  // plain mode: [G][N][N] complex input
+  float2* scratch;    // [G][N][N]
+  const float2* tw;
+};
+
+// packed coefficient X + iY of transform `d` at mode (i, j)
+__device__ __forceinline__ float2 packed_coef(const XformDesc& d, float4 s, int i, int j, int n,
+                                              float dk, float g, float chop) {
+  const float kx = dk * (float)(i - n / 2);
+  const float kz = dk * (float)(j - n / 2);
+  const float k2 = kx * kx + kz * kz;
+  if (k2 == 0.0f) return make_float2(0.f, 0.f);
+  const float k = sqrtf(k2);
+  const float inv_k = 1.0f / k;
+  float mr, mi;
+  float2 base;
+  switch (d.kind) {
+    case kSurfHDx: {  // h~ (1 - ux chop)
+      mr = 1.0f - kx * inv_k * chop;
+      mi = 0.f;
+      base = make_float2(s.x, s.y);
+      break;
+    }
+    case kSurfDzDxDx: {  // i chop (uz + kx ux) h~
+      mr = 0.f;
+      mi = chop * (kz * inv_k + kx * kx * inv_k);
+      base = make_float2(s.x, s.y);
+      break;
+    }
+    case kSurfDzDxDzDz: {  // chop uz (kx + i kz) h~
+      const float f = chop * kz * inv_k;
+      mr = f * kx;
+      mi = f * kz;
+      base = make_float2(s.x, s.y);
+      break;
+    }
+    case kSurfHxHz: {  // (-kz + i kx) h~
+      mr = -kz;
+      mi = kx;
+      base = make_float2(s.x, s.y);
+      break;
+    }
+    case kVelXZ: {  // -(g/w) E(y0) (kx + i kz) G
+      const float w = sqrtf(g * k);
+      const float e = d.y0 > 0.f ? 1.0f + k * d.y0 : expf(k * d.y0);
+      const float f = -(g / w) * e;
+      mr = f * kx;
+      mi = f * kz;
+      base = make_float2(s.z, s.w);
+      break;
+    }
+    case kVelYPair: {  // w (-E(y1) + i E(y0)) G
+      const float w = sqrtf(g * k);
+      const float e0 = d.y0 > 0.f ? 1.0f + k * d.y0 : expf(k * d.y0);
+      const float e1 = d.y1 > 0.f ? 1.0f + k * d.y1 : expf(k * d.y1);
+      mr = -w * e1;
+      mi = w * e0;
+      base = make_float2(s.z, s.w);
+      break;
+    }
+    default: {  // kVelYSingle: i w E(y0) G
+      const float w = sqrtf(g * k);
+      const float e0 = d.y0 > 0.f ? 1.0f + k * d.y0 : expf(k * d.y0);
+      mr = 0.f;
+      mi = w * e0;
+      base = make_float2(s.z, s.w);
+      break;
+    }
+  }
+  return make_float2(base.x * mr - base.y * mi, base.x * mi + base.y * mr);
+}
+
+template <int N, bool PLAIN>
+__global__ void __launch_bounds__(Launch<N>::THREADS) k_rows(const RowArgs a) {
+  using L = Launch<N>;
+  extern __shared__ float2 smem[];
+  const int local = threadIdx.x / L::T;
+  const int t = threadIdx.x - local * L::T;
+  const int item = blockIdx.x * L::PER_CTA + local;
+  const bool valid = item < a.items;
+  const int row = valid ? item / a.G : 0;
+  const int gi = valid ? item - row * a.G : 0;
+  float2* sm = smem + local * L::STRIDE;
+  float2* out = a.scratch + ((size_t)gi * N + row) * N;
+  if constexpr (PLAIN) {
+    const float2* in = a.src + ((size_t)gi * N + row) * N;
+    fft::cta_fft<N>(
+        t, sm, a.tw, [&](int j) { return valid ? __ldg(in + j) : make_float2(0.f, 0.f); },
+        [&](int k, float2 x) {
+          if (valid) out[k] = x;
+        });
+  } else {
+    const XformDesc d = a.desc[gi];
+    const float4* srow = a.spec + (size_t)row * N;
+    fft::cta_fft<N>(
+        t, sm, a.tw,
+        [&](int j) {
+          if (!valid) return make_float2(0.f, 0.f);
+          return packed_coef(d, __ldg(srow + j), row, j, N, a.dk, a.gravity, a.chop);
+        },
+        [&](int k, float2 x) {
+          if (valid) out[k] = x;
+        });
+  }
+}
+
+// ------------------------------------------------------------------ columns
+struct ColArgs {
+  const float2* scratch;  // [G][N][N]
+  const XformDesc* desc;  // split outputs per transform
+  float2* out_c;          // complex mode: [G][N][N]
+  const float2* tw;
+};
+
+template <int N, bool COMPLEX_OUT>
+__global__ void __launch_bounds__(Launch<N>::THREADS) k_cols(const ColArgs a) {
+  using L = Launch<N>;
+  extern __shared__ float2 smem[];
+  const int c = threadIdx.x % L::PER_CTA;  // column within the tile (fastest)
+  const int t = threadIdx.x / L::PER_CTA;
+  const int col = blockIdx.x * L::PER_CTA + c;
+  const int xf = blockIdx.y;
+  const bool valid = col < N;
+  float2* sm = smem + c * L::STRIDE;
+  const float2* in = a.scratch + (size_t)xf * N * N + (valid ? col : 0);
+  if constexpr (COMPLEX_OUT) {
+    float2* out = a.out_c + (size_t)xf * N * N;
+    fft::cta_fft<N>(
+        t, sm, a.tw, [&](int i) { return __ldg(in + (size_t)i * N); },
+        [&](int r, float2 x) {
+          if (!valid) return;
+          const float s = ((r + col) & 1) ? -1.f : 1.f;  // fft.cpp:73-75
+          out[(size_t)r * N + col] = make_float2(s * x.x, s * x.y);
+        });
+  } else {
+    const XformDesc d = a.desc[xf];
+    fft::cta_fft<N>(
+        t, sm, a.tw, [&](int i) { return __ldg(in + (size_t)i * N); },
+        [&](int r, float2 x) {
+          if (!valid) return;
+          const float s = ((r + col) & 1) ? -1.f : 1.f;
+          d.out_re[(size_t)r * N + col] = s * x.x;  // fft.cpp:93-99 split
+          if (d.out_im) d.out_im[(size_t)r * N + col] = s * x.y;
+        });
+  }
+}
+
+// fp64 interleaved pair -> fp32 X + iY (fft.cpp:88-91)
+__global__ void k_pack_pair(size_t nn, const double2* x, const double2* y, float2* out) {
+  for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < nn;
+       q += (size_t)gridDim.x * blockDim.x) {
+    const double2 a = x[q];
+    const double2 b = y ? y[q] : make_double2(0.0, 0.0);
+    out[q] = make_float2((float)(a.x - b.y), (float)(a.y + b.x));
+  }
+}
+
+__global__ void k_f32_to_f64(size_t n, const float* in, double* out) {
+  for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n;
+       q += (size_t)gridDim.x * blockDim.x)
+    out[q] = (double)in[q];
+}
+
+__global__ void k_c32_to_c64(size_t n, const float2* in, double2* out) {
+  for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n;
+       q += (size_t)gridDim.x * blockDim.x)
+    out[q] = make_double2(in[q].x, in[q].y);
+}
+
+int grid_for(ocn_ctx* ctx, size_t n, int threads = 256) {
+  size_t b = (n + threads - 1) / threads;
+  size_t cap = (size_t)ctx->sm_count * 16;
+  return (int)(b < cap ? (b ? b : 1) : cap);
+}
+
+#define OCN_DISPATCH_N(n, MACRO)                            \
+  switch (n) {                                              \
+    case 2: MACRO(2); break;                                \
+    case 4: MACRO(4); break;                                \
+    case 8: MACRO(8); break;                                \
+    case 16: MACRO(16); break;                              \
+    case 32: MACRO(32); break;                              \
+    case 64: MACRO(64); break;                              \
+    case 128: MACRO(128); break;                            \
+    case 256: MACRO(256); break;                            \
+    case 512: MACRO(512); break;                            \
+    case 1024: MACRO(1024); break;                          \
+    case 2048: MACRO(2048); break;                          \
+    case 4096: MACRO(4096); break;                          \
+    case 8192: MACRO(8192); break;                          \
+    case 16384: MACRO(16384); break;                        \
+    default: fail(OCN_ERR_CONFIG, "FFT size %d is not a supported power of two", n); \
+  }
+
+template <int N>
+void set_smem_attrs() {
+  static bool done = false;  // per process; attributes are per-function
+  if (done) return;
+  using L = Launch<N>;
+  if (L::SMEM_BYTES > 48 * 1024) {
+    OCN_CUDA(cudaFuncSetAttribute(k_rows<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)L::SMEM_BYTES));
+    OCN_CUDA(cudaFuncSetAttribute(k_rows<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)L::SMEM_BYTES));
+    OCN_CUDA(cudaFuncSetAttribute(k_cols<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)L::SMEM_BYTES));
+    OCN_CUDA(cudaFuncSetAttribute(k_cols<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)L::SMEM_BYTES));
+  }
+  done = true;
+}
+
+template <int N>
+void launch_rows(ocn_ctx* ctx, const RowArgs& a, bool plain) {
+  using L = Launch<N>;
+  set_smem_attrs<N>();
+  const int blocks = (a.items + L::PER_CTA - 1) / L::PER_CTA;
+  if (plain)
+    k_rows<N, true><<<blocks, L::THREADS, L::SMEM_BYTES, ctx->stream>>>(a);
+  else
+    k_rows<N, false><<<blocks, L::THREADS, L::SMEM_BYTES, ctx->stream>>>(a);
+  OCN_LAUNCHED(ctx);
+}
+
+template <int N>
+void launch_cols(ocn_ctx* ctx, const ColArgs& a, int G, bool complex_out) {
+  using L = Launch<N>;
+  set_smem_attrs<N>();
+  dim3 grid((N + L::PER_CTA - 1) / L::PER_CTA, G);
+  if (complex_out)
+    k_cols<N, true><<<grid, L::THREADS, L::SMEM_BYTES, ctx->stream>>>(a);
+  else
+    k_cols<N, false><<<grid, L::THREADS, L::SMEM_BYTES, ctx->stream>>>(a);
+  OCN_LAUNCHED(ctx);
+}
+
+void rows_dispatch(ocn_ctx* ctx, int n, const RowArgs& a, bool plain) {
+#define OCN_ROWS(NN) launch_rows<NN>(ctx, a, plain)
+  OCN_DISPATCH_N(n, OCN_ROWS)
+#undef OCN_ROWS
+}
+void cols_dispatch(ocn_ctx* ctx, int n, const ColArgs& a, int G, bool complex_out) {
+#define OCN_COLS(NN) launch_cols<NN>(ctx, a, G, complex_out)
+  OCN_DISPATCH_N(n, OCN_COLS)
+#undef OCN_COLS
+}
+
+template <int N>
+int tw_size_of() {
+  return fft::Plan<N>::tw_size();
+}
+
+// Inter-pass twiddle table for length n (layout of fft_core.cuh), fp64 -> fp32.
+std::vector<float2> make_twiddles(int n) {
+  std::vector<float2> out;
+  int E = n >= 32 ? 32 : n;
+  int logn = ilog2(n), loge = ilog2(E);
+  int P = loge ? 1 + (logn - loge + loge - 1) / loge : 1;
+  auto ipow = [](int b, int e) {
+    int r = 1;
+    while (e--) r *= b;
+    return r;
+  };
+  for (int p = 1; p < P; ++p) {
+    int R = p < P - 1 ? E : n / ipow(E, P - 1);
+    int NS = ipow(E, p);
+    for (int r = 0; r < R; ++r)
+      for (int b = 0; b < NS; ++b) {
+        // exp(+2 pi i b r / (NS R)) via an exact integer reduction of the angle
+        long long num = (long long)b * r % ((long long)NS * R);
+        double ang = 2.0 * kPi * (double)num / (double)((long long)NS * R);
+        out.push_back(make_float2((float)cos(ang), (float)sin(ang)));
+      }
+  }
+  if (out.empty()) out.push_back(make_float2(1.f, 0.f));
+  return out;
+}
+
+size_t group_for(int n, int total) {
+  const size_t budget = 48ull << 20;  // keep scratch L2-resident (126 MB L2)
+  size_t per = (size_t)n * n * sizeof(float2);
+  size_t g = budget / per;
+  if (g < 1) g = 1;
+  if (g > (size_t)total) g = total;
+  return g;
+}
+
+}  // namespace
+
+// Builds (or fetches) the transform list of one spectral step.
+static SpectralPlan* get_plan(ocn_cascades* cas, ocn_maps* maps, ocn_slices* slices) {
+  auto key = std::make_pair((const void*)maps, (const void*)slices);
+  auto it = cas->plans.find(key);
+  if (it != cas->plans.end()) return it->second.get();
+  auto plan = std::make_unique<SpectralPlan>();
+  plan->need_surface = maps != nullptr;
+  plan->need_velocity = slices != nullptr;
+  for (int c = 0; c < cas->count; ++c) {
+    plan->first.push_back((int)plan->host_desc.size());
+    if (maps) {
+      static const int pairs[4][2] = {{OCN_FIELD_H, OCN_FIELD_DX},
+                                      {OCN_FIELD_DZ, OCN_FIELD_DXDX},
+                                      {OCN_FIELD_DZDX, OCN_FIELD_DZDZ},
+                                      {OCN_FIELD_HX, OCN_FIELD_HZ}};
+      for (int p = 0; p < 4; ++p)
+        plan->host_desc.push_back({c, p, 0.f, 0.f, maps->field(c, pairs[p][0]),
+                                   maps->field(c, pairs[p][1])});
+    }
+    if (slices) {
+      int D = slices->cfg.count;
+      for (int d = 0; d < D; ++d)
+        plan->host_desc.push_back({c, kVelXZ, (float)slices->depths[d], 0.f,
+                                   slices->field(d, c, 0), slices->field(d, c, 2)});
+      for (int d0 = 0; d0 < D; d0 += 2) {
+        if (d0 + 1 < D)
+          plan->host_desc.push_back({c, kVelYPair, (float)slices->depths[d0],
+                                     (float)slices->depths[d0 + 1], slices->field(d0, c, 1),
+                                     slices->field(d0 + 1, c, 1)});
+        else
+          plan->host_desc.push_back({c, kVelYSingle, (float)slices->depths[d0], 0.f,
+                                     slices->field(d0, c, 1), nullptr});
+      }
+    }
+    plan->count.push_back((int)plan->host_desc.size() - plan->first.back());
+  }
+  plan->desc.alloc(plan->host_desc.size());
+  OCN_CUDA(cudaMemcpy(plan->desc.p, plan->host_desc.data(),
+                      plan->host_desc.size() * sizeof(XformDesc), cudaMemcpyHostToDevice));
+  SpectralPlan* raw = plan.get();
+  cas->plans[key] = std::move(plan);
+  return raw;
+}
+
+static void forget_plans(ocn_cascades* cas, const void* obj) {
+  for (auto it = cas->plans.begin(); it != cas->plans.end();) {
+    if (it->first.first == obj || it->first.second == obj)
+      it = cas->plans.erase(it);
+    else
+      ++it;
+  }
+}
+
+void spectral_step(ocn_cascades* cas, ocn_maps* maps, ocn_slices* slices, double t,
+                   double choppiness) {
+  ocn_ctx* ctx = cas->ctx;
+  DeviceScope ds(ctx);
+  SpectralPlan* plan = get_plan(cas, maps, slices);
+  const int n = cas->n;
+  const size_t nn = (size_t)n * n;
+  ProfWindow whole(ctx, OCN_PROF_SPECTRAL);
+  for (int c = 0; c < cas->count; ++c) {
+    const double dk = 2.0 * kPi / cas->lengths[c];
+    float4* spec = cas->spec.p + (size_t)c * nn;
+    {
+      ProfWindow pw(ctx, OCN_PROF_EVOLVE);
+      k_evolve<<<grid_for(ctx, nn), 256, 0, ctx->stream>>>(n, dk, cas->params.gravity, t,
+                                                          cas->h0.p + (size_t)c * nn, spec);
+      OCN_LAUNCHED(ctx);
+    }
+    const int first = plan->first[c], total = plan->count[c];
+    const int G = cas->group;
+    for (int g0 = 0; g0 < total; g0 += G) {
+      const int g = std::min(G, total - g0);
+      RowArgs ra{};
+      ra.items = n * g;
+      ra.G = g;
+      ra.desc = plan->desc.p + first + g0;
+      ra.spec = spec;
+      ra.dk = (float)dk;
+      ra.gravity = (float)cas->params.gravity;
+      ra.chop = (float)choppiness;
+      ra.scratch = cas->scratch.p;
+      ra.tw = cas->twiddle.p;
+      {
+        ProfWindow pw(ctx, OCN_PROF_ROWS);
+        rows_dispatch(ctx, n, ra, false);
+      }
+      ColArgs ca{};
+      ca.scratch = cas->scratch.p;
+      ca.desc = plan->desc.p + first + g0;
+      ca.tw = cas->twiddle.p;
+      {
+        ProfWindow pw(ctx, OCN_PROF_COLS);
+        cols_dispatch(ctx, n, ca, g, false);
+      }
+    }
+  }
+  if (maps) {
+    maps->time = t;
+    maps->choppiness = choppiness;
+  }
+  if (slices) slices->time = t;
+}
+
+// Plain packed transform(s) on device buffers: src [G][n][n] -> split or complex.
+static void plain_ifft(ocn_ctx* ctx, int n, int G, const float2* src, float2* scratch,
+                       const float2* tw, const XformDesc* d_desc, float2* out_c) {
+  RowArgs ra{};
+  ra.items = n * G;
+  ra.G = G;
+  ra.src = src;
+  ra.scratch = scratch;
+  ra.tw = tw;
+  rows_dispatch(ctx, n, ra, true);
+  ColArgs ca{};
+  ca.scratch = scratch;
+  ca.desc = d_desc;
+  ca.out_c = out_c;
+  ca.tw = tw;
+  cols_dispatch(ctx, n, ca, G, out_c != nullptr);
+}
+
+}  // namespace ocn
+
+using namespace ocn;
+
+// =========================================================================== C-ABI
+extern "C" {
+
+int ocn_abi_version(void) { return OCN_ABI_VERSION; }
+
+int ocn_ctx_create(int device, ocn_ctx** out) {
+  return api_call(nullptr, [&] {
+    OCN_REQUIRE(out, "ocn_ctx_create: out is NULL");
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0) {
+      cudaGetLastError();
+      fail(OCN_ERR_CUDA, "no CUDA device available (%s)", cudaGetErrorString(e));
+    }
+    OCN_REQUIRE(device >= 0 && device < ndev, "ocn_ctx_create: device %d out of range", device);
+    auto ctx = std::make_unique<ocn_ctx>();
+    ctx->device = device;
+    OCN_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    OCN_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+      fail(OCN_ERR_CUDA, "libocean_b200 is built for sm_100a; device %d is sm_%d%d", device,
+           prop.major, prop.minor);
+    ctx->sm_count = prop.multiProcessorCount;
+    OCN_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    *out = ctx.release();
+  });
+}
+
+int ocn_ctx_destroy(ocn_ctx* ctx) {
+  ocn::ctx_release(ctx);
+  return OCN_OK;
+}
+
+const char* ocn_last_error(const ocn_ctx* ctx) {
+  return ctx ? ctx->last_error.c_str() : ocn::global_error().c_str();
+}
+
+int ocn_ctx_synchronize(ocn_ctx* ctx) {
+  return api_call(ctx, [&] {
+    OCN_REQUIRE(ctx, "null context");
+    OCN_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int ocn_ctx_profile(ocn_ctx* ctx, int enable) {
+  if (!ctx) return OCN_ERR_ARG;
+  ctx->profiling = enable != 0;
+  return OCN_OK;
+}
+
+static void prof_resolve(ocn_ctx* ctx) {
+  OCN_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (auto& w : ctx->prof_pending) {
+    float ms = 0.f;
+    OCN_CUDA(cudaEventElapsedTime(&ms, w.start, w.stop));
+    ctx->prof_ms[w.cat] += ms;
+    ctx->prof_count[w.cat] += 1;
+    ctx->prof_pool.push_back(w.start);
+    ctx->prof_pool.push_back(w.stop);
+  }
+  ctx->prof_pending.clear();
+}
+
+int ocn_ctx_profile_read(ocn_ctx* ctx, int category, double* total_ms, uint64_t* count) {
+  return api_call(ctx, [&] {
+    OCN_REQUIRE(ctx && category >= 0 && category < OCN_PROF_COUNT, "bad profile category");
+    DeviceScope ds(ctx);
+    prof_resolve(ctx);
+    if (total_ms) *total_ms = ctx->prof_ms[category];
+    if (count) *count = ctx->prof_count[category];
+  });
+}
+
+int ocn_ctx_profile_reset(ocn_ctx* ctx) {
+  return api_call(ctx, [&] {
+    OCN_REQUIRE(ctx, "null context");
+    DeviceScope ds(ctx);
+    prof_resolve(ctx);
+    for (int k = 0; k < OCN_PROF_COUNT; ++k) ctx->prof_ms[k] = 0.0, ctx->prof_count[k] = 0;
+  });
+}
+
+void* ocn_ctx_stream(ocn_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+uint64_t ocn_ctx_kernel_launches(const ocn_ctx* ctx) {
+  return ctx ? ctx->launches.load(std::memory_order_relaxed) : 0;
+}
+
+// ---- spectrum scalars (host evaluation of the same __host__ __device__ code)
+int ocn_spectrum_validate(const ocn_spectrum_params* p) {
+  return api_call(nullptr, [&] {
+    OCN_REQUIRE(p, "null params");
+    if (!(p->wind_speed > 0.0)) fail(OCN_ERR_CONFIG, "wind_speed must be > 0");
+    if (!(p->fetch > 0.0)) fail(OCN_ERR_CONFIG, "fetch must be > 0");
+    if (p->swell < 0.0 || p->swell > 1.0) fail(OCN_ERR_CONFIG, "swell must be in [0, 1]");
+    if (p->direction_mix < 0.0 || p->direction_mix > 1.0)
+      fail(OCN_ERR_CONFIG, "direction_mix must be in [0, 1]");
+    if (!(p->gravity > 0.0)) fail(OCN_ERR_CONFIG, "gravity must be > 0");
+    if (p->has_peak_omega_override && !(p->peak_omega_override > 0.0))
+      fail(OCN_ERR_CONFIG, "peak_omega_override must be > 0");
+  });
+}
+double ocn_alpha(const ocn_spectrum_params* p) { return sm::alpha(*p); }
+double ocn_peak_omega(const ocn_spectrum_params* p) { return sm::peak_omega(*p); }
+double ocn_standard_peak_omega(const ocn_spectrum_params* p) { return sm::standard_peak_omega(*p); }
+double ocn_dispersion(double k, double g) { return sqrt(g * k); }
+int ocn_jonswap(double omega, const ocn_spectrum_params* p, double* out) {
+  return api_call(nullptr, [&] {
+    if (!sm::jonswap(omega, *p, out)) fail(OCN_ERR_DOMAIN, "jonswap: omega must be > 0");
+  });
+}
+double ocn_beta_s(double r) { return sm::beta_s(r); }
+double ocn_directional_kernel(double b, double t) { return sm::directional_kernel(b, t); }
+double ocn_donelan_banner(double w, double t, double wp) { return sm::donelan_banner(w, t, wp); }
+double ocn_swell_spread(double w, double t, double wp, double xi) {
+  return sm::swell_spread(w, t, wp, xi);
+}
+double ocn_q_dbxi_approx(double r) { return sm::q_dbxi_approx(r); }
+double ocn_q_dbxi_quadrature(double r, double xi, int panels) {
+  // composite Simpson over [-pi, pi] (spectra.cpp:84-98)
+  double beta = sm::beta_s(r);
+  double s = 16.0 * tanh(1.0 / r) * xi * xi;
+  auto f = [&](double th) {
+    double c = fabs(cos(0.5 * th));
+    double spread = (s == 0.0) ? 1.0 : (c == 0.0 ? 0.0 : pow(c, 2.0 * s));
+    return sm::directional_kernel(beta, th) * spread;
+  };
+  double h = 2.0 * kPi / panels;
+  double acc = f(-kPi) + f(kPi);
+  for (int i = 1; i < panels; ++i) acc += f(-kPi + h * i) * ((i & 1) ? 4.0 : 2.0);
+  return 1.0 / (acc * h / 3.0);
+}
+double ocn_directional(double w, double t, const ocn_spectrum_params* p) {
+  return sm::directional(w, t, *p);
+}
+double ocn_h0_variance(double kx, double kz, double k, double omega, double L,
+                       const ocn_spectrum_params* p) {
+  return sm::h0_variance(kx, kz, k, omega, L, *p);
+}
+double ocn_damping_factor(double speed, double d0, double d_max, double v_max) {
+  return sm::damping_factor(speed, d0, d_max, v_max);
+}
+double ocn_attenuation(double k, double y) { return sm::attenuation(k, y); }
+int ocn_log_distribution(double y, double y_min, double* out) {
+  return api_call(nullptr, [&] {
+    if (!(y_min < 0.0)) fail(OCN_ERR_DOMAIN, "log_distribution: y_min must be negative");
+    const double alpha = 0.0001;
+    double beta = -y_min / (2.0 * log(alpha * y_min * y_min + 1.0));
+    double v = beta * log(alpha * y * y + 1.0);
+    *out = y > 0.0 ? v : -v;
+  });
+}
+int ocn_exp_interp(double a, double fa, double b, double fb, double x, double* out) {
+  return api_call(nullptr, [&] {
+    if (a == b) fail(OCN_ERR_DOMAIN, "exp_interp: endpoints coincide");
+    bool degenerate = fabs(fa) < 1e-12 || fabs(fb) < 1e-12 || ((fa < 0.0) != (fb < 0.0));
+    if (degenerate) {
+      *out = fa + (fb - fa) * ((x - a) / (b - a));
+      return;
+    }
+    double beta = (log(fabs(fb)) - log(fabs(fa))) / (b - a);
+    *out = fa * exp(beta * (x - a));
+  });
+}
+int ocn_slice_depths(const ocn_slice_config* cfg, double* depths) {
+  return api_call(nullptr, [&] {
+    OCN_REQUIRE(cfg && depths, "null argument");
+    if (!(cfg->y_min < cfg->y_max)) fail(OCN_ERR_CONFIG, "slice interval requires y_min < y_max");
+    if (cfg->count < 2) fail(OCN_ERR_CONFIG, "at least two depth slices are required");
+    if (cfg->distribution == OCN_DEPTH_LOGARITHMIC && !(cfg->y_min < 0.0))
+      fail(OCN_ERR_CONFIG, "logarithmic distribution requires y_min < 0");
+    std::vector<double> d(cfg->count);
+    for (int i = 0; i < cfg->count; ++i) {
+      double pre = cfg->y_min + (cfg->y_max - cfg->y_min) * i / (cfg->count - 1);
+      if (cfg->distribution == OCN_DEPTH_LOGARITHMIC)
+        ocn_log_distribution(pre, cfg->y_min, &d[i]);
+      else
+        d[i] = pre;
+    }
+    std::sort(d.begin(), d.end());
+    std::memcpy(depths, d.data(), d.size() * sizeof(double));
+  });
+}
+
+// ---- cascades (K1)
+int ocn_cascades_create(ocn_ctx* ctx, int resolution, int count, const double* lengths,
+                        const double* band_min, const double* band_max,
+                        const uint32_t* cascade_index, const ocn_spectrum_params* params,
+                        ocn_cascades** out) {
+  return api_call(ctx, [&] {
+    OCN_REQUIRE(ctx && out && lengths && band_min && band_max && params, "null argument");
+    OCN_REQUIRE(count >= 1 && count <= kMaxCascades, "cascade count %d out of range", count);
+    if (!is_pow2(resolution) || resolution < 2)
+      fail(OCN_ERR_CONFIG, "grid resolution must be a power of two >= 2");
+    if (resolution > 16384) fail(OCN_ERR_CONFIG, "grid resolution above 16384 is not supported");
+    for (int c = 0; c < count; ++c) {
+      if (!(lengths[c] > 0.0)) fail(OCN_ERR_CONFIG, "cascade length must be > 0");
+      if (!(band_min[c] >= 0.0) || !(band_max[c] > band_min[c]))
+        fail(OCN_ERR_CONFIG, "cascade band must satisfy 0 <= band_min < band_max");
+    }
+    int st = ocn_spectrum_validate(params);
+    if (st) fail(st, "%s", global_error().c_str());
+    DeviceScope ds(ctx);
+    auto cas = std::make_unique<ocn_cascades>();
+    cas->ctx = ctx;
+    cas->n = resolution;
+    cas->count = count;
+    cas->lengths.assign(lengths, lengths + count);
+    cas->band_min.assign(band_min, band_min + count);
+    cas->band_max.assign(band_max, band_max + count);
+    for (int c = 0; c < count; ++c)
+      cas->cascade_index.push_back(cascade_index ? cascade_index[c] : (uint32_t)c);
+    cas->params = *params;
+    const size_t nn = (size_t)resolution * resolution;
+    cas->h0_f64.alloc(nn * count);
+    cas->h0.alloc(nn * count);
+    cas->in_band.alloc(nn * count);
+    cas->spec.alloc(nn * count);
+    InitArgs a{};
+    a.n = resolution;
+    a.count = count;
+    for (int c = 0; c < count; ++c) {
+      a.dk[c] = 2.0 * kPi / lengths[c];
+      a.length[c] = lengths[c];
+      a.band_min[c] = band_min[c];
+      a.band_max[c] = band_max[c];
+      a.cindex[c] = cas->cascade_index[c];
+    }
+    a.p = *params;
+    a.h0_f64 = cas->h0_f64.p;
+    a.h0 = cas->h0.p;
+    a.in_band = cas->in_band.p;
+    k_spectrum_init<<<grid_for(ctx, nn * count), 256, 0, ctx->stream>>>(a);
+    OCN_LAUNCHED(ctx);
+    std::vector<float2> tw = make_twiddles(resolution);
+    cas->twiddle.alloc(tw.size());
+    OCN_CUDA(cudaMemcpyAsync(cas->twiddle.p, tw.data(), tw.size() * sizeof(float2),
+                             cudaMemcpyHostToDevice, ctx->stream));
+    cas->group = (int)group_for(resolution, 1 << 30);
+    cas->scratch.alloc((size_t)cas->group * nn);
+    OCN_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx_retain(ctx);
+    *out = cas.release();
+  });
+}
+
+int ocn_cascades_destroy(ocn_cascades* c) {
+  cascades_release(c);
+  return OCN_OK;
+}
+
+int ocn_cascades_info(const ocn_cascades* c, int* resolution, int* count) {
+  if (!c) return OCN_ERR_ARG;
+  if (resolution) *resolution = c->n;
+  if (count) *count = c->count;
+  return OCN_OK;
+}
+
+int ocn_cascades_download(ocn_cascades* c, int grid, double* h0, double* h0cn, uint8_t* in_band,
+                          double* waves) {
+  return api_call(c ? c->ctx : nullptr, [&] {
+    OCN_REQUIRE(c && grid >= 0 && grid < c->count, "bad cascade handle / index");
+    ocn_ctx* ctx = c->ctx;
+    DeviceScope ds(ctx);
+    const size_t nn = (size_t)c->n * c->n;
+    const double2* src = c->h0_f64.p + (size_t)grid * nn;
+    if (h0)
+      OCN_CUDA(cudaMemcpyAsync(h0, src, nn * sizeof(double2), cudaMemcpyDeviceToHost, ctx->stream));
+    if (in_band)
+      OCN_CUDA(cudaMemcpyAsync(in_band, c->in_band.p + (size_t)grid * nn, nn,
+                               cudaMemcpyDeviceToHost, ctx->stream));
+    if (h0cn || waves) {
+      DevBuf<double2> d_cn(h0cn ? nn : 0);
+      DevBuf<double4> d_w(waves ? nn : 0);
+      k_grid_extras<<<grid_for(ctx, nn), 256, 0, ctx->stream>>>(
+          c->n, 2.0 * kPi / c->lengths[grid], c->params.gravity, src, d_cn.p, d_w.p);
+      OCN_LAUNCHED(ctx);
+      if (h0cn)
+        OCN_CUDA(cudaMemcpyAsync(h0cn, d_cn.p, nn * sizeof(double2), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+      if (waves)
+        OCN_CUDA(cudaMemcpyAsync(waves, d_w.p, nn * sizeof(double4), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+      OCN_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+    OCN_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+// ---- maps
+int ocn_maps_create(ocn_cascades* c, ocn_maps** out) {
+  return api_call(c ? c->ctx : nullptr, [&] {
+    OCN_REQUIRE(c && out, "null argument");
+    DeviceScope ds(c->ctx);
+    auto m = std::make_unique<ocn_maps>();
+    m->cas = c;
+    const size_t nn = (size_t)c->n * c->n;
+    m->fields.alloc(nn * 8 * c->count);
+    OCN_CUDA(cudaMemsetAsync(m->fields.p, 0, m->fields.bytes(), c->ctx->stream));
+    ++c->refs;
+    *out = m.release();
+  });
+}
+
+int ocn_maps_destroy(ocn_maps* m) {
+  if (!m) return OCN_OK;
+  ocn_cascades* c = m->cas;
+  {
+    DeviceScope ds(c->ctx);
+    cudaStreamSynchronize(c->ctx->stream);
+    forget_plans(c, m);
+    delete m;
+  }
+  cascades_release(c);
+  return OCN_OK;
+}
+
+int ocn_surface_generate(ocn_maps* m, double t, double choppiness) {
+  return api_call(m ? m->cas->ctx : nullptr, [&] {
+    OCN_REQUIRE(m, "null maps");
+    spectral_step(m->cas, m, nullptr, t, choppiness);
+  });
+}
+
+int ocn_maps_time(const ocn_maps* m, double* t) {
+  if (!m || !t) return OCN_ERR_ARG;
+  *t = m->time;
+  return OCN_OK;
+}
+
+int ocn_maps_download(ocn_maps* m, int cascade, int field, double* out) {
+  return api_call(m ? m->cas->ctx : nullptr, [&] {
+    OCN_REQUIRE(m && out && cascade >= 0 && cascade < m->cas->count && field >= 0 && field < 8,
+                "bad maps download arguments");
+    ocn_ctx* ctx = m->cas->ctx;
+    DeviceScope ds(ctx);
+    const size_t nn = (size_t)m->cas->n * m->cas->n;
+    DevBuf<double> tmp(nn);
+    k_f32_to_f64<<<grid_for(ctx, nn), 256, 0, ctx->stream>>>(nn, m->field(cascade, field), tmp.p);
+    OCN_LAUNCHED(ctx);
+    OCN_CUDA(cudaMemcpyAsync(out, tmp.p, nn * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    OCN_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int ocn_maps_download_f32(ocn_maps* m, int cascade, int field, float* out) {
+  return api_call(m ? m->cas->ctx : nullptr, [&] {
+    OCN_REQUIRE(m && out && cascade >= 0 && cascade < m->cas->count && field >= 0 && field < 8,
+                "bad maps download arguments");
+    ocn_ctx* ctx = m->cas->ctx;
+    DeviceScope ds(ctx);
+    const size_t nn = (size_t)m->cas->n * m->cas->n;
+    OCN_CUDA(cudaMemcpyAsync(out, m->field(cascade, field), nn * sizeof(float),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+    OCN_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int ocn_maps_device_field(ocn_maps* m, int cascade, int field, const float** dev_out) {
+  if (!m || !dev_out || cascade < 0 || cascade >= m->cas->count || field < 0 || field >= 8)
+    return OCN_ERR_ARG;
+  *dev_out = m->field(cascade, field);
+  return OCN_OK;
+}
+
+// ---- slices
+int ocn_slices_create(ocn_cascades* c, const ocn_slice_config* cfg, ocn_slices** out) {
+  return api_call(c ? c->ctx : nullptr, [&] {
+    OCN_REQUIRE(c && cfg && out, "null argument");
+    std::vector<double> d(cfg->count > 0 ? cfg->count : 1);
+    int st = ocn_slice_depths(cfg, d.data());
+    if (st) fail(st, "%s", global_error().c_str());
+    DeviceScope ds(c->ctx);
+    auto s = std::make_unique<ocn_slices>();
+    s->cas = c;
+    s->cfg = *cfg;
+    s->depths = d;
+    s->d_depths.alloc(d.size());
+    OCN_CUDA(cudaMemcpy(s->d_depths.p, d.data(), d.size() * sizeof(double), cudaMemcpyHostToDevice));
+    const size_t nn = (size_t)c->n * c->n;
+    s->fields.alloc(nn * 3 * c->count * cfg->count);
+    OCN_CUDA(cudaMemsetAsync(s->fields.p, 0, s->fields.bytes(), c->ctx->stream));
+    ++c->refs;
+    *out = s.release();
+  });
+}
+
+int ocn_slices_destroy(ocn_slices* s) {
+  if (!s) return OCN_OK;
+  ocn_cascades* c = s->cas;
+  {
+    DeviceScope ds(c->ctx);
+    cudaStreamSynchronize(c->ctx->stream);
+    forget_plans(c, s);
+    delete s;
+  }
+  cascades_release(c);
+  return OCN_OK;
+}
+
+int ocn_velocity_build(ocn_slices* s, double t) {
+  return api_call(s ? s->cas->ctx : nullptr, [&] {
+    OCN_REQUIRE(s, "null slices");
+    spectral_step(s->cas, nullptr, s, t, 1.0);
+  });
+}
+
+int ocn_slices_depths(const ocn_slices* s, int* count, double* depths) {
+  if (!s) return OCN_ERR_ARG;
+  if (count) *count = s->cfg.count;
+  if (depths) std::memcpy(depths, s->depths.data(), s->depths.size() * sizeof(double));
+  return OCN_OK;
+}
+
+int ocn_slices_download(ocn_slices* s, int depth, int cascade, int comp, double* out) {
+  return api_call(s ? s->cas->ctx : nullptr, [&] {
+    OCN_REQUIRE(s && out && depth >= 0 && depth < s->cfg.count && cascade >= 0 &&
+                    cascade < s->cas->count && comp >= 0 && comp < 3,
+                "bad slices download arguments");
+    ocn_ctx* ctx = s->cas->ctx;
+    DeviceScope ds(ctx);
+    const size_t nn = (size_t)s->cas->n * s->cas->n;
+    DevBuf<double> tmp(nn);
+    k_f32_to_f64<<<grid_for(ctx, nn), 256, 0, ctx->stream>>>(nn, s->field(depth, cascade, comp),
+                                                            tmp.p);
+    OCN_LAUNCHED(ctx);
+    OCN_CUDA(cudaMemcpyAsync(out, tmp.p, nn * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    OCN_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int ocn_spectral_step(ocn_maps* m, ocn_slices* s, double t, double choppiness) {
+  ocn_cascades* cas = m ? m->cas : (s ? s->cas : nullptr);
+  return api_call(cas ? cas->ctx : nullptr, [&] {
+    OCN_REQUIRE(cas, "ocn_spectral_step: maps and slices are both NULL");
+    OCN_REQUIRE(!m || !s || m->cas == s->cas, "maps and slices belong to different cascades");
+    spectral_step(cas, m, s, t, choppiness);
+  });
+}
+
+// ---- standalone FFT (fp64 host buffers in and out)
+static void host_ifft(ocn_ctx* ctx, int n, const double* x, const double* y, double* re,
+                      double* im, double* complex_out) {
+  if (n < 2 || !is_pow2(n))
+    fail(OCN_ERR_CONFIG, "FFT field size must be a power of two >= 2, got %d", n);
+  if (n > 16384) fail(OCN_ERR_CONFIG, "FFT size %d above 16384 is not supported", n);
+  DeviceScope ds(ctx);
+  const size_t nn = (size_t)n * n;
+  DevBuf<double2> dx(nn), dy(y ? nn : 0);
+  DevBuf<float2> packed(nn), scratch(nn), outc(complex_out ? nn : 0);
+  DevBuf<float> dre(complex_out ? 0 : nn), dim(complex_out ? 0 : nn);
+  OCN_CUDA(cudaMemcpyAsync(dx.p, x, nn * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
+  if (y)
+    OCN_CUDA(cudaMemcpyAsync(dy.p, y, nn * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
+  k_pack_pair<<<grid_for(ctx, nn), 256, 0, ctx->stream>>>(nn, dx.p, dy.p, packed.p);
+  OCN_LAUNCHED(ctx);
+  std::vector<float2> tw = make_twiddles(n);
+  DevBuf<float2> dtw(tw.size());
+  OCN_CUDA(cudaMemcpyAsync(dtw.p, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice,
+                           ctx->stream));
+  XformDesc hd{0, 0, 0.f, 0.f, dre.p, dim.p};
+  DevBuf<XformDesc> dd(1);
+  OCN_CUDA(cudaMemcpyAsync(dd.p, &hd, sizeof(hd), cudaMemcpyHostToDevice, ctx->stream));
+  plain_ifft(ctx, n, 1, packed.p, scratch.p, dtw.p, dd.p, complex_out ? outc.p : nullptr);
+  if (complex_out) {
+    DevBuf<double2> o64(nn);
+    k_c32_to_c64<<<grid_for(ctx, nn), 256, 0, ctx->stream>>>(nn, outc.p, o64.p);
+    OCN_LAUNCHED(ctx);
+    OCN_CUDA(cudaMemcpyAsync(complex_out, o64.p, nn * sizeof(double2), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    OCN_CUDA(cudaStreamSynchronize(ctx->stream));
+  } else {
+    DevBuf<double> o64(nn);
+    if (re) {
+      k_f32_to_f64<<<grid_for(ctx, nn), 256, 0, ctx->stream>>>(nn, dre.p, o64.p);
+      OCN_LAUNCHED(ctx);
+      OCN_CUDA(cudaMemcpyAsync(re, o64.p, nn * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+      OCN_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+    if (im) {
+      k_f32_to_f64<<<grid_for(ctx, nn), 256, 0, ctx->stream>>>(nn, dim.p, o64.p);
+      OCN_LAUNCHED(ctx);
+      OCN_CUDA(cudaMemcpyAsync(im, o64.p, nn * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+      OCN_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+  }
+  OCN_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+int ocn_ifft2_centered(ocn_ctx* ctx, int n, const double* in, double* out) {
+  return api_call(ctx, [&] {
+    OCN_REQUIRE(ctx && in && out, "null argument");
+    host_ifft(ctx, n, in, nullptr, nullptr, nullptr, out);
+  });
+}
+
+int ocn_ifft2_pair(ocn_ctx* ctx, int n, const double* x, const double* y, double* re, double* im) {
+  return api_call(ctx, [&] {
+    OCN_REQUIRE(ctx && x && y, "null argument");
+    host_ifft(ctx, n, x, y, re, im, nullptr);
+  });
+}
+
+}  // extern "C"
