@@ -1,0 +1,445 @@
+#!/usr/bin/env python
+"""bench.py — per-frame Arc Blanc hot path on B200 (BASELINE.json metric).
+
+Workload (one "step" = one frame): the 4-cascade 1024^2
+spectrum (U=20, F=1e5, theta0=0.4, xi=0.5, delta=0.5, standard peak, seed 42;
+lengths 1024/256/16/4 m) evolved to t, its 8 surface maps + 32 logarithmic
+velocity-at-depth slices (208 packed 1024^2 inverse FFTs), fluid-to-solid
+forces on the 100,352-triangle UV-ellipsoid hull (height_at + velocity_at
+samplers, deterministic reductions, waterline), the waterline mask and one
+2048^2 Cords-Staadt FDM step. Metric: ocean grid points / s (= 4 * 1024^2 per
+frame / frame time) and ms / frame.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+N > 1 (torchrun, one rank per GPU): independent replicas of the frame on every
+GPU (configs 2/3 do not shard), weak scaling, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+N_GRID = 1024
+LENGTHS = [1024.0, 256.0, 16.0, 4.0]
+CUTOFFS = [12 * math.pi / 256, 12 * math.pi / 16, 12 * math.pi / 4]
+DEPTHS = 32
+DT = 1.0 / 60.0
+FDM_N, FDM_MARGIN, BODY_SIZE = 2048, 16, 40.0
+WIND = (5.0, 0.0, 2.0)
+YAW = 0.3
+POINTS_PER_FRAME = len(LENGTHS) * N_GRID * N_GRID
+# compulsory bytes of the spectral pipeline per frame: fp32-complex
+# h0 read once (8 B / cascade-point) + every output field written once in fp32
+SPECTRAL_FIELDS = 8 + 3 * DEPTHS
+SPECTRAL_BYTES = POINTS_PER_FRAME * (8 + 4 * SPECTRAL_FIELDS)
+WORKLOAD = ("config3: 4 cascades x 1024^2 (8 surface maps + 32 velocity slices, 208 packed "
+            "2D iFFTs) + 100,352-tri hull forces + waterline mask + 2048^2 FDM step")
+
+
+def _params():
+    from paper_2503_03326_b200._types import SpectrumParams
+    p = SpectrumParams.make(wind_speed=20.0, fetch=1e5, wind_direction=0.4, swell=0.5,
+                            direction_mix=0.5, rng_seed=42)
+    p.has_peak_omega_override = 1
+    p.peak_omega_override = p.standard_peak_omega()
+    return p
+
+
+def _pose(centroid):
+    from paper_2503_03326_b200._types import Pose
+    return Pose.make(position=(3.0, 0.5, 7.0), orientation=(math.cos(YAW / 2), 0.0, math.sin(YAW / 2), 0.0),
+                     linear_velocity=(1.0, 0.0, 4.0), angular_velocity=(0.01, 0.05, 0.02),
+                     com_body=centroid)
+
+
+# ----------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------- our arm
+class Frame:
+    """One frame of the hot path through the C-ABI (device-resident state)."""
+
+    def __init__(self, device: int):
+        from paper_2503_03326_b200 import ocean as oc
+        from paper_2503_03326_b200._types import FdmConfig, MaskFrame, MaskParams, SliceConfig
+        from paper_2503_03326_b200.meshgen import uv_ellipsoid
+        self.oc = oc
+        self.L = oc.lib()
+        self.ctx = oc.Context(device)
+        self.cs = oc.CascadeSet(oc.CascadeConfig(N_GRID, LENGTHS, CUTOFFS), _params(), ctx=self.ctx)
+        self.maps = oc.SurfaceMaps(self.cs)
+        self.slices = oc.VelocitySlices(self.cs, SliceConfig.make(count=DEPTHS))
+        v, t = uv_ellipsoid()
+        self.mesh = oc.TriMesh(v, t, ctx=self.ctx)
+        self.pose = _pose(self.mesh.centroid)
+        self.fluid, self._keep = oc._fluid_struct(oc.FluidQuery(maps=self.maps, slices=self.slices,
+                                                                wind=WIND), oc.DragCoefficients())
+        self.zone = oc.FdmZone(FdmConfig.make(grid_size=FDM_N, margin=FDM_MARGIN), BODY_SIZE,
+                               (self.pose.position[0], self.pose.position[2]), DT, ctx=self.ctx)
+        ext = self.mesh.bbox_max - self.mesh.bbox_min
+        self.frame = MaskFrame.make(center_x=0.0, half_beam=ext[0], z_min=self.mesh.bbox_min[2],
+                                    z_max=self.mesh.bbox_max[2], mesh_height=self.mesh.height())
+        self.mparams = MaskParams.make()
+        self.speed = float(np.linalg.norm(list(self.pose.linear_velocity)))
+        self.t = 0.0
+        from paper_2503_03326_b200._types import HydroReport
+        self.report = HydroReport()
+
+    def step(self, read_report: bool = False):
+        """sim.cpp:59-109 minus the rigid integrator: spectral step, forces,
+        stability, mask from the device waterline, FDM step (all async)."""
+        L, oc = self.L, self.oc
+        self.t += DT
+        oc.check(L.ocn_spectral_step(self.maps.h, self.slices.h, self.t, 1.0), self.ctx.h, "spectral")
+        oc.check(L.ocn_hydro_aggregate(self.mesh.h, C.byref(self.pose), C.byref(self.fluid), None,
+                                       None), self.ctx.h, "aggregate")
+        oc.check(L.ocn_zone_update_stability(self.zone.h, self.speed, DT), self.ctx.h, "stability")
+        px, pz = self.pose.position[0], self.pose.position[2]
+        oc.check(L.ocn_zone_mask_from_hydro(self.zone.h, self.mesh.h, YAW, px, pz, self.speed,
+                                            C.byref(self.frame), C.byref(self.mparams)), self.ctx.h,
+                 "mask")
+        # the body advances with its velocity (the rigid integrator is out of scope)
+        for k in range(3):
+            self.pose.position[k] += self.pose.linear_velocity[k] * DT
+        oc.check(L.ocn_zone_step(self.zone.h, DT, self.pose.position[0], self.pose.position[2]),
+                 self.ctx.h, "fdm")
+        if read_report:
+            oc.check(L.ocn_hydro_report_get(self.mesh.h, C.byref(self.report)), self.ctx.h, "report")
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws <= 1:
+        return None, 0, 1, 0
+    import torch
+    import torch.distributed as dist
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl")
+    return dist, dist.get_rank(), ws, local
+
+
+def _max_over_ranks(dist, x: float) -> float:
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def _traffic():
+    """dram bytes per frame of the spectral pipeline from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "roofline_traffic.json")) as f:
+            return json.load(f).get("spectral_dram_bytes_per_frame")
+    except Exception:
+        return None
+
+
+def run_ours(args):
+    dist, rank, world, local = _dist()
+    fr = Frame(local)
+    L, ctx = fr.L, fr.ctx
+    for _ in range(max(args.warmup, 3)):
+        fr.step()
+    ctx.synchronize()
+    # ---- timed region: device time with CUDA events on the library stream
+    import torch
+    stream = torch.cuda.ExternalStream(ctx.stream, device=f"cuda:{local}")
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    launches0 = ctx.kernel_launches()
+    with ClockSampler(local) as clk:
+        _barrier(dist)
+        ctx.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            fr.step()
+        ev1.record(stream)
+        ctx.synchronize()
+        _barrier(dist)
+        ms_total = ev0.elapsed_time(ev1)
+        launches = ctx.kernel_launches() - launches0
+        # ---- roofline pass: same K frames with per-stage CUDA-event windows
+        L.ocn_ctx_profile(ctx.h, 1)
+        L.ocn_ctx_profile_reset(ctx.h)
+        for _ in range(args.steps):
+            fr.step()
+        ctx.synchronize()
+        stages = {}
+        for name, cat in [("evolve", 0), ("fft_rows", 1), ("fft_cols", 2), ("hydro", 3), ("mask", 4),
+                          ("fdm", 5), ("spectral", 6)]:
+            ms, cnt = C.c_double(), C.c_uint64()
+            L.ocn_ctx_profile_read(ctx.h, cat, C.byref(ms), C.byref(cnt))
+            stages[name] = ms.value / args.steps
+        L.ocn_ctx_profile(ctx.h, 0)
+        # ---- e2e: through the C-ABI with host inputs (t, pose) and the host
+        # read of each frame's hydro report (forces / torque), wall clock
+        _barrier(dist)
+        ctx.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            fr.step(read_report=True)
+        ctx.synchronize()
+        e2e_s = time.perf_counter() - t0
+    ms_frame = _max_over_ranks(dist, ms_total / args.steps)
+    e2e_frame = _max_over_ranks(dist, e2e_s / args.steps)
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    value = world * POINTS_PER_FRAME / (ms_frame / 1e3)
+    peak, peak_kind = _peaks()
+    spec_ms = stages["spectral"]
+    achieved = SPECTRAL_BYTES / (spec_ms / 1e3) / 1e9
+    h2d = C.sizeof(fr.pose) + 8
+    d2h = C.sizeof(fr.report)
+    line = {
+        "metric": "ocean grid points/sec (spectrum+iFFT+forces) at 1024^2 x 4 cascades",
+        "value": value,
+        "unit": "grid-points/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": max(args.warmup, 3),
+        "ms_per_step": ms_frame,
+        "ms_per_frame": ms_frame,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32 (fields, FFT) / f64 (spectrum init, phases, samplers, forces)",
+        "data": "synthetic (SURVEY 8d config 3 spectrum, seed 42; UV-ellipsoid hull)",
+        "config": {"workload": WORKLOAD, "grid": N_GRID, "cascades": len(LENGTHS),
+                   "depth_slices": DEPTHS, "hull_triangles": int(fr.mesh.triangles.shape[0]),
+                   "fdm_grid": FDM_N, "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                   "l2": "per-frame working set 1.8 GB of outputs > 126 MB L2 (no explicit flush)"},
+        "stages_ms": stages,
+        "roofline": {"kernel": "spectral pipeline (k_evolve + k_rows + k_cols)", "bound": "hbm",
+                     "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": _traffic(),
+                     "algorithmic_bytes_per_frame": SPECTRAL_BYTES},
+        "e2e": {"value": world * POINTS_PER_FRAME / e2e_frame, "unit": "grid-points/s",
+                "ms_per_frame": e2e_frame * 1e3, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(frames=1, warmup=0)
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------- reference (CPU)
+def _ref_lib():
+    from oracle.oracle import REF_SO, build, ref_available
+    if not ref_available():
+        build(reference=True)
+    lib = C.CDLL(REF_SO)
+    return lib
+
+
+def cpu_baseline(frames: int = 1, warmup: int = 0, budget_s: float = 1e9):
+    """The reference's own CPU implementation (oracle/_ref: the unmodified
+    reference library compiled from its sources) on this host, all threads
+    (set_worker_count(nproc)); spectral stages stay single-threaded in the
+    reference (256-item chunks, parallel.cpp:29). Sample: full generate_maps
+    (4 x 1024^2), build_slices at 2 of the 32 depths (scaled x16: its cost is
+    linear in the depth count), full aggregate / compute_mask / FDM step."""
+    from paper_2503_03326_b200._types import FdmConfig, SliceConfig
+    from paper_2503_03326_b200.meshgen import uv_ellipsoid
+    from oracle.oracle import P
+    lib = _ref_lib()
+    ncpu = os.cpu_count() or 1
+    lib.ref_set_worker_count.argtypes = [C.c_int]
+    lib.ref_set_worker_count(ncpu)
+    v, t = uv_ellipsoid()
+    from oracle.oracle import Oracle
+    mesh = Oracle("port").mesh_build(v, t)
+    pose = _pose(mesh["centroid"])
+    p = _params()
+    sc = SliceConfig.make(count=DEPTHS)
+    fc = FdmConfig.make(grid_size=FDM_N, margin=FDM_MARGIN)
+    la = np.ascontiguousarray(LENGTHS)
+    cu = np.ascontiguousarray(CUTOFFS + [0.0])
+    wind = np.ascontiguousarray(WIND)
+    lib.ref_bench_create.restype = C.c_void_p
+    lib.ref_bench_create.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                     C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                     C.c_double, C.c_double, C.c_void_p, C.POINTER(C.c_int)]
+    lib.ref_bench_frame.argtypes = [C.c_void_p, C.c_double, C.c_int, C.c_void_p]
+    lib.ref_bench_destroy.argtypes = [C.c_void_p]
+    st = C.c_int()
+    vv = np.ascontiguousarray(v)
+    tt = np.ascontiguousarray(mesh["tris"])
+    t_init = time.perf_counter()
+    b = lib.ref_bench_create(N_GRID, len(LENGTHS), P(la), P(cu), C.byref(p), C.byref(sc), v.shape[0],
+                             P(vv), t.shape[0], tt.ctypes.data, C.byref(pose), C.byref(fc), BODY_SIZE,
+                             DT, P(wind), C.byref(st))
+    t_init = time.perf_counter() - t_init
+    if st.value != 0:
+        raise RuntimeError("reference bench setup failed")
+    sample_depths = 2
+    stage = np.zeros(5)
+    for _ in range(warmup):
+        lib.ref_bench_frame(b, DT, sample_depths, P(stage))
+    ests, done = [], 0
+    t_start = time.perf_counter()
+    for _ in range(frames):
+        lib.ref_bench_frame(b, DT, sample_depths, P(stage))
+        est = stage[0] + stage[1] * (DEPTHS / sample_depths) + stage[2] + stage[3] + stage[4]
+        ests.append((est, stage.copy()))
+        done += 1
+        if time.perf_counter() - t_start > budget_s:
+            break
+    lib.ref_bench_destroy(b)
+    est = float(np.mean([e for e, _ in ests]))
+    st_mean = np.mean([s for _, s in ests], axis=0)
+    return {
+        "value": POINTS_PER_FRAME / est,
+        "unit": "grid-points/s",
+        "ms_per_frame": est * 1e3,
+        "cores": ncpu,
+        "kind": "reference",
+        "frames": done,
+        "stage_s": {"generate_maps": st_mean[0], "build_slices_32_est": st_mean[1] * DEPTHS / sample_depths,
+                    "aggregate": st_mean[2], "stability_mask": st_mean[3], "fdm": st_mean[4],
+                    "cascade_init_once": t_init},
+        "sample": (f"{done} frame(s) of config 3 through the reference library (oracle/_ref, g++ -O2): "
+                   f"full generate_maps + aggregate + compute_mask + FdmZone::step, build_slices at "
+                   f"{sample_depths} of {DEPTHS} depths scaled x{DEPTHS // sample_depths}; "
+                   f"set_worker_count({ncpu})"),
+    }
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    budget = 150.0
+    cb = cpu_baseline(frames=args.steps, warmup=min(args.warmup, 1), budget_s=budget)
+    line = {
+        "impl": "reference",
+        "metric": "ocean grid points/sec (spectrum+iFFT+forces) at 1024^2 x 4 cascades",
+        "value": cb["value"],
+        "unit": "grid-points/s",
+        "n_gpus": world,
+        "steps": cb["frames"],
+        "steps_requested": args.steps,
+        "warmup": min(args.warmup, 1),
+        "ms_per_step": cb["ms_per_frame"],
+        "ms_per_frame": cb["ms_per_frame"],
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (SURVEY 8d config 3)",
+        "config": {"workload": WORKLOAD, "grid": N_GRID, "cascades": len(LENGTHS),
+                   "depth_slices": DEPTHS, "fdm_grid": FDM_N, "parallelism": "host CPU"},
+        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": cb["value"], "unit": "grid-points/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "stage_s": cb["stage_s"],
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()
