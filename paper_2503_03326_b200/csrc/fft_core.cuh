@@ -166,17 +166,31 @@ __device__ __forceinline__ int pad32(int i) { return i + (i >> 5); }
 // shared buffer (Plan<N>::SMEM float2). `tw` = the per-N twiddle table.
 // Every thread of the CTA must call this the same number of times (it
 // contains __syncthreads when P > 1).
-template <int N, class Load, class Store>
+//   WARP     : the T threads of a transform are inside one warp (T <= 32):
+//              exchanges synchronise with __syncwarp instead of __syncthreads
+//   LOAD_SM  : `load` reads `sm` itself (adds a sync before pass 0 overwrites it)
+//   STORE_SM : `store` writes `sm` itself (adds a sync before the last stores)
+template <bool WARP>
+__device__ __forceinline__ void fft_sync() {
+  if constexpr (WARP) __syncwarp();
+  else __syncthreads();
+}
+
+template <int N, bool WARP = false, bool LOAD_SM = false, bool STORE_SM = false, class Load,
+          class Store>
 __device__ __forceinline__ void cta_fft(int t, float2* sm, const float2* __restrict__ tw,
                                         Load&& load, Store&& store) {
   using PL = Plan<N>;
   constexpr int E = PL::E, T = PL::T, P = PL::P;
+  static_assert(!WARP || T <= 32, "warp-synchronous FFT needs T <= 32");
   float2 v[E];
   // ---- pass 0: radix E, Ns = 1, no twiddles
 #pragma unroll
   for (int r = 0; r < E; ++r) v[r] = load(t + r * T);
+  if constexpr (LOAD_SM) fft_sync<WARP>();
   dft_dif<E>(v);
   if constexpr (P == 1) {
+    if constexpr (STORE_SM && !LOAD_SM) fft_sync<WARP>();
     static_for<0, E>([&](auto ri) {
       constexpr int r = decltype(ri)::value;
       store(r, v[bitrev(r, PL::LOGE)]);
@@ -186,7 +200,7 @@ __device__ __forceinline__ void cta_fft(int t, float2* sm, const float2* __restr
       constexpr int r = decltype(ri)::value;
       sm[pad32(t * E + r)] = v[bitrev(r, PL::LOGE)];
     });
-    __syncthreads();
+    fft_sync<WARP>();
     static_for<1, P>([&](auto pi) {
       constexpr int p = decltype(pi)::value;
       constexpr int R = PL::radix(p);
@@ -210,6 +224,7 @@ __device__ __forceinline__ void cta_fft(int t, float2* sm, const float2* __restr
         dft_dif<R, q * R>(v);
       });
       if constexpr (p == P - 1) {
+        if constexpr (STORE_SM) fft_sync<WARP>();
         static_for<0, Q>([&](auto qi) {
           constexpr int q = decltype(qi)::value;
           const int b = t + q * T;
@@ -219,7 +234,7 @@ __device__ __forceinline__ void cta_fft(int t, float2* sm, const float2* __restr
           });
         });
       } else {
-        __syncthreads();
+        fft_sync<WARP>();
         static_for<0, Q>([&](auto qi) {
           constexpr int q = decltype(qi)::value;
           const int b = t + q * T;
@@ -229,7 +244,7 @@ __device__ __forceinline__ void cta_fft(int t, float2* sm, const float2* __restr
             sm[pad32(base + r * NS)] = v[q * R + bitrev(r, LOGR)];
           });
         });
-        __syncthreads();
+        fft_sync<WARP>();
       }
     });
   }

@@ -35,6 +35,15 @@ struct XformDesc {
 
 struct SpectralPlan {
   DevBuf<XformDesc> desc;
+  // CUDA graph of the whole step (everything but the time upload), captured on
+  // the second use of the plan; rebuilt when the choppiness changes.
+  cudaGraphExec_t exec = nullptr;
+  double graph_chop = 0.0;
+  uint64_t graph_kernels = 0;
+  int uses = 0;
+  ~SpectralPlan() {
+    if (exec) cudaGraphExecDestroy(exec);
+  }
   std::vector<XformDesc> host_desc;
   std::vector<int> first;  // per cascade: first transform index
   std::vector<int> count;  // per cascade: number of transforms
@@ -56,6 +65,7 @@ struct ocn_cascades {
   ocn::DevBuf<float2> twiddle;  // per-N inter-pass twiddles (fft_core.cuh)
   ocn::DevBuf<float4> spec;     // [C][N][N] evolved (h~, G) at the current frame
   ocn::DevBuf<float2> scratch;  // row-pass intermediates of one transform group
+  ocn::DevBuf<double> d_time;   // frame time read by k_evolve (set per frame)
   int group = 1;                // transforms per group
   std::map<std::pair<const void*, const void*>, std::unique_ptr<ocn::SpectralPlan>> plans;
 };

@@ -133,9 +133,12 @@ __global__ void k_grid_extras(int n, double dk, double g, const double2* h0, dou
 
 // ------------------------------------------------------------------ evolve
 // h~ and G (surface.cpp:49-50; velocity.cpp:16-20) at time t, one cascade.
-__global__ void __launch_bounds__(256) k_evolve(int n, double dk, double g, double t,
+__global__ void k_set_time(double* d_time, double t) { *d_time = t; }
+
+__global__ void __launch_bounds__(256) k_evolve(int n, double dk, double g, const double* d_time,
                                                 const float2* __restrict__ h0, float4* spec) {
   const int nn = n * n;
+  const double t = *d_time;
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nn; q += gridDim.x * blockDim.x) {
     const int i = q / n, j = q - i * n;
     const int ni = i == 0 ? 0 : n - i, nj = j == 0 ? 0 : n - j;
@@ -268,13 +271,203 @@ __global__ void __launch_bounds__(Launch<N>::THREADS) k_rows(const RowArgs a) {
   }
 }
 
-// ------------------------------------------------------------------ columns
 struct ColArgs {
   const float2* scratch;  // [G][N][N]
   const XformDesc* desc;  // split outputs per transform
   float2* out_c;          // complex mode: [G][N][N]
   const float2* tw;
 };
+
+// ------------------------------------------------------------------ rows (N <= 1024)
+// Warp-synchronous variant: one CTA per row handles every transform of the
+// group (warp w takes transform slots w, w + W, ...). The row's (h~, G) and
+// the per-mode kz, |k|, 1/|k|, omega are staged once in shared memory; the
+// per-transform multiplier is selected once per warp (no per-element switch),
+// coefficients are written to the warp's FFT buffer and transformed with
+// __syncwarp-only exchanges.
+template <int N>
+struct WarpLaunch {
+  using PL = fft::Plan<N>;
+  static_assert(PL::T <= 32, "warp kernels need T <= 32");
+  static constexpr int T = PL::T;
+  static constexpr int TPW = 32 / T;  // transforms per warp
+  static constexpr int STRIDE = Launch<N>::STRIDE;
+  static constexpr int COLS_WARPS = 8;
+  static constexpr int CC = COLS_WARPS * TPW;  // columns per column-CTA
+};
+
+__device__ __forceinline__ float atten_f(float k, float y) {
+  return y > 0.f ? 1.0f + k * y : __expf(k * y);
+}
+
+template <int N, bool PLAIN>
+__global__ void __launch_bounds__(256) k_rows_w(const RowArgs a) {
+  using W = WarpLaunch<N>;
+  constexpr int T = W::T, E = fft::Plan<N>::E;
+  extern __shared__ float4 smem4[];
+  // per mode of this row, shared by every transform of the group:
+  //   sa = (h~.re, h~.im, V0.re, V0.im),  V0 = G (-g / w) (kx + i kz)
+  //   sb = (W0.re, W0.im, |k|, 1/|k|),    W0 = G w
+  // so a velocity coefficient is V0 E(y) or W0 (-E(y1) + i E(y0)).
+  float4* sa = smem4;
+  float4* sb = smem4 + N;
+  float2* bufs = reinterpret_cast<float2*>(PLAIN ? smem4 : smem4 + 2 * N);
+  const int row = blockIdx.x;
+  const int warps = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sub = lane / T, t = lane - sub * T;
+  const float kx = a.dk * (float)(row - N / 2);
+  if constexpr (!PLAIN) {
+    const float4* srow = a.spec + (size_t)row * N;
+    const float g = a.gravity;
+    for (int j = threadIdx.x; j < N; j += blockDim.x) {
+      const float kz = a.dk * (float)(j - N / 2);
+      const float k2 = kx * kx + kz * kz;
+      const float k = sqrtf(k2);
+      const float inv = k2 > 0.f ? 1.0f / k : 0.f;
+      const float w = sqrtf(g * k);
+      const float4 s = __ldg(srow + j);  // (h~, G)
+      const float f = k2 > 0.f ? -g / w : 0.f;
+      const float v0r = f * (s.z * kx - s.w * kz), v0i = f * (s.z * kz + s.w * kx);
+      sa[j] = make_float4(s.x, s.y, v0r, v0i);
+      sb[j] = make_float4(s.z * w, s.w * w, k, inv);
+    }
+    __syncthreads();
+  }
+  const int slots = (a.G + W::TPW - 1) / W::TPW;
+  float2* buf = bufs + (size_t)(warp * W::TPW + sub) * W::STRIDE;
+  for (int slot = warp; slot < slots; slot += warps) {
+    const int gi = slot * W::TPW + sub;
+    const bool valid = gi < a.G;
+    // ---- coefficients X + iY of this transform at j = t + r T
+    if constexpr (PLAIN) {
+      const float2* in = a.src + ((size_t)(valid ? gi : 0) * N + row) * N;
+#pragma unroll 4
+      for (int r = 0; r < E; ++r) {
+        const int j = t + r * T;
+        buf[fft::pad32(j)] = valid ? __ldg(in + j) : make_float2(0.f, 0.f);
+      }
+    } else {
+      const XformDesc d = a.desc[valid ? gi : 0];
+      const float chop = a.chop;
+      if (d.kind == kVelXZ) {
+        const float y0 = d.y0 * 1.4426950408889634f;  // exp(k y) = exp2(k y log2 e)
+        const bool above = d.y0 > 0.f;
+#pragma unroll 4
+        for (int r = 0; r < E; ++r) {
+          const int j = t + r * T;
+          const float4 A = sa[j];
+          const float k = sb[j].z;
+          const float e = above ? 1.0f + k * d.y0 : exp2f(k * y0);
+          buf[fft::pad32(j)] = make_float2(A.z * e, A.w * e);
+        }
+      } else if (d.kind == kVelYPair || d.kind == kVelYSingle) {
+        const bool pair = d.kind == kVelYPair;
+        const float l0 = d.y0 * 1.4426950408889634f, l1 = d.y1 * 1.4426950408889634f;
+#pragma unroll 4
+        for (int r = 0; r < E; ++r) {
+          const int j = t + r * T;
+          const float4 B = sb[j];
+          const float e0 = d.y0 > 0.f ? 1.0f + B.z * d.y0 : exp2f(B.z * l0);
+          const float e1 = pair ? (d.y1 > 0.f ? 1.0f + B.z * d.y1 : exp2f(B.z * l1)) : 0.f;
+          // W0 (-e1 + i e0)
+          buf[fft::pad32(j)] = make_float2(-B.x * e1 - B.y * e0, B.x * e0 - B.y * e1);
+        }
+      } else {
+#pragma unroll 2
+        for (int r = 0; r < E; ++r) {
+          const int j = t + r * T;
+          const float4 A = sa[j];
+          const float inv = sb[j].w;
+          const float kz = a.dk * (float)(j - N / 2);
+          float mr, mi;
+          if (d.kind == kSurfHDx) {
+            mr = 1.0f - kx * inv * chop, mi = 0.f;
+          } else if (d.kind == kSurfDzDxDx) {
+            mr = 0.f, mi = chop * (kz + kx * kx) * inv;
+          } else if (d.kind == kSurfDzDxDzDz) {
+            const float f = chop * kz * inv;
+            mr = f * kx, mi = f * kz;
+          } else {
+            mr = -kz, mi = kx;
+          }
+          if (inv == 0.f) mr = mi = 0.f;  // k = 0 mode
+          buf[fft::pad32(j)] = make_float2(A.x * mr - A.y * mi, A.x * mi + A.y * mr);
+        }
+      }
+    }
+    __syncwarp();
+    float2* out = a.scratch + ((size_t)(valid ? gi : 0) * N + row) * N;
+    fft::cta_fft<N, true, true, false>(
+        t, buf, a.tw, [&](int n) { return buf[fft::pad32(n)]; },
+        [&](int k, float2 x) {
+          if (valid) out[k] = x;
+        });
+    __syncwarp();
+  }
+}
+
+// Column pass, warp per column: the tile [N][CC] is loaded with coalesced row
+// segments into per-column shared buffers, each warp transforms its columns,
+// the results go back through shared memory and leave as coalesced row
+// segments with the (-1)^(i+j) sign and the Re / Im split fused in.
+template <int N, bool COMPLEX_OUT>
+__global__ void __launch_bounds__(256) k_cols_w(const ColArgs a) {
+  using W = WarpLaunch<N>;
+  constexpr int T = W::T, CC = W::CC;
+  extern __shared__ float2 tile[];  // [CC][STRIDE]
+  const int col0 = blockIdx.x * CC;
+  const int xf = blockIdx.y;
+  const float2* in = a.scratch + (size_t)xf * N * N;
+  constexpr int NT = 32 * W::COLS_WARPS;
+  constexpr int ITER = N * CC / NT;
+  static_assert(ITER * NT == N * CC, "tile must split evenly");
+  {
+    float2 v[ITER];  // all loads in flight before the shared-memory stores
+#pragma unroll
+    for (int it = 0; it < ITER; ++it) {
+      const int idx = threadIdx.x + it * NT;
+      const int row = idx / CC, c = idx - row * CC;
+      v[it] = __ldg(in + (size_t)row * N + col0 + c);
+    }
+#pragma unroll
+    for (int it = 0; it < ITER; ++it) {
+      const int idx = threadIdx.x + it * NT;
+      const int row = idx / CC, c = idx - row * CC;
+      tile[c * W::STRIDE + fft::pad32(row)] = v[it];
+    }
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sub = lane / T, t = lane - sub * T;
+  const int c = warp * W::TPW + sub;
+  float2* buf = tile + c * W::STRIDE;
+  fft::cta_fft<N, true, true, true>(
+      t, buf, a.tw, [&](int n) { return buf[fft::pad32(n)]; },
+      [&](int k, float2 x) { buf[fft::pad32(k)] = x; });
+  __syncthreads();
+  if constexpr (COMPLEX_OUT) {
+    float2* out = a.out_c + (size_t)xf * N * N;
+    for (int idx = threadIdx.x; idx < N * CC; idx += blockDim.x) {
+      const int row = idx / CC, cc = idx - row * CC, col = col0 + cc;
+      const float2 x = tile[cc * W::STRIDE + fft::pad32(row)];
+      const float s = ((row + col) & 1) ? -1.f : 1.f;
+      out[(size_t)row * N + col] = make_float2(s * x.x, s * x.y);
+    }
+  } else {
+    const XformDesc d = a.desc[xf];
+#pragma unroll 8
+    for (int idx = threadIdx.x; idx < N * CC; idx += NT) {
+      const int row = idx / CC, cc = idx - row * CC, col = col0 + cc;
+      const float2 x = tile[cc * W::STRIDE + fft::pad32(row)];
+      const float s = ((row + col) & 1) ? -1.f : 1.f;  // fft.cpp:73-75
+      d.out_re[(size_t)row * N + col] = s * x.x;       // fft.cpp:93-99
+      if (d.out_im) d.out_im[(size_t)row * N + col] = s * x.y;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ columns
 
 template <int N, bool COMPLEX_OUT>
 __global__ void __launch_bounds__(Launch<N>::THREADS) k_cols(const ColArgs a) {
@@ -375,7 +568,33 @@ void set_smem_attrs() {
 }
 
 template <int N>
+constexpr bool use_warp_kernels() {
+  return N >= 128 && N <= 1024;
+}
+
+template <int N>
 void launch_rows(ocn_ctx* ctx, const RowArgs& a, bool plain) {
+  if constexpr (use_warp_kernels<N>()) {
+    using W = WarpLaunch<N>;
+    const int slots = (a.G + W::TPW - 1) / W::TPW;
+    const int warps = slots < 8 ? slots : 8;
+    const size_t smem = (plain ? 0 : 2 * N * sizeof(float4)) +
+                        (size_t)warps * W::TPW * W::STRIDE * sizeof(float2);
+    static bool attr = false;
+    if (!attr) {
+      const int cap = 2 * N * sizeof(float4) + 8 * W::TPW * W::STRIDE * sizeof(float2);
+      OCN_CUDA(cudaFuncSetAttribute(k_rows_w<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap));
+      OCN_CUDA(cudaFuncSetAttribute(k_rows_w<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap));
+      attr = true;
+    }
+    const int rows = a.items / a.G;
+    if (plain)
+      k_rows_w<N, true><<<rows, 32 * warps, smem, ctx->stream>>>(a);
+    else
+      k_rows_w<N, false><<<rows, 32 * warps, smem, ctx->stream>>>(a);
+    OCN_LAUNCHED(ctx);
+    return;
+  }
   using L = Launch<N>;
   set_smem_attrs<N>();
   const int blocks = (a.items + L::PER_CTA - 1) / L::PER_CTA;
@@ -386,8 +605,38 @@ void launch_rows(ocn_ctx* ctx, const RowArgs& a, bool plain) {
   OCN_LAUNCHED(ctx);
 }
 
+// The CTA-synchronous column kernel (direct coalesced global loads / stores,
+// no tile round trips) measured faster than the warp-per-column one at
+// N = 1024 on B200 (0.98 vs 1.17 ms / frame); OCN_COLS_WARP=1 selects the latter.
+static bool cols_generic() {
+  static const bool on = [] {
+    const char* e = getenv("OCN_COLS_WARP");
+    return !(e && *e && *e != '0');
+  }();
+  return on;
+}
+
 template <int N>
 void launch_cols(ocn_ctx* ctx, const ColArgs& a, int G, bool complex_out) {
+  if constexpr (use_warp_kernels<N>()) {
+   if (!cols_generic()) {
+    using W = WarpLaunch<N>;
+    const size_t smem = (size_t)W::CC * W::STRIDE * sizeof(float2);
+    static bool attr = false;
+    if (!attr) {
+      OCN_CUDA(cudaFuncSetAttribute(k_cols_w<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      OCN_CUDA(cudaFuncSetAttribute(k_cols_w<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = true;
+    }
+    dim3 grid(N / W::CC > 0 ? N / W::CC : 1, G);
+    if (complex_out)
+      k_cols_w<N, true><<<grid, 32 * W::COLS_WARPS, smem, ctx->stream>>>(a);
+    else
+      k_cols_w<N, false><<<grid, 32 * W::COLS_WARPS, smem, ctx->stream>>>(a);
+    OCN_LAUNCHED(ctx);
+    return;
+   }
+  }
   using L = Launch<N>;
   set_smem_attrs<N>();
   dim3 grid((N + L::PER_CTA - 1) / L::PER_CTA, G);
@@ -441,7 +690,7 @@ std::vector<float2> make_twiddles(int n) {
 }
 
 size_t group_for(int n, int total) {
-  const size_t budget = 48ull << 20;  // keep scratch L2-resident (126 MB L2)
+  const size_t budget = 64ull << 20;  // keep scratch L2-resident (126 MB L2)
   size_t per = (size_t)n * n * sizeof(float2);
   size_t g = budget / per;
   if (g < 1) g = 1;
@@ -504,11 +753,8 @@ static void forget_plans(ocn_cascades* cas, const void* obj) {
   }
 }
 
-void spectral_step(ocn_cascades* cas, ocn_maps* maps, ocn_slices* slices, double t,
-                   double choppiness) {
+static void enqueue_spectral(ocn_cascades* cas, SpectralPlan* plan, double choppiness) {
   ocn_ctx* ctx = cas->ctx;
-  DeviceScope ds(ctx);
-  SpectralPlan* plan = get_plan(cas, maps, slices);
   const int n = cas->n;
   const size_t nn = (size_t)n * n;
   ProfWindow whole(ctx, OCN_PROF_SPECTRAL);
@@ -517,7 +763,7 @@ void spectral_step(ocn_cascades* cas, ocn_maps* maps, ocn_slices* slices, double
     float4* spec = cas->spec.p + (size_t)c * nn;
     {
       ProfWindow pw(ctx, OCN_PROF_EVOLVE);
-      k_evolve<<<grid_for(ctx, nn), 256, 0, ctx->stream>>>(n, dk, cas->params.gravity, t,
+      k_evolve<<<grid_for(ctx, nn), 256, 0, ctx->stream>>>(n, dk, cas->params.gravity, cas->d_time.p,
                                                           cas->h0.p + (size_t)c * nn, spec);
       OCN_LAUNCHED(ctx);
     }
@@ -549,6 +795,50 @@ void spectral_step(ocn_cascades* cas, ocn_maps* maps, ocn_slices* slices, double
       }
     }
   }
+}
+
+static bool graphs_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("OCN_NO_GRAPH");
+    return !(e && *e && *e != '0');
+  }();
+  return on;
+}
+
+void spectral_step(ocn_cascades* cas, ocn_maps* maps, ocn_slices* slices, double t,
+                   double choppiness) {
+  ocn_ctx* ctx = cas->ctx;
+  DeviceScope ds(ctx);
+  SpectralPlan* plan = get_plan(cas, maps, slices);
+  k_set_time<<<1, 1, 0, ctx->stream>>>(cas->d_time.p, t);
+  OCN_LAUNCHED(ctx);
+  const bool use_graph = graphs_enabled() && !ctx->profiling && plan->uses > 0;
+  if (use_graph && (!plan->exec || plan->graph_chop != choppiness)) {
+    if (plan->exec) cudaGraphExecDestroy(plan->exec), plan->exec = nullptr;
+    const uint64_t before = ctx->launches.load();
+    cudaGraph_t graph;
+    OCN_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeRelaxed));
+    try {
+      enqueue_spectral(cas, plan, choppiness);
+    } catch (...) {
+      cudaStreamEndCapture(ctx->stream, &graph);
+      throw;
+    }
+    OCN_CUDA(cudaStreamEndCapture(ctx->stream, &graph));
+    cudaError_t e = cudaGraphInstantiate(&plan->exec, graph, 0);
+    cudaGraphDestroy(graph);
+    OCN_CUDA(e);
+    plan->graph_kernels = ctx->launches.load() - before;
+    ctx->launches.fetch_sub(plan->graph_kernels);  // captured, not executed
+    plan->graph_chop = choppiness;
+  }
+  if (use_graph) {
+    OCN_CUDA(cudaGraphLaunch(plan->exec, ctx->stream));
+    ctx->launches.fetch_add(plan->graph_kernels);
+  } else {
+    enqueue_spectral(cas, plan, choppiness);
+  }
+  ++plan->uses;
   if (maps) {
     maps->time = t;
     maps->choppiness = choppiness;
@@ -818,6 +1108,7 @@ int ocn_cascades_create(ocn_ctx* ctx, int resolution, int count, const double* l
     OCN_CUDA(cudaMemcpyAsync(cas->twiddle.p, tw.data(), tw.size() * sizeof(float2),
                              cudaMemcpyHostToDevice, ctx->stream));
     cas->group = (int)group_for(resolution, 1 << 30);
+    cas->d_time.alloc(1);
     cas->scratch.alloc((size_t)cas->group * nn);
     OCN_CUDA(cudaStreamSynchronize(ctx->stream));
     ctx_retain(ctx);
