@@ -102,10 +102,24 @@ __device__ __forceinline__ void derotate(const MaskArgs& A, double px, double pz
 // One block: keep loops with >= 4 points (interactive.cpp:160), de-rotate them,
 // loop bounding box, candidate cell box (interactive.cpp:172-181).
 // loops: n_loops from *nloops_dev (or nloops_host when nloops_dev == null)
+constexpr int kMaskBins = 1024;
+
+__device__ __forceinline__ int mask_bin(double x, double lo, double w) {
+  int b = (int)floor(__ddiv_rn(__dsub_rn(x, lo), w));
+  return b < 0 ? 0 : (b >= kMaskBins ? kMaskBins - 1 : b);
+}
+
+// Edges binned by their x-range [min, max] (an edge can only change the +z
+// ray parity of p when min(ax, bx) <= p.x < max(ax, bx)), so a cell tests the
+// few edges of its bin; the per-edge test is untouched, so the parity (and the
+// cell set) is exactly the reference's.
 __global__ void __launch_bounds__(1024) k_mask_prepare(MaskArgs A, const int* nloops_dev,
                                                        int nloops_host, const int* off,
                                                        const double* pts, double* out_xz,
-                                                       int* out_off, double* bbox, int* box) {
+                                                       int* out_off, double* bbox, int* box,
+                                                       int* bin_off, int* bin_edges,
+                                                       int bin_cap) {
+  __shared__ int s_cnt[kMaskBins + 1];
   __shared__ int s_kept;
   __shared__ double s_lo[2][1024], s_hi[2][1024];
   const int nl = nloops_dev ? nloops_dev[0] : nloops_host;
@@ -154,8 +168,49 @@ __global__ void __launch_bounds__(1024) k_mask_prepare(MaskArgs A, const int* nl
       }
     __syncthreads();
   }
+  const double lo_x = s_lo[0][0], hi_x = s_hi[0][0];
+  double w = __ddiv_rn(__dsub_rn(hi_x, lo_x), (double)kMaskBins);
+  if (!(w > 0.0)) w = 1.0;
+  const int np = out_off[kept];
+  auto edge_ok = [&](int q) {  // q -> q+1 inside one kept loop
+    if (q + 1 >= np) return false;
+    for (int l = 1; l <= kept; ++l)
+      if (q + 1 == out_off[l]) return false;
+    return true;
+  };
+  for (int b = threadIdx.x; b <= kMaskBins; b += blockDim.x) s_cnt[b] = 0;
+  __syncthreads();
+  for (int q = threadIdx.x; q < np; q += blockDim.x) {
+    if (!edge_ok(q)) continue;
+    const double ax = out_xz[2 * q], bx = out_xz[2 * q + 2];
+    const int b0 = mask_bin(fmin(ax, bx), lo_x, w), b1 = mask_bin(fmax(ax, bx), lo_x, w);
+    for (int b = b0; b <= b1; ++b) atomicAdd(&s_cnt[b], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int b = 0; b < kMaskBins; ++b) {
+      const int c = s_cnt[b];
+      s_cnt[b] = acc;
+      bin_off[b] = acc;
+      acc += c;
+    }
+    bin_off[kMaskBins] = acc;
+    s_cnt[kMaskBins] = acc;
+  }
+  __syncthreads();
+  const bool fits = s_cnt[kMaskBins] <= bin_cap;
+  if (fits)
+    for (int q = threadIdx.x; q < np; q += blockDim.x) {
+      if (!edge_ok(q)) continue;
+      const double ax = out_xz[2 * q], bx = out_xz[2 * q + 2];
+      const int b0 = mask_bin(fmin(ax, bx), lo_x, w), b1 = mask_bin(fmax(ax, bx), lo_x, w);
+      for (int b = b0; b <= b1; ++b) bin_edges[atomicAdd(&s_cnt[b], 1)] = q;
+    }
   if (threadIdx.x != 0) return;
   bbox[0] = s_lo[0][0], bbox[1] = s_lo[1][0], bbox[2] = s_hi[0][0], bbox[3] = s_hi[1][0];
+  bbox[4] = w;
+  box[5] = fits ? 1 : 0;
   if (kept == 0) {
     box[0] = box[1] = box[2] = box[3] = 0;
     box[4] = 0;
@@ -179,7 +234,8 @@ __global__ void __launch_bounds__(256) k_mask_cells(MaskArgs A, const int* box,
                                                     const double* bbox, const int* loop_off,
                                                     const double* loops_xz, int box_w_cap,
                                                     double* mask_h, unsigned char* mask_f,
-                                                    float* curr, int apply, int* count) {
+                                                    float* curr, int apply, int* count,
+                                                    const int* bin_off, const int* bin_edges) {
   extern __shared__ double sm_pts[];
   const int i0 = box[0], i1 = box[1], j0 = box[2], j1 = box[3], kept = box[4];
   if (kept == 0 || i1 <= i0 || j1 <= j0) return;
@@ -188,7 +244,8 @@ __global__ void __launch_bounds__(256) k_mask_cells(MaskArgs A, const int* box,
   for (int q = threadIdx.x; q < 2 * np && cached; q += blockDim.x) sm_pts[q] = loops_xz[q];
   __syncthreads();
   const double* P = cached ? sm_pts : loops_xz;
-  const double lox = bbox[0], loz = bbox[1], hix = bbox[2], hiz = bbox[3];
+  const double lox = bbox[0], loz = bbox[1], hix = bbox[2], hiz = bbox[3], bw_x = bbox[4];
+  const bool binned = box[5] != 0;
   double vr = A.frame.volume_ratio;
   if (A.vw) vr = A.mesh_volume > 0.0 ? __ddiv_rn(A.vw[0], A.mesh_volume) : 0.0;
   const int bw = j1 - j0;
@@ -205,16 +262,20 @@ __global__ void __launch_bounds__(256) k_mask_cells(MaskArgs A, const int* box,
     double h = 0.0;
     if (!(lx < lox || lx > hix || lz < loz || lz > hiz)) {
       int crossings = 0;
-      for (int l = 0; l < kept; ++l) {
-        const int e0 = loop_off[l], e1 = loop_off[l + 1];
-        for (int e = e0; e + 1 < e1; ++e) {
-          const double ax = P[2 * e], az = P[2 * e + 1], bx = P[2 * e + 2], bz = P[2 * e + 3];
-          if ((ax > lx) == (bx > lx)) continue;
-          const double zi =
-              __dadd_rn(az, __dmul_rn(__ddiv_rn(__dsub_rn(lx, ax), __dsub_rn(bx, ax)),
-                                      __dsub_rn(bz, az)));
-          if (zi > lz) ++crossings;
-        }
+      auto test = [&](int e) {
+        const double ax = P[2 * e], az = P[2 * e + 1], bx = P[2 * e + 2], bz = P[2 * e + 3];
+        if ((ax > lx) == (bx > lx)) return;
+        const double zi =
+            __dadd_rn(az, __dmul_rn(__ddiv_rn(__dsub_rn(lx, ax), __dsub_rn(bx, ax)),
+                                    __dsub_rn(bz, az)));
+        if (zi > lz) ++crossings;
+      };
+      if (binned) {
+        const int b = mask_bin(lx, lox, bw_x);
+        for (int q = bin_off[b]; q < bin_off[b + 1]; ++q) test(bin_edges[q]);
+      } else {
+        for (int l = 0; l < kept; ++l)
+          for (int e = loop_off[l]; e + 1 < loop_off[l + 1]; ++e) test(e);
       }
       if (crossings & 1) {
         inside = 1;
@@ -261,8 +322,12 @@ void mask_launch(ocn_zone* z, MaskArgs A, const int* nloops_dev, int nloops_host
   z->mask_f.ensure(box_cap);
   ProfWindow pw(ctx, OCN_PROF_MASK);
   OCN_CUDA(cudaMemsetAsync(z->mask_count.p, 0, sizeof(int), st));
+  const int bin_cap = 8 * std::max(max_points, 1) + 16 * kMaskBins;
+  z->bin_off.ensure(kMaskBins + 1);
+  z->bin_edges.ensure(bin_cap);
   k_mask_prepare<<<1, 1024, 0, st>>>(A, nloops_dev, nloops_host, d_off, d_pts, z->loops_xz.p,
-                                     z->loops_off.p, z->loop_bbox.p, z->mask_box.p);
+                                     z->loops_off.p, z->loop_bbox.p, z->mask_box.p, z->bin_off.p,
+                                     z->bin_edges.p, bin_cap);
   OCN_LAUNCHED(ctx);
   const size_t smem = kMaskEdgesSmem * 2 * sizeof(double);
   static bool attr = false;
@@ -274,7 +339,7 @@ void mask_launch(ocn_zone* z, MaskArgs A, const int* nloops_dev, int nloops_host
   k_mask_cells<<<ctx->sm_count * 4, 256, smem, st>>>(A, z->mask_box.p, z->loop_bbox.p,
                                                      z->loops_off.p, z->loops_xz.p, (int)box_cap,
                                                      z->mask_h.p, z->mask_f.p, z->curr(), apply,
-                                                     z->mask_count.p);
+                                                     z->mask_count.p, z->bin_off.p, z->bin_edges.p);
   OCN_LAUNCHED(ctx);
 }
 
@@ -327,10 +392,10 @@ int ocn_zone_create(ocn_ctx* ctx, const ocn_fdm_config* cfg, double body_size, d
     z->c = std::sqrt(0.49) * z->delta / dt;
     z->origin[0] = bx - 0.5 * z->n * z->delta;
     z->origin[1] = bz - 0.5 * z->n * z->delta;
-    z->mask_box.alloc(5);
-    z->loop_bbox.alloc(4);
+    z->mask_box.alloc(6);
+    z->loop_bbox.alloc(5);
     z->mask_count.alloc(1);
-    OCN_CUDA(cudaMemsetAsync(z->mask_box.p, 0, 5 * sizeof(int), ctx->stream));
+    OCN_CUDA(cudaMemsetAsync(z->mask_box.p, 0, 6 * sizeof(int), ctx->stream));
     OCN_CUDA(cudaMemsetAsync(z->mask_count.p, 0, sizeof(int), ctx->stream));
     OCN_CUDA(cudaStreamSynchronize(ctx->stream));
     ctx_retain(ctx);

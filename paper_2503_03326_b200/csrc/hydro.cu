@@ -18,6 +18,7 @@
 //                enter through its first edge, last-writer crossing points.
 // All reductions are fixed trees over a fixed state->thread mapping, so the
 // report is bit-identical run to run.
+#include <algorithm>
 #include <cstring>
 
 #include "hydro_internal.cuh"
@@ -431,22 +432,14 @@ __global__ void k_chain_partner(const SegDev* segs, const int2* total, int hcap,
 // Sequential walk with the reference's visiting order (hydro.cpp:167-213) in
 // shared memory. Emits point references e = 2*segment + side: the crossing
 // point of that key as stored by the larger segment (std::map last writer).
-constexpr int kChainSmem = 12288;  // segments held in shared memory
+constexpr int kChainSeq = 12288;  // segments of the sequential fallback in shared memory
+constexpr int kChainPar = 4096;   // segments of the parallel path (2 nodes each)
+constexpr int kChainThreads = 1024;
 
-__global__ void __launch_bounds__(256) k_chain_walk(const int2* total, const int* partner_g,
-                                                    unsigned char* used_g, int* loop_off,
-                                                    int* point_ref, int* counts_out) {
-  extern __shared__ int sm_chain[];
-  const int nseg = total->y;
-  const bool in_smem = nseg <= kChainSmem;
-  const int* partner = in_smem ? sm_chain : partner_g;
-  unsigned char* used =
-      in_smem ? reinterpret_cast<unsigned char*>(sm_chain + 2 * kChainSmem) : used_g;
-  if (in_smem)
-    for (int e = threadIdx.x; e < 2 * nseg; e += blockDim.x) sm_chain[e] = partner_g[e];
-  for (int s = threadIdx.x; s < nseg; s += blockDim.x) used[s] = 0;
-  __syncthreads();
-  if (threadIdx.x != 0) return;
+// Reference walk (hydro.cpp:167-213) by one thread: general topology
+// (open chains, any size). partner / used may live in shared or global memory.
+__device__ void chain_walk_seq(int nseg, const int* partner, unsigned char* used, int* loop_off,
+                               int* point_ref, int* counts_out) {
   int nl = 0, np = 0;
   loop_off[0] = 0;
   auto canon = [&](int e) {
@@ -482,6 +475,199 @@ __global__ void __launch_bounds__(256) k_chain_walk(const int2* total, const int
   }
   counts_out[0] = nl;
   counts_out[1] = np;
+}
+
+// Waterline chaining with the reference's visiting order. On a closed mesh
+// every crossed edge has exactly two segments, so "segment s entered through
+// side x" nodes form a permutation next(e) = partner[e ^ 1] whose cycles are
+// the loops (each in both orientations). The reference walks the cycle of its
+// lowest unused segment s0, entering through side 0: that is the orientation
+// whose minimum node id is even (2 s0). Pointer jumping gives every node its
+// cycle minimum and its distance to the start node, hence its position in the
+// loop; loops are numbered by increasing s0 exactly as the reference emits
+// them. Open topology (a crossed edge with one segment) or huge waterlines
+// take the sequential walk.
+__global__ void __launch_bounds__(kChainThreads) k_chain(const int2* total, const int* partner_g,
+                                                         unsigned char* used_g, int* loop_off,
+                                                         int* point_ref, int* counts_out) {
+  extern __shared__ int sm_chain[];
+  __shared__ int s_open;
+  __shared__ int s_wsum[kChainThreads / 32];
+  const int nseg = total->y;
+  const int tid = threadIdx.x;
+  if (tid == 0) s_open = 0;
+  __syncthreads();
+  const int nodes = 2 * nseg;
+  for (int e = tid; e < nodes; e += blockDim.x)
+    if (partner_g[e] < 0) s_open = 1;
+  __syncthreads();
+  if (s_open || nseg > kChainPar) {
+    // sequential fallback
+    const bool in_smem = nseg <= kChainSeq;
+    int* partner = in_smem ? sm_chain : const_cast<int*>(partner_g);
+    unsigned char* used =
+        in_smem ? reinterpret_cast<unsigned char*>(sm_chain + 2 * kChainSeq) : used_g;
+    if (in_smem)
+      for (int e = tid; e < nodes; e += blockDim.x) sm_chain[e] = partner_g[e];
+    for (int q = tid; q < nseg; q += blockDim.x) used[q] = 0;
+    __syncthreads();
+    if (tid == 0) chain_walk_seq(nseg, partner, used, loop_off, point_ref, counts_out);
+    return;
+  }
+  int* prt = sm_chain;                 // [nodes] partner
+  int* cmin = sm_chain + 2 * kChainPar;  // [nodes]
+  int* jp = sm_chain + 4 * kChainPar;    // [nodes]
+  int* dist = sm_chain + 6 * kChainPar;  // [nodes]
+  int* segoff = sm_chain + 8 * kChainPar;  // [nseg] point offset of the loop starting there
+  for (int e = tid; e < nodes; e += blockDim.x) {
+    prt[e] = partner_g[e];
+  }
+  __syncthreads();
+  for (int e = tid; e < nodes; e += blockDim.x) {
+    cmin[e] = e;
+    jp[e] = prt[e ^ 1];
+  }
+  __syncthreads();
+  // ---- phase A: cycle minimum node id
+  for (int span = 1; span < nodes; span <<= 1) {
+    int nm[8], nj[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int e = tid + k * kChainThreads;
+      if (e < nodes) {
+        const int j = jp[e];
+        nm[k] = min(cmin[e], cmin[j]);
+        nj[k] = jp[j];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int e = tid + k * kChainThreads;
+      if (e < nodes) cmin[e] = nm[k], jp[e] = nj[k];
+    }
+    __syncthreads();
+  }
+  // ---- phase B: distance to the start node (live orientation only)
+  for (int e = tid; e < nodes; e += blockDim.x) {
+    const int st = cmin[e];
+    const bool live = (st & 1) == 0;
+    dist[e] = (!live || e == st) ? 0 : 1;
+    jp[e] = (!live || e == st) ? e : prt[e ^ 1];
+  }
+  __syncthreads();
+  for (int span = 1; span < nodes; span <<= 1) {
+    int nd[8], nj[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int e = tid + k * kChainThreads;
+      if (e < nodes) {
+        const int j = jp[e];
+        nd[k] = dist[e] + dist[j];
+        nj[k] = jp[j];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int e = tid + k * kChainThreads;
+      if (e < nodes) dist[e] = nd[k], jp[e] = nj[k];
+    }
+    __syncthreads();
+  }
+  // ---- loop sizes at the start segments, exclusive scan in segment order
+  // node 2 s is a start iff its cycle minimum is itself; length L = dist(next) + 1
+  int keep_len[4];
+  int local = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int q = tid * 4 + k;
+    int v = 0;
+    if (q < nseg) {
+      const int e = 2 * q;
+      if (cmin[e] == e) {
+        const int L = dist[prt[e ^ 1]] + 1;
+        if (L >= 3) v = L + 1;
+      }
+    }
+    keep_len[k] = v;
+    local += v;
+  }
+  // block exclusive scan of `local` (thread order = segment order)
+  int incl = local;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if ((tid & 31) >= o) incl += y;
+  }
+  if ((tid & 31) == 31) s_wsum[tid >> 5] = incl;
+  __syncthreads();
+  if (tid < 32) {
+    int w = tid < kChainThreads / 32 ? s_wsum[tid] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (tid >= o) w += y;
+    }
+    s_wsum[tid] = w;  // inclusive warp sums
+  }
+  __syncthreads();
+  int base = incl - local + ((tid >> 5) ? s_wsum[(tid >> 5) - 1] : 0);
+  // loop numbering: count kept starts before each (second scan on 0/1 flags)
+  int cnt_local = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) cnt_local += keep_len[k] > 0;
+  int cincl = cnt_local;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, cincl, o);
+    if ((tid & 31) >= o) cincl += y;
+  }
+  __shared__ int s_csum[kChainThreads / 32];
+  if ((tid & 31) == 31) s_csum[tid >> 5] = cincl;
+  __syncthreads();
+  if (tid < 32) {
+    int w = tid < kChainThreads / 32 ? s_csum[tid] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (tid >= o) w += y;
+    }
+    s_csum[tid] = w;
+  }
+  __syncthreads();
+  int cbase = cincl - cnt_local + ((tid >> 5) ? s_csum[(tid >> 5) - 1] : 0);
+  // segoff[q] = point offset of the loop starting at segment q (or -1)
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int q = tid * 4 + k;
+    if (q >= nseg) break;
+    if (keep_len[k] > 0) {
+      segoff[q] = base;
+      loop_off[cbase + 1] = base + keep_len[k];
+      ++cbase;
+    } else {
+      segoff[q] = -1;
+    }
+    base += keep_len[k];
+  }
+  if (tid == kChainThreads - 1) {
+    counts_out[0] = s_csum[kChainThreads / 32 - 1];
+    counts_out[1] = s_wsum[kChainThreads / 32 - 1];
+    loop_off[0] = 0;
+  }
+  __syncthreads();
+  // ---- scatter point references: position = (L - dist) mod L, closing point at L
+  auto canon = [&](int e) {
+    const int p = prt[e];
+    return (p >= 0 && (p >> 1) > (e >> 1)) ? p : e;
+  };
+  for (int e = tid; e < nodes; e += blockDim.x) {
+    const int st = cmin[e];
+    if (st & 1) continue;  // orientation the reference never walks
+    const int off = segoff[st >> 1];
+    if (off < 0) continue;  // loop shorter than 3 points
+    const int L = dist[prt[st ^ 1]] + 1;
+    const int pos = (L - dist[e]) % L;
+    point_ref[off + pos] = canon(e);
+    if (e == st) point_ref[off + L] = canon(e);
+  }
 }
 
 __global__ void k_chain_points(const SegDev* segs, const int* counts, const int* point_ref,
@@ -598,15 +784,16 @@ void hydro_evaluate(ocn_mesh* m, const ocn_pose* pose, const ocn_fluid* fluid,
   k_chain_partner<<<grid_of(ctx, 2 * nt, 256), 256, 0, st>>>(m->segs.p, m->total.p, m->hcap,
                                                              m->hkeys.p, m->hvals.p, m->partner.p);
   OCN_LAUNCHED(ctx);
-  const size_t chain_smem = 2 * kChainSmem * sizeof(int) + kChainSmem;
+  const size_t chain_smem = std::max(9 * kChainPar * sizeof(int),
+                                     2 * kChainSeq * sizeof(int) + kChainSeq);
   static bool attr = false;
   if (!attr) {
-    OCN_CUDA(cudaFuncSetAttribute(k_chain_walk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    OCN_CUDA(cudaFuncSetAttribute(k_chain, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)chain_smem));
     attr = true;
   }
-  k_chain_walk<<<1, 256, chain_smem, st>>>(m->total.p, m->partner.p, m->used.p, m->loop_off.p,
-                                           m->point_ref.p, m->loop_counts.p);
+  k_chain<<<1, kChainThreads, chain_smem, st>>>(m->total.p, m->partner.p, m->used.p, m->loop_off.p,
+                                                m->point_ref.p, m->loop_counts.p);
   OCN_LAUNCHED(ctx);
   k_chain_points<<<grid_of(ctx, nt, 256), 256, 0, st>>>(m->segs.p, m->loop_counts.p,
                                                         m->point_ref.p, m->loop_points.p);

@@ -80,6 +80,7 @@ struct ocn_zone {
   ocn::DevBuf<int> loops_off;
   ocn::DevBuf<double> loop_bbox;      // lo.x, lo.z, hi.x, hi.z
   ocn::DevBuf<int> mask_count;
+  ocn::DevBuf<int> bin_off, bin_edges;  // x-binned loop edges (k_mask_prepare)
   float* curr() { return buf[icurr].p; }
   float* prev() { return buf[iprev].p; }
 };
