@@ -275,6 +275,13 @@ OCN_API int ocn_cascades_info(const ocn_cascades* c, int* resolution, int* count
 OCN_API int ocn_cascades_download(ocn_cascades* c, int grid, double* host_h0, double* host_h0cn,
                           uint8_t* host_in_band, double* host_waves);
 
+/* assemble_coefficients (surface.cpp:39-68) of one grid at time t on the
+ * device (fp64): out = 8 interleaved complex fields (8 * 2*N*N doubles) in
+ * SurfaceField order. Not on the per-frame path (the spectral step generates
+ * its packed coefficients in registers); provided for the drop-in API. */
+OCN_API int ocn_assemble_coefficients(ocn_cascades* c, int grid, double t, double choppiness,
+                                      double* host_out);
+
 /* =========================== surface maps (K2+K4) ========================= */
 /* SurfaceMaps (surface.hpp:65-80): 8 fp32 fields per cascade, device-resident. */
 OCN_API int ocn_maps_create(ocn_cascades* c, ocn_maps** out);
@@ -286,6 +293,12 @@ OCN_API int ocn_maps_time(const ocn_maps* m, double* t);
 OCN_API int ocn_maps_download(ocn_maps* m, int cascade, int field, double* host_out);
 OCN_API int ocn_maps_download_f32(ocn_maps* m, int cascade, int field, float* host_out);
 OCN_API int ocn_maps_device_field(ocn_maps* m, int cascade, int field, const float** dev_out);
+/* Maps not produced by a spectral step (e.g. SurfaceMaps assembled by the
+ * caller): `count` cascades of tile lengths host_lengths at resolution n,
+ * filled with ocn_maps_upload; usable by every sampler. */
+OCN_API int ocn_maps_create_bare(ocn_ctx* ctx, int resolution, int count,
+                                 const double* host_lengths, ocn_maps** out);
+OCN_API int ocn_maps_upload(ocn_maps* m, int cascade, int field, const double* host_in);
 
 /* ========================= velocity slices (K3+K4) ======================== */
 OCN_API int ocn_slices_create(ocn_cascades* c, const ocn_slice_config* cfg, ocn_slices** out);

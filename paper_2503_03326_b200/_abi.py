@@ -101,7 +101,10 @@ SIGNATURES = {
     "ocn_cascades_destroy": (ci, [vp]),
     "ocn_cascades_info": (ci, [vp, C.POINTER(ci), C.POINTER(ci)]),
     "ocn_cascades_download": (ci, [vp, ci, d, d, u8, d]),
+    "ocn_assemble_coefficients": (ci, [vp, ci, cd, cd, d]),
     "ocn_maps_create": (ci, [vp, pvp]),
+    "ocn_maps_create_bare": (ci, [vp, ci, ci, d, pvp]),
+    "ocn_maps_upload": (ci, [vp, ci, ci, d]),
     "ocn_maps_destroy": (ci, [vp]),
     "ocn_surface_generate": (ci, [vp, cd, cd]),
     "ocn_maps_time": (ci, [vp, d]),

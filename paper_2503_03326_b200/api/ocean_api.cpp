@@ -1,0 +1,1002 @@
+// ocean_api.cpp — the C++ drop-in API (include/ocean/*.hpp) over the C-ABI of
+// libocean_b200.so. Host code here is bookkeeping (validation, handle
+// lifetimes, lazy materialisation of device results); every hot-path
+// computation is a call into the sm_100a kernels.
+#include <algorithm>
+#include <atomic>
+#include <cstdlib>
+#include <fstream>
+#include <map>
+#include <mutex>
+#include <sstream>
+#include <thread>
+
+#include "ocean/device.hpp"
+#include "ocean/hydro.hpp"
+#include "ocean/interactive.hpp"
+#include "ocean/parallel.hpp"
+#include "ocean/rng.hpp"
+#include "ocean/spectra.hpp"
+#include "ocean/surface.hpp"
+#include "ocean/velocity.hpp"
+#include "ocean_b200.h"
+
+namespace ocean {
+
+// ============================================================ device context
+namespace {
+std::mutex g_ctx_mu;
+ocn_ctx* g_ctx = nullptr;
+int g_device = -1;
+
+ocn_spectrum_params to_c(const SpectrumParams& p) {
+  ocn_spectrum_params c{};
+  c.wind_speed = p.wind_speed;
+  c.fetch = p.fetch;
+  c.wind_direction = p.wind_direction;
+  c.swell = p.swell;
+  c.direction_mix = p.direction_mix;
+  c.gravity = p.gravity;
+  c.rng_seed = p.rng_seed;
+  c.has_peak_omega_override = p.peak_omega_override.has_value();
+  c.peak_omega_override = p.peak_omega_override.value_or(0.0);
+  return c;
+}
+}  // namespace
+
+void throw_on_status(int st, const char* where) {
+  if (st == OCN_OK) return;
+  std::string msg = ocn_last_error(g_ctx);
+  if (msg.empty()) msg = ocn_last_error(nullptr);
+  switch (st) {
+    case OCN_ERR_CONFIG: throw ConfigError(msg);
+    case OCN_ERR_MESH: throw MeshError(msg);
+    case OCN_ERR_NUMERIC: throw NumericError(msg);
+    case OCN_ERR_IO: throw IoError(msg);
+    case OCN_ERR_DOMAIN: throw DomainError(msg);
+    case OCN_ERR_CUDA: throw DeviceError(std::string(where) + ": " + msg);
+    default: throw std::invalid_argument(std::string(where) + ": " + msg);
+  }
+}
+#define OCN_CALL(expr) ::ocean::throw_on_status((expr), #expr)
+
+void set_device(int device) {
+  std::lock_guard<std::mutex> lk(g_ctx_mu);
+  if (g_ctx) throw ConfigError("set_device: the device context already exists");
+  g_device = device;
+}
+
+ocn_ctx* device_context() {
+  std::lock_guard<std::mutex> lk(g_ctx_mu);
+  if (!g_ctx) {
+    int dev = g_device;
+    if (dev < 0) {
+      const char* e = std::getenv("OCEAN_DEVICE");
+      dev = e ? std::atoi(e) : 0;
+    }
+    ocn_ctx* c = nullptr;
+    int st = ocn_ctx_create(dev, &c);
+    if (st != OCN_OK) throw DeviceError(std::string("no usable B200: ") + ocn_last_error(nullptr));
+    g_ctx = c;
+  }
+  return g_ctx;
+}
+
+void synchronize() { OCN_CALL(ocn_ctx_synchronize(device_context())); }
+
+// ============================================================ core
+Mat3 Mat3::operator*(const Mat3& o) const {
+  Mat3 r = zero();
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      for (int k = 0; k < 3; ++k) r.m[i][j] += m[i][k] * o.m[k][j];
+  return r;
+}
+Mat3 Mat3::transposed() const {
+  Mat3 r;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) r.m[i][j] = m[j][i];
+  return r;
+}
+Mat3 Mat3::inverse() const {
+  auto c = [&](int r0, int c0, int r1, int c1) { return m[r0][c0] * m[r1][c1] - m[r0][c1] * m[r1][c0]; };
+  const double det = m[0][0] * c(1, 1, 2, 2) - m[0][1] * c(1, 0, 2, 2) + m[0][2] * c(1, 0, 2, 1);
+  if (det == 0.0) throw NumericError("singular 3x3 matrix");
+  const double id = 1.0 / det;
+  Mat3 r;
+  r.m[0][0] = c(1, 1, 2, 2) * id, r.m[0][1] = -c(0, 1, 2, 2) * id, r.m[0][2] = c(0, 1, 1, 2) * id;
+  r.m[1][0] = -c(1, 0, 2, 2) * id, r.m[1][1] = c(0, 0, 2, 2) * id, r.m[1][2] = -c(0, 0, 1, 2) * id;
+  r.m[2][0] = c(1, 0, 2, 1) * id, r.m[2][1] = -c(0, 0, 2, 1) * id, r.m[2][2] = c(0, 0, 1, 1) * id;
+  return r;
+}
+Quat Quat::from_axis_angle(const Vec3& axis, double angle) {
+  const double n = axis.norm();
+  if (n < 1e-300) return {};
+  const double h = 0.5 * angle, s = std::sin(h) / n;
+  return {std::cos(h), axis.x * s, axis.y * s, axis.z * s};
+}
+Quat Quat::operator*(const Quat& o) const {
+  return {w * o.w - x * o.x - y * o.y - z * o.z, w * o.x + x * o.w + y * o.z - z * o.y,
+          w * o.y - x * o.z + y * o.w + z * o.x, w * o.z + x * o.y - y * o.x + z * o.w};
+}
+Quat Quat::normalized() const {
+  const double n = std::sqrt(w * w + x * x + y * y + z * z);
+  return {w / n, x / n, y / n, z / n};
+}
+Mat3 Quat::to_matrix() const {
+  Mat3 r;
+  r.m[0][0] = 1 - 2 * (y * y + z * z), r.m[0][1] = 2 * (x * y - w * z), r.m[0][2] = 2 * (x * z + w * y);
+  r.m[1][0] = 2 * (x * y + w * z), r.m[1][1] = 1 - 2 * (x * x + z * z), r.m[1][2] = 2 * (y * z - w * x);
+  r.m[2][0] = 2 * (x * z - w * y), r.m[2][1] = 2 * (y * z + w * x), r.m[2][2] = 1 - 2 * (x * x + y * y);
+  return r;
+}
+double wrap_angle(double a) {
+  a = std::fmod(a + kPi, 2.0 * kPi);
+  if (a <= 0.0) a += 2.0 * kPi;
+  return a - kPi;
+}
+
+// ============================================================ parallel (host utilities)
+namespace {
+std::atomic<int> g_workers{0};
+}
+int worker_count() {
+  const int n = g_workers.load();
+  if (n > 0) return n;
+  const unsigned hw = std::thread::hardware_concurrency();
+  return hw ? static_cast<int>(hw) : 1;
+}
+void set_worker_count(int n) { g_workers.store(n); }
+void parallel_for(size_t n, const std::function<void(size_t, size_t)>& fn) {
+  if (n) fn(0, n);  // host-side helper only; device kernels carry the data parallelism
+}
+
+// ============================================================ rng (host)
+Philox::Block Philox::operator()(uint64_t ctr_lo, uint64_t ctr_hi) const {
+  uint32_t k0 = static_cast<uint32_t>(lo_) ^ static_cast<uint32_t>(hi_);
+  uint32_t k1 = static_cast<uint32_t>(lo_ >> 32) ^ static_cast<uint32_t>(hi_ >> 32);
+  uint32_t c[4] = {static_cast<uint32_t>(ctr_lo), static_cast<uint32_t>(ctr_lo >> 32),
+                   static_cast<uint32_t>(ctr_hi), static_cast<uint32_t>(ctr_hi >> 32)};
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t a = 0xD2511F53ull * c[0], b = 0xCD9E8D57ull * c[2];
+    const uint32_t n0 = static_cast<uint32_t>(b >> 32) ^ c[1] ^ k0;
+    const uint32_t n2 = static_cast<uint32_t>(a >> 32) ^ c[3] ^ k1;
+    c[1] = static_cast<uint32_t>(b), c[3] = static_cast<uint32_t>(a), c[0] = n0, c[2] = n2;
+    k0 += 0x9E3779B9u, k1 += 0xBB67AE85u;
+  }
+  return {{c[0], c[1], c[2], c[3]}};
+}
+cplx gaussian_complex(uint64_t seed, uint32_t stream, uint32_t i, uint32_t j) {
+  const auto b = Philox(seed, 0x6F63656E00000000ull | stream)((static_cast<uint64_t>(i) << 32) | j, 0);
+  const double r = std::sqrt(-2.0 * std::log(uniform_open(b.v[0])));
+  const double a = 2.0 * kPi * uniform_open(b.v[1]);
+  return {r * std::cos(a) / std::sqrt(2.0), r * std::sin(a) / std::sqrt(2.0)};
+}
+
+// ============================================================ spectra
+double SpectrumParams::alpha() const {
+  auto c = to_c(*this);
+  return ocn_alpha(&c);
+}
+double SpectrumParams::peak_omega() const {
+  auto c = to_c(*this);
+  return ocn_peak_omega(&c);
+}
+double SpectrumParams::standard_peak_omega() const {
+  auto c = to_c(*this);
+  return ocn_standard_peak_omega(&c);
+}
+void SpectrumParams::validate() const {
+  auto c = to_c(*this);
+  OCN_CALL(ocn_spectrum_validate(&c));
+}
+double dispersion(double k, double g) { return ocn_dispersion(k, g); }
+double jonswap(double omega, const SpectrumParams& p) {
+  auto c = to_c(p);
+  double out = 0.0;
+  OCN_CALL(ocn_jonswap(omega, &c, &out));
+  return out;
+}
+double beta_s(double r) { return ocn_beta_s(r); }
+double directional_kernel(double b, double t) { return ocn_directional_kernel(b, t); }
+double donelan_banner(double w, double t, double wp) { return ocn_donelan_banner(w, t, wp); }
+double swell_spread(double w, double t, double wp, double xi) { return ocn_swell_spread(w, t, wp, xi); }
+double q_dbxi_approx(double r) { return ocn_q_dbxi_approx(r); }
+double q_dbxi_quadrature(double r, double xi, int panels) { return ocn_q_dbxi_quadrature(r, xi, panels); }
+double directional(double w, double t, const SpectrumParams& p) {
+  auto c = to_c(p);
+  return ocn_directional(w, t, &c);
+}
+double h0_variance(const WaveVector& w, double L, const SpectrumParams& p) {
+  auto c = to_c(p);
+  return ocn_h0_variance(w.kx, w.kz, w.k, w.omega, L, &c);
+}
+void GridConfig::validate() const {
+  if (!is_power_of_two(resolution) || resolution < 2)
+    throw ConfigError("grid resolution must be a power of two >= 2");
+  if (!(length > 0.0)) throw ConfigError("cascade length must be > 0");
+  if (!(band_min >= 0.0) || !(band_max > band_min))
+    throw ConfigError("cascade band must satisfy 0 <= band_min < band_max");
+}
+
+namespace detail {
+struct CascadeHandle {
+  ocn_cascades* h = nullptr;
+  std::mutex mu;
+  std::vector<std::shared_ptr<struct MapsHandle>> maps_pool;
+  std::vector<std::shared_ptr<struct SlicesHandle>> slices_pool;
+  ~CascadeHandle();
+};
+struct MapsHandle {
+  ocn_maps* h = nullptr;
+  std::shared_ptr<CascadeHandle> owner;
+  ~MapsHandle() {
+    if (h) ocn_maps_destroy(h);
+  }
+};
+struct SlicesHandle {
+  ocn_slices* h = nullptr;
+  SliceConfig cfg;
+  std::shared_ptr<CascadeHandle> owner;
+  ~SlicesHandle() {
+    if (h) ocn_slices_destroy(h);
+  }
+};
+CascadeHandle::~CascadeHandle() {
+  maps_pool.clear();
+  slices_pool.clear();
+  if (h) ocn_cascades_destroy(h);
+}
+struct MeshHandle {
+  ocn_mesh* h = nullptr;
+  ~MeshHandle() {
+    if (h) ocn_mesh_destroy(h);
+  }
+};
+struct ZoneHandle {
+  ocn_zone* h = nullptr;
+  ~ZoneHandle() {
+    if (h) ocn_zone_destroy(h);
+  }
+};
+}  // namespace detail
+
+struct WaveGrid::Host {
+  std::vector<WaveVector> waves;
+  std::vector<char> band;
+  ComplexField h0, h0cn;
+};
+
+const WaveGrid::Host& WaveGrid::host() const {
+  if (!host_) throw ConfigError("WaveGrid: empty grid");
+  std::lock_guard<std::mutex> lk(dev_->mu);
+  if (host_->waves.empty()) {
+    const size_t nn = static_cast<size_t>(n_) * n_;
+    std::vector<double> h0(2 * nn), cn(2 * nn), w(4 * nn);
+    std::vector<uint8_t> band(nn);
+    OCN_CALL(ocn_cascades_download(dev_->h, index_, h0.data(), cn.data(), band.data(), w.data()));
+    host_->waves.resize(nn);
+    host_->band.assign(band.begin(), band.end());
+    host_->h0 = ComplexField(n_);
+    host_->h0cn = ComplexField(n_);
+    for (size_t q = 0; q < nn; ++q) {
+      host_->waves[q] = {w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]};
+      host_->h0.data()[q] = {h0[2 * q], h0[2 * q + 1]};
+      host_->h0cn.data()[q] = {cn[2 * q], cn[2 * q + 1]};
+    }
+  }
+  return *host_;
+}
+const WaveVector& WaveGrid::wave(int i, int j) const { return host().waves[static_cast<size_t>(i) * n_ + j]; }
+const ComplexField& WaveGrid::h0() const { return host().h0; }
+const ComplexField& WaveGrid::h0_conj_neg() const { return host().h0cn; }
+bool WaveGrid::in_band(int i, int j) const { return host().band[static_cast<size_t>(i) * n_ + j] != 0; }
+ocn_cascades* WaveGrid::device_handle() const { return dev_ ? dev_->h : nullptr; }
+
+WaveGrid generate_h0(const GridConfig& config, const SpectrumParams& params, uint32_t cascade_index) {
+  config.validate();
+  params.validate();
+  auto c = to_c(params);
+  auto dev = std::make_shared<detail::CascadeHandle>();
+  OCN_CALL(ocn_cascades_create(device_context(), config.resolution, 1, &config.length, &config.band_min,
+                               &config.band_max, &cascade_index, &c, &dev->h));
+  WaveGrid g;
+  g.n_ = config.resolution;
+  g.length_ = config.length;
+  g.band_min_ = config.band_min;
+  g.band_max_ = config.band_max;
+  g.gravity_ = params.gravity;
+  g.dev_ = dev;
+  g.host_ = std::make_shared<WaveGrid::Host>();
+  return g;
+}
+
+// ============================================================ fft
+bool is_conjugate_symmetric(const ComplexField& f, double tol) {
+  const int n = f.size();
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j)
+      if (std::abs(f.at(i, j) - std::conj(f.at(neg_index(i, n), neg_index(j, n)))) > tol) return false;
+  return true;
+}
+ComplexField ifft2_centered(ComplexField field) {
+  const int n = field.size();
+  ComplexField out(n);
+  OCN_CALL(ocn_ifft2_centered(device_context(), n, reinterpret_cast<const double*>(field.data()),
+                              reinterpret_cast<double*>(out.data())));
+  return out;
+}
+std::pair<RealField, RealField> ifft2_hermitian_pair(const ComplexField& x, const ComplexField& y,
+                                                     bool check) {
+  const int n = x.size();
+  if (n < 2 || !is_power_of_two(n))
+    throw ConfigError("FFT field size must be a power of two >= 2, got " + std::to_string(n));
+  if (x.size() != y.size()) throw ConfigError("paired FFT fields must have equal size");
+  if (check && (!is_conjugate_symmetric(x) || !is_conjugate_symmetric(y)))
+    throw NumericError("ifft2_hermitian_pair: inputs are not conjugate-symmetric");
+  RealField re(n), im(n);
+  OCN_CALL(ocn_ifft2_pair(device_context(), n, reinterpret_cast<const double*>(x.data()),
+                          reinterpret_cast<const double*>(y.data()), re.data(), im.data()));
+  return {std::move(re), std::move(im)};
+}
+
+// ============================================================ surface
+void CascadeConfig::validate() const {
+  if (lengths.empty()) throw ConfigError("at least one cascade is required");
+  if (cutoffs.size() + 1 != lengths.size())
+    throw ConfigError("cascade cutoffs must number one less than cascade lengths");
+  for (size_t i = 1; i < lengths.size(); ++i)
+    if (!(lengths[i] < lengths[i - 1])) throw ConfigError("cascade lengths must be strictly decreasing");
+  for (size_t i = 1; i < cutoffs.size(); ++i)
+    if (!(cutoffs[i] > cutoffs[i - 1])) throw ConfigError("cascade cutoffs must be increasing");
+  if (!is_power_of_two(resolution) || resolution < 2)
+    throw ConfigError("cascade resolution must be a power of two >= 2");
+}
+
+CascadeSet::CascadeSet(const CascadeConfig& config, const SpectrumParams& params)
+    : config_(config), params_(params) {
+  config.validate();
+  params.validate();
+  const int C = static_cast<int>(config.lengths.size());
+  std::vector<double> lo(C), hi(C);
+  std::vector<uint32_t> idx(C);
+  for (int c = 0; c < C; ++c) {
+    lo[c] = c == 0 ? 0.0 : config.cutoffs[c - 1];
+    hi[c] = c + 1 < C ? config.cutoffs[c] : 1e300;
+    idx[c] = static_cast<uint32_t>(c);
+  }
+  auto c = to_c(params);
+  dev_ = std::make_shared<detail::CascadeHandle>();
+  OCN_CALL(ocn_cascades_create(device_context(), config.resolution, C, config.lengths.data(), lo.data(),
+                               hi.data(), idx.data(), &c, &dev_->h));
+  for (int k = 0; k < C; ++k) {
+    WaveGrid g;
+    g.n_ = config.resolution;
+    g.index_ = k;
+    g.length_ = config.lengths[k];
+    g.band_min_ = lo[k];
+    g.band_max_ = hi[k];
+    g.gravity_ = params.gravity;
+    g.dev_ = dev_;
+    g.host_ = std::make_shared<WaveGrid::Host>();
+    grids_.push_back(g);
+  }
+}
+ocn_cascades* CascadeSet::device_handle() const { return dev_ ? dev_->h : nullptr; }
+
+std::array<ComplexField, kFieldCount> assemble_coefficients(const WaveGrid& grid, double t,
+                                                            double choppiness) {
+  const int n = grid.resolution();
+  std::vector<double> buf(static_cast<size_t>(kFieldCount) * 2 * n * n);
+  OCN_CALL(ocn_assemble_coefficients(grid.device_handle(), grid.device_index(), t, choppiness, buf.data()));
+  std::array<ComplexField, kFieldCount> out;
+  const size_t nn = static_cast<size_t>(n) * n;
+  for (int f = 0; f < kFieldCount; ++f) {
+    out[f] = ComplexField(n);
+    for (size_t q = 0; q < nn; ++q) out[f].data()[q] = {buf[2 * (f * nn + q)], buf[2 * (f * nn + q) + 1]};
+  }
+  return out;
+}
+
+namespace {
+// a pooled device maps buffer of this cascade set not referenced by any SurfaceMaps
+std::shared_ptr<detail::MapsHandle> acquire_maps(const std::shared_ptr<detail::CascadeHandle>& cas) {
+  std::lock_guard<std::mutex> lk(cas->mu);
+  for (auto& m : cas->maps_pool)
+    if (m.use_count() == 1) return m;
+  auto m = std::make_shared<detail::MapsHandle>();
+  OCN_CALL(ocn_maps_create(cas->h, &m->h));
+  cas->maps_pool.push_back(m);
+  return m;
+}
+}  // namespace
+
+SurfaceMaps generate_maps(const CascadeSet& cascades, double t, const SurfaceGenOptions& options) {
+  const auto& cas = cascades.device_shared();
+  if (!cas) throw ConfigError("generate_maps: empty cascade set");
+  SurfaceMaps maps;
+  maps.time = t;
+  maps.device = acquire_maps(cas);
+  OCN_CALL(ocn_surface_generate(maps.device->h, t, options.choppiness));
+  const int C = static_cast<int>(cascades.config().lengths.size());
+  const int n = cascades.config().resolution;
+  maps.cascades.resize(C);
+  for (int c = 0; c < C; ++c) {
+    maps.cascades[c].length = cascades.config().lengths[c];
+    if (!options.materialize) continue;
+    for (int f = 0; f < kFieldCount; ++f) {
+      maps.cascades[c].fields[f] = RealField(n);
+      OCN_CALL(ocn_maps_download(maps.device->h, c, f, maps.cascades[c].fields[f].data()));
+    }
+  }
+  return maps;
+}
+
+ocn_maps* SurfaceMaps::device_handle() const {
+  if (device) return device->h;
+  // maps assembled by the caller: upload them once into spectrum-less device maps
+  if (cascades.empty()) throw ConfigError("SurfaceMaps: no cascades");
+  const int n = cascades.front().fields[0].size();
+  std::vector<double> lengths;
+  for (const auto& c : cascades) lengths.push_back(c.length);
+  auto m = std::make_shared<detail::MapsHandle>();
+  OCN_CALL(ocn_maps_create_bare(device_context(), n, static_cast<int>(cascades.size()), lengths.data(),
+                                &m->h));
+  for (size_t c = 0; c < cascades.size(); ++c)
+    for (int f = 0; f < kFieldCount; ++f)
+      if (cascades[c].fields[f].size() == n)
+        OCN_CALL(ocn_maps_upload(m->h, static_cast<int>(c), f, cascades[c].fields[f].data()));
+  device = m;
+  return device->h;
+}
+
+double SurfaceMaps::sample(SurfaceField field, Vec2 x) const {
+  double xz[2] = {x.x, x.z}, out = 0.0;
+  OCN_CALL(ocn_maps_sample(device_handle(), field, 1, xz, &out));
+  return out;
+}
+SurfaceMaps::Displacement SurfaceMaps::sample_displacement(Vec2 x) const {
+  double xz[2] = {x.x, x.z}, out[3];
+  OCN_CALL(ocn_sample_displacement(device_handle(), 1, xz, out));
+  return {out[0], out[1], out[2]};
+}
+double height_at(const SurfaceMaps& maps, Vec2 x) {
+  double xz[2] = {x.x, x.z}, out = 0.0;
+  OCN_CALL(ocn_height_at(maps.device_handle(), 1, xz, &out));
+  return out;
+}
+std::vector<double> height_at(const SurfaceMaps& maps, const std::vector<Vec2>& xs) {
+  std::vector<double> out(xs.size());
+  if (xs.empty()) return out;
+  OCN_CALL(ocn_height_at(maps.device_handle(), static_cast<int64_t>(xs.size()),
+                         reinterpret_cast<const double*>(xs.data()), out.data()));
+  return out;
+}
+double height_at_tolerance(const SurfaceMaps& maps, Vec2 x, double tol, int max_iters, int* iterations) {
+  double xz[2] = {x.x, x.z}, out = 0.0;
+  int32_t it = 0;
+  OCN_CALL(ocn_height_at_tolerance(maps.device_handle(), 1, xz, tol, max_iters, &out, &it));
+  if (iterations) *iterations = it;
+  return out;
+}
+
+// ============================================================ velocity
+double attenuation(double k, double y) { return ocn_attenuation(k, y); }
+double log_distribution(double y, double y_min) {
+  double out = 0.0;
+  OCN_CALL(ocn_log_distribution(y, y_min, &out));
+  return out;
+}
+double exp_interp(double a, double fa, double b, double fb, double x) {
+  double out = 0.0;
+  OCN_CALL(ocn_exp_interp(a, fa, b, fb, x, &out));
+  return out;
+}
+namespace {
+ocn_slice_config to_c(const SliceConfig& c) {
+  ocn_slice_config s{};
+  s.y_min = c.y_min;
+  s.y_max = c.y_max;
+  s.count = c.count;
+  s.distribution = c.distribution == DepthDistribution::Uniform ? OCN_DEPTH_UNIFORM : OCN_DEPTH_LOGARITHMIC;
+  s.single_precision = c.single_precision;
+  return s;
+}
+}  // namespace
+void SliceConfig::validate() const {
+  if (!(y_min < y_max)) throw ConfigError("slice interval requires y_min < y_max");
+  if (count < 2) throw ConfigError("at least two depth slices are required");
+  if (distribution == DepthDistribution::Logarithmic && !(y_min < 0.0))
+    throw ConfigError("logarithmic distribution requires y_min < 0");
+}
+std::vector<double> slice_depths(const SliceConfig& config) {
+  config.validate();
+  auto c = to_c(config);
+  std::vector<double> d(config.count);
+  OCN_CALL(ocn_slice_depths(&c, d.data()));
+  return d;
+}
+
+VelocitySlices build_slices(const CascadeSet& cascades, double t, const SliceConfig& config) {
+  config.validate();
+  const auto& cas = cascades.device_shared();
+  if (!cas) throw ConfigError("build_slices: empty cascade set");
+  std::shared_ptr<detail::SlicesHandle> h;
+  {
+    std::lock_guard<std::mutex> lk(cas->mu);
+    for (auto& s : cas->slices_pool)
+      if (s.use_count() == 1 && s->cfg.count == config.count && s->cfg.y_min == config.y_min &&
+          s->cfg.y_max == config.y_max && s->cfg.distribution == config.distribution) {
+        h = s;
+        break;
+      }
+    if (!h) {
+      h = std::make_shared<detail::SlicesHandle>();
+      auto c = to_c(config);
+      OCN_CALL(ocn_slices_create(cas->h, &c, &h->h));
+      h->cfg = config;
+      cas->slices_pool.push_back(h);
+    }
+  }
+  OCN_CALL(ocn_velocity_build(h->h, t));
+  VelocitySlices out;
+  out.dev_ = h;
+  out.y_min_ = config.y_min;
+  out.y_max_ = config.y_max;
+  out.depths_.resize(config.count);
+  int cnt = 0;
+  OCN_CALL(ocn_slices_depths(h->h, &cnt, out.depths_.data()));
+  return out;
+}
+ocn_slices* VelocitySlices::device_handle() const { return dev_ ? dev_->h : nullptr; }
+Vec3 VelocitySlices::sample_slice(size_t i, Vec2 x) const {
+  double xz[2] = {x.x, x.z}, out[3];
+  OCN_CALL(ocn_sample_slice(device_handle(), static_cast<int>(i), 1, xz, out));
+  return {out[0], out[1], out[2]};
+}
+Vec3 velocity_at(const VelocitySlices& slices, Vec2 x, double y, DepthInterp interp) {
+  double q[3] = {x.x, x.z, y}, out[3];
+  OCN_CALL(ocn_velocity_at(slices.device_handle(), 1, q,
+                           interp == DepthInterp::Linear ? OCN_INTERP_LINEAR : OCN_INTERP_EXPONENTIAL, 0,
+                           out));
+  return {out[0], out[1], out[2]};
+}
+std::vector<Vec3> velocity_at(const VelocitySlices& slices, const std::vector<Vec3>& xzy,
+                              DepthInterp interp, bool clamp) {
+  std::vector<Vec3> out(xzy.size());
+  if (xzy.empty()) return out;
+  OCN_CALL(ocn_velocity_at(slices.device_handle(), static_cast<int64_t>(xzy.size()),
+                           reinterpret_cast<const double*>(xzy.data()),
+                           interp == DepthInterp::Linear ? OCN_INTERP_LINEAR : OCN_INTERP_EXPONENTIAL,
+                           clamp ? 1 : 0, reinterpret_cast<double*>(out.data())));
+  return out;
+}
+
+// ============================================================ mesh (load-time host code)
+TriMesh::TriMesh(std::vector<Vec3> vertices, std::vector<Tri> triangles)
+    : vertices_(std::move(vertices)), triangles_(std::move(triangles)) {
+  if (vertices_.empty() || triangles_.empty()) throw MeshError("empty mesh");
+  const long long nv = static_cast<long long>(vertices_.size());
+  std::vector<std::pair<long long, long long>> directed;
+  directed.reserve(triangles_.size() * 3);
+  for (const Tri& t : triangles_)
+    for (int e = 0; e < 3; ++e) {
+      const long long a = t.v[e], b = t.v[(e + 1) % 3];
+      if (a < 0 || b < 0 || a >= nv || b >= nv) throw MeshError("mesh: face references a missing vertex");
+      if (a == b) throw MeshError("mesh: face repeats a vertex");
+      directed.emplace_back(a, b);
+    }
+  std::sort(directed.begin(), directed.end());
+  if (std::adjacent_find(directed.begin(), directed.end()) != directed.end())
+    throw MeshError("mesh: duplicated directed edge (inconsistent winding)");
+  for (const auto& [a, b] : directed)
+    if (!std::binary_search(directed.begin(), directed.end(), std::make_pair(b, a)))
+      throw MeshError("mesh: open mesh, edge " + std::to_string(a) + "-" + std::to_string(b) +
+                      " has no partner");
+  auto corner = [&](const Tri& t, int k) -> const Vec3& { return vertices_[t.v[k]]; };
+  double signed_vol = 0.0;
+  for (const Tri& t : triangles_) signed_vol += dot(corner(t, 0), cross(corner(t, 1), corner(t, 2))) / 6.0;
+  if (signed_vol < 0.0)
+    for (Tri& t : triangles_) std::swap(t.v[1], t.v[2]);
+  bbox_min_ = bbox_max_ = vertices_[0];
+  for (const Vec3& v : vertices_) {
+    bbox_min_ = {std::min(bbox_min_.x, v.x), std::min(bbox_min_.y, v.y), std::min(bbox_min_.z, v.z)};
+    bbox_max_ = {std::max(bbox_max_.x, v.x), std::max(bbox_max_.y, v.y), std::max(bbox_max_.z, v.z)};
+  }
+  normals_.resize(triangles_.size());
+  areas_.resize(triangles_.size());
+  double vol = 0.0, second[3][3] = {};
+  Vec3 first;
+  for (size_t i = 0; i < triangles_.size(); ++i) {
+    const Vec3 &a = corner(triangles_[i], 0), &b = corner(triangles_[i], 1), &c = corner(triangles_[i], 2);
+    const Vec3 n = cross(b - a, c - a);
+    const double len = n.norm();
+    areas_[i] = 0.5 * len;
+    if (len < 1e-14) {
+      ++degenerate_;
+      normals_[i] = {};
+    } else {
+      normals_[i] = n / len;
+    }
+    total_area_ += areas_[i];
+    const double vt = dot(a, cross(b, c)) / 6.0;  // signed tetrahedron against the origin
+    vol += vt;
+    const Vec3 s = a + b + c;
+    first += s * (vt / 4.0);
+    const Vec3 pts[4] = {a, b, c, s};
+    for (int r = 0; r < 3; ++r)
+      for (int q = 0; q < 3; ++q) {
+        double acc = 0.0;
+        for (const Vec3& p : pts) {
+          const double pr[3] = {p.x, p.y, p.z};
+          acc += pr[r] * pr[q];
+        }
+        second[r][q] += vt / 20.0 * acc;
+      }
+  }
+  if (!(vol > 0.0)) throw MeshError("mesh volume must be positive");
+  volume_ = vol;
+  centroid_ = first / vol;
+  const double cm[3] = {centroid_.x, centroid_.y, centroid_.z};
+  double tr = 0.0;
+  for (int r = 0; r < 3; ++r) {
+    for (int q = 0; q < 3; ++q) second[r][q] -= vol * cm[r] * cm[q];
+    tr += second[r][r];
+  }
+  unit_inertia_ = Mat3::zero();
+  for (int r = 0; r < 3; ++r)
+    for (int q = 0; q < 3; ++q) unit_inertia_.m[r][q] = (r == q ? tr : 0.0) - second[r][q];
+}
+
+ocn_mesh* TriMesh::device_handle() const {
+  if (!dev_) {
+    auto h = std::make_shared<detail::MeshHandle>();
+    std::vector<int32_t> tris(3 * triangles_.size());
+    for (size_t i = 0; i < triangles_.size(); ++i)
+      for (int k = 0; k < 3; ++k) tris[3 * i + k] = triangles_[i].v[k];
+    OCN_CALL(ocn_mesh_create(device_context(), static_cast<int>(vertices_.size()),
+                             reinterpret_cast<const double*>(vertices_.data()),
+                             static_cast<int>(triangles_.size()), tris.data(),
+                             reinterpret_cast<const double*>(normals_.data()), areas_.data(), volume_,
+                             &h->h));
+    dev_ = h;
+  }
+  return dev_->h;
+}
+
+TriMesh load_obj(std::istream& in, const std::string& name) {
+  std::vector<Vec3> verts;
+  std::vector<TriMesh::Tri> tris;
+  std::string line;
+  for (int lineno = 1; std::getline(in, line); ++lineno) {
+    std::istringstream ls(line);
+    std::string tag;
+    if (!(ls >> tag) || tag[0] == '#') continue;
+    if (tag == "v") {
+      Vec3 v;
+      if (!(ls >> v.x >> v.y >> v.z)) throw MeshError(name + ":" + std::to_string(lineno) + ": malformed vertex");
+      verts.push_back(v);
+    } else if (tag == "f") {
+      std::vector<int> idx;
+      for (std::string tok; ls >> tok;) {
+        int i = std::stoi(tok.substr(0, tok.find('/')));  // v, v/vt, v//vn, v/vt/vn
+        if (i < 0) i += static_cast<int>(verts.size()) + 1;
+        idx.push_back(i - 1);
+      }
+      if (idx.size() != 3)
+        throw MeshError(name + ":" + std::to_string(lineno) + ": faces must be triangles, got " +
+                        std::to_string(idx.size()));
+      tris.push_back({{idx[0], idx[1], idx[2]}});
+    }
+  }
+  return TriMesh(std::move(verts), std::move(tris));
+}
+TriMesh load_obj_file(const std::string& path) {
+  std::ifstream in(path);
+  if (!in) throw MeshError("cannot open mesh file: " + path);
+  return load_obj(in, path);
+}
+void write_obj(std::ostream& out, const TriMesh& mesh) {
+  out << "# " << mesh.vertices().size() << " vertices, " << mesh.triangles().size() << " triangles\n";
+  for (const Vec3& v : mesh.vertices()) out << "v " << v.x << ' ' << v.y << ' ' << v.z << '\n';
+  for (const auto& t : mesh.triangles()) out << "f " << t.v[0] + 1 << ' ' << t.v[1] + 1 << ' ' << t.v[2] + 1 << '\n';
+}
+TriMesh make_icosphere(double radius, int subdivisions) {
+  const double p = (1.0 + std::sqrt(5.0)) / 2.0;
+  std::vector<Vec3> v = {{-1, p, 0}, {1, p, 0}, {-1, -p, 0}, {1, -p, 0}, {0, -1, p}, {0, 1, p},
+                         {0, -1, -p}, {0, 1, -p}, {p, 0, -1}, {p, 0, 1}, {-p, 0, -1}, {-p, 0, 1}};
+  std::vector<TriMesh::Tri> f = {{{0, 11, 5}}, {{0, 5, 1}}, {{0, 1, 7}}, {{0, 7, 10}}, {{0, 10, 11}},
+                                 {{1, 5, 9}}, {{5, 11, 4}}, {{11, 10, 2}}, {{10, 7, 6}}, {{7, 1, 8}},
+                                 {{3, 9, 4}}, {{3, 4, 2}}, {{3, 2, 6}}, {{3, 6, 8}}, {{3, 8, 9}},
+                                 {{4, 9, 5}}, {{2, 4, 11}}, {{6, 2, 10}}, {{8, 6, 7}}, {{9, 8, 1}}};
+  for (int s = 0; s < subdivisions; ++s) {
+    std::map<std::pair<int, int>, int> mid;
+    auto midpoint = [&](int a, int b) {
+      auto key = std::minmax(a, b);
+      auto it = mid.find(key);
+      if (it != mid.end()) return it->second;
+      const int id = static_cast<int>(v.size());
+      v.push_back((v[a] + v[b]) / 2.0);
+      mid.emplace(key, id);
+      return id;
+    };
+    std::vector<TriMesh::Tri> nf;
+    for (const auto& t : f) {
+      const int ab = midpoint(t.v[0], t.v[1]), bc = midpoint(t.v[1], t.v[2]), ca = midpoint(t.v[2], t.v[0]);
+      nf.push_back({{t.v[0], ab, ca}});
+      nf.push_back({{t.v[1], bc, ab}});
+      nf.push_back({{t.v[2], ca, bc}});
+      nf.push_back({{ab, bc, ca}});
+    }
+    f.swap(nf);
+  }
+  for (Vec3& x : v) x = x * (radius / x.norm());
+  return TriMesh(std::move(v), std::move(f));
+}
+
+// ============================================================ hydro
+double FluidQuery::density_at(double y) const {
+  if (density_profile.empty()) return water_density;
+  if (y <= density_profile.front().first) return density_profile.front().second;
+  if (y >= density_profile.back().first) return density_profile.back().second;
+  for (size_t i = 1; i < density_profile.size(); ++i)
+    if (y <= density_profile[i].first) {
+      const auto [y0, r0] = density_profile[i - 1];
+      const auto [y1, r1] = density_profile[i];
+      return lerp(r0, r1, (y - y0) / (y1 - y0));
+    }
+  return water_density;
+}
+FluidQuery FluidQuery::still_water() {
+  FluidQuery q;
+  q.surface_height = [](Vec2) { return 0.0; };
+  return q;  // no water_velocity: still water (zero medium velocity)
+}
+
+namespace {
+ocn_pose to_c(const BodyPose& p) {
+  ocn_pose c{};
+  const double v[][3] = {{p.position.x, p.position.y, p.position.z},
+                         {p.linear_velocity.x, p.linear_velocity.y, p.linear_velocity.z},
+                         {p.angular_velocity.x, p.angular_velocity.y, p.angular_velocity.z},
+                         {p.com_body.x, p.com_body.y, p.com_body.z}};
+  std::copy(v[0], v[0] + 3, c.position);
+  std::copy(v[1], v[1] + 3, c.linear_velocity);
+  std::copy(v[2], v[2] + 3, c.angular_velocity);
+  std::copy(v[3], v[3] + 3, c.com_body);
+  c.orientation[0] = p.orientation.w, c.orientation[1] = p.orientation.x;
+  c.orientation[2] = p.orientation.y, c.orientation[3] = p.orientation.z;
+  return c;
+}
+
+// Runs aggregate on the device and leaves the results in the mesh handle.
+ocn_hydro_report run_hydro(const TriMesh& mesh, const BodyPose& pose, const FluidQuery& fluid,
+                           const DragCoefficients& cd) {
+  ocn_fluid f{};
+  std::vector<void*> zones;
+  for (const FdmZone* z : fluid.zones) zones.push_back(z->device_handle());
+  f.maps = fluid.maps ? fluid.maps->device_handle() : nullptr;
+  f.slices = fluid.slices ? fluid.slices->device_handle() : nullptr;
+  if (fluid.water_velocity && !fluid.slices)
+    throw ConfigError("aggregate: host water_velocity callbacks are not supported on the B200 path; "
+                      "pass the device VelocitySlices in FluidQuery::slices");
+  f.velocity_clamp = fluid.velocity_clamp;
+  f.n_zones = static_cast<int>(zones.size());
+  f.zones = zones.data();
+  f.wind[0] = fluid.wind.x, f.wind[1] = fluid.wind.y, f.wind[2] = fluid.wind.z;
+  f.water_density = fluid.water_density;
+  f.air_density = fluid.air_density;
+  f.cd_water = cd.water;
+  f.cd_air = cd.air;
+  std::vector<double> profile;
+  for (const auto& [y, r] : fluid.density_profile) profile.push_back(y), profile.push_back(r);
+  f.n_profile = static_cast<int>(fluid.density_profile.size());
+  f.host_profile = profile.empty() ? nullptr : profile.data();
+  std::vector<double> depth;
+  if (!fluid.maps) {
+    if (!fluid.surface_height && zones.empty())
+      throw ConfigError("classify_clip: missing surface sampler");
+    if (fluid.surface_height) {  // caller's host sampler, evaluated per vertex
+      depth.resize(mesh.vertices().size());
+      for (size_t i = 0; i < depth.size(); ++i) {
+        const Vec3 w = pose.to_world(mesh.vertices()[i]);
+        double h = fluid.surface_height(w.xz());
+        for (const FdmZone* z : fluid.zones) h += z->sample(w.xz());
+        depth[i] = w.y - h;
+      }
+    }
+  }
+  const ocn_pose p = to_c(pose);
+  ocn_hydro_report r{};
+  OCN_CALL(ocn_hydro_aggregate(mesh.device_handle(), &p, &f, depth.empty() ? nullptr : depth.data(), &r));
+  return r;
+}
+
+std::vector<std::vector<Vec3>> download_waterline(const TriMesh& mesh) {
+  int nl = 0, np = 0;
+  OCN_CALL(ocn_hydro_waterline(mesh.device_handle(), &nl, &np, nullptr, nullptr));
+  std::vector<int32_t> off(nl + 1);
+  std::vector<Vec3> pts(std::max(np, 1));
+  OCN_CALL(ocn_hydro_waterline(mesh.device_handle(), &nl, &np, off.data(), reinterpret_cast<double*>(pts.data())));
+  std::vector<std::vector<Vec3>> loops(nl);
+  for (int l = 0; l < nl; ++l) loops[l].assign(pts.begin() + off[l], pts.begin() + off[l + 1]);
+  return loops;
+}
+Vec3 v3(const double* d) { return {d[0], d[1], d[2]}; }
+}  // namespace
+
+ClipResult classify_clip(const TriMesh& mesh, const BodyPose& pose, const FluidQuery& fluid) {
+  const ocn_hydro_report r = run_hydro(mesh, pose, fluid, {});
+  ClipResult out;
+  std::vector<ocn_triangle_state> st(std::max(r.state_count, 1));
+  int n = 0;
+  OCN_CALL(ocn_hydro_states(mesh.device_handle(), r.state_count, st.data(), &n));
+  out.states.resize(n);
+  for (int i = 0; i < n; ++i)
+    out.states[i] = {st[i].parent, st[i].status == 0 ? TriStatus::Submerged : TriStatus::Dry, st[i].area,
+                     v3(st[i].centroid), st[i].depth, v3(st[i].normal)};
+  out.waterline = download_waterline(mesh);
+  out.submerged_area = r.submerged_area;
+  out.dry_area = r.dry_area;
+  out.degenerate_skipped = r.degenerate_skipped;
+  return out;
+}
+
+HydroReport aggregate(const TriMesh& mesh, const BodyPose& pose, const FluidQuery& fluid,
+                      const DragCoefficients& cd) {
+  const ocn_hydro_report r = run_hydro(mesh, pose, fluid, cd);
+  HydroReport out;
+  out.submerged_volume = r.submerged_volume;
+  out.volume_clamped = r.volume_clamped;
+  if (r.has_center_of_immersion) out.center_of_immersion = v3(r.center_of_immersion);
+  out.waterline = download_waterline(mesh);
+  out.buoyancy_force = v3(r.buoyancy_force);
+  out.water_drag = v3(r.water_drag);
+  out.air_drag = v3(r.air_drag);
+  out.water_center = v3(r.water_center);
+  out.air_center = v3(r.air_center);
+  out.submerged_area = r.submerged_area;
+  out.dry_area = r.dry_area;
+  return out;
+}
+
+// host reductions over host state vectors (hydro.cpp:217-251 definitions)
+double submerged_volume(const std::vector<TriangleState>& states) {
+  return deterministic_sum(states.size(), 0.0, [&](size_t i) {
+    const TriangleState& s = states[i];
+    return s.status == TriStatus::Submerged ? s.area * s.depth * s.normal.y : 0.0;
+  });
+}
+std::optional<Vec3> center_of_immersion(const std::vector<TriangleState>& states) {
+  double vw = 0.0;
+  Vec3 m;
+  for (const auto& s : states) {
+    if (s.status != TriStatus::Submerged) continue;
+    const double w = s.area * s.depth * s.normal.y;
+    vw += w;
+    m += Vec3{s.centroid.x, s.centroid.y - 0.5 * s.depth, s.centroid.z} * w;
+  }
+  if (!(vw > 1e-12)) return std::nullopt;
+  return m / vw;
+}
+Vec3 buoyancy(double v_w, double rho, const Vec3& gravity) { return -(v_w * rho) * gravity; }
+Vec3 drag(const TriangleState& tri, const Vec3& medium, double rho, double c_d, const BodyPose& pose) {
+  const Vec3 rel = pose.point_velocity(tri.centroid) - medium;
+  const double speed = rel.norm();
+  if (speed < 1e-12 || tri.area <= 0.0) return {};
+  const double facing = dot(tri.normal, rel / speed);
+  if (facing <= 0.0) return {};
+  return -(0.5 * c_d * rho * tri.area * facing * speed) * rel;
+}
+
+// ============================================================ interactive
+double damping_factor(double speed, const DampingParams& p) {
+  return ocn_damping_factor(speed, p.d0, p.d_max, p.v_max);
+}
+void FdmConfig::validate() const {
+  if (grid_size < 8) throw ConfigError("FDM grid size too small");
+  if (margin <= 1 || 2 * margin >= grid_size) throw ConfigError("FDM margin must satisfy 1 < m < grid_size/2");
+}
+double mask_height(double x, double z, const MaskFrame& f, double speed, const MaskParams& p) {
+  if (!(f.half_beam > 0.0) || !(f.z_max > f.z_min)) throw DomainError("mask_height: degenerate body frame");
+  const double fx = std::fabs(x - f.center_x) / f.half_beam;
+  const double h_f = speed * f.mesh_height * p.intensity * f.volume_ratio;
+  const double a = (h_f - p.back_height) / (f.z_max - f.z_min);
+  const double b = p.back_height - a * f.z_min;
+  return p.amplitude * (fx + a * z + b);
+}
+
+namespace {
+ocn_zone_state zone_state(const detail::ZoneHandle& h) {
+  ocn_zone_state s{};
+  OCN_CALL(ocn_zone_get_state(h.h, &s));
+  return s;
+}
+}  // namespace
+
+FdmZone::FdmZone(const FdmConfig& config, double body_size, Vec2 body_position, double dt) : config_(config) {
+  config.validate();
+  ocn_fdm_config c{};
+  c.grid_size = config.grid_size;
+  c.margin = config.margin;
+  c.delta_min = config.delta_min;
+  c.delta_max = config.delta_max;
+  c.delta_rate_limit = config.delta_rate_limit;
+  c.d0 = config.damping.d0;
+  c.d_max = config.damping.d_max;
+  c.v_max = config.damping.v_max;
+  dev_ = std::make_shared<detail::ZoneHandle>();
+  OCN_CALL(ocn_zone_create(device_context(), &c, body_size, body_position.x, body_position.z, dt, &dev_->h));
+  const ocn_zone_state s = zone_state(*dev_);
+  config_.delta_min = s.delta_min;
+  config_.delta_max = s.delta_max;
+}
+int FdmZone::grid_size() const { return config_.grid_size; }
+int FdmZone::margin() const { return config_.margin; }
+double FdmZone::spacing() const { return zone_state(*dev_).spacing; }
+double FdmZone::wave_speed() const { return zone_state(*dev_).wave_speed; }
+double FdmZone::current_damping() const { return zone_state(*dev_).damping; }
+Vec2 FdmZone::origin() const {
+  const auto s = zone_state(*dev_);
+  return {s.origin[0], s.origin[1]};
+}
+int FdmZone::dropped_wake_count() const { return zone_state(*dev_).dropped_wake; }
+const RealField& FdmZone::field() const {
+  host_ = RealField(config_.grid_size);
+  OCN_CALL(ocn_zone_download(dev_->h, host_.data(), nullptr));
+  return host_;
+}
+void FdmZone::set_field(const RealField& f) {
+  if (f.size() != config_.grid_size) throw ConfigError("FdmZone::set_field: size mismatch");
+  OCN_CALL(ocn_zone_upload(dev_->h, f.data(), nullptr));
+}
+void FdmZone::update_stability(double speed, double dt) { OCN_CALL(ocn_zone_update_stability(dev_->h, speed, dt)); }
+void FdmZone::step(double dt, Vec2 p) { OCN_CALL(ocn_zone_step(dev_->h, dt, p.x, p.z)); }
+void FdmZone::apply_mask(const std::vector<MaskCell>& cells) {
+  std::vector<int32_t> ij;
+  std::vector<double> h;
+  for (const auto& c : cells) ij.push_back(c.i), ij.push_back(c.j), h.push_back(c.height);
+  OCN_CALL(ocn_zone_apply_cells(dev_->h, static_cast<int>(cells.size()), ij.data(), h.data()));
+}
+double FdmZone::sample(Vec2 world) const {
+  double xz[2] = {world.x, world.z}, out = 0.0;
+  OCN_CALL(ocn_zone_sample(dev_->h, 1, xz, &out));
+  return out;
+}
+ocn_zone* FdmZone::device_handle() const { return dev_->h; }
+
+std::vector<MaskCell> compute_mask(const FdmZone& zone, const std::vector<std::vector<Vec3>>& loops,
+                                   double yaw, Vec2 pos, double speed, const MaskFrame& frame,
+                                   const MaskParams& params) {
+  std::vector<int32_t> off = {0};
+  std::vector<double> pts;
+  for (const auto& l : loops) {
+    for (const Vec3& p : l) pts.push_back(p.x), pts.push_back(p.y), pts.push_back(p.z);
+    off.push_back(off.back() + static_cast<int32_t>(l.size()));
+  }
+  ocn_mask_frame f{frame.center_x, frame.half_beam, frame.z_min, frame.z_max, frame.mesh_height,
+                   frame.volume_ratio};
+  ocn_mask_params mp{params.back_height, params.intensity, params.amplitude};
+  int n = 0;
+  OCN_CALL(ocn_zone_compute_mask(zone.device_handle(), static_cast<int>(loops.size()), off.data(),
+                                 pts.empty() ? nullptr : pts.data(), yaw, pos.x, pos.z, speed, &f, &mp, 0, &n));
+  std::vector<int32_t> ij(2 * std::max(n, 1));
+  std::vector<double> h(std::max(n, 1));
+  OCN_CALL(ocn_zone_mask_download(zone.device_handle(), n, ij.data(), h.data(), &n));
+  std::vector<MaskCell> cells(n);
+  for (int q = 0; q < n; ++q) cells[q] = {ij[2 * q], ij[2 * q + 1], h[q]};
+  return cells;
+}
+
+bool point_in_loops(Vec2 p, const std::vector<std::vector<Vec2>>& loops) {
+  int crossings = 0;
+  for (const auto& loop : loops)
+    for (size_t e = 0; e + 1 < loop.size(); ++e) {
+      const Vec2 a = loop[e], b = loop[e + 1];
+      if ((a.x > p.x) == (b.x > p.x)) continue;
+      if (a.z + (p.x - a.x) / (b.x - a.x) * (b.z - a.z) > p.z) ++crossings;
+    }
+  return crossings & 1;
+}
+
+}  // namespace ocean

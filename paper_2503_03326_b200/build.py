@@ -21,6 +21,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "lib", "libocean_b200.so")
+API_LIB = os.path.join(PKG, "lib", "libocean_api.so")
+API_TEST = os.path.join(OBJ, "test_api")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
@@ -55,7 +57,33 @@ def build(force: bool = False, jobs: int = 8) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    build_api(force)
     return LIB
+
+
+def build_api(force: bool = False) -> str:
+    """The C++ drop-in API (include/ocean/*.hpp) over the C-ABI + its test program."""
+    srcs = sorted(glob.glob(os.path.join(PKG, "api", "*.cpp")))
+    hdrs = glob.glob(os.path.join(ROOT, "include", "ocean", "*.hpp"))
+    newest = max([os.path.getmtime(f) for f in srcs + hdrs] + [os.path.getmtime(LIB)])
+    if force or not os.path.exists(API_LIB) or os.path.getmtime(API_LIB) < newest:
+        cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-I" + os.path.join(ROOT, "include"),
+               *srcs, "-L" + os.path.dirname(LIB), "-locean_b200", "-Wl,-rpath,$ORIGIN",
+               "-o", API_LIB]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"C++ API build failed:\n{r.stderr}")
+    test_src = os.path.join(ROOT, "tests", "cpp", "test_api.cpp")
+    if os.path.exists(test_src) and (force or not os.path.exists(API_TEST) or
+                                     os.path.getmtime(API_TEST) < max(newest, os.path.getmtime(test_src),
+                                                                      os.path.getmtime(API_LIB))):
+        cmd = ["g++", "-std=c++20", "-O2", "-I" + os.path.join(ROOT, "include"), test_src,
+               "-L" + os.path.dirname(LIB), "-locean_api", "-locean_b200",
+               "-Wl,-rpath,$ORIGIN/../lib", "-o", API_TEST]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"C++ API test build failed:\n{r.stderr}")
+    return API_LIB
 
 
 if __name__ == "__main__":

@@ -131,6 +131,42 @@ __global__ void k_grid_extras(int n, double dk, double g, const double2* h0, dou
   }
 }
 
+// assemble_coefficients (surface.cpp:39-68) in fp64 for the drop-in API
+__global__ void k_assemble_coef(int n, double dk, double g, double t, double chop,
+                                const double2* h0, const uint8_t* band, double2* out) {
+  const size_t nn = (size_t)n * n;
+  for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < nn;
+       q += (size_t)gridDim.x * blockDim.x) {
+    double2 f[8];
+    for (int m = 0; m < 8; ++m) f[m] = make_double2(0.0, 0.0);
+    if (band[q]) {
+      const int i = (int)(q / n), j = (int)(q % n);
+      const int ni = i == 0 ? 0 : n - i, nj = j == 0 ? 0 : n - j;
+      const double kx = dk * (i - n / 2), kz = dk * (j - n / 2);
+      const double k = sm::hypot_ref(kx, kz);
+      const double w = sqrt(g * k);
+      double sn, cs;
+      sincos(w * t, &sn, &cs);
+      const double2 a = h0[q], bm = h0[(size_t)ni * n + nj];
+      const double2 b = make_double2(bm.x, -bm.y);  // conj(h0(-k))
+      const double htr = (a.x * cs - a.y * sn) + (b.x * cs + b.y * sn);
+      const double hti = (a.x * sn + a.y * cs) + (b.y * cs - b.x * sn);
+      const double ux = kx / k, uz = kz / k;
+      const double2 dx = make_double2(-ux * hti * chop, ux * htr * chop);
+      const double2 dz = make_double2(-uz * hti * chop, uz * htr * chop);
+      f[0] = make_double2(htr, hti);
+      f[1] = dx;
+      f[2] = dz;
+      f[3] = make_double2(kx * dx.y, -kx * dx.x);   // (0, -kx) * Dx
+      f[4] = make_double2(kx * dz.y, -kx * dz.x);   // (0, -kx) * Dz
+      f[5] = make_double2(kz * dz.y, -kz * dz.x);   // (0, -kz) * Dz
+      f[6] = make_double2(-kx * hti, kx * htr);     // (0, kx) * h~
+      f[7] = make_double2(-kz * hti, kz * htr);     // (0, kz) * h~
+    }
+    for (int m = 0; m < 8; ++m) out[(size_t)m * nn + q] = f[m];
+  }
+}
+
 // ------------------------------------------------------------------ evolve
 // h~ and G (surface.cpp:49-50; velocity.cpp:16-20) at time t, one cascade.
 __global__ void k_set_time(double* d_time, double t) { *d_time = t; }
@@ -809,6 +845,7 @@ void spectral_step(ocn_cascades* cas, ocn_maps* maps, ocn_slices* slices, double
                    double choppiness) {
   ocn_ctx* ctx = cas->ctx;
   DeviceScope ds(ctx);
+  OCN_REQUIRE(cas->h0.p, "these maps carry no spectrum (ocn_maps_create_bare)");
   SpectralPlan* plan = get_plan(cas, maps, slices);
   k_set_time<<<1, 1, 0, ctx->stream>>>(cas->d_time.p, t);
   OCN_LAUNCHED(ctx);
@@ -1159,6 +1196,22 @@ int ocn_cascades_download(ocn_cascades* c, int grid, double* h0, double* h0cn, u
   });
 }
 
+int ocn_assemble_coefficients(ocn_cascades* c, int grid, double t, double chop, double* out) {
+  return api_call(c ? c->ctx : nullptr, [&] {
+    OCN_REQUIRE(c && out && grid >= 0 && grid < c->count, "bad arguments");
+    ocn_ctx* ctx = c->ctx;
+    DeviceScope ds(ctx);
+    const size_t nn = (size_t)c->n * c->n;
+    DevBuf<double2> d(8 * nn);
+    k_assemble_coef<<<grid_for(ctx, nn), 256, 0, ctx->stream>>>(
+        c->n, 2.0 * kPi / c->lengths[grid], c->params.gravity, t, chop,
+        c->h0_f64.p + (size_t)grid * nn, c->in_band.p + (size_t)grid * nn, d.p);
+    OCN_LAUNCHED(ctx);
+    OCN_CUDA(cudaMemcpyAsync(out, d.p, 8 * nn * sizeof(double2), cudaMemcpyDeviceToHost, ctx->stream));
+    OCN_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
 // ---- maps
 int ocn_maps_create(ocn_cascades* c, ocn_maps** out) {
   return api_call(c ? c->ctx : nullptr, [&] {
@@ -1224,6 +1277,55 @@ int ocn_maps_download_f32(ocn_maps* m, int cascade, int field, float* out) {
     const size_t nn = (size_t)m->cas->n * m->cas->n;
     OCN_CUDA(cudaMemcpyAsync(out, m->field(cascade, field), nn * sizeof(float),
                              cudaMemcpyDeviceToHost, ctx->stream));
+    OCN_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+__global__ void k_f64_to_f32_s(size_t n, const double* in, float* out) {
+  for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n;
+       q += (size_t)gridDim.x * blockDim.x)
+    out[q] = (float)in[q];
+}
+
+int ocn_maps_create_bare(ocn_ctx* ctx, int n, int count, const double* lengths, ocn_maps** out) {
+  return api_call(ctx, [&] {
+    OCN_REQUIRE(ctx && lengths && out, "null argument");
+    OCN_REQUIRE(count >= 1 && count <= kMaxCascades, "cascade count %d out of range", count);
+    if (!is_pow2(n) || n < 2) fail(OCN_ERR_CONFIG, "grid resolution must be a power of two >= 2");
+    DeviceScope ds(ctx);
+    // a spectrum-less cascade set carrying only the tile geometry
+    auto cas = std::make_unique<ocn_cascades>();
+    cas->ctx = ctx;
+    cas->n = n;
+    cas->count = count;
+    cas->lengths.assign(lengths, lengths + count);
+    cas->band_min.assign(count, 0.0);
+    cas->band_max.assign(count, 1e300);
+    for (int c = 0; c < count; ++c) cas->cascade_index.push_back((uint32_t)c);
+    cas->params.gravity = kGravity;
+    ctx_retain(ctx);
+    auto m = std::make_unique<ocn_maps>();
+    m->cas = cas.release();
+    m->fields.alloc((size_t)n * n * 8 * count);
+    OCN_CUDA(cudaMemsetAsync(m->fields.p, 0, m->fields.bytes(), ctx->stream));
+    ++m->cas->refs;
+    ocn_cascades* bare = m->cas;
+    *out = m.release();
+    ocn_cascades_destroy(bare);  // the maps now hold the only reference
+  });
+}
+
+int ocn_maps_upload(ocn_maps* m, int cascade, int field, const double* in) {
+  return api_call(m ? m->cas->ctx : nullptr, [&] {
+    OCN_REQUIRE(m && in && cascade >= 0 && cascade < m->cas->count && field >= 0 && field < 8,
+                "bad maps upload arguments");
+    ocn_ctx* ctx = m->cas->ctx;
+    DeviceScope ds(ctx);
+    const size_t nn = (size_t)m->cas->n * m->cas->n;
+    DevBuf<double> tmp(nn);
+    OCN_CUDA(cudaMemcpyAsync(tmp.p, in, nn * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    k_f64_to_f32_s<<<grid_for(ctx, nn), 256, 0, ctx->stream>>>(nn, tmp.p, m->field(cascade, field));
+    OCN_LAUNCHED(ctx);
     OCN_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }

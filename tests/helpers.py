@@ -33,8 +33,11 @@ def pose_from_array(a):
 
 def normwise_rel(a, b):
     """max|a - b| / max|b| (SURVEY 8d tolerance definition)."""
-    a = np.asarray(a, np.float64)
-    b = np.asarray(b, np.float64)
+    a = np.asarray(a)
+    b = np.asarray(b)
+    if not (np.iscomplexobj(a) or np.iscomplexobj(b)):
+        a = a.astype(np.float64)
+        b = b.astype(np.float64)
     den = np.abs(b).max()
     return float(np.abs(a - b).max() / (den if den > 0 else 1.0))
 
