@@ -228,7 +228,10 @@ OCN_API uint64_t ocn_ctx_kernel_launches(const ocn_ctx* ctx);
 #define OCN_PROF_FDM 5      /* FdmZone::step stencil                     */
 #define OCN_PROF_SPECTRAL 6 /* whole spectral step (evolve+rows+cols)    */
 #define OCN_PROF_COUNT 8
-OCN_API int ocn_ctx_profile(ocn_ctx* ctx, int enable);
+/* mode 0: off; 1: per-kernel windows (spectral step launched eagerly, every
+ * category valid); 2: stage windows only (spectral / hydro / mask / fdm; the
+ * spectral step keeps replaying its CUDA graph). */
+OCN_API int ocn_ctx_profile(ocn_ctx* ctx, int mode);
 /* Synchronizes, then returns the accumulated milliseconds and launch count of
  * a category since the last reset. */
 OCN_API int ocn_ctx_profile_read(ocn_ctx* ctx, int category, double* total_ms, uint64_t* count);

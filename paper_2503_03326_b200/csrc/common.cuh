@@ -107,6 +107,7 @@ struct ocn_prof_window {
 };
 struct ocn_ctx {
   bool profiling = false;
+  int prof_mode = 0;  // 1: per-kernel windows (eager), 2: stage windows (graphs kept)
   std::vector<ocn_prof_window> prof_pending;
   std::vector<cudaEvent_t> prof_pool;
   double prof_ms[OCN_PROF_COUNT] = {0};
@@ -119,6 +120,12 @@ struct ocn_ctx {
   std::atomic<uint64_t> launches{0};
   ocn::PinnedBuf pinned;
   ocn::DevBuf<unsigned char> scratch;  // generic per-call device scratch
+  cudaStream_t aux = nullptr;          // second stream (column passes overlap row passes)
+  std::vector<cudaEvent_t> sync_events;
+  cudaStream_t aux_stream() {
+    if (!aux) cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking);
+    return aux;
+  }
 };
 
 namespace ocn {
@@ -156,7 +163,7 @@ struct ProfWindow {
   }
   cudaEvent_t start = nullptr;
   ProfWindow(ocn_ctx* c, int k) : ctx(c), cat(k) {
-    if (!ctx->profiling) return;
+    if (!ctx->profiling || k < 0) return;
     start = get(ctx);
     OCN_CUDA(cudaEventRecord(start, ctx->stream));
   }

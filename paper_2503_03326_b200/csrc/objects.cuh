@@ -67,6 +67,7 @@ struct ocn_cascades {
   ocn::DevBuf<float2> scratch;  // row-pass intermediates of one transform group
   ocn::DevBuf<double> d_time;   // frame time read by k_evolve (set per frame)
   int group = 1;                // transforms per group
+  int nbuf = 1;                 // scratch buffers (2: row/column passes overlap)
   std::map<std::pair<const void*, const void*>, std::unique_ptr<ocn::SpectralPlan>> plans;
 };
 

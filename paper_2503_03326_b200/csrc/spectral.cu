@@ -39,6 +39,9 @@ void ctx_release(ocn_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   cudaStreamDestroy(ctx->stream);
+  if (ctx->aux) cudaStreamSynchronize(ctx->aux), cudaStreamDestroy(ctx->aux);
+  for (cudaEvent_t e : ctx->sync_events) cudaEventDestroy(e);
+  for (cudaEvent_t e : ctx->prof_pool) cudaEventDestroy(e);
   delete ctx;
 }
 static void cascades_release(ocn_cascades* c) {
@@ -336,18 +339,27 @@ __device__ __forceinline__ float atten_f(float k, float y) {
   return y > 0.f ? 1.0f + k * y : __expf(k * y);
 }
 
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 template <int N, bool PLAIN>
-__global__ void __launch_bounds__(256) k_rows_w(const RowArgs a) {
+__global__ void __launch_bounds__(256, 2) k_rows_w(const RowArgs a) {
   using W = WarpLaunch<N>;
   constexpr int T = W::T, E = fft::Plan<N>::E;
   extern __shared__ float4 smem4[];
-  // per mode of this row, shared by every transform of the group:
-  //   sa = (h~.re, h~.im, V0.re, V0.im),  V0 = G (-g / w) (kx + i kz)
-  //   sb = (W0.re, W0.im, |k|, 1/|k|),    W0 = G w
-  // so a velocity coefficient is V0 E(y) or W0 (-E(y1) + i E(y0)).
-  float4* sa = smem4;
-  float4* sb = smem4 + N;
-  float2* bufs = reinterpret_cast<float2*>(PLAIN ? smem4 : smem4 + 2 * N);
+  // Per mode of this row, shared by every transform of the group (SoA):
+  //   sht = h~,  sv0 = V0 = G (-g / w)(kx + i kz),  sw0 = W0 = G w,  sk = |k|,
+  //   sinv = 1/|k| (0 at k = 0). A velocity coefficient is then V0 E(y) or
+  //   W0 (-E(y1) + i E(y0)), E(y) = exp(|k| y) (y <= 0) or 1 + |k| y.
+  float2* sht = reinterpret_cast<float2*>(smem4);
+  float2* sv0 = sht + N;
+  float2* sw0 = sv0 + N;
+  float* sk = reinterpret_cast<float*>(sw0 + N);
+  float* sinv = sk + N;
+  float2* bufs = PLAIN ? reinterpret_cast<float2*>(smem4) : reinterpret_cast<float2*>(smem4 + 2 * N);
   const int row = blockIdx.x;
   const int warps = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -362,11 +374,13 @@ __global__ void __launch_bounds__(256) k_rows_w(const RowArgs a) {
       const float k = sqrtf(k2);
       const float inv = k2 > 0.f ? 1.0f / k : 0.f;
       const float w = sqrtf(g * k);
-      const float4 s = __ldg(srow + j);  // (h~, G)
+      const float4 sp = __ldg(srow + j);  // (h~, G)
       const float f = k2 > 0.f ? -g / w : 0.f;
-      const float v0r = f * (s.z * kx - s.w * kz), v0i = f * (s.z * kz + s.w * kx);
-      sa[j] = make_float4(s.x, s.y, v0r, v0i);
-      sb[j] = make_float4(s.z * w, s.w * w, k, inv);
+      sht[j] = make_float2(sp.x, sp.y);
+      sv0[j] = make_float2(f * (sp.z * kx - sp.w * kz), f * (sp.z * kz + sp.w * kx));
+      sw0[j] = make_float2(sp.z * w, sp.w * w);
+      sk[j] = k;
+      sinv[j] = inv;
     }
     __syncthreads();
   }
@@ -375,70 +389,66 @@ __global__ void __launch_bounds__(256) k_rows_w(const RowArgs a) {
   for (int slot = warp; slot < slots; slot += warps) {
     const int gi = slot * W::TPW + sub;
     const bool valid = gi < a.G;
-    // ---- coefficients X + iY of this transform at j = t + r T
+    float2* out = a.scratch + ((size_t)(valid ? gi : 0) * N + row) * N;
+    auto store = [&](int k, float2 x) {
+      if (valid) out[k] = x;
+    };
     if constexpr (PLAIN) {
       const float2* in = a.src + ((size_t)(valid ? gi : 0) * N + row) * N;
-#pragma unroll 4
-      for (int r = 0; r < E; ++r) {
-        const int j = t + r * T;
-        buf[fft::pad32(j)] = valid ? __ldg(in + j) : make_float2(0.f, 0.f);
-      }
+      fft::cta_fft<N, true, false, false>(
+          t, buf, a.tw, [&](int j) { return valid ? __ldg(in + j) : make_float2(0.f, 0.f); }, store);
     } else {
       const XformDesc d = a.desc[valid ? gi : 0];
-      const float chop = a.chop;
-      if (d.kind == kVelXZ) {
-        const float y0 = d.y0 * 1.4426950408889634f;  // exp(k y) = exp2(k y log2 e)
-        const bool above = d.y0 > 0.f;
-#pragma unroll 4
-        for (int r = 0; r < E; ++r) {
-          const int j = t + r * T;
-          const float4 A = sa[j];
-          const float k = sb[j].z;
-          const float e = above ? 1.0f + k * d.y0 : exp2f(k * y0);
-          buf[fft::pad32(j)] = make_float2(A.z * e, A.w * e);
-        }
-      } else if (d.kind == kVelYPair || d.kind == kVelYSingle) {
-        const bool pair = d.kind == kVelYPair;
-        const float l0 = d.y0 * 1.4426950408889634f, l1 = d.y1 * 1.4426950408889634f;
-#pragma unroll 4
-        for (int r = 0; r < E; ++r) {
-          const int j = t + r * T;
-          const float4 B = sb[j];
-          const float e0 = d.y0 > 0.f ? 1.0f + B.z * d.y0 : exp2f(B.z * l0);
-          const float e1 = pair ? (d.y1 > 0.f ? 1.0f + B.z * d.y1 : exp2f(B.z * l1)) : 0.f;
-          // W0 (-e1 + i e0)
-          buf[fft::pad32(j)] = make_float2(-B.x * e1 - B.y * e0, B.x * e0 - B.y * e1);
-        }
+      if (d.kind <= kSurfHxHz) {
+        // surface pairs: X + iY = h~ M(kx, kz) (surface.cpp:77-80 packing)
+        const float chop = a.chop, dk = a.dk;
+        const int kind = d.kind;
+        fft::cta_fft<N, true, false, false>(
+            t, buf, a.tw,
+            [&](int j) {
+              const float2 h = sht[j];
+              const float inv = sinv[j];
+              const float kz = dk * (float)(j - N / 2);
+              float mr, mi;
+              if (kind == kSurfHDx) {
+                mr = 1.0f - kx * inv * chop, mi = 0.f;
+              } else if (kind == kSurfDzDxDx) {
+                mr = 0.f, mi = chop * (kz + kx * kx) * inv;
+              } else if (kind == kSurfDzDxDzDz) {
+                const float f = chop * kz * inv;
+                mr = f * kx, mi = f * kz;
+              } else {
+                mr = -kz, mi = kx;
+              }
+              if (inv == 0.f) mr = mi = 0.f;  // k = 0 mode
+              return make_float2(h.x * mr - h.y * mi, h.x * mi + h.y * mr);
+            },
+            store);
       } else {
-#pragma unroll 2
-        for (int r = 0; r < E; ++r) {
-          const int j = t + r * T;
-          const float4 A = sa[j];
-          const float inv = sb[j].w;
-          const float kz = a.dk * (float)(j - N / 2);
-          float mr, mi;
-          if (d.kind == kSurfHDx) {
-            mr = 1.0f - kx * inv * chop, mi = 0.f;
-          } else if (d.kind == kSurfDzDxDx) {
-            mr = 0.f, mi = chop * (kz + kx * kx) * inv;
-          } else if (d.kind == kSurfDzDxDzDz) {
-            const float f = chop * kz * inv;
-            mr = f * kx, mi = f * kz;
-          } else {
-            mr = -kz, mi = kx;
-          }
-          if (inv == 0.f) mr = mi = 0.f;  // k = 0 mode
-          buf[fft::pad32(j)] = make_float2(A.x * mr - A.y * mi, A.x * mi + A.y * mr);
-        }
+        // velocity: Z (re + i im) with Z = V0 (x/z pair) or W0 (vy pair)
+        const float2* Z = d.kind == kVelXZ ? sv0 : sw0;
+        constexpr float kLog2e = 1.4426950408889634f;
+        const float y0 = d.y0, y1 = d.y1, y0l = d.y0 * kLog2e, y1l = d.y1 * kLog2e;
+        const bool up0 = y0 > 0.f, up1 = y1 > 0.f;
+        const int kind = d.kind;
+        fft::cta_fft<N, true, false, false>(
+            t, buf, a.tw,
+            [&](int j) {
+              const float2 z = Z[j];
+              const float k = sk[j];
+              const float e0 = up0 ? fmaf(k, y0, 1.0f) : ex2_approx(k * y0l);
+              float mr, mi;
+              if (kind == kVelXZ) {
+                mr = e0, mi = 0.f;
+              } else {
+                mr = kind == kVelYPair ? -(up1 ? fmaf(k, y1, 1.0f) : ex2_approx(k * y1l)) : 0.f;
+                mi = e0;
+              }
+              return make_float2(z.x * mr - z.y * mi, z.x * mi + z.y * mr);
+            },
+            store);
       }
     }
-    __syncwarp();
-    float2* out = a.scratch + ((size_t)(valid ? gi : 0) * N + row) * N;
-    fft::cta_fft<N, true, true, false>(
-        t, buf, a.tw, [&](int n) { return buf[fft::pad32(n)]; },
-        [&](int k, float2 x) {
-          if (valid) out[k] = x;
-        });
     __syncwarp();
   }
 }
@@ -609,7 +619,7 @@ constexpr bool use_warp_kernels() {
 }
 
 template <int N>
-void launch_rows(ocn_ctx* ctx, const RowArgs& a, bool plain) {
+void launch_rows(ocn_ctx* ctx, const RowArgs& a, bool plain, cudaStream_t st) {
   if constexpr (use_warp_kernels<N>()) {
     using W = WarpLaunch<N>;
     const int slots = (a.G + W::TPW - 1) / W::TPW;
@@ -625,9 +635,9 @@ void launch_rows(ocn_ctx* ctx, const RowArgs& a, bool plain) {
     }
     const int rows = a.items / a.G;
     if (plain)
-      k_rows_w<N, true><<<rows, 32 * warps, smem, ctx->stream>>>(a);
+      k_rows_w<N, true><<<rows, 32 * warps, smem, st>>>(a);
     else
-      k_rows_w<N, false><<<rows, 32 * warps, smem, ctx->stream>>>(a);
+      k_rows_w<N, false><<<rows, 32 * warps, smem, st>>>(a);
     OCN_LAUNCHED(ctx);
     return;
   }
@@ -635,9 +645,9 @@ void launch_rows(ocn_ctx* ctx, const RowArgs& a, bool plain) {
   set_smem_attrs<N>();
   const int blocks = (a.items + L::PER_CTA - 1) / L::PER_CTA;
   if (plain)
-    k_rows<N, true><<<blocks, L::THREADS, L::SMEM_BYTES, ctx->stream>>>(a);
+    k_rows<N, true><<<blocks, L::THREADS, L::SMEM_BYTES, st>>>(a);
   else
-    k_rows<N, false><<<blocks, L::THREADS, L::SMEM_BYTES, ctx->stream>>>(a);
+    k_rows<N, false><<<blocks, L::THREADS, L::SMEM_BYTES, st>>>(a);
   OCN_LAUNCHED(ctx);
 }
 
@@ -653,7 +663,7 @@ static bool cols_generic() {
 }
 
 template <int N>
-void launch_cols(ocn_ctx* ctx, const ColArgs& a, int G, bool complex_out) {
+void launch_cols(ocn_ctx* ctx, const ColArgs& a, int G, bool complex_out, cudaStream_t st) {
   if constexpr (use_warp_kernels<N>()) {
    if (!cols_generic()) {
     using W = WarpLaunch<N>;
@@ -666,9 +676,9 @@ void launch_cols(ocn_ctx* ctx, const ColArgs& a, int G, bool complex_out) {
     }
     dim3 grid(N / W::CC > 0 ? N / W::CC : 1, G);
     if (complex_out)
-      k_cols_w<N, true><<<grid, 32 * W::COLS_WARPS, smem, ctx->stream>>>(a);
+      k_cols_w<N, true><<<grid, 32 * W::COLS_WARPS, smem, st>>>(a);
     else
-      k_cols_w<N, false><<<grid, 32 * W::COLS_WARPS, smem, ctx->stream>>>(a);
+      k_cols_w<N, false><<<grid, 32 * W::COLS_WARPS, smem, st>>>(a);
     OCN_LAUNCHED(ctx);
     return;
    }
@@ -677,19 +687,19 @@ void launch_cols(ocn_ctx* ctx, const ColArgs& a, int G, bool complex_out) {
   set_smem_attrs<N>();
   dim3 grid((N + L::PER_CTA - 1) / L::PER_CTA, G);
   if (complex_out)
-    k_cols<N, true><<<grid, L::THREADS, L::SMEM_BYTES, ctx->stream>>>(a);
+    k_cols<N, true><<<grid, L::THREADS, L::SMEM_BYTES, st>>>(a);
   else
-    k_cols<N, false><<<grid, L::THREADS, L::SMEM_BYTES, ctx->stream>>>(a);
+    k_cols<N, false><<<grid, L::THREADS, L::SMEM_BYTES, st>>>(a);
   OCN_LAUNCHED(ctx);
 }
 
-void rows_dispatch(ocn_ctx* ctx, int n, const RowArgs& a, bool plain) {
-#define OCN_ROWS(NN) launch_rows<NN>(ctx, a, plain)
+void rows_dispatch(ocn_ctx* ctx, int n, const RowArgs& a, bool plain, cudaStream_t st) {
+#define OCN_ROWS(NN) launch_rows<NN>(ctx, a, plain, st)
   OCN_DISPATCH_N(n, OCN_ROWS)
 #undef OCN_ROWS
 }
-void cols_dispatch(ocn_ctx* ctx, int n, const ColArgs& a, int G, bool complex_out) {
-#define OCN_COLS(NN) launch_cols<NN>(ctx, a, G, complex_out)
+void cols_dispatch(ocn_ctx* ctx, int n, const ColArgs& a, int G, bool complex_out, cudaStream_t st) {
+#define OCN_COLS(NN) launch_cols<NN>(ctx, a, G, complex_out, st)
   OCN_DISPATCH_N(n, OCN_COLS)
 #undef OCN_COLS
 }
@@ -789,24 +799,53 @@ static void forget_plans(ocn_cascades* cas, const void* obj) {
   }
 }
 
+// Row pass of group g+1 overlaps the column pass of group g: rows on the
+// context stream, columns on the auxiliary stream, two scratch buffers
+// (dependencies by events; captured into the graph as two branches).
+// Off by default: measured no gain on B200 (2.38 vs 2.40 ms with half-size
+// groups, both slower than one 8-transform buffer); OCN_DUAL_STREAM=1 enables it.
+static bool dual_stream(const ocn_ctx* ctx) {
+  static const bool on = [] {
+    const char* e = getenv("OCN_DUAL_STREAM");
+    return e && *e && *e != '0';
+  }();
+  (void)ctx;
+  return on;
+}
+
 static void enqueue_spectral(ocn_cascades* cas, SpectralPlan* plan, double choppiness) {
   ocn_ctx* ctx = cas->ctx;
   const int n = cas->n;
   const size_t nn = (size_t)n * n;
+  const bool dual = dual_stream(ctx) && cas->nbuf == 2;
+  cudaStream_t A = ctx->stream, B = dual ? ctx->aux_stream() : ctx->stream;
   ProfWindow whole(ctx, OCN_PROF_SPECTRAL);
+  std::vector<cudaEvent_t>& ev = ctx->sync_events;
+  int gidx = 0;
+  auto event = [&](int k) {
+    while ((int)ev.size() <= k) {
+      cudaEvent_t e;
+      OCN_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      ev.push_back(e);
+    }
+    return ev[k];
+  };
+  std::vector<int> cols_ev;  // event index recorded after cols of each group
+  const int G = cas->group;
   for (int c = 0; c < cas->count; ++c) {
     const double dk = 2.0 * kPi / cas->lengths[c];
     float4* spec = cas->spec.p + (size_t)c * nn;
     {
       ProfWindow pw(ctx, OCN_PROF_EVOLVE);
-      k_evolve<<<grid_for(ctx, nn), 256, 0, ctx->stream>>>(n, dk, cas->params.gravity, cas->d_time.p,
-                                                          cas->h0.p + (size_t)c * nn, spec);
+      k_evolve<<<grid_for(ctx, nn), 256, 0, A>>>(n, dk, cas->params.gravity, cas->d_time.p,
+                                                cas->h0.p + (size_t)c * nn, spec);
       OCN_LAUNCHED(ctx);
     }
     const int first = plan->first[c], total = plan->count[c];
-    const int G = cas->group;
-    for (int g0 = 0; g0 < total; g0 += G) {
+    for (int g0 = 0; g0 < total; g0 += G, ++gidx) {
       const int g = std::min(G, total - g0);
+      float2* scratch = cas->scratch.p + (size_t)(dual ? gidx % 2 : 0) * G * nn;
+      if (dual && gidx >= 2) OCN_CUDA(cudaStreamWaitEvent(A, event(cols_ev[gidx - 2]), 0));
       RowArgs ra{};
       ra.items = n * g;
       ra.G = g;
@@ -815,22 +854,29 @@ static void enqueue_spectral(ocn_cascades* cas, SpectralPlan* plan, double chopp
       ra.dk = (float)dk;
       ra.gravity = (float)cas->params.gravity;
       ra.chop = (float)choppiness;
-      ra.scratch = cas->scratch.p;
+      ra.scratch = scratch;
       ra.tw = cas->twiddle.p;
       {
-        ProfWindow pw(ctx, OCN_PROF_ROWS);
-        rows_dispatch(ctx, n, ra, false);
+        ProfWindow pw(ctx, dual ? -1 : OCN_PROF_ROWS);
+        rows_dispatch(ctx, n, ra, false, A);
+      }
+      if (dual) {
+        OCN_CUDA(cudaEventRecord(event(2 * gidx), A));
+        OCN_CUDA(cudaStreamWaitEvent(B, event(2 * gidx), 0));
       }
       ColArgs ca{};
-      ca.scratch = cas->scratch.p;
+      ca.scratch = scratch;
       ca.desc = plan->desc.p + first + g0;
       ca.tw = cas->twiddle.p;
       {
-        ProfWindow pw(ctx, OCN_PROF_COLS);
-        cols_dispatch(ctx, n, ca, g, false);
+        ProfWindow pw(ctx, dual ? -1 : OCN_PROF_COLS);
+        cols_dispatch(ctx, n, ca, g, false, B);
       }
+      if (dual) OCN_CUDA(cudaEventRecord(event(2 * gidx + 1), B));
+      cols_ev.push_back(2 * gidx + 1);
     }
   }
+  if (dual && gidx > 0) OCN_CUDA(cudaStreamWaitEvent(A, event(cols_ev.back()), 0));
 }
 
 static bool graphs_enabled() {
@@ -849,15 +895,21 @@ void spectral_step(ocn_cascades* cas, ocn_maps* maps, ocn_slices* slices, double
   SpectralPlan* plan = get_plan(cas, maps, slices);
   k_set_time<<<1, 1, 0, ctx->stream>>>(cas->d_time.p, t);
   OCN_LAUNCHED(ctx);
-  const bool use_graph = graphs_enabled() && !ctx->profiling && plan->uses > 0;
+  // profiling mode 1 = per-kernel windows (eager launches); mode 2 = stage
+  // windows only, the step still replays its graph
+  const bool use_graph = graphs_enabled() && ctx->prof_mode != 1 && plan->uses > 0;
   if (use_graph && (!plan->exec || plan->graph_chop != choppiness)) {
     if (plan->exec) cudaGraphExecDestroy(plan->exec), plan->exec = nullptr;
     const uint64_t before = ctx->launches.load();
     cudaGraph_t graph;
+    const bool prof = ctx->profiling;
+    ctx->profiling = false;  // no event windows inside the captured graph
     OCN_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeRelaxed));
     try {
       enqueue_spectral(cas, plan, choppiness);
+      ctx->profiling = prof;
     } catch (...) {
+      ctx->profiling = prof;
       cudaStreamEndCapture(ctx->stream, &graph);
       throw;
     }
@@ -870,6 +922,7 @@ void spectral_step(ocn_cascades* cas, ocn_maps* maps, ocn_slices* slices, double
     plan->graph_chop = choppiness;
   }
   if (use_graph) {
+    ProfWindow pw(ctx, OCN_PROF_SPECTRAL);
     OCN_CUDA(cudaGraphLaunch(plan->exec, ctx->stream));
     ctx->launches.fetch_add(plan->graph_kernels);
   } else {
@@ -892,13 +945,13 @@ static void plain_ifft(ocn_ctx* ctx, int n, int G, const float2* src, float2* sc
   ra.src = src;
   ra.scratch = scratch;
   ra.tw = tw;
-  rows_dispatch(ctx, n, ra, true);
+  rows_dispatch(ctx, n, ra, true, ctx->stream);
   ColArgs ca{};
   ca.scratch = scratch;
   ca.desc = d_desc;
   ca.out_c = out_c;
   ca.tw = tw;
-  cols_dispatch(ctx, n, ca, G, out_c != nullptr);
+  cols_dispatch(ctx, n, ca, G, out_c != nullptr, ctx->stream);
 }
 
 }  // namespace ocn
@@ -950,9 +1003,10 @@ int ocn_ctx_synchronize(ocn_ctx* ctx) {
   });
 }
 
-int ocn_ctx_profile(ocn_ctx* ctx, int enable) {
+int ocn_ctx_profile(ocn_ctx* ctx, int mode) {
   if (!ctx) return OCN_ERR_ARG;
-  ctx->profiling = enable != 0;
+  ctx->profiling = mode != 0;
+  ctx->prof_mode = mode;
   return OCN_OK;
 }
 
@@ -1145,8 +1199,12 @@ int ocn_cascades_create(ocn_ctx* ctx, int resolution, int count, const double* l
     OCN_CUDA(cudaMemcpyAsync(cas->twiddle.p, tw.data(), tw.size() * sizeof(float2),
                              cudaMemcpyHostToDevice, ctx->stream));
     cas->group = (int)group_for(resolution, 1 << 30);
+    // two half-size scratch buffers let the row pass of the next group overlap
+    // the column pass of the current one (same L2 footprint)
+    cas->nbuf = dual_stream(ctx) && cas->group >= 2 ? 2 : 1;
+    if (cas->nbuf == 2) cas->group /= 2;
     cas->d_time.alloc(1);
-    cas->scratch.alloc((size_t)cas->group * nn);
+    cas->scratch.alloc((size_t)cas->nbuf * cas->group * nn);
     OCN_CUDA(cudaStreamSynchronize(ctx->stream));
     ctx_retain(ctx);
     *out = cas.release();
