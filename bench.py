@@ -175,6 +175,50 @@ class Frame:
             oc.check(L.ocn_hydro_report_get(self.mesh.h, C.byref(self.report)), self.ctx.h, "report")
 
 
+# ---------------------------------------------------------------- config 4
+C4_INSTANCES, C4_N = 64, 512
+C4_LENGTHS = [256.0, 16.0, 4.0]
+C4_CUTOFFS = [12 * math.pi / 16, 12 * math.pi / 4]
+C4_POINTS = C4_INSTANCES * len(C4_LENGTHS) * C4_N * C4_N
+C4_WORKLOAD = ("config4: 64 independent instances x 3 cascades x 512^2 (8 surface maps each), "
+               "instances sharded across ranks, no collective")
+
+
+class Frame4:
+    """This rank's share of the 64 instances as one batched spectral set."""
+
+    def __init__(self, device: int, rank: int, world: int):
+        from paper_2503_03326_b200 import ocean as oc
+        self.oc, self.L = oc, oc.lib()
+        self.ctx = oc.Context(device)
+        per = C4_INSTANCES // world
+        lo = rank * per
+        params = []
+        for seed in range(lo, lo + per):
+            p = _params()
+            p.rng_seed = seed
+            params.append(p)
+        self.inst = oc.CascadeInstances(oc.CascadeConfig(C4_N, C4_LENGTHS, C4_CUTOFFS), params,
+                                        ctx=self.ctx)
+        self.maps = oc.SurfaceMaps(self.inst)
+        self.points = per * len(C4_LENGTHS) * C4_N * C4_N
+        self.t = 0.0
+        self.probe = C.c_float()
+
+    def step(self, read_report: bool = False):
+        self.t += DT
+        self.oc.check(self.L.ocn_surface_generate(self.maps.h, self.t, 1.0), self.ctx.h, "maps")
+        if read_report:  # the frame's result: instance 0's height map (fp32) -> host
+            self.oc.check(self.L.ocn_maps_download_f32(self.maps.h, 0, 0, self._hmap), self.ctx.h,
+                          "download")
+
+    _hmap_arr = np.zeros(C4_N * C4_N, np.float32)
+
+    @property
+    def _hmap(self):
+        return self._hmap_arr.ctypes.data_as(C.POINTER(C.c_float))
+
+
 def _dist():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     if ws <= 1:
@@ -221,7 +265,8 @@ def _traffic():
 
 def run_ours(args):
     dist, rank, world, local = _dist()
-    fr = Frame(local)
+    c4 = args.config == 4
+    fr = Frame4(local, rank, world) if c4 else Frame(local)
     L, ctx = fr.L, fr.ctx
     for _ in range(max(args.warmup, 3)):
         fr.step()
@@ -243,6 +288,7 @@ def run_ours(args):
         _barrier(dist)
         ms_total = ev0.elapsed_time(ev1)
         launches = ctx.kernel_launches() - launches0
+
         # ---- roofline pass: same K frames with CUDA-event windows per stage
         # (mode 2: the spectral step still replays its graph) ...
         def profiled(mode, names):
@@ -259,10 +305,12 @@ def run_ours(args):
             L.ocn_ctx_profile(ctx.h, 0)
             return out
         stages = profiled(2, [("spectral", 6), ("hydro", 3), ("mask", 4), ("fdm", 5)])
+        if c4:
+            stages = {"spectral": stages["spectral"]}
         # ... and the kernel split of the spectral step (mode 1: eager launches)
         kernels = profiled(1, [("evolve", 0), ("fft_rows", 1), ("fft_cols", 2), ("spectral_eager", 6)])
         # ---- e2e: through the C-ABI with host inputs (t, pose) and the host
-        # read of each frame's hydro report (forces / torque), wall clock
+        # read of each frame's result, wall clock
         _barrier(dist)
         ctx.synchronize()
         t0 = time.perf_counter()
@@ -276,14 +324,32 @@ def run_ours(args):
         if dist:
             dist.destroy_process_group()
         return
-    value = world * POINTS_PER_FRAME / (ms_frame / 1e3)
     peak, peak_kind = _peaks()
+    if c4:
+        points = C4_POINTS if world > 1 else fr.points * world
+        alg_bytes = fr.points * (8 + 4 * 8)  # per rank and frame
+        metric = "ocean grid points/sec (64 x 3 x 512^2 instances, surface synthesis)"
+        workload, h2d, d2h = C4_WORKLOAD, 8, C4_N * C4_N * 4
+        cfg = {"workload": workload, "grid": C4_N, "instances": C4_INSTANCES,
+               "cascades_per_instance": len(C4_LENGTHS),
+               "parallelism": f"instances sharded {C4_INSTANCES // world}/rank x {world}",
+               "l2": "per-frame outputs 1.6 GB / world > 126 MB L2 (no explicit flush)"}
+        scaling = "strong"
+    else:
+        points = world * POINTS_PER_FRAME
+        alg_bytes = SPECTRAL_BYTES
+        metric = "ocean grid points/sec (spectrum+iFFT+forces) at 1024^2 x 4 cascades"
+        workload, h2d, d2h = WORKLOAD, C.sizeof(fr.pose) + 8, C.sizeof(fr.report)
+        cfg = {"workload": workload, "grid": N_GRID, "cascades": len(LENGTHS),
+               "depth_slices": DEPTHS, "hull_triangles": int(fr.mesh.triangles.shape[0]),
+               "fdm_grid": FDM_N, "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+               "l2": "per-frame working set 1.8 GB of outputs > 126 MB L2 (no explicit flush)"}
+        scaling = "weak"
+    value = points / (ms_frame / 1e3)
     spec_ms = stages["spectral"]
-    achieved = SPECTRAL_BYTES / (spec_ms / 1e3) / 1e9
-    h2d = C.sizeof(fr.pose) + 8
-    d2h = C.sizeof(fr.report)
+    achieved = alg_bytes / (spec_ms / 1e3) / 1e9
     line = {
-        "metric": "ocean grid points/sec (spectrum+iFFT+forces) at 1024^2 x 4 cascades",
+        "metric": metric,
         "value": value,
         "unit": "grid-points/s",
         "n_gpus": world,
@@ -292,30 +358,55 @@ def run_ours(args):
         "ms_per_step": ms_frame,
         "ms_per_frame": ms_frame,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": scaling,
         "vs_baseline": None,
         "dtype": "f32 (fields, FFT) / f64 (spectrum init, phases, samplers, forces)",
-        "data": "synthetic (SURVEY 8d config 3 spectrum, seed 42; UV-ellipsoid hull)",
-        "config": {"workload": WORKLOAD, "grid": N_GRID, "cascades": len(LENGTHS),
-                   "depth_slices": DEPTHS, "hull_triangles": int(fr.mesh.triangles.shape[0]),
-                   "fdm_grid": FDM_N, "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
-                   "l2": "per-frame working set 1.8 GB of outputs > 126 MB L2 (no explicit flush)"},
+        "data": "synthetic (SURVEY 8d spectrum presets; UV-ellipsoid hull)",
+        "config": cfg,
         "stages_ms": stages,
         "spectral_kernels_ms_eager": kernels,
-        "roofline": {"kernel": "spectral pipeline (k_evolve + k_rows + k_cols)", "bound": "hbm",
-                     "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": _traffic(),
-                     "algorithmic_bytes_per_frame": SPECTRAL_BYTES},
-        "e2e": {"value": world * POINTS_PER_FRAME / e2e_frame, "unit": "grid-points/s",
-                "ms_per_frame": e2e_frame * 1e3, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "roofline": {"kernel": "spectral pipeline (k_evolve + k_rows_w + k_cols, one CUDA graph)",
+                     "bound": "hbm", "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": _traffic(),
+                     "algorithmic_bytes_per_frame": alg_bytes},
+        "e2e": {"value": points / e2e_frame, "unit": "grid-points/s", "ms_per_frame": e2e_frame * 1e3,
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(frames=1, warmup=0)
+        line["cpu_baseline"] = cpu_baseline_c4() if c4 else cpu_baseline(frames=1, warmup=0)
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def cpu_baseline_c4(sample_instances: int = 2):
+    """Reference generate_maps per instance (3 x 512^2, no batch API in the
+    reference), `sample_instances` of the 64 timed and scaled."""
+    from oracle.oracle import P
+    from paper_2503_03326_b200._types import SpectrumParams  # noqa: F401
+    lib = _ref_lib()
+    ncpu = os.cpu_count() or 1
+    lib.ref_set_worker_count.argtypes = [C.c_int]
+    lib.ref_set_worker_count(ncpu)
+    f = lib.ref_generate_maps_timed
+    f.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int,
+                  C.POINTER(C.c_double)]
+    la = np.ascontiguousarray(C4_LENGTHS)
+    cu = np.ascontiguousarray(C4_CUTOFFS + [0.0])
+    per = []
+    for k in range(sample_instances):
+        p = _params()
+        p.rng_seed = k
+        sec = C.c_double()
+        f(C4_N, 3, P(la), P(cu), C.byref(p), DT, 1, C.byref(sec))  # generate_maps only
+        per.append(sec.value)
+    dt = float(np.mean(per)) * C4_INSTANCES
+    return {"value": C4_POINTS / dt, "unit": "grid-points/s", "ms_per_frame": dt * 1e3, "cores": ncpu,
+            "kind": "reference",
+            "sample": f"{sample_instances} of 64 instances: reference generate_maps (3 x 512^2, "
+                      f"CascadeSet built outside the timing), scaled x{C4_INSTANCES // sample_instances}"}
 
 
 # ---------------------------------------------------------- reference (CPU)
@@ -440,6 +531,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--config", type=int, default=3, choices=[3, 4],
+                    help="3: the BASELINE metric frame (default); 4: 64 batched 512^2 instances")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

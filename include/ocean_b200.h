@@ -270,6 +270,15 @@ OCN_API int ocn_cascades_create(ocn_ctx* ctx, int resolution, int count, const d
                         const double* host_band_min, const double* host_band_max,
                         const uint32_t* host_cascade_index, const ocn_spectrum_params* params,
                         ocn_cascades** out);
+/* Batched spectral sets (independent instances): `count`
+ * grids with their own spectrum parameters (params has count entries). One
+ * spectral step then evolves and transforms every grid. Samplers over maps of
+ * such a set sum at most 16 grids (a set of instances is for synthesis). */
+OCN_API int ocn_cascades_create_multi(ocn_ctx* ctx, int resolution, int count,
+                                      const double* host_lengths, const double* host_band_min,
+                                      const double* host_band_max,
+                                      const uint32_t* host_cascade_index,
+                                      const ocn_spectrum_params* params, ocn_cascades** out);
 OCN_API int ocn_cascades_destroy(ocn_cascades* c);
 OCN_API int ocn_cascades_info(const ocn_cascades* c, int* resolution, int* count);
 /* WaveGrid accessors (spectra.hpp:95-104): h0 / h0_conj_neg as interleaved

@@ -706,3 +706,18 @@ extern "C" int ref_bench_frame(void* bp, double dt, int depth_sample, double* st
     stage[4] = t5 - t4;
   });
 }
+
+// generate_maps timed alone (CascadeSet built outside the timed region).
+extern "C" int ref_generate_maps_timed(int n, int C, const double* lengths, const double* cutoffs,
+                                       const ocn_spectrum_params* p, double t, int frames,
+                                       double* seconds) {
+  return guard([&] {
+    CascadeSet cs(to_cascades(n, C, lengths, cutoffs), to_params(p));
+    double t0 = now_s();
+    for (int f = 0; f < frames; ++f) {
+      SurfaceMaps m = generate_maps(cs, t + f * (1.0 / 60.0), {});
+      (void)m;
+    }
+    *seconds = (now_s() - t0) / frames;
+  });
+}

@@ -98,6 +98,7 @@ SIGNATURES = {
     "ocn_exp_interp": (ci, [cd, cd, cd, cd, cd, d]),
     "ocn_slice_depths": (ci, [C.POINTER(SliceConfig), d]),
     "ocn_cascades_create": (ci, [vp, ci, ci, d, d, d, u32, C.POINTER(SpectrumParams), pvp]),
+    "ocn_cascades_create_multi": (ci, [vp, ci, ci, d, d, d, u32, C.POINTER(SpectrumParams), pvp]),
     "ocn_cascades_destroy": (ci, [vp]),
     "ocn_cascades_info": (ci, [vp, C.POINTER(ci), C.POINTER(ci)]),
     "ocn_cascades_download": (ci, [vp, ci, d, d, u8, d]),

@@ -12,7 +12,24 @@
 
 namespace ocn {
 
-constexpr int kMaxCascades = 16;
+constexpr int kMaxCascades = 16;   // cascades summed by one sampler (maps / slices)
+constexpr int kMaxGrids = 1 << 16;  // grids of one spectral set (cascades x instances)
+
+// Per-grid constants of a spectral set (device array).
+struct GridConst {
+  double dk, length, band_min, band_max;
+  uint32_t cindex;
+  int32_t pad;
+  ocn_spectrum_params p;
+};
+
+// A run of consecutive transforms of one grid inside a transform group.
+struct GroupSeg {
+  int grid;   // cascade / grid index
+  int first;  // first transform, relative to the group
+  int count;
+  int pad;
+};
 
 // One packed C2C transform of the spectral step (X + iY of one field pair).
 enum XformKind : int {
@@ -35,6 +52,14 @@ struct XformDesc {
 
 struct SpectralPlan {
   DevBuf<XformDesc> desc;
+  // transform groups (G consecutive transforms, possibly spanning grids) and
+  // their per-grid segments
+  struct Group {
+    int first, count, seg0, nseg, max_seg;
+    int family;  // 0: surface pairs, 1: velocity
+  };
+  std::vector<Group> groups;
+  DevBuf<GroupSeg> segs;
   // CUDA graph of the whole step (everything but the time upload), captured on
   // the second use of the plan; rebuilt when the choppiness changes.
   cudaGraphExec_t exec = nullptr;
@@ -58,7 +83,9 @@ struct ocn_cascades {
   int n = 0, count = 0;
   std::vector<double> lengths, band_min, band_max;
   std::vector<uint32_t> cascade_index;
-  ocn_spectrum_params params{};
+  ocn_spectrum_params params{};             // of grid 0 (all grids for plain cascade sets)
+  std::vector<ocn_spectrum_params> grid_params;
+  ocn::DevBuf<ocn::GridConst> gconst;      // [count]
   ocn::DevBuf<double2> h0_f64;  // [C][N][N] fp64 amplitudes (API download)
   ocn::DevBuf<float2> h0;       // [C][N][N] fp32 hot-path table
   ocn::DevBuf<uint8_t> in_band; // [C][N][N]

@@ -8,6 +8,9 @@
 namespace ocn {
 
 SurfView make_surf_view(ocn_maps* m) {
+  if (m->cas->count > kMaxCascades)
+    fail(OCN_ERR_CONFIG, "samplers sum at most %d cascades (maps of a %d-grid set)", kMaxCascades,
+         m->cas->count);
   SurfView v{};
   v.n = m->cas->n;
   v.C = m->cas->count;
@@ -17,6 +20,9 @@ SurfView make_surf_view(ocn_maps* m) {
 }
 
 SliceView make_slice_view(ocn_slices* s) {
+  if (s->cas->count > kMaxCascades)
+    fail(OCN_ERR_CONFIG, "samplers sum at most %d cascades (slices of a %d-grid set)", kMaxCascades,
+         s->cas->count);
   SliceView v{};
   v.n = s->cas->n;
   v.C = s->cas->count;
@@ -150,8 +156,8 @@ extern "C" {
 int ocn_maps_sample(ocn_maps* m, int field, int64_t n, const double* xz, double* out) {
   if (!m || field < 0 || field >= 8) return OCN_ERR_ARG;
   ocn_ctx* ctx = m->cas->ctx;
-  SurfView v = make_surf_view(m);
   return sample_call(ctx, n, xz, 2, out, 1, [&](const double* i, double* o) {
+    const SurfView v = make_surf_view(m);
     k_maps_sample<<<blocks_for(ctx, n), 128, 0, ctx->stream>>>(v, field, n, i, o);
   });
 }
@@ -159,8 +165,8 @@ int ocn_maps_sample(ocn_maps* m, int field, int64_t n, const double* xz, double*
 int ocn_sample_displacement(ocn_maps* m, int64_t n, const double* xz, double* out) {
   if (!m) return OCN_ERR_ARG;
   ocn_ctx* ctx = m->cas->ctx;
-  SurfView v = make_surf_view(m);
   return sample_call(ctx, n, xz, 2, out, 3, [&](const double* i, double* o) {
+    const SurfView v = make_surf_view(m);
     k_sample_disp<<<blocks_for(ctx, n), 128, 0, ctx->stream>>>(v, n, i, o);
   });
 }
@@ -168,8 +174,8 @@ int ocn_sample_displacement(ocn_maps* m, int64_t n, const double* xz, double* ou
 int ocn_height_at(ocn_maps* m, int64_t n, const double* xz, double* out) {
   if (!m) return OCN_ERR_ARG;
   ocn_ctx* ctx = m->cas->ctx;
-  SurfView v = make_surf_view(m);
   return sample_call(ctx, n, xz, 2, out, 1, [&](const double* i, double* o) {
+    const SurfView v = make_surf_view(m);
     k_height_at<<<blocks_for(ctx, n), 128, 0, ctx->stream>>>(v, n, i, o);
   });
 }
@@ -178,8 +184,8 @@ int ocn_height_at_tolerance(ocn_maps* m, int64_t n, const double* xz, double tol
                             double* out, int32_t* iterations) {
   if (!m) return OCN_ERR_ARG;
   ocn_ctx* ctx = m->cas->ctx;
-  SurfView v = make_surf_view(m);
   return api_call(ctx, [&] {
+    const SurfView v = make_surf_view(m);
     OCN_REQUIRE(n >= 0 && (n == 0 || (xz && out)), "bad sampler arguments");
     if (n == 0) return;
     DeviceScope ds(ctx);
@@ -199,8 +205,8 @@ int ocn_height_at_tolerance(ocn_maps* m, int64_t n, const double* xz, double tol
 int ocn_surface_assemble(ocn_maps* m, int64_t n, const double* xz, double* out) {
   if (!m) return OCN_ERR_ARG;
   ocn_ctx* ctx = m->cas->ctx;
-  SurfView v = make_surf_view(m);
   return sample_call(ctx, n, xz, 2, out, 10, [&](const double* i, double* o) {
+    const SurfView v = make_surf_view(m);
     k_assemble<<<blocks_for(ctx, n), 128, 0, ctx->stream>>>(v, n, i, o);
   });
 }
@@ -208,8 +214,8 @@ int ocn_surface_assemble(ocn_maps* m, int64_t n, const double* xz, double* out) 
 int ocn_sample_slice(ocn_slices* s, int depth, int64_t n, const double* xz, double* out) {
   if (!s || depth < 0 || depth >= s->cfg.count) return OCN_ERR_ARG;
   ocn_ctx* ctx = s->cas->ctx;
-  SliceView v = make_slice_view(s);
   return sample_call(ctx, n, xz, 2, out, 3, [&](const double* i, double* o) {
+    const SliceView v = make_slice_view(s);
     k_sample_slice<<<blocks_for(ctx, n), 128, 0, ctx->stream>>>(v, depth, n, i, o);
   });
 }
@@ -218,8 +224,8 @@ int ocn_velocity_at(ocn_slices* s, int64_t n, const double* xzy, int interp, int
                     double* out) {
   if (!s) return OCN_ERR_ARG;
   ocn_ctx* ctx = s->cas->ctx;
-  SliceView v = make_slice_view(s);
   return api_call(ctx, [&] {
+    const SliceView v = make_slice_view(s);
     OCN_REQUIRE(n >= 0 && (n == 0 || (xzy && out)), "bad sampler arguments");
     if (n == 0) return;
     DeviceScope ds(ctx);

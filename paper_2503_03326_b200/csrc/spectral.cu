@@ -72,45 +72,36 @@ struct Launch {
 };
 
 // ------------------------------------------------------------------ K1
-struct InitArgs {
-  int n, count;
-  double dk[kMaxCascades];
-  double length[kMaxCascades];
-  double band_min[kMaxCascades], band_max[kMaxCascades];
-  uint32_t cindex[kMaxCascades];
-  ocn_spectrum_params p;
-  double2* h0_f64;
-  float2* h0;
-  uint8_t* in_band;
-};
-
-// generate_h0, spectra.cpp:150-169, one thread per mode (fp64, bit-exact
-// Philox and band mask).
-__global__ void __launch_bounds__(256) k_spectrum_init(const InitArgs a) {
-  const size_t nn = (size_t)a.n * a.n;
-  const size_t total = nn * a.count;
+// generate_h0, spectra.cpp:150-169, one thread per mode of every grid (fp64,
+// bit-exact Philox and band mask; per-grid spectrum parameters).
+__global__ void __launch_bounds__(256) k_spectrum_init(int n, int count, const GridConst* gc,
+                                                       double2* h0_f64, float2* h0,
+                                                       uint8_t* in_band) {
+  const size_t nn = (size_t)n * n;
+  const size_t total = nn * count;
   for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
        idx += (size_t)gridDim.x * blockDim.x) {
     const int c = (int)(idx / nn);
     const size_t q = idx - (size_t)c * nn;
-    const int i = (int)(q / a.n), j = (int)(q - (size_t)i * a.n);
-    const double dk = a.dk[c];
-    const double kx = dk * (i - a.n / 2);
-    const double kz = dk * (j - a.n / 2);
+    const int i = (int)(q / n), j = (int)(q - (size_t)i * n);
+    const GridConst& G = gc[c];
+    const double dk = G.dk;
+    const double kx = dk * (i - n / 2);
+    const double kz = dk * (j - n / 2);
     const double k = sm::hypot_ref(kx, kz);
-    const double omega = sqrt(a.p.gravity * k);
-    const bool banded = k > 0.0 && k >= a.band_min[c] && k < a.band_max[c];
+    const double omega = sqrt(G.p.gravity * k);
+    const bool banded = k > 0.0 && k >= G.band_min && k < G.band_max;
     double hr = 0.0, hi = 0.0;
     if (banded) {
       double gr, gi;
-      sm::gaussian_complex(a.p.rng_seed, a.cindex[c], (uint32_t)i, (uint32_t)j, &gr, &gi);
-      const double amp = sqrt(sm::h0_variance(kx, kz, k, omega, a.length[c], a.p));
+      sm::gaussian_complex(G.p.rng_seed, G.cindex, (uint32_t)i, (uint32_t)j, &gr, &gi);
+      const double amp = sqrt(sm::h0_variance(kx, kz, k, omega, G.length, G.p));
       hr = gr * amp;
       hi = gi * amp;
     }
-    a.h0_f64[idx] = make_double2(hr, hi);
-    a.h0[idx] = make_float2((float)hr, (float)hi);
-    a.in_band[idx] = banded ? 1 : 0;
+    h0_f64[idx] = make_double2(hr, hi);
+    h0[idx] = make_float2((float)hr, (float)hi);
+    in_band[idx] = banded ? 1 : 0;
   }
 }
 
@@ -174,36 +165,45 @@ __global__ void k_assemble_coef(int n, double dk, double g, double t, double cho
 // h~ and G (surface.cpp:49-50; velocity.cpp:16-20) at time t, one cascade.
 __global__ void k_set_time(double* d_time, double t) { *d_time = t; }
 
-__global__ void __launch_bounds__(256) k_evolve(int n, double dk, double g, const double* d_time,
+__global__ void __launch_bounds__(256) k_evolve(int n, int count, const GridConst* gc,
+                                                const double* d_time,
                                                 const float2* __restrict__ h0, float4* spec) {
-  const int nn = n * n;
+  const size_t nn = (size_t)n * n;
+  const size_t total = nn * count;
   const double t = *d_time;
-  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nn; q += gridDim.x * blockDim.x) {
+  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    const int c = (int)(idx / nn);
+    const int q = (int)(idx - (size_t)c * nn);
     const int i = q / n, j = q - i * n;
     const int ni = i == 0 ? 0 : n - i, nj = j == 0 ? 0 : n - j;
-    const float2 a = __ldg(h0 + q);
-    const float2 m = __ldg(h0 + ni * n + nj);
+    const float2* h = h0 + (size_t)c * nn;
+    const float2 a = __ldg(h + q);
+    const float2 m = __ldg(h + ni * n + nj);
     const float2 b = make_float2(m.x, -m.y);  // conj(h0(-k))
+    const double dk = gc[c].dk;
     const double kx = dk * (i - n / 2), kz = dk * (j - n / 2);
-    const double omega = sqrt(g * sqrt(kx * kx + kz * kz));
+    const double omega = sqrt(gc[c].p.gravity * sqrt(kx * kx + kz * kz));
     double ph = omega * t;
     ph -= 6.283185307179586476925 * rint(ph * 0.15915494309189533577);
-    float s, c;
-    sincosf((float)ph, &s, &c);
+    float s, cs;
+    sincosf((float)ph, &s, &cs);
     // A = a e^{i ph}, B = b e^{-i ph}
-    const float ar = a.x * c - a.y * s, ai = a.x * s + a.y * c;
-    const float br = b.x * c + b.y * s, bi = b.y * c - b.x * s;
-    spec[q] = make_float4(ar + br, ai + bi, ar - br, ai - bi);
+    const float ar = a.x * cs - a.y * s, ai = a.x * s + a.y * cs;
+    const float br = b.x * cs + b.y * s, bi = b.y * cs - b.x * s;
+    spec[idx] = make_float4(ar + br, ai + bi, ar - br, ai - bi);
   }
 }
 
 // ------------------------------------------------------------------ rows
 struct RowArgs {
-  int items;  // N * G
+  int items;  // N * G (generic kernel)
   int G;
-  const XformDesc* desc;  // group descriptors (spectral mode)
-  const float4* spec;     // cascade's (h~, G) table
-  float dk, gravity, chop;
+  const XformDesc* desc;   // group descriptors
+  const GroupSeg* segs;    // per-grid segments of the group (warp kernel)
+  const float4* spec;      // (h~, G) of every grid, [grid][N][N]
+  const GridConst* gc;     // per-grid constants
+  float chop;
   const float2* src;  // plain mode: [G][N][N] complex input
   float2* scratch;    // [G][N][N]
   const float2* tw;
@@ -297,12 +297,13 @@ __global__ void __launch_bounds__(Launch<N>::THREADS) k_rows(const RowArgs a) {
         });
   } else {
     const XformDesc d = a.desc[gi];
-    const float4* srow = a.spec + (size_t)row * N;
+    const float4* srow = a.spec + ((size_t)d.cascade * N + row) * N;
+    const float dk = (float)a.gc[d.cascade].dk, g = (float)a.gc[d.cascade].p.gravity;
     fft::cta_fft<N>(
         t, sm, a.tw,
         [&](int j) {
           if (!valid) return make_float2(0.f, 0.f);
-          return packed_coef(d, __ldg(srow + j), row, j, N, a.dk, a.gravity, a.chop);
+          return packed_coef(d, __ldg(srow + j), row, j, N, dk, g, a.chop);
         },
         [&](int k, float2 x) {
           if (valid) out[k] = x;
@@ -345,8 +346,11 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
-template <int N, bool PLAIN>
+enum RowMode : int { kRowPlain = 0, kRowSurface = 1, kRowVelocity = 2 };
+
+template <int N, int MODE>
 __global__ void __launch_bounds__(256, 2) k_rows_w(const RowArgs a) {
+  constexpr bool PLAIN = MODE == kRowPlain;
   using W = WarpLaunch<N>;
   constexpr int T = W::T, E = fft::Plan<N>::E;
   extern __shared__ float4 smem4[];
@@ -364,12 +368,19 @@ __global__ void __launch_bounds__(256, 2) k_rows_w(const RowArgs a) {
   const int warps = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int sub = lane / T, t = lane - sub * T;
-  const float kx = a.dk * (float)(row - N / 2);
+  // this CTA: one row of one grid, the transforms [first, first + count) of the group
+  int seg_first = 0, seg_count = a.G, grid = 0;
   if constexpr (!PLAIN) {
-    const float4* srow = a.spec + (size_t)row * N;
-    const float g = a.gravity;
+    const GroupSeg sg = a.segs[blockIdx.y];
+    seg_first = sg.first, seg_count = sg.count, grid = sg.grid;
+  }
+  const float dkf = PLAIN ? 0.f : (float)a.gc[grid].dk;
+  const float kx = dkf * (float)(row - N / 2);
+  if constexpr (!PLAIN) {
+    const float4* srow = a.spec + ((size_t)grid * N + row) * N;
+    const float g = (float)a.gc[grid].p.gravity;
     for (int j = threadIdx.x; j < N; j += blockDim.x) {
-      const float kz = a.dk * (float)(j - N / 2);
+      const float kz = dkf * (float)(j - N / 2);
       const float k2 = kx * kx + kz * kz;
       const float k = sqrtf(k2);
       const float inv = k2 > 0.f ? 1.0f / k : 0.f;
@@ -384,24 +395,27 @@ __global__ void __launch_bounds__(256, 2) k_rows_w(const RowArgs a) {
     }
     __syncthreads();
   }
-  const int slots = (a.G + W::TPW - 1) / W::TPW;
+  const int slots = (seg_count + W::TPW - 1) / W::TPW;
   float2* buf = bufs + (size_t)(warp * W::TPW + sub) * W::STRIDE;
   for (int slot = warp; slot < slots; slot += warps) {
-    const int gi = slot * W::TPW + sub;
-    const bool valid = gi < a.G;
-    float2* out = a.scratch + ((size_t)(valid ? gi : 0) * N + row) * N;
+    const int li = slot * W::TPW + sub;
+    const bool valid = li < seg_count;
+    const int gi = seg_first + (valid ? li : 0);  // transform index within the group
+    float2* out = a.scratch + ((size_t)gi * N + row) * N;
     auto store = [&](int k, float2 x) {
       if (valid) out[k] = x;
     };
     if constexpr (PLAIN) {
-      const float2* in = a.src + ((size_t)(valid ? gi : 0) * N + row) * N;
-      fft::cta_fft<N, true, false, false>(
-          t, buf, a.tw, [&](int j) { return valid ? __ldg(in + j) : make_float2(0.f, 0.f); }, store);
+      const float2* in = a.src + ((size_t)gi * N + row) * N;
+      for (int j = t; j < N; j += T) buf[fft::pad32(j)] = valid ? __ldg(in + j) : make_float2(0.f, 0.f);
+      __syncwarp();
+      fft::cta_fft<N, true, true, false>(
+          t, buf, a.tw, [&](int j) { return buf[fft::pad32(j)]; }, store);
     } else {
-      const XformDesc d = a.desc[valid ? gi : 0];
-      if (d.kind <= kSurfHxHz) {
+      const XformDesc d = a.desc[gi];
+      if constexpr (MODE == kRowSurface) {
         // surface pairs: X + iY = h~ M(kx, kz) (surface.cpp:77-80 packing)
-        const float chop = a.chop, dk = a.dk;
+        const float chop = a.chop, dk = dkf;
         const int kind = d.kind;
         fft::cta_fft<N, true, false, false>(
             t, buf, a.tw,
@@ -425,6 +439,7 @@ __global__ void __launch_bounds__(256, 2) k_rows_w(const RowArgs a) {
             },
             store);
       } else {
+        static_assert(MODE == kRowVelocity, "row mode");
         // velocity: Z (re + i im) with Z = V0 (x/z pair) or W0 (vy pair)
         const float2* Z = d.kind == kVelXZ ? sv0 : sw0;
         constexpr float kLog2e = 1.4426950408889634f;
@@ -619,25 +634,29 @@ constexpr bool use_warp_kernels() {
 }
 
 template <int N>
-void launch_rows(ocn_ctx* ctx, const RowArgs& a, bool plain, cudaStream_t st) {
+void launch_rows(ocn_ctx* ctx, const RowArgs& a, bool plain, cudaStream_t st, int nseg,
+                 int max_seg, int family) {
   if constexpr (use_warp_kernels<N>()) {
     using W = WarpLaunch<N>;
-    const int slots = (a.G + W::TPW - 1) / W::TPW;
+    const int slots = (max_seg + W::TPW - 1) / W::TPW;
     const int warps = slots < 8 ? slots : 8;
     const size_t smem = (plain ? 0 : 2 * N * sizeof(float4)) +
                         (size_t)warps * W::TPW * W::STRIDE * sizeof(float2);
     static bool attr = false;
     if (!attr) {
       const int cap = 2 * N * sizeof(float4) + 8 * W::TPW * W::STRIDE * sizeof(float2);
-      OCN_CUDA(cudaFuncSetAttribute(k_rows_w<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap));
-      OCN_CUDA(cudaFuncSetAttribute(k_rows_w<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap));
+      OCN_CUDA(cudaFuncSetAttribute(k_rows_w<N, kRowPlain>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap));
+      OCN_CUDA(cudaFuncSetAttribute(k_rows_w<N, kRowSurface>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap));
+      OCN_CUDA(cudaFuncSetAttribute(k_rows_w<N, kRowVelocity>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap));
       attr = true;
     }
-    const int rows = a.items / a.G;
+    const dim3 grid(N, plain ? 1 : nseg);
     if (plain)
-      k_rows_w<N, true><<<rows, 32 * warps, smem, st>>>(a);
+      k_rows_w<N, kRowPlain><<<grid, 32 * warps, smem, st>>>(a);
+    else if (family == 0)
+      k_rows_w<N, kRowSurface><<<grid, 32 * warps, smem, st>>>(a);
     else
-      k_rows_w<N, false><<<rows, 32 * warps, smem, st>>>(a);
+      k_rows_w<N, kRowVelocity><<<grid, 32 * warps, smem, st>>>(a);
     OCN_LAUNCHED(ctx);
     return;
   }
@@ -693,8 +712,10 @@ void launch_cols(ocn_ctx* ctx, const ColArgs& a, int G, bool complex_out, cudaSt
   OCN_LAUNCHED(ctx);
 }
 
-void rows_dispatch(ocn_ctx* ctx, int n, const RowArgs& a, bool plain, cudaStream_t st) {
-#define OCN_ROWS(NN) launch_rows<NN>(ctx, a, plain, st)
+void rows_dispatch(ocn_ctx* ctx, int n, const RowArgs& a, bool plain, cudaStream_t st,
+                   int nseg = 1, int max_seg = 0, int family = 0) {
+  if (max_seg <= 0) max_seg = a.G;
+#define OCN_ROWS(NN) launch_rows<NN>(ctx, a, plain, st, nseg, max_seg, family)
   OCN_DISPATCH_N(n, OCN_ROWS)
 #undef OCN_ROWS
 }
@@ -754,19 +775,21 @@ static SpectralPlan* get_plan(ocn_cascades* cas, ocn_maps* maps, ocn_slices* sli
   auto plan = std::make_unique<SpectralPlan>();
   plan->need_surface = maps != nullptr;
   plan->need_velocity = slices != nullptr;
-  for (int c = 0; c < cas->count; ++c) {
-    plan->first.push_back((int)plan->host_desc.size());
-    if (maps) {
-      static const int pairs[4][2] = {{OCN_FIELD_H, OCN_FIELD_DX},
-                                      {OCN_FIELD_DZ, OCN_FIELD_DXDX},
-                                      {OCN_FIELD_DZDX, OCN_FIELD_DZDZ},
-                                      {OCN_FIELD_HX, OCN_FIELD_HZ}};
+  // Surface transforms of every grid first, then the velocity transforms, so
+  // that every transform group is of one family (one row-kernel variant each).
+  if (maps) {
+    static const int pairs[4][2] = {{OCN_FIELD_H, OCN_FIELD_DX},
+                                    {OCN_FIELD_DZ, OCN_FIELD_DXDX},
+                                    {OCN_FIELD_DZDX, OCN_FIELD_DZDZ},
+                                    {OCN_FIELD_HX, OCN_FIELD_HZ}};
+    for (int c = 0; c < cas->count; ++c)
       for (int p = 0; p < 4; ++p)
         plan->host_desc.push_back({c, p, 0.f, 0.f, maps->field(c, pairs[p][0]),
                                    maps->field(c, pairs[p][1])});
-    }
-    if (slices) {
-      int D = slices->cfg.count;
+  }
+  if (slices) {
+    const int D = slices->cfg.count;
+    for (int c = 0; c < cas->count; ++c) {
       for (int d = 0; d < D; ++d)
         plan->host_desc.push_back({c, kVelXZ, (float)slices->depths[d], 0.f,
                                    slices->field(d, c, 0), slices->field(d, c, 2)});
@@ -780,11 +803,38 @@ static SpectralPlan* get_plan(ocn_cascades* cas, ocn_maps* maps, ocn_slices* sli
                                      slices->field(d0, c, 1), nullptr});
       }
     }
-    plan->count.push_back((int)plan->host_desc.size() - plan->first.back());
   }
   plan->desc.alloc(plan->host_desc.size());
   OCN_CUDA(cudaMemcpy(plan->desc.p, plan->host_desc.data(),
                       plan->host_desc.size() * sizeof(XformDesc), cudaMemcpyHostToDevice));
+  // groups of G consecutive transforms (spanning grids), split into per-grid segments
+  std::vector<GroupSeg> segs;
+  const int total = (int)plan->host_desc.size();
+  auto family = [&](int i) { return plan->host_desc[i].kind <= kSurfHxHz ? 0 : 1; };
+  for (int g0 = 0; g0 < total;) {
+    int cnt = std::min(cas->group, total - g0);
+    for (int i = 1; i < cnt; ++i)
+      if (family(g0 + i) != family(g0)) {
+        cnt = i;  // keep groups single-family
+        break;
+      }
+    SpectralPlan::Group gr{g0, cnt, (int)segs.size(), 0, 0, family(g0)};
+    for (int i = 0; i < gr.count; ++i) {
+      const int c = plan->host_desc[g0 + i].cascade;
+      if (gr.nseg == 0 || segs.back().grid != c) {
+        segs.push_back({c, i, 0, 0});
+        ++gr.nseg;
+      }
+      ++segs.back().count;
+      gr.max_seg = std::max(gr.max_seg, segs.back().count);
+    }
+    plan->groups.push_back(gr);
+    g0 += cnt;
+  }
+  plan->segs.alloc(std::max<size_t>(segs.size(), 1));
+  if (!segs.empty())
+    OCN_CUDA(cudaMemcpy(plan->segs.p, segs.data(), segs.size() * sizeof(GroupSeg),
+                        cudaMemcpyHostToDevice));
   SpectralPlan* raw = plan.get();
   cas->plans[key] = std::move(plan);
   return raw;
@@ -821,7 +871,6 @@ static void enqueue_spectral(ocn_cascades* cas, SpectralPlan* plan, double chopp
   cudaStream_t A = ctx->stream, B = dual ? ctx->aux_stream() : ctx->stream;
   ProfWindow whole(ctx, OCN_PROF_SPECTRAL);
   std::vector<cudaEvent_t>& ev = ctx->sync_events;
-  int gidx = 0;
   auto event = [&](int k) {
     while ((int)ev.size() <= k) {
       cudaEvent_t e;
@@ -830,53 +879,47 @@ static void enqueue_spectral(ocn_cascades* cas, SpectralPlan* plan, double chopp
     }
     return ev[k];
   };
-  std::vector<int> cols_ev;  // event index recorded after cols of each group
-  const int G = cas->group;
-  for (int c = 0; c < cas->count; ++c) {
-    const double dk = 2.0 * kPi / cas->lengths[c];
-    float4* spec = cas->spec.p + (size_t)c * nn;
-    {
-      ProfWindow pw(ctx, OCN_PROF_EVOLVE);
-      k_evolve<<<grid_for(ctx, nn), 256, 0, A>>>(n, dk, cas->params.gravity, cas->d_time.p,
-                                                cas->h0.p + (size_t)c * nn, spec);
-      OCN_LAUNCHED(ctx);
-    }
-    const int first = plan->first[c], total = plan->count[c];
-    for (int g0 = 0; g0 < total; g0 += G, ++gidx) {
-      const int g = std::min(G, total - g0);
-      float2* scratch = cas->scratch.p + (size_t)(dual ? gidx % 2 : 0) * G * nn;
-      if (dual && gidx >= 2) OCN_CUDA(cudaStreamWaitEvent(A, event(cols_ev[gidx - 2]), 0));
-      RowArgs ra{};
-      ra.items = n * g;
-      ra.G = g;
-      ra.desc = plan->desc.p + first + g0;
-      ra.spec = spec;
-      ra.dk = (float)dk;
-      ra.gravity = (float)cas->params.gravity;
-      ra.chop = (float)choppiness;
-      ra.scratch = scratch;
-      ra.tw = cas->twiddle.p;
-      {
-        ProfWindow pw(ctx, dual ? -1 : OCN_PROF_ROWS);
-        rows_dispatch(ctx, n, ra, false, A);
-      }
-      if (dual) {
-        OCN_CUDA(cudaEventRecord(event(2 * gidx), A));
-        OCN_CUDA(cudaStreamWaitEvent(B, event(2 * gidx), 0));
-      }
-      ColArgs ca{};
-      ca.scratch = scratch;
-      ca.desc = plan->desc.p + first + g0;
-      ca.tw = cas->twiddle.p;
-      {
-        ProfWindow pw(ctx, dual ? -1 : OCN_PROF_COLS);
-        cols_dispatch(ctx, n, ca, g, false, B);
-      }
-      if (dual) OCN_CUDA(cudaEventRecord(event(2 * gidx + 1), B));
-      cols_ev.push_back(2 * gidx + 1);
-    }
+  {
+    ProfWindow pw(ctx, OCN_PROF_EVOLVE);  // every grid in one launch
+    k_evolve<<<grid_for(ctx, nn * cas->count), 256, 0, A>>>(n, cas->count, cas->gconst.p,
+                                                            cas->d_time.p, cas->h0.p, cas->spec.p);
+    OCN_LAUNCHED(ctx);
   }
-  if (dual && gidx > 0) OCN_CUDA(cudaStreamWaitEvent(A, event(cols_ev.back()), 0));
+  const int G = cas->group;
+  for (size_t gidx = 0; gidx < plan->groups.size(); ++gidx) {
+    const SpectralPlan::Group& gr = plan->groups[gidx];
+    float2* scratch = cas->scratch.p + (size_t)(dual ? gidx % 2 : 0) * G * nn;
+    if (dual && gidx >= 2) OCN_CUDA(cudaStreamWaitEvent(A, event(2 * (int)gidx - 3), 0));
+    RowArgs ra{};
+    ra.items = n * gr.count;
+    ra.G = gr.count;
+    ra.desc = plan->desc.p + gr.first;
+    ra.segs = plan->segs.p + gr.seg0;
+    ra.spec = cas->spec.p;
+    ra.gc = cas->gconst.p;
+    ra.chop = (float)choppiness;
+    ra.scratch = scratch;
+    ra.tw = cas->twiddle.p;
+    {
+      ProfWindow pw(ctx, dual ? -1 : OCN_PROF_ROWS);
+      rows_dispatch(ctx, n, ra, false, A, gr.nseg, gr.max_seg, gr.family);
+    }
+    if (dual) {
+      OCN_CUDA(cudaEventRecord(event(2 * (int)gidx), A));
+      OCN_CUDA(cudaStreamWaitEvent(B, event(2 * (int)gidx), 0));
+    }
+    ColArgs ca{};
+    ca.scratch = scratch;
+    ca.desc = plan->desc.p + gr.first;
+    ca.tw = cas->twiddle.p;
+    {
+      ProfWindow pw(ctx, dual ? -1 : OCN_PROF_COLS);
+      cols_dispatch(ctx, n, ca, gr.count, false, B);
+    }
+    if (dual) OCN_CUDA(cudaEventRecord(event(2 * (int)gidx + 1), B));
+  }
+  if (dual && !plan->groups.empty())
+    OCN_CUDA(cudaStreamWaitEvent(A, event(2 * (int)plan->groups.size() - 1), 0));
 }
 
 static bool graphs_enabled() {
@@ -1145,13 +1188,13 @@ int ocn_slice_depths(const ocn_slice_config* cfg, double* depths) {
 }
 
 // ---- cascades (K1)
-int ocn_cascades_create(ocn_ctx* ctx, int resolution, int count, const double* lengths,
-                        const double* band_min, const double* band_max,
-                        const uint32_t* cascade_index, const ocn_spectrum_params* params,
-                        ocn_cascades** out) {
+int ocn_cascades_create_multi(ocn_ctx* ctx, int resolution, int count, const double* lengths,
+                              const double* band_min, const double* band_max,
+                              const uint32_t* cascade_index, const ocn_spectrum_params* params,
+                              ocn_cascades** out) {
   return api_call(ctx, [&] {
     OCN_REQUIRE(ctx && out && lengths && band_min && band_max && params, "null argument");
-    OCN_REQUIRE(count >= 1 && count <= kMaxCascades, "cascade count %d out of range", count);
+    OCN_REQUIRE(count >= 1 && count <= kMaxGrids, "grid count %d out of range", count);
     if (!is_pow2(resolution) || resolution < 2)
       fail(OCN_ERR_CONFIG, "grid resolution must be a power of two >= 2");
     if (resolution > 16384) fail(OCN_ERR_CONFIG, "grid resolution above 16384 is not supported");
@@ -1159,9 +1202,9 @@ int ocn_cascades_create(ocn_ctx* ctx, int resolution, int count, const double* l
       if (!(lengths[c] > 0.0)) fail(OCN_ERR_CONFIG, "cascade length must be > 0");
       if (!(band_min[c] >= 0.0) || !(band_max[c] > band_min[c]))
         fail(OCN_ERR_CONFIG, "cascade band must satisfy 0 <= band_min < band_max");
+      int st = ocn_spectrum_validate(params + c);
+      if (st) fail(st, "%s", global_error().c_str());
     }
-    int st = ocn_spectrum_validate(params);
-    if (st) fail(st, "%s", global_error().c_str());
     DeviceScope ds(ctx);
     auto cas = std::make_unique<ocn_cascades>();
     cas->ctx = ctx;
@@ -1172,35 +1215,33 @@ int ocn_cascades_create(ocn_ctx* ctx, int resolution, int count, const double* l
     cas->band_max.assign(band_max, band_max + count);
     for (int c = 0; c < count; ++c)
       cas->cascade_index.push_back(cascade_index ? cascade_index[c] : (uint32_t)c);
-    cas->params = *params;
+    cas->params = params[0];
+    cas->grid_params.assign(params, params + count);
     const size_t nn = (size_t)resolution * resolution;
     cas->h0_f64.alloc(nn * count);
     cas->h0.alloc(nn * count);
     cas->in_band.alloc(nn * count);
     cas->spec.alloc(nn * count);
-    InitArgs a{};
-    a.n = resolution;
-    a.count = count;
+    std::vector<GridConst> gc(count);
     for (int c = 0; c < count; ++c) {
-      a.dk[c] = 2.0 * kPi / lengths[c];
-      a.length[c] = lengths[c];
-      a.band_min[c] = band_min[c];
-      a.band_max[c] = band_max[c];
-      a.cindex[c] = cas->cascade_index[c];
+      gc[c].dk = 2.0 * kPi / lengths[c];
+      gc[c].length = lengths[c];
+      gc[c].band_min = band_min[c];
+      gc[c].band_max = band_max[c];
+      gc[c].cindex = cas->cascade_index[c];
+      gc[c].p = params[c];
     }
-    a.p = *params;
-    a.h0_f64 = cas->h0_f64.p;
-    a.h0 = cas->h0.p;
-    a.in_band = cas->in_band.p;
-    k_spectrum_init<<<grid_for(ctx, nn * count), 256, 0, ctx->stream>>>(a);
+    cas->gconst.alloc(count);
+    OCN_CUDA(cudaMemcpyAsync(cas->gconst.p, gc.data(), count * sizeof(GridConst),
+                             cudaMemcpyHostToDevice, ctx->stream));
+    k_spectrum_init<<<grid_for(ctx, nn * count), 256, 0, ctx->stream>>>(
+        resolution, count, cas->gconst.p, cas->h0_f64.p, cas->h0.p, cas->in_band.p);
     OCN_LAUNCHED(ctx);
     std::vector<float2> tw = make_twiddles(resolution);
     cas->twiddle.alloc(tw.size());
     OCN_CUDA(cudaMemcpyAsync(cas->twiddle.p, tw.data(), tw.size() * sizeof(float2),
                              cudaMemcpyHostToDevice, ctx->stream));
     cas->group = (int)group_for(resolution, 1 << 30);
-    // two half-size scratch buffers let the row pass of the next group overlap
-    // the column pass of the current one (same L2 footprint)
     cas->nbuf = dual_stream(ctx) && cas->group >= 2 ? 2 : 1;
     if (cas->nbuf == 2) cas->group /= 2;
     cas->d_time.alloc(1);
@@ -1209,6 +1250,20 @@ int ocn_cascades_create(ocn_ctx* ctx, int resolution, int count, const double* l
     ctx_retain(ctx);
     *out = cas.release();
   });
+}
+
+int ocn_cascades_create(ocn_ctx* ctx, int resolution, int count, const double* lengths,
+                        const double* band_min, const double* band_max,
+                        const uint32_t* cascade_index, const ocn_spectrum_params* params,
+                        ocn_cascades** out) {
+  if (!params || count < 1 || count > kMaxGrids) {
+    global_error() = "bad cascade arguments";
+    if (ctx) ctx->last_error = global_error();
+    return OCN_ERR_ARG;
+  }
+  std::vector<ocn_spectrum_params> ps(count, *params);
+  return ocn_cascades_create_multi(ctx, resolution, count, lengths, band_min, band_max,
+                                   cascade_index, ps.data(), out);
 }
 
 int ocn_cascades_destroy(ocn_cascades* c) {
@@ -1240,7 +1295,7 @@ int ocn_cascades_download(ocn_cascades* c, int grid, double* h0, double* h0cn, u
       DevBuf<double2> d_cn(h0cn ? nn : 0);
       DevBuf<double4> d_w(waves ? nn : 0);
       k_grid_extras<<<grid_for(ctx, nn), 256, 0, ctx->stream>>>(
-          c->n, 2.0 * kPi / c->lengths[grid], c->params.gravity, src, d_cn.p, d_w.p);
+          c->n, 2.0 * kPi / c->lengths[grid], c->grid_params[grid].gravity, src, d_cn.p, d_w.p);
       OCN_LAUNCHED(ctx);
       if (h0cn)
         OCN_CUDA(cudaMemcpyAsync(h0cn, d_cn.p, nn * sizeof(double2), cudaMemcpyDeviceToHost,
@@ -1262,7 +1317,7 @@ int ocn_assemble_coefficients(ocn_cascades* c, int grid, double t, double chop, 
     const size_t nn = (size_t)c->n * c->n;
     DevBuf<double2> d(8 * nn);
     k_assemble_coef<<<grid_for(ctx, nn), 256, 0, ctx->stream>>>(
-        c->n, 2.0 * kPi / c->lengths[grid], c->params.gravity, t, chop,
+        c->n, 2.0 * kPi / c->lengths[grid], c->grid_params[grid].gravity, t, chop,
         c->h0_f64.p + (size_t)grid * nn, c->in_band.p + (size_t)grid * nn, d.p);
     OCN_LAUNCHED(ctx);
     OCN_CUDA(cudaMemcpyAsync(out, d.p, 8 * nn * sizeof(double2), cudaMemcpyDeviceToHost, ctx->stream));

@@ -206,6 +206,47 @@ class CascadeSet:
         return self._grids
 
 
+class CascadeInstances:
+    """Batched independent scenes: every instance is a
+    CascadeSet of `config` with its own SpectrumParams (e.g. its own seed); one
+    spectral step synthesises all of them (ocn_cascades_create_multi)."""
+
+    def __init__(self, config: CascadeConfig, params_list: Sequence[SpectrumParams],
+                 ctx: Context = None):
+        config.validate()
+        self.config = config
+        self.instances = len(params_list)
+        C_ = len(config.lengths)
+        lengths, bmin, bmax, cidx, ps = [], [], [], [], []
+        for p in params_list:
+            for c in range(C_):
+                lengths.append(config.lengths[c])
+                bmin.append(0.0 if c == 0 else config.cutoffs[c - 1])
+                bmax.append(config.cutoffs[c] if c + 1 < C_ else 1e300)
+                cidx.append(c)
+                ps.append(p)
+        self.ctx = ctx or Context.default()
+        arr = (SpectrumParams * len(ps))(*ps)
+        la = np.ascontiguousarray(lengths, np.float64)
+        bl = np.ascontiguousarray(bmin, np.float64)
+        bh = np.ascontiguousarray(bmax, np.float64)
+        ci = np.ascontiguousarray(cidx, np.uint32)
+        h = C.c_void_p()
+        check(lib().ocn_cascades_create_multi(self.ctx.h, config.resolution, len(ps), _dp(la), _dp(bl),
+                                              _dp(bh), ci.ctypes.data_as(_abi.u32), arr, C.byref(h)),
+              self.ctx.h, "cascade instances")
+        self.h = h
+        self.grids = len(ps)
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().ocn_cascades_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
 # --------------------------------------------------------------------- surface
 @dataclass
 class SurfaceGenOptions:

@@ -180,3 +180,20 @@ def test_assembly_properties(oc, port):
     J_fd = jx[:, 0] * jz[:, 1] - jx[:, 1] * jz[:, 0]
     corr = np.corrcoef(J_fd, a[:, 6])[0, 1]
     assert corr > 0.9, corr
+
+
+def test_instances_batched(oc, port):
+    """Config 4 shape: independent instances (own seeds) synthesised by one
+    spectral step over a multi-grid set; each instance equals its own oracle run."""
+    from paper_2503_03326_b200._types import SpectrumParams
+    cfg = oc.CascadeConfig(64, [256.0, 16.0, 4.0], [12 * math.pi / 16, 12 * math.pi / 4])
+    params = [config2_params(seed=s) for s in (0, 7, 63)]
+    inst = oc.CascadeInstances(cfg, params)
+    maps = oc.SurfaceMaps(inst)
+    maps.generate(2.0)
+    for k, p in enumerate(params):
+        want = port.generate_maps(64, list(cfg.lengths), list(cfg.cutoffs), p, 2.0)
+        for c in range(3):
+            for f in range(8):
+                got = maps.field(3 * k + c, f)
+                assert normwise_rel(got, want[c, f]) < TOL, (k, c, f)
