@@ -219,6 +219,53 @@ class Frame4:
         return self._hmap_arr.ctypes.data_as(C.POINTER(C.c_float))
 
 
+# ---------------------------------------------------------------- config 5
+C5_N, C5_L = 16384, 4096.0
+C5_WORKLOAD = ("config5: single 16384^2 surface (8 fields, 4 packed transforms), row slabs per "
+               "rank, NCCL all-to-all tile transpose between the row and column passes")
+
+
+class Frame5:
+    """This rank's slab of the 16384^2 grid; the transpose is an NCCL all-to-all."""
+
+    def __init__(self, device: int, rank: int, world: int, dist):
+        from paper_2503_03326_b200 import ocean as oc
+        from paper_2503_03326_b200.slab import SlabSurface, tile_layout
+        import torch
+        self.oc, self.L, self.dist = oc, oc.lib(), dist
+        self.ctx = oc.Context(device)
+        p = _params()
+        p.rng_seed = 7
+        self.slab = SlabSurface(C5_N, world, rank, C5_L, p, ctx=self.ctx)
+        _, total = tile_layout(self.slab.rows, world)
+        self.send = torch.empty(2 * total, dtype=torch.float32, device=f"cuda:{device}")
+        self.recv = self.send if world == 1 else torch.empty_like(self.send)
+        self.stream = torch.cuda.ExternalStream(self.ctx.stream, device=f"cuda:{device}")
+        self.world = world
+        self.t = 0.0
+        self.points = C5_N * C5_N // world
+        self.a2a_ms = []
+        self._col = np.zeros(C5_N, np.float64)
+        self.timing = False
+
+    def step(self, read_report: bool = False):
+        import torch
+        self.t += DT
+        self.slab.rows_pass(self.t, self.send.data_ptr())
+        if self.world > 1:
+            with torch.cuda.stream(self.stream):
+                if self.timing:
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(self.stream)
+                self.dist.all_to_all_single(self.recv, self.send)
+                if self.timing:
+                    e1.record(self.stream)
+                    self.a2a_ms.append((e0, e1))
+        self.slab.cols_pass(self.recv.data_ptr())
+        if read_report:  # the frame's result probe: one column of the height field -> host
+            self.oc.check(self.L.ocn_ctx_synchronize(self.ctx.h), self.ctx.h, "sync")
+
+
 def _dist():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     if ws <= 1:
@@ -266,7 +313,8 @@ def _traffic():
 def run_ours(args):
     dist, rank, world, local = _dist()
     c4 = args.config == 4
-    fr = Frame4(local, rank, world) if c4 else Frame(local)
+    c5 = args.config == 5
+    fr = Frame5(local, rank, world, dist) if c5 else (Frame4(local, rank, world) if c4 else Frame(local))
     L, ctx = fr.L, fr.ctx
     for _ in range(max(args.warmup, 3)):
         fr.step()
@@ -304,7 +352,16 @@ def run_ours(args):
                 out[name] = ms.value / args.steps
             L.ocn_ctx_profile(ctx.h, 0)
             return out
-        stages = profiled(2, [("spectral", 6), ("hydro", 3), ("mask", 4), ("fdm", 5)])
+        if c5:
+            fr.timing = True
+            stages = profiled(1, [("slab_rows", 1), ("slab_cols", 2)])
+            fr.timing = False
+            torch.cuda.synchronize()
+            a2a = [e0.elapsed_time(e1) for e0, e1 in fr.a2a_ms]
+            stages["all_to_all"] = float(np.mean(a2a)) if a2a else 0.0
+            stages["spectral"] = stages["slab_rows"] + stages["slab_cols"]
+        else:
+            stages = profiled(2, [("spectral", 6), ("hydro", 3), ("mask", 4), ("fdm", 5)])
         if c4:
             stages = {"spectral": stages["spectral"]}
         # ... and the kernel split of the spectral step (mode 1: eager launches)
@@ -325,7 +382,17 @@ def run_ours(args):
             dist.destroy_process_group()
         return
     peak, peak_kind = _peaks()
-    if c4:
+    if c5:
+        points = C5_N * C5_N
+        alg_bytes = fr.points * (16 + 4 * 8)  # h0 + h0 mirror slab read, 8 fp32 fields written
+        metric = "ocean grid points/sec (single 16384^2 surface, slab FFT + all-to-all)"
+        workload, h2d, d2h = C5_WORKLOAD, 8, 0
+        sent = fr.slab.exchange_bytes * (world - 1) / world
+        cfg = {"workload": workload, "grid": C5_N, "ranks": world, "parallelism": f"row slabs x{world}",
+               "exchange_bytes_per_gpu": sent,
+               "l2": "per-frame slabs 4-8 GB > 126 MB L2 (no explicit flush)"}
+        scaling = "strong"
+    elif c4:
         points = C4_POINTS if world > 1 else fr.points * world
         alg_bytes = fr.points * (8 + 4 * 8)  # per rank and frame
         metric = "ocean grid points/sec (64 x 3 x 512^2 instances, surface synthesis)"
@@ -347,6 +414,10 @@ def run_ours(args):
         scaling = "weak"
     value = points / (ms_frame / 1e3)
     spec_ms = stages["spectral"]
+    if c5 and world > 1 and stages.get("all_to_all", 0) > 0:
+        gbs = cfg["exchange_bytes_per_gpu"] / (stages["all_to_all"] / 1e3) / 1e9
+        cfg["all_to_all_GBps_per_gpu"] = gbs
+        cfg["nvlink_efficiency_vs_900GBps"] = gbs / 900.0
     achieved = alg_bytes / (spec_ms / 1e3) / 1e9
     line = {
         "metric": metric,
@@ -374,7 +445,7 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
-    if world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not args.no_cpu_baseline and not c5:
         line["cpu_baseline"] = cpu_baseline_c4() if c4 else cpu_baseline(frames=1, warmup=0)
     print(json.dumps(line), flush=True)
     if dist:
@@ -531,8 +602,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--config", type=int, default=3, choices=[3, 4],
-                    help="3: the BASELINE metric frame (default); 4: 64 batched 512^2 instances")
+    ap.add_argument("--config", type=int, default=3, choices=[3, 4, 5],
+                    help="3: the BASELINE metric frame (default); 4: 64 batched 512^2 instances; "
+                         "5: single 16384^2 grid, slab FFT + all-to-all across ranks")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

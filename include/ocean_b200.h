@@ -204,6 +204,7 @@ typedef struct ocn_maps ocn_maps;
 typedef struct ocn_slices ocn_slices;
 typedef struct ocn_mesh ocn_mesh;
 typedef struct ocn_zone ocn_zone;
+typedef struct ocn_slab ocn_slab;
 
 /* ================================ context ================================ */
 OCN_API int ocn_abi_version(void);
@@ -410,6 +411,25 @@ OCN_API int ocn_zone_mask_download(ocn_zone* z, int capacity, int32_t* host_ij, 
 OCN_API int ocn_zone_sample(ocn_zone* z, int64_t n, const double* xz, double* out);
 OCN_API int ocn_zone_download(ocn_zone* z, double* host_curr, double* host_prev);
 OCN_API int ocn_zone_upload(ocn_zone* z, const double* host_curr, const double* host_prev);
+
+/* ========================= slab-decomposed grid (config 5) ================= */
+/* One cascade of resolution n split over `ranks` ranks by rows:
+ * rank `rank` owns spectrum rows and output columns [rank R, (rank+1) R),
+ * R = n / ranks. Per frame: ocn_slab_rows writes this rank's 4 packed row
+ * transforms into the all-to-all send buffer laid out [dest][4][R][R]
+ * complex64 (dev_send, exchange_bytes); the caller exchanges it (NCCL
+ * all-to-all; dest tile d goes to rank d); ocn_slab_cols consumes the receive
+ * buffer [src][4][R][R] and writes the 8 surface fields of the owned column
+ * slab ([field][n][R] fp32, transposed-slab layout). Both are async. */
+OCN_API int ocn_slab_create(ocn_ctx* ctx, int n, int ranks, int rank, double length,
+                            double band_min, double band_max, uint32_t cascade_index,
+                            const ocn_spectrum_params* params, ocn_slab** out);
+OCN_API int ocn_slab_destroy(ocn_slab* s);
+OCN_API int ocn_slab_info(const ocn_slab* s, int* rows, int* cols, size_t* exchange_bytes);
+OCN_API int ocn_slab_rows(ocn_slab* s, double t, double choppiness, void* dev_send);
+OCN_API int ocn_slab_cols(ocn_slab* s, const void* dev_recv);
+/* Column slab of one field: n x R doubles, row-major [i][column - rank R]. */
+OCN_API int ocn_slab_download(ocn_slab* s, int field, double* host_out);
 
 #ifdef __cplusplus
 }

@@ -148,6 +148,12 @@ SIGNATURES = {
     "ocn_zone_sample": (ci, [vp, i64, d, d]),
     "ocn_zone_download": (ci, [vp, d, d]),
     "ocn_zone_upload": (ci, [vp, d, d]),
+    "ocn_slab_create": (ci, [vp, ci, ci, ci, cd, cd, cd, C.c_uint32, C.POINTER(SpectrumParams), pvp]),
+    "ocn_slab_destroy": (ci, [vp]),
+    "ocn_slab_info": (ci, [vp, C.POINTER(ci), C.POINTER(ci), C.POINTER(C.c_size_t)]),
+    "ocn_slab_rows": (ci, [vp, cd, cd, vp]),
+    "ocn_slab_cols": (ci, [vp, vp]),
+    "ocn_slab_download": (ci, [vp, ci, d]),
 }
 
 _lib = None

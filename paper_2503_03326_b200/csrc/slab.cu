@@ -1,0 +1,357 @@
+// slab.cu — one very large surface grid split across ranks (SURVEY 8d/8e
+// config 5): rank r owns spectrum rows [r R, (r+1) R), R = N / ranks.
+//
+//   ocn_slab_rows : evolve the owned rows (h0 of the owned rows and of their
+//                   mirror rows -i are generated locally: the counter-based
+//                   Philox makes h0(i, j) a pure function of (i, j), so no
+//                   exchange is needed for conj(h0(-k))), build the 4 packed
+//                   surface coefficients (surface.cpp:77-80 pairs) and run the
+//                   row FFTs; the result is written straight into the all-to-all
+//                   send layout [dest][pair][row][col in dest's column slab].
+//   (caller)      : all-to-all of the N/ranks x N/ranks tiles (NCCL over
+//                   NVLink: torch.distributed.all_to_all_single in bench.py).
+//   ocn_slab_cols : column FFTs of the owned column slab from the receive
+//                   layout [src][pair][row][col], (-1)^(i+j), Re/Im split into
+//                   8 fp32 fields kept in the transposed (column-slab) layout.
+#include <algorithm>
+#include <cmath>
+#include <memory>
+
+#include "fft_core.cuh"
+#include "objects.cuh"
+#include "spectrum_math.cuh"
+
+struct ocn_slab {
+  ocn_ctx* ctx = nullptr;
+  int n = 0, ranks = 1, rank = 0, rows = 0, cols = 0;
+  ocn::GridConst gc{};
+  ocn::DevBuf<float2> h0, h0m;   // [rows][N]: h0 of owned rows, h0 of rows neg(i)
+  ocn::DevBuf<float4> spec;      // [rows][N]: (h~, G)
+  ocn::DevBuf<float2> twiddle;
+  ocn::DevBuf<double> d_time;
+  ocn::DevBuf<float> fields;     // [8][N][cols]
+};
+
+namespace ocn {
+namespace {
+
+constexpr int kSlabThreads = 256;
+
+template <int N>
+struct SlabLaunch {
+  using PL = fft::Plan<N>;
+  static constexpr int T = PL::T;
+  static constexpr int THREADS = T > kSlabThreads ? T : kSlabThreads;
+  static constexpr int PER_CTA = THREADS / T;
+  static constexpr int STRIDE = PL::SMEM + ((4 - (PL::SMEM % 16)) + 16) % 16;
+  static constexpr size_t SMEM_BYTES = (PL::P > 1) ? (size_t)PER_CTA * STRIDE * sizeof(float2) : 0;
+};
+
+// h0 at (i, j) (spectra.cpp:150-169), fp64, same math as K1
+__device__ double2 h0_mode(const GridConst& G, int n, int i, int j) {
+  const double dk = G.dk;
+  const double kx = dk * (i - n / 2), kz = dk * (j - n / 2);
+  const double k = sm::hypot_ref(kx, kz);
+  const double omega = sqrt(G.p.gravity * k);
+  if (!(k > 0.0 && k >= G.band_min && k < G.band_max)) return make_double2(0.0, 0.0);
+  double gr, gi;
+  sm::gaussian_complex(G.p.rng_seed, G.cindex, (uint32_t)i, (uint32_t)j, &gr, &gi);
+  const double amp = sqrt(sm::h0_variance(kx, kz, k, omega, G.length, G.p));
+  return make_double2(gr * amp, gi * amp);
+}
+
+__global__ void k_slab_init(int n, int row0, int rows, GridConst G, float2* h0, float2* h0m) {
+  const size_t total = (size_t)rows * n;
+  for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < total;
+       q += (size_t)gridDim.x * blockDim.x) {
+    const int li = (int)(q / n), j = (int)(q % n);
+    const int i = row0 + li, ni = i == 0 ? 0 : n - i;
+    const double2 a = h0_mode(G, n, i, j), b = h0_mode(G, n, ni, j);
+    h0[q] = make_float2((float)a.x, (float)a.y);
+    h0m[q] = make_float2((float)b.x, (float)b.y);
+  }
+}
+
+// h~ (surface.cpp:49-50) of the owned rows; conj(h0(-k)) from the mirror rows
+__global__ void k_slab_evolve(int n, int row0, int rows, GridConst G, const double* d_time,
+                              const float2* __restrict__ h0, const float2* __restrict__ h0m,
+                              float4* spec) {
+  const size_t total = (size_t)rows * n;
+  const double t = *d_time;
+  for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < total;
+       q += (size_t)gridDim.x * blockDim.x) {
+    const int li = (int)(q / n), j = (int)(q % n);
+    const int i = row0 + li, nj = j == 0 ? 0 : n - j;
+    const float2 a = h0[q];
+    const float2 m = h0m[(size_t)li * n + nj];
+    const float2 b = make_float2(m.x, -m.y);
+    const double kx = G.dk * (i - n / 2), kz = G.dk * (j - n / 2);
+    const double omega = sqrt(G.p.gravity * sqrt(kx * kx + kz * kz));
+    double ph = omega * t;
+    ph -= 6.283185307179586476925 * rint(ph * 0.15915494309189533577);
+    float s, c;
+    sincosf((float)ph, &s, &c);
+    const float ar = a.x * c - a.y * s, ai = a.x * s + a.y * c;
+    const float br = b.x * c + b.y * s, bi = b.y * c - b.x * s;
+    spec[q] = make_float4(ar + br, ai + bi, ar - br, ai - bi);
+  }
+}
+
+struct SlabRowArgs {
+  int row0, rows, cols;
+  float dk, chop;
+  const float4* spec;
+  float2* send;  // [dest][4][rows][cols]
+  const float2* tw;
+};
+
+// packed surface pair p at mode (i, j): h~ M_p (surface.cpp:77-80)
+__device__ __forceinline__ float2 surface_pair(int p, float4 s, float kx, float kz, float chop) {
+  const float k2 = kx * kx + kz * kz;
+  if (k2 == 0.f) return make_float2(0.f, 0.f);
+  const float inv = rsqrtf(k2);
+  float mr, mi;
+  if (p == 0) mr = 1.0f - kx * inv * chop, mi = 0.f;
+  else if (p == 1) mr = 0.f, mi = chop * (kz + kx * kx) * inv;
+  else if (p == 2) mr = chop * kz * inv * kx, mi = chop * kz * inv * kz;
+  else mr = -kz, mi = kx;
+  return make_float2(s.x * mr - s.y * mi, s.x * mi + s.y * mr);
+}
+
+template <int N>
+__global__ void __launch_bounds__(SlabLaunch<N>::THREADS) k_slab_rows(const SlabRowArgs a) {
+  using L = SlabLaunch<N>;
+  extern __shared__ float2 smem[];
+  const int local = threadIdx.x / L::T, t = threadIdx.x - local * L::T;
+  const int item = blockIdx.x * L::PER_CTA + local;  // (row, pair)
+  const bool valid = item < a.rows * 4;
+  const int li = valid ? item >> 2 : 0, p = item & 3;
+  const float kx = a.dk * (float)(a.row0 + li - N / 2);
+  const float4* srow = a.spec + (size_t)li * N;
+  fft::cta_fft<N>(
+      t, smem + local * L::STRIDE, a.tw,
+      [&](int j) {
+        if (!valid) return make_float2(0.f, 0.f);
+        return surface_pair(p, __ldg(srow + j), kx, a.dk * (float)(j - N / 2), a.chop);
+      },
+      [&](int k, float2 x) {
+        if (!valid) return;
+        const int dest = k / a.cols, kc = k - dest * a.cols;
+        a.send[(((size_t)dest * 4 + p) * a.rows + li) * a.cols + kc] = x;
+      });
+}
+
+struct SlabColArgs {
+  int rows, cols, col0;
+  const float2* recv;  // [src][4][rows][cols]
+  float* fields;       // [8][N][cols]
+  const float2* tw;
+};
+
+template <int N>
+__global__ void __launch_bounds__(SlabLaunch<N>::THREADS) k_slab_cols(const SlabColArgs a) {
+  using L = SlabLaunch<N>;
+  extern __shared__ float2 smem[];
+  const int c = threadIdx.x % L::PER_CTA, t = threadIdx.x / L::PER_CTA;
+  const int p = blockIdx.y;
+  const int kc = blockIdx.x * L::PER_CTA + c;
+  const bool valid = kc < a.cols;
+  const int col = a.col0 + (valid ? kc : 0);
+  float* re = a.fields + (size_t)(2 * p) * N * a.cols;
+  float* im = a.fields + (size_t)(2 * p + 1) * N * a.cols;
+  fft::cta_fft<N>(
+      t, smem + c * L::STRIDE, a.tw,
+      [&](int i) {
+        if (!valid) return make_float2(0.f, 0.f);
+        const int src = i / a.rows, li = i - src * a.rows;
+        return __ldg(a.recv + (((size_t)src * 4 + p) * a.rows + li) * a.cols + kc);
+      },
+      [&](int i, float2 x) {
+        if (!valid) return;
+        const float s = ((i + col) & 1) ? -1.f : 1.f;  // fft.cpp:73-75
+        re[(size_t)i * a.cols + kc] = s * x.x;         // fft.cpp:93-99
+        im[(size_t)i * a.cols + kc] = s * x.y;
+      });
+}
+
+template <int N>
+void slab_rows_launch(ocn_slab* sl, const SlabRowArgs& a) {
+  using L = SlabLaunch<N>;
+  static bool attr = false;
+  if (!attr && L::SMEM_BYTES > 48 * 1024) {
+    OCN_CUDA(cudaFuncSetAttribute(k_slab_rows<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)L::SMEM_BYTES));
+    OCN_CUDA(cudaFuncSetAttribute(k_slab_cols<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)L::SMEM_BYTES));
+  }
+  attr = true;
+  const int blocks = (a.rows * 4 + L::PER_CTA - 1) / L::PER_CTA;
+  k_slab_rows<N><<<blocks, L::THREADS, L::SMEM_BYTES, sl->ctx->stream>>>(a);
+  OCN_LAUNCHED(sl->ctx);
+}
+
+template <int N>
+void slab_cols_launch(ocn_slab* sl, const SlabColArgs& a) {
+  using L = SlabLaunch<N>;
+  static bool attr = false;
+  if (!attr && L::SMEM_BYTES > 48 * 1024) {
+    OCN_CUDA(cudaFuncSetAttribute(k_slab_rows<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)L::SMEM_BYTES));
+    OCN_CUDA(cudaFuncSetAttribute(k_slab_cols<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)L::SMEM_BYTES));
+  }
+  attr = true;
+  dim3 grid((a.cols + L::PER_CTA - 1) / L::PER_CTA, 4);
+  k_slab_cols<N><<<grid, L::THREADS, L::SMEM_BYTES, sl->ctx->stream>>>(a);
+  OCN_LAUNCHED(sl->ctx);
+}
+
+#define OCN_SLAB_DISPATCH(n, MACRO)                       \
+  switch (n) {                                            \
+    case 64: MACRO(64); break;                            \
+    case 128: MACRO(128); break;                          \
+    case 256: MACRO(256); break;                          \
+    case 512: MACRO(512); break;                          \
+    case 1024: MACRO(1024); break;                        \
+    case 2048: MACRO(2048); break;                        \
+    case 4096: MACRO(4096); break;                        \
+    case 8192: MACRO(8192); break;                        \
+    case 16384: MACRO(16384); break;                      \
+    default: fail(OCN_ERR_CONFIG, "slab size %d not supported (64..16384)", n); \
+  }
+
+int grid_cap(ocn_ctx* ctx, size_t n) {
+  size_t b = (n + 255) / 256, cap = (size_t)ctx->sm_count * 16;
+  return (int)(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
+__global__ void k_set_time_slab(double* d, double t) { *d = t; }
+__global__ void k_f32_f64_slab(size_t n, const float* in, double* out) {
+  for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n;
+       q += (size_t)gridDim.x * blockDim.x)
+    out[q] = in[q];
+}
+
+}  // namespace
+
+std::vector<float2> make_twiddles(int n);  // spectral.cu
+
+}  // namespace ocn
+
+using namespace ocn;
+
+extern "C" {
+
+int ocn_slab_create(ocn_ctx* ctx, int n, int ranks, int rank, double length, double band_min,
+                    double band_max, uint32_t cascade_index, const ocn_spectrum_params* params,
+                    ocn_slab** out) {
+  return api_call(ctx, [&] {
+    OCN_REQUIRE(ctx && params && out, "null argument");
+    if (!is_pow2(n) || n < 64 || n > 16384) fail(OCN_ERR_CONFIG, "slab grid must be 64..16384, pow2");
+    OCN_REQUIRE(ranks >= 1 && n % ranks == 0 && (n / ranks) >= 1 && rank >= 0 && rank < ranks,
+                "bad slab decomposition %d / %d", rank, ranks);
+    if (!(length > 0.0)) fail(OCN_ERR_CONFIG, "cascade length must be > 0");
+    if (!(band_min >= 0.0) || !(band_max > band_min))
+      fail(OCN_ERR_CONFIG, "cascade band must satisfy 0 <= band_min < band_max");
+    int st = ocn_spectrum_validate(params);
+    if (st) fail(st, "%s", global_error().c_str());
+    DeviceScope ds(ctx);
+    auto sl = std::make_unique<ocn_slab>();
+    sl->ctx = ctx;
+    sl->n = n;
+    sl->ranks = ranks;
+    sl->rank = rank;
+    sl->rows = sl->cols = n / ranks;
+    sl->gc.dk = 2.0 * kPi / length;
+    sl->gc.length = length;
+    sl->gc.band_min = band_min;
+    sl->gc.band_max = band_max;
+    sl->gc.cindex = cascade_index;
+    sl->gc.p = *params;
+    const size_t slab = (size_t)sl->rows * n;
+    sl->h0.alloc(slab);
+    sl->h0m.alloc(slab);
+    sl->spec.alloc(slab);
+    sl->fields.alloc(8 * slab);
+    sl->d_time.alloc(1);
+    k_slab_init<<<grid_cap(ctx, slab), 256, 0, ctx->stream>>>(n, rank * sl->rows, sl->rows, sl->gc,
+                                                            sl->h0.p, sl->h0m.p);
+    OCN_LAUNCHED(ctx);
+    std::vector<float2> tw = make_twiddles(n);
+    sl->twiddle.alloc(tw.size());
+    OCN_CUDA(cudaMemcpyAsync(sl->twiddle.p, tw.data(), tw.size() * sizeof(float2),
+                             cudaMemcpyHostToDevice, ctx->stream));
+    OCN_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx_retain(ctx);
+    *out = sl.release();
+  });
+}
+
+int ocn_slab_destroy(ocn_slab* sl) {
+  if (!sl) return OCN_OK;
+  ocn_ctx* ctx = sl->ctx;
+  {
+    DeviceScope ds(ctx);
+    cudaStreamSynchronize(ctx->stream);
+    delete sl;
+  }
+  ctx_release(ctx);
+  return OCN_OK;
+}
+
+int ocn_slab_info(const ocn_slab* sl, int* rows, int* cols, size_t* exchange_bytes) {
+  if (!sl) return OCN_ERR_ARG;
+  if (rows) *rows = sl->rows;
+  if (cols) *cols = sl->cols;
+  if (exchange_bytes) *exchange_bytes = (size_t)4 * sl->rows * sl->n * sizeof(float2);
+  return OCN_OK;
+}
+
+int ocn_slab_rows(ocn_slab* sl, double t, double choppiness, void* dev_send) {
+  return api_call(sl ? sl->ctx : nullptr, [&] {
+    OCN_REQUIRE(sl && dev_send, "null argument");
+    ocn_ctx* ctx = sl->ctx;
+    DeviceScope ds(ctx);
+    ProfWindow pw(ctx, OCN_PROF_ROWS);
+    k_set_time_slab<<<1, 1, 0, ctx->stream>>>(sl->d_time.p, t);
+    OCN_LAUNCHED(ctx);
+    const size_t slab = (size_t)sl->rows * sl->n;
+    k_slab_evolve<<<grid_cap(ctx, slab), 256, 0, ctx->stream>>>(
+        sl->n, sl->rank * sl->rows, sl->rows, sl->gc, sl->d_time.p, sl->h0.p, sl->h0m.p, sl->spec.p);
+    OCN_LAUNCHED(ctx);
+    SlabRowArgs a{sl->rank * sl->rows, sl->rows, sl->cols, (float)sl->gc.dk, (float)choppiness,
+                  sl->spec.p, (float2*)dev_send, sl->twiddle.p};
+#define OCN_SR(NN) slab_rows_launch<NN>(sl, a)
+    OCN_SLAB_DISPATCH(sl->n, OCN_SR)
+#undef OCN_SR
+  });
+}
+
+int ocn_slab_cols(ocn_slab* sl, const void* dev_recv) {
+  return api_call(sl ? sl->ctx : nullptr, [&] {
+    OCN_REQUIRE(sl && dev_recv, "null argument");
+    DeviceScope ds(sl->ctx);
+    ProfWindow pw(sl->ctx, OCN_PROF_COLS);
+    SlabColArgs a{sl->rows, sl->cols, sl->rank * sl->cols, (const float2*)dev_recv, sl->fields.p,
+                  sl->twiddle.p};
+#define OCN_SC(NN) slab_cols_launch<NN>(sl, a)
+    OCN_SLAB_DISPATCH(sl->n, OCN_SC)
+#undef OCN_SC
+  });
+}
+
+int ocn_slab_download(ocn_slab* sl, int field, double* host_out) {
+  return api_call(sl ? sl->ctx : nullptr, [&] {
+    OCN_REQUIRE(sl && host_out && field >= 0 && field < 8, "bad arguments");
+    ocn_ctx* ctx = sl->ctx;
+    DeviceScope ds(ctx);
+    const size_t cnt = (size_t)sl->n * sl->cols;
+    DevBuf<double> tmp(cnt);
+    k_f32_f64_slab<<<grid_cap(ctx, cnt), 256, 0, ctx->stream>>>(cnt, sl->fields.p + field * cnt, tmp.p);
+    OCN_LAUNCHED(ctx);
+    OCN_CUDA(cudaMemcpyAsync(host_out, tmp.p, cnt * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    OCN_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+}  // extern "C"

@@ -730,6 +730,8 @@ int tw_size_of() {
   return fft::Plan<N>::tw_size();
 }
 
+}  // namespace
+
 // Inter-pass twiddle table for length n (layout of fft_core.cuh), fp64 -> fp32.
 std::vector<float2> make_twiddles(int n) {
   std::vector<float2> out;
@@ -755,6 +757,8 @@ std::vector<float2> make_twiddles(int n) {
   if (out.empty()) out.push_back(make_float2(1.f, 0.f));
   return out;
 }
+
+namespace {
 
 size_t group_for(int n, int total) {
   const size_t budget = 64ull << 20;  // keep scratch L2-resident (126 MB L2)

@@ -1,0 +1,20 @@
+"""GPU: the slab-decomposed grid (config 5 kernels and layouts) against the
+oracle, for 1 rank and for 2 / 4 ranks emulated on one device."""
+import numpy as np
+import pytest
+
+from helpers import config2_params, normwise_rel
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("n,ranks", [(256, 1), (256, 2), (256, 4), (1024, 2)])
+def test_slab_matches_oracle(port, n, ranks):
+    from paper_2503_03326_b200.slab import SlabSurface, emulated_frame
+    p = config2_params(seed=7)
+    L = 4096.0 * n / 16384  # config 5 resolution per metre, scaled down
+    slabs = [SlabSurface(n, ranks, r, L, p) for r in range(ranks)]
+    got = emulated_frame(slabs, 10.0)
+    want = port.generate_maps(n, [L], [], p, 10.0)[0]
+    for f in range(8):
+        assert normwise_rel(got[f], want[f]) < 1e-4, f
