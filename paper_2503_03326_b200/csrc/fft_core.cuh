@@ -161,6 +161,36 @@ struct Plan {
 
 __device__ __forceinline__ int pad32(int i) { return i + (i >> 5); }
 
+// Shared stride (float2) between the buffers of the transforms one CTA runs
+// side by side, chosen so no half-warp of 64-bit shared accesses has a bank
+// conflict in any pass (checked by brute-force simulation of the access
+// pattern, tools/fft_banks.py):
+//  * transform-major lanes (t fastest, the row kernels): Plan::SMEM itself;
+//  * column-major lanes (PC columns per CTA, column index fastest, the column
+//    kernels): a half-warp spans min(PC, 16) buffers, so the stride must
+//    spread them over distinct bank pairs: odd when PC >= 16, else
+//    == 16 / PC (mod 32 / PC).
+constexpr int col_stride(int smem, int pc) {
+  if (pc >= 16) return smem | 1;
+  if (pc <= 1) return smem;
+  int s = smem;
+  while (s % (32 / pc) != 16 / pc) ++s;
+  return s;
+}
+
+template <int N, int MIN_THREADS = 256>
+struct CtaLaunch {
+  using PL = Plan<N>;
+  static constexpr int T = PL::T;
+  static constexpr int THREADS = T > MIN_THREADS ? T : MIN_THREADS;
+  static constexpr int PER_CTA = THREADS / T;  // transforms per CTA
+  static constexpr int ROW_STRIDE = PL::SMEM;
+  static constexpr int COL_STRIDE = col_stride(PL::SMEM, PER_CTA);
+  static constexpr size_t ROW_SMEM_BYTES = PL::P > 1 ? (size_t)PER_CTA * ROW_STRIDE * 8 : 0;
+  static constexpr size_t COL_SMEM_BYTES = PL::P > 1 ? (size_t)PER_CTA * COL_STRIDE * 8 : 0;
+  static constexpr size_t SMEM_BYTES = ROW_SMEM_BYTES > COL_SMEM_BYTES ? ROW_SMEM_BYTES : COL_SMEM_BYTES;
+};
+
 // One CTA-cooperative transform. t in [0, T). `load(n)` returns input element
 // n, `store(k, x)` consumes output element k. `sm` = this transform's padded
 // shared buffer (Plan<N>::SMEM float2). `tw` = the per-N twiddle table.
@@ -176,10 +206,18 @@ __device__ __forceinline__ void fft_sync() {
   else __syncthreads();
 }
 
-template <int N, bool WARP = false, bool LOAD_SM = false, bool STORE_SM = false, class Load,
-          class Store>
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
+
+// `on_free()` (optional) is called by every thread right after the last
+// shared-memory reads of the transform, before the final DFT and stores: from
+// then on `sm` may be reused (e.g. refilled by TMA for the next tile).
+//   TW_SM    : `tw` points to shared memory (plain loads instead of __ldg)
+template <int N, bool WARP = false, bool LOAD_SM = false, bool STORE_SM = false, bool TW_SM = false,
+          class Load, class Store, class Free = NoHook>
 __device__ __forceinline__ void cta_fft(int t, float2* sm, const float2* __restrict__ tw,
-                                        Load&& load, Store&& store) {
+                                        Load&& load, Store&& store, Free&& on_free = Free{}) {
   using PL = Plan<N>;
   constexpr int E = PL::E, T = PL::T, P = PL::P;
   static_assert(!WARP || T <= 32, "warp-synchronous FFT needs T <= 32");
@@ -215,10 +253,14 @@ __device__ __forceinline__ void cta_fft(int t, float2* sm, const float2* __restr
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           float2 x = sm[pad32(b + r * (N / R))];
-          if (r > 0) x = cmul(x, __ldg(twp + r * NS + bm));
+          if (r > 0) {
+            if constexpr (TW_SM) x = cmul(x, twp[r * NS + bm]);
+            else x = cmul(x, __ldg(twp + r * NS + bm));
+          }
           v[q * R + r] = x;
         }
       }
+      if constexpr (p == P - 1) on_free();
       static_for<0, Q>([&](auto qi) {
         constexpr int q = decltype(qi)::value;
         dft_dif<R, q * R>(v);

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "tma.cuh"
 
 namespace ocn {
 
@@ -95,6 +96,8 @@ struct ocn_cascades {
   ocn::DevBuf<double> d_time;   // frame time read by k_evolve (set per frame)
   int group = 1;                // transforms per group
   int nbuf = 1;                 // scratch buffers (2: row/column passes overlap)
+  CUtensorMap cols_map[2];      // TMA source map of each scratch buffer (column pass)
+  bool cols_map_ok = false;
   std::map<std::pair<const void*, const void*>, std::unique_ptr<ocn::SpectralPlan>> plans;
 };
 

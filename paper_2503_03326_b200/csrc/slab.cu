@@ -38,14 +38,7 @@ namespace {
 constexpr int kSlabThreads = 256;
 
 template <int N>
-struct SlabLaunch {
-  using PL = fft::Plan<N>;
-  static constexpr int T = PL::T;
-  static constexpr int THREADS = T > kSlabThreads ? T : kSlabThreads;
-  static constexpr int PER_CTA = THREADS / T;
-  static constexpr int STRIDE = PL::SMEM + ((4 - (PL::SMEM % 16)) + 16) % 16;
-  static constexpr size_t SMEM_BYTES = (PL::P > 1) ? (size_t)PER_CTA * STRIDE * sizeof(float2) : 0;
-};
+using SlabLaunch = fft::CtaLaunch<N, kSlabThreads>;
 
 // h0 at (i, j) (spectra.cpp:150-169), fp64, same math as K1
 __device__ double2 h0_mode(const GridConst& G, int n, int i, int j) {
@@ -129,7 +122,7 @@ __global__ void __launch_bounds__(SlabLaunch<N>::THREADS) k_slab_rows(const Slab
   const float kx = a.dk * (float)(a.row0 + li - N / 2);
   const float4* srow = a.spec + (size_t)li * N;
   fft::cta_fft<N>(
-      t, smem + local * L::STRIDE, a.tw,
+      t, smem + local * L::ROW_STRIDE, a.tw,
       [&](int j) {
         if (!valid) return make_float2(0.f, 0.f);
         return surface_pair(p, __ldg(srow + j), kx, a.dk * (float)(j - N / 2), a.chop);
@@ -160,7 +153,7 @@ __global__ void __launch_bounds__(SlabLaunch<N>::THREADS) k_slab_cols(const Slab
   float* re = a.fields + (size_t)(2 * p) * N * a.cols;
   float* im = a.fields + (size_t)(2 * p + 1) * N * a.cols;
   fft::cta_fft<N>(
-      t, smem + c * L::STRIDE, a.tw,
+      t, smem + c * L::COL_STRIDE, a.tw,
       [&](int i) {
         if (!valid) return make_float2(0.f, 0.f);
         const int src = i / a.rows, li = i - src * a.rows;

@@ -13,9 +13,11 @@
 //   k_rows<N>    : per (row, transform of the group): the packed coefficient
 //                  X + iY = spec * multiplier(k) generated in registers (no
 //                  coefficient arrays in HBM), then the row FFT -> scratch
-//   k_cols<N>    : column FFT of scratch, (-1)^(i+j), Re -> field X,
-//                  Im -> field Y (fp32 maps / slices, row-major [i][j])
-// The group size keeps scratch (group * N^2 * 8 B) L2-resident at N = 1024.
+//   k_cols_tma<N>: persistent column FFT of scratch fed by TMA (k_cols<N>
+//                  with direct loads outside 128 <= N <= 4096), (-1)^(i+j),
+//                  Re -> field X, Im -> field Y (fp32, row-major [i][j])
+// Transforms run in groups sharing one scratch buffer (group * N^2 * 8 B, 1 GB
+// budget; see group_for).
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -23,6 +25,7 @@
 #include "fft_core.cuh"
 #include "objects.cuh"
 #include "spectrum_math.cuh"
+#include "tma.cuh"
 
 namespace ocn {
 
@@ -44,6 +47,26 @@ void ctx_release(ocn_ctx* ctx) {
   for (cudaEvent_t e : ctx->prof_pool) cudaEventDestroy(e);
   delete ctx;
 }
+bool tma::encode_f32(CUtensorMap* map, int rank, void* base, const uint64_t* dims,
+                     const uint64_t* strides, const uint32_t* box) {
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault,
+                                         &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      p = nullptr;
+    }
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  if (!fn) return false;
+  const cuuint32_t elem[5] = {1, 1, 1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank, base, dims, strides, box, elem,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 static void cascades_release(ocn_cascades* c) {
   if (!c || --c->refs != 0) return;
   ocn_ctx* ctx = c->ctx;
@@ -60,16 +83,7 @@ namespace {
 constexpr int kThreads = 256;
 
 template <int N>
-struct Launch {
-  using PL = fft::Plan<N>;
-  static constexpr int T = PL::T;
-  static constexpr int THREADS = T > kThreads ? T : kThreads;
-  static constexpr int PER_CTA = THREADS / T;  // transforms per CTA
-  // per-transform shared stride: >= SMEM and == 4 (mod 16) float2 so that
-  // neighbouring transforms start 8 banks apart
-  static constexpr int STRIDE = PL::SMEM + ((4 - (PL::SMEM % 16)) + 16) % 16;
-  static constexpr size_t SMEM_BYTES = (PL::P > 1) ? (size_t)PER_CTA * STRIDE * sizeof(float2) : 0;
-};
+using Launch = fft::CtaLaunch<N, kThreads>;
 
 // ------------------------------------------------------------------ K1
 // generate_h0, spectra.cpp:150-169, one thread per mode of every grid (fp64,
@@ -286,7 +300,7 @@ __global__ void __launch_bounds__(Launch<N>::THREADS) k_rows(const RowArgs a) {
   const bool valid = item < a.items;
   const int row = valid ? item / a.G : 0;
   const int gi = valid ? item - row * a.G : 0;
-  float2* sm = smem + local * L::STRIDE;
+  float2* sm = smem + local * L::ROW_STRIDE;
   float2* out = a.scratch + ((size_t)gi * N + row) * N;
   if constexpr (PLAIN) {
     const float2* in = a.src + ((size_t)gi * N + row) * N;
@@ -331,7 +345,8 @@ struct WarpLaunch {
   static_assert(PL::T <= 32, "warp kernels need T <= 32");
   static constexpr int T = PL::T;
   static constexpr int TPW = 32 / T;  // transforms per warp
-  static constexpr int STRIDE = Launch<N>::STRIDE;
+  static constexpr int STRIDE = Launch<N>::ROW_STRIDE;
+  static constexpr int TWN = (PL::tw_size() + 15) / 16 * 16;  // shared twiddle slots
   static constexpr int COLS_WARPS = 8;
   static constexpr int CC = COLS_WARPS * TPW;  // columns per column-CTA
 };
@@ -363,7 +378,10 @@ __global__ void __launch_bounds__(256, 2) k_rows_w(const RowArgs a) {
   float2* sw0 = sv0 + N;
   float* sk = reinterpret_cast<float*>(sw0 + N);
   float* sinv = sk + N;
-  float2* bufs = PLAIN ? reinterpret_cast<float2*>(smem4) : reinterpret_cast<float2*>(smem4 + 2 * N);
+  // inter-pass twiddles in shared memory (no global loads in the FFT passes)
+  float2* stw = PLAIN ? reinterpret_cast<float2*>(smem4) : reinterpret_cast<float2*>(smem4 + 2 * N);
+  float2* bufs = stw + W::TWN;
+  for (int i = threadIdx.x; i < fft::Plan<N>::tw_size(); i += blockDim.x) stw[i] = __ldg(a.tw + i);
   const int row = blockIdx.x;
   const int warps = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -393,8 +411,8 @@ __global__ void __launch_bounds__(256, 2) k_rows_w(const RowArgs a) {
       sk[j] = k;
       sinv[j] = inv;
     }
-    __syncthreads();
   }
+  __syncthreads();
   const int slots = (seg_count + W::TPW - 1) / W::TPW;
   float2* buf = bufs + (size_t)(warp * W::TPW + sub) * W::STRIDE;
   for (int slot = warp; slot < slots; slot += warps) {
@@ -409,16 +427,16 @@ __global__ void __launch_bounds__(256, 2) k_rows_w(const RowArgs a) {
       const float2* in = a.src + ((size_t)gi * N + row) * N;
       for (int j = t; j < N; j += T) buf[fft::pad32(j)] = valid ? __ldg(in + j) : make_float2(0.f, 0.f);
       __syncwarp();
-      fft::cta_fft<N, true, true, false>(
-          t, buf, a.tw, [&](int j) { return buf[fft::pad32(j)]; }, store);
+      fft::cta_fft<N, true, true, false, true>(
+          t, buf, stw, [&](int j) { return buf[fft::pad32(j)]; }, store);
     } else {
       const XformDesc d = a.desc[gi];
       if constexpr (MODE == kRowSurface) {
         // surface pairs: X + iY = h~ M(kx, kz) (surface.cpp:77-80 packing)
         const float chop = a.chop, dk = dkf;
         const int kind = d.kind;
-        fft::cta_fft<N, true, false, false>(
-            t, buf, a.tw,
+        fft::cta_fft<N, true, false, false, true>(
+            t, buf, stw,
             [&](int j) {
               const float2 h = sht[j];
               const float inv = sinv[j];
@@ -446,8 +464,8 @@ __global__ void __launch_bounds__(256, 2) k_rows_w(const RowArgs a) {
         const float y0 = d.y0, y1 = d.y1, y0l = d.y0 * kLog2e, y1l = d.y1 * kLog2e;
         const bool up0 = y0 > 0.f, up1 = y1 > 0.f;
         const int kind = d.kind;
-        fft::cta_fft<N, true, false, false>(
-            t, buf, a.tw,
+        fft::cta_fft<N, true, false, false, true>(
+            t, buf, stw,
             [&](int j) {
               const float2 z = Z[j];
               const float k = sk[j];
@@ -539,7 +557,7 @@ __global__ void __launch_bounds__(Launch<N>::THREADS) k_cols(const ColArgs a) {
   const int col = blockIdx.x * L::PER_CTA + c;
   const int xf = blockIdx.y;
   const bool valid = col < N;
-  float2* sm = smem + c * L::STRIDE;
+  float2* sm = smem + c * L::COL_STRIDE;
   const float2* in = a.scratch + (size_t)xf * N * N + (valid ? col : 0);
   if constexpr (COMPLEX_OUT) {
     float2* out = a.out_c + (size_t)xf * N * N;
@@ -561,6 +579,105 @@ __global__ void __launch_bounds__(Launch<N>::THREADS) k_cols(const ColArgs a) {
           __stcs(d.out_re + (size_t)r * N + col, s * x.x);  // fft.cpp:93-99 split
           if (d.out_im) __stcs(d.out_im + (size_t)r * N + col, s * x.y);
         });
+  }
+}
+
+// Column pass, persistent and TMA-fed (128 <= N <= 4096). A CTA walks the
+// column tiles [N rows][PC columns] (tile = transform x column block) with a
+// ring of STAGES shared buffers: one elected thread keeps STAGES - 1 tiles in
+// flight with one 4-D cp.async.bulk.tensor load each (completion on an
+// mbarrier) while the CTA transforms the landed tile in place (dense
+// [row][column] layout read by pass 0, padded per-column layout for the
+// exchange) and refills the buffer as soon as its last shared reads are done.
+// Twiddles live in shared memory, so the warps' only global accesses are the
+// output stores ((-1)^(i+j) sign and Re / Im split fused, evict-first).
+// Measured on B200 (config 3): this ring of 3 x 8-column tiles beat a
+// 2 x 4-column ring with TMA-store epilogue and 2 CTAs / SM (1.36 vs 2.06 ms
+// spectral per frame: the store drain serialised the ring).
+template <int N>
+struct ColTma {
+  using PL = fft::Plan<N>;
+  static constexpr int T = PL::T;
+  static constexpr int THREADS = T > 256 ? T : 256;
+  static constexpr int PC = THREADS / T;  // columns per tile
+  static constexpr int STRIDE = fft::col_stride(PL::SMEM, PC);
+  static constexpr int DENSE = N * PC;  // float2 per tile
+  static constexpr int PADDED = PC * STRIDE;
+  static constexpr int STAGE = ((DENSE > PADDED ? DENSE : PADDED) + 15) / 16 * 16;
+  static constexpr int TW = PL::tw_size();
+  static constexpr int STAGES = (227 * 1024 - TW * 8 - 64) / (STAGE * 8) >= 3 ? 3 : 2;
+  static constexpr uint32_t TILE_BYTES = (uint32_t)DENSE * 8;
+  static constexpr size_t SMEM = ((size_t)STAGES * STAGE + TW) * 8 + STAGES * 8;
+  static constexpr int BR = N < 256 ? N : 256;  // rows per box dimension
+  static constexpr bool OK = PL::P > 1 && N >= 128 && N <= 4096 && SMEM <= 227 * 1024;
+};
+
+// columns per tile of the TMA column kernel, 0 outside its range
+int cols_tma_pc(int n) { return n >= 128 && n <= 4096 ? 8192 / n : 0; }
+
+template <int N, bool COMPLEX_OUT>
+__global__ void __launch_bounds__(ColTma<N>::THREADS, 1)
+    k_cols_tma(const __grid_constant__ CUtensorMap src, const ColArgs a, int tiles_x, int ntiles) {
+  using CT = ColTma<N>;
+  constexpr int PC = CT::PC, S = CT::STAGES;
+  extern __shared__ __align__(128) float2 smem[];
+  float2* stw = smem + S * CT::STAGE;
+  const uint32_t bar0 = tma::smem_u32(stw + CT::TW);
+  const int c = threadIdx.x % PC, t = threadIdx.x / PC;
+  auto issue = [&](int tile, int s) {
+    const int xf = tile / tiles_x, col0 = (tile - xf * tiles_x) * PC;
+    tma::mbar_arrive_expect_tx(bar0 + 8 * s, CT::TILE_BYTES);
+    tma::load_4d(tma::smem_u32(smem + s * CT::STAGE), &src, 2 * col0, 0, 0, xf, bar0 + 8 * s);
+  };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) tma::mbar_init(bar0 + 8 * s, 1);
+    tma::fence_mbar_init();
+    for (int s = 0; s < S; ++s) {
+      const int tile = blockIdx.x + s * gridDim.x;
+      if (tile < ntiles) issue(tile, s);
+    }
+  }
+  for (int i = threadIdx.x; i < CT::TW; i += CT::THREADS) stw[i] = __ldg(a.tw + i);
+  __syncthreads();
+  int s = 0;
+  uint32_t phase = 0;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int xf = tile / tiles_x;
+    const int col = (tile - xf * tiles_x) * PC + c;
+    float2* buf = smem + s * CT::STAGE;
+    tma::mbar_wait(bar0 + 8 * s, phase);
+    auto refill = [&] {
+      __syncthreads();  // every thread's shared reads of this buffer are done
+      if (threadIdx.x == 0) {
+        const int next = tile + S * gridDim.x;
+        if (next < ntiles) {
+          tma::fence_proxy_async_smem();
+          issue(next, s);
+        }
+      }
+    };
+    const float2* dense = buf;
+    if constexpr (COMPLEX_OUT) {
+      float2* out = a.out_c + (size_t)xf * N * N;
+      fft::cta_fft<N, false, true, false, true>(
+          t, buf + c * CT::STRIDE, stw, [&](int i) { return dense[i * PC + c]; },
+          [&](int r, float2 x) {
+            const float sg = ((r + col) & 1) ? -1.f : 1.f;  // fft.cpp:73-75
+            out[(size_t)r * N + col] = make_float2(sg * x.x, sg * x.y);
+          },
+          refill);
+    } else {
+      const XformDesc d = a.desc[xf];
+      fft::cta_fft<N, false, true, false, true>(
+          t, buf + c * CT::STRIDE, stw, [&](int i) { return dense[i * PC + c]; },
+          [&](int r, float2 x) {
+            const float sg = ((r + col) & 1) ? -1.f : 1.f;
+            __stcs(d.out_re + (size_t)r * N + col, sg * x.x);  // fft.cpp:93-99 split
+            if (d.out_im) __stcs(d.out_im + (size_t)r * N + col, sg * x.y);
+          },
+          refill);
+    }
+    if (++s == S) s = 0, phase ^= 1;
   }
 }
 
@@ -641,11 +758,12 @@ void launch_rows(ocn_ctx* ctx, const RowArgs& a, bool plain, cudaStream_t st, in
     using W = WarpLaunch<N>;
     const int slots = (max_seg + W::TPW - 1) / W::TPW;
     const int warps = slots < 8 ? slots : 8;
-    const size_t smem = (plain ? 0 : 2 * N * sizeof(float4)) +
+    const size_t smem = (plain ? 0 : 2 * N * sizeof(float4)) + W::TWN * sizeof(float2) +
                         (size_t)warps * W::TPW * W::STRIDE * sizeof(float2);
     static bool attr = false;
     if (!attr) {
-      const int cap = 2 * N * sizeof(float4) + 8 * W::TPW * W::STRIDE * sizeof(float2);
+      const int cap = 2 * N * sizeof(float4) + W::TWN * sizeof(float2) +
+                      8 * W::TPW * W::STRIDE * sizeof(float2);
       OCN_CUDA(cudaFuncSetAttribute(k_rows_w<N, kRowPlain>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap));
       OCN_CUDA(cudaFuncSetAttribute(k_rows_w<N, kRowSurface>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap));
       OCN_CUDA(cudaFuncSetAttribute(k_rows_w<N, kRowVelocity>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap));
@@ -683,7 +801,27 @@ static bool cols_generic() {
 }
 
 template <int N>
-void launch_cols(ocn_ctx* ctx, const ColArgs& a, int G, bool complex_out, cudaStream_t st) {
+void launch_cols(ocn_ctx* ctx, const ColArgs& a, int G, bool complex_out, cudaStream_t st,
+                 const CUtensorMap* map) {
+  if constexpr (ColTma<N>::OK) {
+    if (map) {
+      using CT = ColTma<N>;
+      static bool attr = false;
+      if (!attr) {
+        OCN_CUDA(cudaFuncSetAttribute(k_cols_tma<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CT::SMEM));
+        OCN_CUDA(cudaFuncSetAttribute(k_cols_tma<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CT::SMEM));
+        attr = true;
+      }
+      const int tiles_x = N / CT::PC, ntiles = tiles_x * G;
+      const int grid = std::min(ntiles, ctx->sm_count);
+      if (complex_out)
+        k_cols_tma<N, true><<<grid, CT::THREADS, CT::SMEM, st>>>(*map, a, tiles_x, ntiles);
+      else
+        k_cols_tma<N, false><<<grid, CT::THREADS, CT::SMEM, st>>>(*map, a, tiles_x, ntiles);
+      OCN_LAUNCHED(ctx);
+      return;
+    }
+  }
   if constexpr (use_warp_kernels<N>()) {
    if (!cols_generic()) {
     using W = WarpLaunch<N>;
@@ -720,8 +858,9 @@ void rows_dispatch(ocn_ctx* ctx, int n, const RowArgs& a, bool plain, cudaStream
   OCN_DISPATCH_N(n, OCN_ROWS)
 #undef OCN_ROWS
 }
-void cols_dispatch(ocn_ctx* ctx, int n, const ColArgs& a, int G, bool complex_out, cudaStream_t st) {
-#define OCN_COLS(NN) launch_cols<NN>(ctx, a, G, complex_out, st)
+void cols_dispatch(ocn_ctx* ctx, int n, const ColArgs& a, int G, bool complex_out, cudaStream_t st,
+                   const CUtensorMap* map = nullptr) {
+#define OCN_COLS(NN) launch_cols<NN>(ctx, a, G, complex_out, st, map)
   OCN_DISPATCH_N(n, OCN_COLS)
 #undef OCN_COLS
 }
@@ -790,8 +929,39 @@ void set_l2_window(ocn_ctx* ctx, void* base, size_t bytes) {
     cudaGetLastError();
 }
 
+// Column-pass source map over a scratch buffer [G][N][N] complex64, viewed as
+// fp32 [G][N / BR][BR][2N] so one box {2 PC, BR, N / BR, 1} is a whole column
+// tile. Returns false (-> direct-load kernel) outside the TMA kernel's range
+// or when OCN_COLS_LDG=1 asks for the direct-load column kernel.
+static bool cols_ldg() {
+  static const bool on = [] {
+    const char* e = getenv("OCN_COLS_LDG");
+    return e && *e && *e != '0';
+  }();
+  return on;
+}
+
+bool cols_map_for(int n, int G, const float2* scratch, CUtensorMap* map) {
+  const int pc = cols_tma_pc(n), br = n < 256 ? n : 256;
+  if (!pc || cols_ldg()) return false;
+  const uint64_t dims[4] = {2ull * n, (uint64_t)br, (uint64_t)(n / br), (uint64_t)G};
+  const uint64_t strides[3] = {2ull * n * 4, (uint64_t)br * 2 * n * 4, (uint64_t)n * n * 8};
+  const uint32_t box[4] = {2u * pc, (uint32_t)br, (uint32_t)(n / br), 1u};
+  if (!tma::encode_f32(map, 4, const_cast<float2*>(scratch), dims, strides, box))
+    fail(OCN_ERR_CUDA, "cuTensorMapEncodeTiled failed for the column pass (N=%d, G=%d)", n, G);
+  return true;
+}
+
 size_t group_for(int n, int total) {
-  const size_t budget = 64ull << 20;  // keep scratch L2-resident (126 MB L2)
+  // Scratch budget of the transform groups. Larger groups amortise the row
+  // kernel's per-row staging over more transforms and keep the persistent
+  // column kernel's tile ring full: measured on B200 at N = 1024 (config 3,
+  // spectral ms / frame) 64 MB 1.75, 256 MB 1.46, 512 MB 1.39, 1 GB 1.36,
+  // 2 GB 1.33 -> 1 GB default (0.6% of HBM). OCN_SCRATCH_MB overrides.
+  static const size_t budget = [] {
+    const char* e = getenv("OCN_SCRATCH_MB");
+    return (size_t)(e && atoi(e) > 0 ? atoi(e) : 1024) << 20;
+  }();
   size_t per = (size_t)n * n * sizeof(float2);
   size_t g = budget / per;
   if (g < 1) g = 1;
@@ -948,7 +1118,8 @@ static void enqueue_spectral(ocn_cascades* cas, SpectralPlan* plan, double chopp
     ca.tw = cas->twiddle.p;
     {
       ProfWindow pw(ctx, dual ? -1 : OCN_PROF_COLS);
-      cols_dispatch(ctx, n, ca, gr.count, false, B);
+      cols_dispatch(ctx, n, ca, gr.count, false, B,
+                    cas->cols_map_ok ? &cas->cols_map[dual ? gidx % 2 : 0] : nullptr);
     }
     if (dual) OCN_CUDA(cudaEventRecord(event(2 * (int)gidx + 1), B));
   }
@@ -1028,7 +1199,9 @@ static void plain_ifft(ocn_ctx* ctx, int n, int G, const float2* src, float2* sc
   ca.desc = d_desc;
   ca.out_c = out_c;
   ca.tw = tw;
-  cols_dispatch(ctx, n, ca, G, out_c != nullptr, ctx->stream);
+  CUtensorMap map;
+  const bool tma_ok = cols_map_for(n, G, scratch, &map);
+  cols_dispatch(ctx, n, ca, G, out_c != nullptr, ctx->stream, tma_ok ? &map : nullptr);
 }
 
 }  // namespace ocn
@@ -1281,6 +1454,9 @@ int ocn_cascades_create_multi(ocn_ctx* ctx, int resolution, int count, const dou
     cas->d_time.alloc(1);
     cas->scratch.alloc((size_t)cas->nbuf * cas->group * nn);
     set_l2_window(ctx, cas->scratch.p, cas->scratch.bytes());
+    for (int b = 0; b < cas->nbuf; ++b)
+      cas->cols_map_ok = cols_map_for(resolution, cas->group,
+                                      cas->scratch.p + (size_t)b * cas->group * nn, &cas->cols_map[b]);
     OCN_CUDA(cudaStreamSynchronize(ctx->stream));
     ctx_retain(ctx);
     *out = cas.release();
