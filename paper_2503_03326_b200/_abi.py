@@ -13,7 +13,8 @@ from ._types import (Fluid, FdmConfig, HydroReport, MaskFrame, MaskParams, Pose,
                      SpectrumParams, TriangleState, ZoneState)
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libocean_b200.so")
+# OCN_LIB: an alternative build of the same library (kernel-variant experiments)
+LIB_PATH = os.environ.get("OCN_LIB") or os.path.join(PKG, "lib", "libocean_b200.so")
 HEADER = os.path.join(os.path.dirname(PKG), "include", "ocean_b200.h")
 
 OCN_OK, OCN_ERR_CONFIG, OCN_ERR_MESH, OCN_ERR_NUMERIC = 0, 2, 3, 4

@@ -200,9 +200,10 @@ struct CtaLaunch {
 //              exchanges synchronise with __syncwarp instead of __syncthreads
 //   LOAD_SM  : `load` reads `sm` itself (adds a sync before pass 0 overwrites it)
 //   STORE_SM : `store` writes `sm` itself (adds a sync before the last stores)
-template <bool WARP>
+template <bool WARP, int BAR = 0, int BAR_THREADS = 0>
 __device__ __forceinline__ void fft_sync() {
   if constexpr (WARP) __syncwarp();
+  else if constexpr (BAR > 0) asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(BAR_THREADS) : "memory");
   else __syncthreads();
 }
 
@@ -214,8 +215,10 @@ struct NoHook {
 // shared-memory reads of the transform, before the final DFT and stores: from
 // then on `sm` may be reused (e.g. refilled by TMA for the next tile).
 //   TW_SM    : `tw` points to shared memory (plain loads instead of __ldg)
+//   BAR, BAR_THREADS : (!WARP) synchronise on named barrier BAR of BAR_THREADS
+//              threads instead of __syncthreads (warp-specialised kernels)
 template <int N, bool WARP = false, bool LOAD_SM = false, bool STORE_SM = false, bool TW_SM = false,
-          class Load, class Store, class Free = NoHook>
+          int BAR = 0, int BAR_THREADS = 0, class Load, class Store, class Free = NoHook>
 __device__ __forceinline__ void cta_fft(int t, float2* sm, const float2* __restrict__ tw,
                                         Load&& load, Store&& store, Free&& on_free = Free{}) {
   using PL = Plan<N>;
@@ -225,10 +228,10 @@ __device__ __forceinline__ void cta_fft(int t, float2* sm, const float2* __restr
   // ---- pass 0: radix E, Ns = 1, no twiddles
 #pragma unroll
   for (int r = 0; r < E; ++r) v[r] = load(t + r * T);
-  if constexpr (LOAD_SM) fft_sync<WARP>();
+  if constexpr (LOAD_SM) fft_sync<WARP, BAR, BAR_THREADS>();
   dft_dif<E>(v);
   if constexpr (P == 1) {
-    if constexpr (STORE_SM && !LOAD_SM) fft_sync<WARP>();
+    if constexpr (STORE_SM && !LOAD_SM) fft_sync<WARP, BAR, BAR_THREADS>();
     static_for<0, E>([&](auto ri) {
       constexpr int r = decltype(ri)::value;
       store(r, v[bitrev(r, PL::LOGE)]);
@@ -238,7 +241,7 @@ __device__ __forceinline__ void cta_fft(int t, float2* sm, const float2* __restr
       constexpr int r = decltype(ri)::value;
       sm[pad32(t * E + r)] = v[bitrev(r, PL::LOGE)];
     });
-    fft_sync<WARP>();
+    fft_sync<WARP, BAR, BAR_THREADS>();
     static_for<1, P>([&](auto pi) {
       constexpr int p = decltype(pi)::value;
       constexpr int R = PL::radix(p);
@@ -266,7 +269,7 @@ __device__ __forceinline__ void cta_fft(int t, float2* sm, const float2* __restr
         dft_dif<R, q * R>(v);
       });
       if constexpr (p == P - 1) {
-        if constexpr (STORE_SM) fft_sync<WARP>();
+        if constexpr (STORE_SM) fft_sync<WARP, BAR, BAR_THREADS>();
         static_for<0, Q>([&](auto qi) {
           constexpr int q = decltype(qi)::value;
           const int b = t + q * T;
@@ -276,7 +279,7 @@ __device__ __forceinline__ void cta_fft(int t, float2* sm, const float2* __restr
           });
         });
       } else {
-        fft_sync<WARP>();
+        fft_sync<WARP, BAR, BAR_THREADS>();
         static_for<0, Q>([&](auto qi) {
           constexpr int q = decltype(qi)::value;
           const int b = t + q * T;
@@ -286,7 +289,7 @@ __device__ __forceinline__ void cta_fft(int t, float2* sm, const float2* __restr
             sm[pad32(base + r * NS)] = v[q * R + bitrev(r, LOGR)];
           });
         });
-        fft_sync<WARP>();
+        fft_sync<WARP, BAR, BAR_THREADS>();
       }
     });
   }

@@ -70,6 +70,12 @@ struct SpectralPlan {
   ~SpectralPlan() {
     if (exec) cudaGraphExecDestroy(exec);
   }
+  // fused row + column step (N = 1024): waves, column-tile prefix, counters
+  bool fused = false;
+  int nwaves = 0;
+  DevBuf<int> fused_waves;  // FusedWave[nwaves] (4 ints each)
+  DevBuf<int> fused_tile0;  // [nwaves + 1]
+  DevBuf<int> fused_ctr;    // [2 + 2 nwaves]
   std::vector<XformDesc> host_desc;
   std::vector<int> first;  // per cascade: first transform index
   std::vector<int> count;  // per cascade: number of transforms
@@ -98,6 +104,8 @@ struct ocn_cascades {
   int nbuf = 1;                 // scratch buffers (2: row/column passes overlap)
   CUtensorMap cols_map[2];      // TMA source map of each scratch buffer (column pass)
   bool cols_map_ok = false;
+  CUtensorMap fused_map;        // TMA source map of the fused step's column tiles
+  bool fused_ok = false;
   std::map<std::pair<const void*, const void*>, std::unique_ptr<ocn::SpectralPlan>> plans;
 };
 

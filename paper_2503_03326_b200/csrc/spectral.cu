@@ -13,9 +13,10 @@
 //   k_rows<N>    : per (row, transform of the group): the packed coefficient
 //                  X + iY = spec * multiplier(k) generated in registers (no
 //                  coefficient arrays in HBM), then the row FFT -> scratch
+//                  (input half-shifted: the (-1)^(i+j) centring, kCentreByShift)
 //   k_cols_tma<N>: persistent column FFT of scratch fed by TMA (k_cols<N>
-//                  with direct loads outside 128 <= N <= 4096), (-1)^(i+j),
-//                  Re -> field X, Im -> field Y (fp32, row-major [i][j])
+//                  with direct loads outside 128 <= N <= 4096), Re -> field X,
+//                  Im -> field Y (fp32, row-major [i][j])
 // Transforms run in groups sharing one scratch buffer (group * N^2 * 8 B, 1 GB
 // budget; see group_for).
 #include <algorithm>
@@ -210,6 +211,13 @@ __global__ void __launch_bounds__(256) k_evolve(int n, int count, const GridCons
 }
 
 // ------------------------------------------------------------------ rows
+// kCentreByShift: the reference centres its inverse FFT by multiplying the
+// output by (-1)^(i+j) (fft.cpp:73-75). For power-of-two N that equals the
+// transform of the input shifted by N/2 in both axes:
+//   sum_k X[k ^ N/2] e^{+2 pi i n k / N} = (-1)^n sum_k X[k] e^{+2 pi i n k / N},
+// so the row pass reads mode (i, j ^ N/2) for FFT input j and writes its
+// result to scratch row i ^ N/2; the column pass then needs no sign multiply.
+// (Same values up to fp32 rounding order; the slab path keeps the explicit sign.)
 struct RowArgs {
   int items;  // N * G (generic kernel)
   int G;
@@ -301,11 +309,12 @@ __global__ void __launch_bounds__(Launch<N>::THREADS) k_rows(const RowArgs a) {
   const int row = valid ? item / a.G : 0;
   const int gi = valid ? item - row * a.G : 0;
   float2* sm = smem + local * L::ROW_STRIDE;
-  float2* out = a.scratch + ((size_t)gi * N + row) * N;
+  constexpr int H = N / 2;  // centring half-shift (see kCentreByShift)
+  float2* out = a.scratch + ((size_t)gi * N + (row ^ H)) * N;
   if constexpr (PLAIN) {
     const float2* in = a.src + ((size_t)gi * N + row) * N;
     fft::cta_fft<N>(
-        t, sm, a.tw, [&](int j) { return valid ? __ldg(in + j) : make_float2(0.f, 0.f); },
+        t, sm, a.tw, [&](int j) { return valid ? __ldg(in + (j ^ H)) : make_float2(0.f, 0.f); },
         [&](int k, float2 x) {
           if (valid) out[k] = x;
         });
@@ -317,7 +326,7 @@ __global__ void __launch_bounds__(Launch<N>::THREADS) k_rows(const RowArgs a) {
         t, sm, a.tw,
         [&](int j) {
           if (!valid) return make_float2(0.f, 0.f);
-          return packed_coef(d, __ldg(srow + j), row, j, N, dk, g, a.chop);
+          return packed_coef(d, __ldg(srow + (j ^ H)), row, j ^ H, N, dk, g, a.chop);
         },
         [&](int k, float2 x) {
           if (valid) out[k] = x;
@@ -368,6 +377,7 @@ __global__ void __launch_bounds__(256, 2) k_rows_w(const RowArgs a) {
   constexpr bool PLAIN = MODE == kRowPlain;
   using W = WarpLaunch<N>;
   constexpr int T = W::T, E = fft::Plan<N>::E;
+  constexpr int H = N / 2;  // centring half-shift (see kCentreByShift)
   extern __shared__ float4 smem4[];
   // Per mode of this row, shared by every transform of the group (SoA):
   //   sht = h~,  sv0 = V0 = G (-g / w)(kx + i kz),  sw0 = W0 = G w,  sk = |k|,
@@ -397,89 +407,124 @@ __global__ void __launch_bounds__(256, 2) k_rows_w(const RowArgs a) {
   if constexpr (!PLAIN) {
     const float4* srow = a.spec + ((size_t)grid * N + row) * N;
     const float g = (float)a.gc[grid].p.gravity;
+    // MUFU reciprocal square roots (no IEEE slow-path calls, so the row's
+    // loads issue back to back); only the arrays this family reads
+#pragma unroll 4
     for (int j = threadIdx.x; j < N; j += blockDim.x) {
+      const float4 sp = __ldg(srow + j);  // (h~, G)
       const float kz = dkf * (float)(j - N / 2);
       const float k2 = kx * kx + kz * kz;
-      const float k = sqrtf(k2);
-      const float inv = k2 > 0.f ? 1.0f / k : 0.f;
-      const float w = sqrtf(g * k);
-      const float4 sp = __ldg(srow + j);  // (h~, G)
-      const float f = k2 > 0.f ? -g / w : 0.f;
-      sht[j] = make_float2(sp.x, sp.y);
-      sv0[j] = make_float2(f * (sp.z * kx - sp.w * kz), f * (sp.z * kz + sp.w * kx));
-      sw0[j] = make_float2(sp.z * w, sp.w * w);
-      sk[j] = k;
-      sinv[j] = inv;
+      const bool zero = k2 == 0.f;  // k = 0: every coefficient vanishes
+      const float inv = zero ? 0.f : rsqrtf(k2);
+      const float k = k2 * inv;
+      if constexpr (MODE == kRowSurface) {
+        sht[j] = make_float2(sp.x, sp.y);
+        sinv[j] = inv;
+      } else {
+        const float rw = zero ? 0.f : rsqrtf(g * k);  // 1 / w
+        const float w = g * k * rw, f = -g * rw;     // w, -g / w
+        sv0[j] = make_float2(f * (sp.z * kx - sp.w * kz), f * (sp.z * kz + sp.w * kx));
+        sw0[j] = make_float2(sp.z * w, sp.w * w);
+        sk[j] = k;
+      }
     }
   }
   __syncthreads();
   const int slots = (seg_count + W::TPW - 1) / W::TPW;
   float2* buf = bufs + (size_t)(warp * W::TPW + sub) * W::STRIDE;
+  // the (kind, y0, y1) of this warp's next transform are loaded one slot ahead
+  auto desc_of = [&](int slot) {
+    const int li = slot * W::TPW + sub;
+    const XformDesc* d = a.desc + seg_first + (li < seg_count ? li : 0);
+    return make_float3(__int_as_float(__ldg(&d->kind)), __ldg(&d->y0), __ldg(&d->y1));
+  };
+  float3 dnext = make_float3(0.f, 0.f, 0.f);
+  if constexpr (!PLAIN) dnext = desc_of(warp < slots ? warp : 0);
   for (int slot = warp; slot < slots; slot += warps) {
     const int li = slot * W::TPW + sub;
     const bool valid = li < seg_count;
     const int gi = seg_first + (valid ? li : 0);  // transform index within the group
-    float2* out = a.scratch + ((size_t)gi * N + row) * N;
+    const float3 dcur = dnext;
+    if constexpr (!PLAIN)
+      if (slot + warps < slots) dnext = desc_of(slot + warps);
+    float2* out = a.scratch + ((size_t)gi * N + (row ^ H)) * N;
     auto store = [&](int k, float2 x) {
       if (valid) out[k] = x;
     };
     if constexpr (PLAIN) {
       const float2* in = a.src + ((size_t)gi * N + row) * N;
-      for (int j = t; j < N; j += T) buf[fft::pad32(j)] = valid ? __ldg(in + j) : make_float2(0.f, 0.f);
+      for (int j = t; j < N; j += T)
+        buf[fft::pad32(j)] = valid ? __ldg(in + (j ^ H)) : make_float2(0.f, 0.f);
       __syncwarp();
       fft::cta_fft<N, true, true, false, true>(
           t, buf, stw, [&](int j) { return buf[fft::pad32(j)]; }, store);
     } else {
-      const XformDesc d = a.desc[gi];
+      const int dkind = __float_as_int(dcur.x);
+      // One branch-free FFT body per transform kind (selected once per
+      // transform, warp-uniform): no per-element kind tests in pass 0.
       if constexpr (MODE == kRowSurface) {
-        // surface pairs: X + iY = h~ M(kx, kz) (surface.cpp:77-80 packing)
+        // surface pairs: X + iY = h~ M(kx, kz) (surface.cpp:77-80 packing),
+        // every kind written as one branch-free form with per-transform
+        // constants (a per-kind body let the compiler hoist the shared loads
+        // of all four and spill):
+        //   Re M = c0 + c3 kz + kx / |k| (c1 + c2 kz)
+        //   Im M = c4 + (c5 (kz + kx^2) + c6 kz^2) / |k|
+        // h~ = 0 at k = 0 (K1 masks it), so that mode needs no special case
         const float chop = a.chop, dk = dkf;
-        const int kind = d.kind;
+        float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f, c4 = 0.f, c5 = 0.f, c6 = 0.f;
+        if (dkind == kSurfHDx) c0 = 1.f, c1 = -chop;             // 1 - chop kx / k
+        else if (dkind == kSurfDzDxDx) c5 = chop;                 // i chop (kz + kx^2) / k
+        else if (dkind == kSurfDzDxDzDz) c2 = chop, c6 = chop;    // chop kz (kx + i kz) / k
+        else c3 = -1.f, c4 = kx;                                  // -kz + i kx
+        const float kx2 = kx * kx;
         fft::cta_fft<N, true, false, false, true>(
             t, buf, stw,
             [&](int j) {
-              const float2 h = sht[j];
-              const float inv = sinv[j];
-              const float kz = dk * (float)(j - N / 2);
-              float mr, mi;
-              if (kind == kSurfHDx) {
-                mr = 1.0f - kx * inv * chop, mi = 0.f;
-              } else if (kind == kSurfDzDxDx) {
-                mr = 0.f, mi = chop * (kz + kx * kx) * inv;
-              } else if (kind == kSurfDzDxDzDz) {
-                const float f = chop * kz * inv;
-                mr = f * kx, mi = f * kz;
-              } else {
-                mr = -kz, mi = kx;
-              }
-              if (inv == 0.f) mr = mi = 0.f;  // k = 0 mode
+              const int jj = j ^ H;
+              const float2 h = sht[jj];
+              const float inv = sinv[jj];
+              const float kz = dk * (float)(jj - N / 2);
+              const float mr = fmaf(inv * kx, fmaf(c2, kz, c1), fmaf(c3, kz, c0));
+              const float mi = fmaf(inv, fmaf(c6 * kz, kz, c5 * (kz + kx2)), c4);
               return make_float2(h.x * mr - h.y * mi, h.x * mi + h.y * mr);
             },
             store);
       } else {
         static_assert(MODE == kRowVelocity, "row mode");
-        // velocity: Z (re + i im) with Z = V0 (x/z pair) or W0 (vy pair)
-        const float2* Z = d.kind == kVelXZ ? sv0 : sw0;
+        // velocity: Z (re + i im) with Z = V0 (x/z pair) or W0 (vy pair);
+        // E(y) = 1 + |k| y above the mean surface, else exp(|k| y) (selected,
+        // not branched: the depth is per transform)
+        const float2* Z = dkind == kVelXZ ? sv0 : sw0;
         constexpr float kLog2e = 1.4426950408889634f;
-        const float y0 = d.y0, y1 = d.y1, y0l = d.y0 * kLog2e, y1l = d.y1 * kLog2e;
+        const float y0 = dcur.y, y1 = dcur.z, y0l = y0 * kLog2e, y1l = y1 * kLog2e;
         const bool up0 = y0 > 0.f, up1 = y1 > 0.f;
-        const int kind = d.kind;
-        fft::cta_fft<N, true, false, false, true>(
-            t, buf, stw,
-            [&](int j) {
-              const float2 z = Z[j];
-              const float k = sk[j];
-              const float e0 = up0 ? fmaf(k, y0, 1.0f) : ex2_approx(k * y0l);
-              float mr, mi;
-              if (kind == kVelXZ) {
-                mr = e0, mi = 0.f;
-              } else {
-                mr = kind == kVelYPair ? -(up1 ? fmaf(k, y1, 1.0f) : ex2_approx(k * y1l)) : 0.f;
-                mi = e0;
-              }
-              return make_float2(z.x * mr - z.y * mi, z.x * mi + z.y * mr);
-            },
-            store);
+        auto run = [&](auto kind_c) {
+          constexpr int KIND = decltype(kind_c)::value;
+          fft::cta_fft<N, true, false, false, true>(
+              t, buf, stw,
+              [&](int j) {
+                const int jj = j ^ H;
+                const float2 z = Z[jj];
+                const float k = sk[jj];
+                const float l0 = fmaf(k, y0, 1.0f), x0 = ex2_approx(k * y0l);
+                const float e0 = up0 ? l0 : x0;
+                if constexpr (KIND == kVelXZ) {
+                  return make_float2(z.x * e0, z.y * e0);
+                } else if constexpr (KIND == kVelYPair) {
+                  const float l1 = fmaf(k, y1, 1.0f), x1 = ex2_approx(k * y1l);
+                  const float mr = -(up1 ? l1 : x1), mi = e0;
+                  return make_float2(z.x * mr - z.y * mi, z.x * mi + z.y * mr);
+                } else {
+                  return make_float2(-z.y * e0, z.x * e0);
+                }
+              },
+              store);
+        };
+        switch (dkind) {
+          case kVelXZ: run(std::integral_constant<int, kVelXZ>{}); break;
+          case kVelYPair: run(std::integral_constant<int, kVelYPair>{}); break;
+          default: run(std::integral_constant<int, kVelYSingle>{}); break;
+        }
       }
     }
     __syncwarp();
@@ -530,8 +575,7 @@ __global__ void __launch_bounds__(256) k_cols_w(const ColArgs a) {
     for (int idx = threadIdx.x; idx < N * CC; idx += blockDim.x) {
       const int row = idx / CC, cc = idx - row * CC, col = col0 + cc;
       const float2 x = tile[cc * W::STRIDE + fft::pad32(row)];
-      const float s = ((row + col) & 1) ? -1.f : 1.f;
-      out[(size_t)row * N + col] = make_float2(s * x.x, s * x.y);
+      out[(size_t)row * N + col] = x;
     }
   } else {
     const XformDesc d = a.desc[xf];
@@ -539,9 +583,8 @@ __global__ void __launch_bounds__(256) k_cols_w(const ColArgs a) {
     for (int idx = threadIdx.x; idx < N * CC; idx += NT) {
       const int row = idx / CC, cc = idx - row * CC, col = col0 + cc;
       const float2 x = tile[cc * W::STRIDE + fft::pad32(row)];
-      const float s = ((row + col) & 1) ? -1.f : 1.f;  // fft.cpp:73-75
-      d.out_re[(size_t)row * N + col] = s * x.x;       // fft.cpp:93-99
-      if (d.out_im) d.out_im[(size_t)row * N + col] = s * x.y;
+      d.out_re[(size_t)row * N + col] = x.x;  // fft.cpp:93-99
+      if (d.out_im) d.out_im[(size_t)row * N + col] = x.y;
     }
   }
 }
@@ -565,8 +608,7 @@ __global__ void __launch_bounds__(Launch<N>::THREADS) k_cols(const ColArgs a) {
         t, sm, a.tw, [&](int i) { return __ldg(in + (size_t)i * N); },
         [&](int r, float2 x) {
           if (!valid) return;
-          const float s = ((r + col) & 1) ? -1.f : 1.f;  // fft.cpp:73-75
-          out[(size_t)r * N + col] = make_float2(s * x.x, s * x.y);
+          out[(size_t)r * N + col] = x;
         });
   } else {
     const XformDesc d = a.desc[xf];
@@ -574,10 +616,9 @@ __global__ void __launch_bounds__(Launch<N>::THREADS) k_cols(const ColArgs a) {
         t, sm, a.tw, [&](int i) { return __ldg(in + (size_t)i * N); },
         [&](int r, float2 x) {
           if (!valid) return;
-          const float s = ((r + col) & 1) ? -1.f : 1.f;
-          // streaming stores: the fields are not re-read by this step, keep L2 for scratch
-          __stcs(d.out_re + (size_t)r * N + col, s * x.x);  // fft.cpp:93-99 split
-          if (d.out_im) __stcs(d.out_im + (size_t)r * N + col, s * x.y);
+          // streaming stores: the fields are not re-read by this step
+          __stcs(d.out_re + (size_t)r * N + col, x.x);  // fft.cpp:93-99 split
+          if (d.out_im) __stcs(d.out_im + (size_t)r * N + col, x.y);
         });
   }
 }
@@ -607,7 +648,8 @@ struct ColTma {
   static constexpr int TW = PL::tw_size();
   static constexpr int STAGES = (227 * 1024 - TW * 8 - 64) / (STAGE * 8) >= 3 ? 3 : 2;
   static constexpr uint32_t TILE_BYTES = (uint32_t)DENSE * 8;
-  static constexpr size_t SMEM = ((size_t)STAGES * STAGE + TW) * 8 + STAGES * 8;
+  static constexpr size_t smem(int stages) { return ((size_t)stages * STAGE + TW) * 8 + stages * 8; }
+  static constexpr size_t SMEM = smem(STAGES);
   static constexpr int BR = N < 256 ? N : 256;  // rows per box dimension
   static constexpr bool OK = PL::P > 1 && N >= 128 && N <= 4096 && SMEM <= 227 * 1024;
 };
@@ -615,11 +657,11 @@ struct ColTma {
 // columns per tile of the TMA column kernel, 0 outside its range
 int cols_tma_pc(int n) { return n >= 128 && n <= 4096 ? 8192 / n : 0; }
 
-template <int N, bool COMPLEX_OUT>
+template <int N, bool COMPLEX_OUT, int S>
 __global__ void __launch_bounds__(ColTma<N>::THREADS, 1)
     k_cols_tma(const __grid_constant__ CUtensorMap src, const ColArgs a, int tiles_x, int ntiles) {
   using CT = ColTma<N>;
-  constexpr int PC = CT::PC, S = CT::STAGES;
+  constexpr int PC = CT::PC;
   extern __shared__ __align__(128) float2 smem[];
   float2* stw = smem + S * CT::STAGE;
   const uint32_t bar0 = tma::smem_u32(stw + CT::TW);
@@ -662,8 +704,7 @@ __global__ void __launch_bounds__(ColTma<N>::THREADS, 1)
       fft::cta_fft<N, false, true, false, true>(
           t, buf + c * CT::STRIDE, stw, [&](int i) { return dense[i * PC + c]; },
           [&](int r, float2 x) {
-            const float sg = ((r + col) & 1) ? -1.f : 1.f;  // fft.cpp:73-75
-            out[(size_t)r * N + col] = make_float2(sg * x.x, sg * x.y);
+            out[(size_t)r * N + col] = x;
           },
           refill);
     } else {
@@ -671,15 +712,16 @@ __global__ void __launch_bounds__(ColTma<N>::THREADS, 1)
       fft::cta_fft<N, false, true, false, true>(
           t, buf + c * CT::STRIDE, stw, [&](int i) { return dense[i * PC + c]; },
           [&](int r, float2 x) {
-            const float sg = ((r + col) & 1) ? -1.f : 1.f;
-            __stcs(d.out_re + (size_t)r * N + col, sg * x.x);  // fft.cpp:93-99 split
-            if (d.out_im) __stcs(d.out_im + (size_t)r * N + col, sg * x.y);
+            __stcs(d.out_re + (size_t)r * N + col, x.x);  // fft.cpp:93-99 split
+            if (d.out_im) __stcs(d.out_im + (size_t)r * N + col, x.y);
           },
           refill);
     }
     if (++s == S) s = 0, phase ^= 1;
   }
 }
+
+#include "spectral_fused.cuh"
 
 // fp64 interleaved pair -> fp32 X + iY (fft.cpp:88-91)
 __global__ void k_pack_pair(size_t nn, const double2* x, const double2* y, float2* out) {
@@ -753,20 +795,21 @@ constexpr bool use_warp_kernels() {
 
 template <int N>
 void launch_rows(ocn_ctx* ctx, const RowArgs& a, bool plain, cudaStream_t st, int nseg,
-                 int max_seg, int family) {
+                 int max_seg, int family, bool lean) {
   if constexpr (use_warp_kernels<N>()) {
     using W = WarpLaunch<N>;
     const int slots = (max_seg + W::TPW - 1) / W::TPW;
-    const int warps = slots < 8 ? slots : 8;
+    const int cap = lean ? 4 : 8;  // lean: co-resides with a column pass
+    const int warps = slots < cap ? slots : cap;
     const size_t smem = (plain ? 0 : 2 * N * sizeof(float4)) + W::TWN * sizeof(float2) +
                         (size_t)warps * W::TPW * W::STRIDE * sizeof(float2);
     static bool attr = false;
     if (!attr) {
-      const int cap = 2 * N * sizeof(float4) + W::TWN * sizeof(float2) +
-                      8 * W::TPW * W::STRIDE * sizeof(float2);
-      OCN_CUDA(cudaFuncSetAttribute(k_rows_w<N, kRowPlain>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap));
-      OCN_CUDA(cudaFuncSetAttribute(k_rows_w<N, kRowSurface>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap));
-      OCN_CUDA(cudaFuncSetAttribute(k_rows_w<N, kRowVelocity>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap));
+      const int smax = 2 * N * sizeof(float4) + W::TWN * sizeof(float2) +
+                       8 * W::TPW * W::STRIDE * sizeof(float2);
+      OCN_CUDA(cudaFuncSetAttribute(k_rows_w<N, kRowPlain>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
+      OCN_CUDA(cudaFuncSetAttribute(k_rows_w<N, kRowSurface>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
+      OCN_CUDA(cudaFuncSetAttribute(k_rows_w<N, kRowVelocity>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
       attr = true;
     }
     const dim3 grid(N, plain ? 1 : nseg);
@@ -802,22 +845,25 @@ static bool cols_generic() {
 
 template <int N>
 void launch_cols(ocn_ctx* ctx, const ColArgs& a, int G, bool complex_out, cudaStream_t st,
-                 const CUtensorMap* map) {
+                 const CUtensorMap* map, bool lean) {
   if constexpr (ColTma<N>::OK) {
     if (map) {
       using CT = ColTma<N>;
       static bool attr = false;
       if (!attr) {
-        OCN_CUDA(cudaFuncSetAttribute(k_cols_tma<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CT::SMEM));
-        OCN_CUDA(cudaFuncSetAttribute(k_cols_tma<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CT::SMEM));
+        OCN_CUDA(cudaFuncSetAttribute(k_cols_tma<N, false, CT::STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CT::SMEM));
+        OCN_CUDA(cudaFuncSetAttribute(k_cols_tma<N, true, CT::STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CT::SMEM));
+        OCN_CUDA(cudaFuncSetAttribute(k_cols_tma<N, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CT::smem(2)));
         attr = true;
       }
       const int tiles_x = N / CT::PC, ntiles = tiles_x * G;
       const int grid = std::min(ntiles, ctx->sm_count);
       if (complex_out)
-        k_cols_tma<N, true><<<grid, CT::THREADS, CT::SMEM, st>>>(*map, a, tiles_x, ntiles);
+        k_cols_tma<N, true, CT::STAGES><<<grid, CT::THREADS, CT::SMEM, st>>>(*map, a, tiles_x, ntiles);
+      else if (lean)  // leaves room on each SM for a concurrent row pass
+        k_cols_tma<N, false, 2><<<grid, CT::THREADS, CT::smem(2), st>>>(*map, a, tiles_x, ntiles);
       else
-        k_cols_tma<N, false><<<grid, CT::THREADS, CT::SMEM, st>>>(*map, a, tiles_x, ntiles);
+        k_cols_tma<N, false, CT::STAGES><<<grid, CT::THREADS, CT::SMEM, st>>>(*map, a, tiles_x, ntiles);
       OCN_LAUNCHED(ctx);
       return;
     }
@@ -852,15 +898,15 @@ void launch_cols(ocn_ctx* ctx, const ColArgs& a, int G, bool complex_out, cudaSt
 }
 
 void rows_dispatch(ocn_ctx* ctx, int n, const RowArgs& a, bool plain, cudaStream_t st,
-                   int nseg = 1, int max_seg = 0, int family = 0) {
+                   int nseg = 1, int max_seg = 0, int family = 0, bool lean = false) {
   if (max_seg <= 0) max_seg = a.G;
-#define OCN_ROWS(NN) launch_rows<NN>(ctx, a, plain, st, nseg, max_seg, family)
+#define OCN_ROWS(NN) launch_rows<NN>(ctx, a, plain, st, nseg, max_seg, family, lean)
   OCN_DISPATCH_N(n, OCN_ROWS)
 #undef OCN_ROWS
 }
 void cols_dispatch(ocn_ctx* ctx, int n, const ColArgs& a, int G, bool complex_out, cudaStream_t st,
-                   const CUtensorMap* map = nullptr) {
-#define OCN_COLS(NN) launch_cols<NN>(ctx, a, G, complex_out, st, map)
+                   const CUtensorMap* map = nullptr, bool lean = false) {
+#define OCN_COLS(NN) launch_cols<NN>(ctx, a, G, complex_out, st, map, lean)
   OCN_DISPATCH_N(n, OCN_COLS)
 #undef OCN_COLS
 }
@@ -941,15 +987,29 @@ static bool cols_ldg() {
   return on;
 }
 
-bool cols_map_for(int n, int G, const float2* scratch, CUtensorMap* map) {
-  const int pc = cols_tma_pc(n), br = n < 256 ? n : 256;
-  if (!pc || cols_ldg()) return false;
+bool cols_map_for(int n, int G, const float2* scratch, CUtensorMap* map, int pc_fused = 0) {
+  const int pc = pc_fused ? pc_fused : cols_tma_pc(n), br = n < 256 ? n : 256;
+  if (!pc || (!pc_fused && cols_ldg())) return false;
   const uint64_t dims[4] = {2ull * n, (uint64_t)br, (uint64_t)(n / br), (uint64_t)G};
   const uint64_t strides[3] = {2ull * n * 4, (uint64_t)br * 2 * n * 4, (uint64_t)n * n * 8};
   const uint32_t box[4] = {2u * pc, (uint32_t)br, (uint32_t)(n / br), 1u};
   if (!tma::encode_f32(map, 4, const_cast<float2*>(scratch), dims, strides, box))
     fail(OCN_ERR_CUDA, "cuTensorMapEncodeTiled failed for the column pass (N=%d, G=%d)", n, G);
   return true;
+}
+
+// The fused row + column step (spectral_fused.cuh, N = 1024) is opt-in
+// (OCN_FUSED=1): measured on B200 (config 3 spectral, ms / frame) 1.88-2.35
+// across wave sizes 8-24 and 2-4 slots, against 1.12 for the two-kernel step.
+// With one 12-warp CTA per SM each row task and column tile exposes its load
+// latency and barrier waits, and the scratch still round-trips HBM
+// (1.7 GB read + 3.4 GB written per frame in the capture).
+static bool fused_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("OCN_FUSED");
+    return e && *e && *e != '0';
+  }();
+  return on;
 }
 
 size_t group_for(int n, int total) {
@@ -1035,6 +1095,30 @@ static SpectralPlan* get_plan(ocn_cascades* cas, ocn_maps* maps, ocn_slices* sli
     plan->groups.push_back(gr);
     g0 += cnt;
   }
+  if (cas->fused_ok && total > 0) {
+    // waves: runs of <= kFuseW consecutive transforms of one grid and family
+    std::vector<FusedWave> waves;
+    std::vector<int> tile0{0};
+    for (int i = 0; i < total;) {
+      const int c = plan->host_desc[i].cascade, f = family(i);
+      int cnt = 1;
+      while (i + cnt < total && cnt < kFuseW && plan->host_desc[i + cnt].cascade == c &&
+             family(i + cnt) == f)
+        ++cnt;
+      waves.push_back({c, f, i, cnt});
+      tile0.push_back(tile0.back() + cnt * Fused<1024>::TILES_PER_XF);
+      i += cnt;
+    }
+    plan->nwaves = (int)waves.size();
+    plan->fused_waves.alloc(4 * waves.size());
+    OCN_CUDA(cudaMemcpy(plan->fused_waves.p, waves.data(), waves.size() * sizeof(FusedWave),
+                        cudaMemcpyHostToDevice));
+    plan->fused_tile0.alloc(tile0.size());
+    OCN_CUDA(cudaMemcpy(plan->fused_tile0.p, tile0.data(), tile0.size() * sizeof(int),
+                        cudaMemcpyHostToDevice));
+    plan->fused_ctr.alloc(2 + 2 * waves.size());
+    plan->fused = true;
+  }
   plan->segs.alloc(std::max<size_t>(segs.size(), 1));
   if (!segs.empty())
     OCN_CUDA(cudaMemcpy(plan->segs.p, segs.data(), segs.size() * sizeof(GroupSeg),
@@ -1089,6 +1173,31 @@ static void enqueue_spectral(ocn_cascades* cas, SpectralPlan* plan, double chopp
                                                             cas->d_time.p, cas->h0.p, cas->spec.p);
     OCN_LAUNCHED(ctx);
   }
+  if (plan->fused) {
+    using F = Fused<1024>;
+    static bool attr = false;
+    if (!attr) {
+      OCN_CUDA(cudaFuncSetAttribute(k_spectral_fused<1024>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F::SMEM));
+      attr = true;
+    }
+    FusedArgs fa{};
+    fa.spec = cas->spec.p;
+    fa.gc = cas->gconst.p;
+    fa.chop = (float)choppiness;
+    fa.desc = plan->desc.p;
+    fa.waves = reinterpret_cast<const FusedWave*>(plan->fused_waves.p);
+    fa.tile0 = plan->fused_tile0.p;
+    fa.nwaves = plan->nwaves;
+    fa.scratch = cas->scratch.p;
+    fa.tw = cas->twiddle.p;
+    fa.ctr = plan->fused_ctr.p;
+    ProfWindow pw(ctx, OCN_PROF_ROWS);  // rows and columns in one kernel
+    OCN_CUDA(cudaMemsetAsync(plan->fused_ctr.p, 0, plan->fused_ctr.bytes(), A));
+    k_spectral_fused<1024><<<ctx->sm_count, F::THREADS, F::SMEM, A>>>(cas->fused_map, fa);
+    OCN_LAUNCHED(ctx);
+    return;
+  }
   const int G = cas->group;
   for (size_t gidx = 0; gidx < plan->groups.size(); ++gidx) {
     const SpectralPlan::Group& gr = plan->groups[gidx];
@@ -1106,7 +1215,7 @@ static void enqueue_spectral(ocn_cascades* cas, SpectralPlan* plan, double chopp
     ra.tw = cas->twiddle.p;
     {
       ProfWindow pw(ctx, dual ? -1 : OCN_PROF_ROWS);
-      rows_dispatch(ctx, n, ra, false, A, gr.nseg, gr.max_seg, gr.family);
+      rows_dispatch(ctx, n, ra, false, A, gr.nseg, gr.max_seg, gr.family, dual);
     }
     if (dual) {
       OCN_CUDA(cudaEventRecord(event(2 * (int)gidx), A));
@@ -1119,7 +1228,7 @@ static void enqueue_spectral(ocn_cascades* cas, SpectralPlan* plan, double chopp
     {
       ProfWindow pw(ctx, dual ? -1 : OCN_PROF_COLS);
       cols_dispatch(ctx, n, ca, gr.count, false, B,
-                    cas->cols_map_ok ? &cas->cols_map[dual ? gidx % 2 : 0] : nullptr);
+                    cas->cols_map_ok ? &cas->cols_map[dual ? gidx % 2 : 0] : nullptr, dual);
     }
     if (dual) OCN_CUDA(cudaEventRecord(event(2 * (int)gidx + 1), B));
   }
@@ -1457,6 +1566,10 @@ int ocn_cascades_create_multi(ocn_ctx* ctx, int resolution, int count, const dou
     for (int b = 0; b < cas->nbuf; ++b)
       cas->cols_map_ok = cols_map_for(resolution, cas->group,
                                       cas->scratch.p + (size_t)b * cas->group * nn, &cas->cols_map[b]);
+    if (resolution == 1024 && fused_enabled() && cas->nbuf == 1 &&
+        cas->group >= kFuseSlots * kFuseW)
+      cas->fused_ok = cols_map_for(1024, kFuseSlots * kFuseW, cas->scratch.p, &cas->fused_map,
+                                   Fused<1024>::PC);
     OCN_CUDA(cudaStreamSynchronize(ctx->stream));
     ctx_retain(ctx);
     *out = cas.release();
