@@ -221,6 +221,7 @@ __global__ void __launch_bounds__(256) k_evolve(int n, int count, const GridCons
 struct RowArgs {
   int items;  // N * G (generic kernel)
   int G;
+  int rpc = 1;  // warp kernel, surface family: rows per CTA
   const XformDesc* desc;   // group descriptors
   const GroupSeg* segs;    // per-grid segments of the group (warp kernel)
   const float4* spec;      // (h~, G) of every grid, [grid][N][N]
@@ -383,16 +384,19 @@ __global__ void __launch_bounds__(256, 2) k_rows_w(const RowArgs a) {
   //   sht = h~,  sv0 = V0 = G (-g / w)(kx + i kz),  sw0 = W0 = G w,  sk = |k|,
   //   sinv = 1/|k| (0 at k = 0). A velocity coefficient is then V0 E(y) or
   //   W0 (-E(y1) + i E(y0)), E(y) = exp(|k| y) (y <= 0) or 1 + |k| y.
+  // Surface CTAs may take a.rpc (<= 2) rows so that all 8 warps have work
+  // when a grid has only 4 surface transforms: sht [rpc][N], sinv [rpc][N].
+  const int rpc = MODE == kRowSurface ? a.rpc : 1;
   float2* sht = reinterpret_cast<float2*>(smem4);
-  float2* sv0 = sht + N;
+  float* sinv = reinterpret_cast<float*>(sht + rpc * N);
+  float2* sv0 = reinterpret_cast<float2*>(smem4);
   float2* sw0 = sv0 + N;
   float* sk = reinterpret_cast<float*>(sw0 + N);
-  float* sinv = sk + N;
   // inter-pass twiddles in shared memory (no global loads in the FFT passes)
   float2* stw = PLAIN ? reinterpret_cast<float2*>(smem4) : reinterpret_cast<float2*>(smem4 + 2 * N);
   float2* bufs = stw + W::TWN;
   for (int i = threadIdx.x; i < fft::Plan<N>::tw_size(); i += blockDim.x) stw[i] = __ldg(a.tw + i);
-  const int row = blockIdx.x;
+  const int row0 = blockIdx.x * rpc;
   const int warps = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int sub = lane / T, t = lane - sub * T;
@@ -403,16 +407,16 @@ __global__ void __launch_bounds__(256, 2) k_rows_w(const RowArgs a) {
     seg_first = sg.first, seg_count = sg.count, grid = sg.grid;
   }
   const float dkf = PLAIN ? 0.f : (float)a.gc[grid].dk;
-  const float kx = dkf * (float)(row - N / 2);
   if constexpr (!PLAIN) {
-    const float4* srow = a.spec + ((size_t)grid * N + row) * N;
+    const float4* srow = a.spec + ((size_t)grid * N + row0) * N;
     const float g = (float)a.gc[grid].p.gravity;
     // MUFU reciprocal square roots (no IEEE slow-path calls, so the row's
     // loads issue back to back); only the arrays this family reads
 #pragma unroll 4
-    for (int j = threadIdx.x; j < N; j += blockDim.x) {
+    for (int j = threadIdx.x; j < rpc * N; j += blockDim.x) {
       const float4 sp = __ldg(srow + j);  // (h~, G)
-      const float kz = dkf * (float)(j - N / 2);
+      const float kx = dkf * (float)(row0 + j / N - N / 2);
+      const float kz = dkf * (float)((j & (N - 1)) - N / 2);
       const float k2 = kx * kx + kz * kz;
       const bool zero = k2 == 0.f;  // k = 0: every coefficient vanishes
       const float inv = zero ? 0.f : rsqrtf(k2);
@@ -431,22 +435,26 @@ __global__ void __launch_bounds__(256, 2) k_rows_w(const RowArgs a) {
   }
   __syncthreads();
   const int slots = (seg_count + W::TPW - 1) / W::TPW;
+  const int items = slots * rpc;  // (row of the CTA, transform slot)
   float2* buf = bufs + (size_t)(warp * W::TPW + sub) * W::STRIDE;
   // the (kind, y0, y1) of this warp's next transform are loaded one slot ahead
-  auto desc_of = [&](int slot) {
-    const int li = slot * W::TPW + sub;
+  auto desc_of = [&](int item) {
+    const int li = (item % slots) * W::TPW + sub;
     const XformDesc* d = a.desc + seg_first + (li < seg_count ? li : 0);
     return make_float3(__int_as_float(__ldg(&d->kind)), __ldg(&d->y0), __ldg(&d->y1));
   };
   float3 dnext = make_float3(0.f, 0.f, 0.f);
-  if constexpr (!PLAIN) dnext = desc_of(warp < slots ? warp : 0);
-  for (int slot = warp; slot < slots; slot += warps) {
+  if constexpr (!PLAIN) dnext = desc_of(warp < items ? warp : 0);
+  for (int item = warp; item < items; item += warps) {
+    const int rr = item / slots, slot = item - rr * slots;
+    const int row = row0 + rr;
+    const float kx = dkf * (float)(row - N / 2);
     const int li = slot * W::TPW + sub;
     const bool valid = li < seg_count;
     const int gi = seg_first + (valid ? li : 0);  // transform index within the group
     const float3 dcur = dnext;
     if constexpr (!PLAIN)
-      if (slot + warps < slots) dnext = desc_of(slot + warps);
+      if (item + warps < items) dnext = desc_of(item + warps);
     float2* out = a.scratch + ((size_t)gi * N + (row ^ H)) * N;
     auto store = [&](int k, float2 x) {
       if (valid) out[k] = x;
@@ -481,8 +489,8 @@ __global__ void __launch_bounds__(256, 2) k_rows_w(const RowArgs a) {
             t, buf, stw,
             [&](int j) {
               const int jj = j ^ H;
-              const float2 h = sht[jj];
-              const float inv = sinv[jj];
+              const float2 h = sht[rr * N + jj];
+              const float inv = sinv[rr * N + jj];
               const float kz = dk * (float)(jj - N / 2);
               const float mr = fmaf(inv * kx, fmaf(c2, kz, c1), fmaf(c3, kz, c0));
               const float mi = fmaf(inv, fmaf(c6 * kz, kz, c5 * (kz + kx2)), c4);
@@ -800,7 +808,12 @@ void launch_rows(ocn_ctx* ctx, const RowArgs& a, bool plain, cudaStream_t st, in
     using W = WarpLaunch<N>;
     const int slots = (max_seg + W::TPW - 1) / W::TPW;
     const int cap = lean ? 4 : 8;  // lean: co-resides with a column pass
-    const int warps = slots < cap ? slots : cap;
+    // surface grids have 4 transforms: two rows per CTA keep 8 warps busy
+    static const bool one_row = getenv("OCN_ROWS_RPC1") != nullptr;
+    const int rpc = (!one_row && !plain && family == 0 && 2 * slots <= cap) ? 2 : 1;
+    const int warps = slots * rpc < cap ? slots * rpc : cap;
+    RowArgs ar = a;
+    ar.rpc = rpc;
     const size_t smem = (plain ? 0 : 2 * N * sizeof(float4)) + W::TWN * sizeof(float2) +
                         (size_t)warps * W::TPW * W::STRIDE * sizeof(float2);
     static bool attr = false;
@@ -812,13 +825,13 @@ void launch_rows(ocn_ctx* ctx, const RowArgs& a, bool plain, cudaStream_t st, in
       OCN_CUDA(cudaFuncSetAttribute(k_rows_w<N, kRowVelocity>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
       attr = true;
     }
-    const dim3 grid(N, plain ? 1 : nseg);
+    const dim3 grid(N / rpc, plain ? 1 : nseg);
     if (plain)
-      k_rows_w<N, kRowPlain><<<grid, 32 * warps, smem, st>>>(a);
+      k_rows_w<N, kRowPlain><<<grid, 32 * warps, smem, st>>>(ar);
     else if (family == 0)
-      k_rows_w<N, kRowSurface><<<grid, 32 * warps, smem, st>>>(a);
+      k_rows_w<N, kRowSurface><<<grid, 32 * warps, smem, st>>>(ar);
     else
-      k_rows_w<N, kRowVelocity><<<grid, 32 * warps, smem, st>>>(a);
+      k_rows_w<N, kRowVelocity><<<grid, 32 * warps, smem, st>>>(ar);
     OCN_LAUNCHED(ctx);
     return;
   }
