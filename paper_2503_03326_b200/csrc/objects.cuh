@@ -97,7 +97,10 @@ struct ocn_cascades {
   ocn::DevBuf<float2> h0;       // [C][N][N] fp32 hot-path table
   ocn::DevBuf<uint8_t> in_band; // [C][N][N]
   ocn::DevBuf<float2> twiddle;  // per-N inter-pass twiddles (fft_core.cuh)
-  ocn::DevBuf<float4> spec;     // [C][N][N] evolved (h~, G) at the current frame
+  ocn::DevBuf<float4> h0p;      // [C][N][N] (h0(k), conj(h0(-k))), built once
+  ocn::DevBuf<double> omega;    // [C][N][N] dispersion w(k), built once
+  ocn::DevBuf<float2> spec_h;   // [C][N][N] evolved h~ at the current frame
+  ocn::DevBuf<float2> spec_g;   // [C][N][N] evolved G (written by velocity plans only)
   ocn::DevBuf<float2> scratch;  // row-pass intermediates of one transform group
   ocn::DevBuf<double> d_time;   // frame time read by k_evolve (set per frame)
   int group = 1;                // transforms per group

@@ -180,12 +180,15 @@ __global__ void k_assemble_coef(int n, double dk, double g, double t, double cho
 // h~ and G (surface.cpp:49-50; velocity.cpp:16-20) at time t, one cascade.
 __global__ void k_set_time(double* d_time, double t) { *d_time = t; }
 
-__global__ void __launch_bounds__(256) k_evolve(int n, int count, const GridConst* gc,
-                                                const double* d_time,
-                                                const float2* __restrict__ h0, float4* spec) {
+// Per-frame tables built once at spectrum creation: h0p = (h0(k), conj(h0(-k)))
+// as one float4 (no mirror gather per frame, spectra.cpp:171-177) and the fp64
+// dispersion w(k) = sqrt(g |k|) (spectra.hpp:44-46), so the frame's evolve is
+// two streaming loads and one or two stores per mode.
+__global__ void __launch_bounds__(256) k_evolve_tables(int n, int count, const GridConst* gc,
+                                                       const float2* __restrict__ h0,
+                                                       float4* h0p, double* omega) {
   const size_t nn = (size_t)n * n;
   const size_t total = nn * count;
-  const double t = *d_time;
   for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
        idx += (size_t)gridDim.x * blockDim.x) {
     const int c = (int)(idx / nn);
@@ -193,20 +196,35 @@ __global__ void __launch_bounds__(256) k_evolve(int n, int count, const GridCons
     const int i = q / n, j = q - i * n;
     const int ni = i == 0 ? 0 : n - i, nj = j == 0 ? 0 : n - j;
     const float2* h = h0 + (size_t)c * nn;
-    const float2 a = __ldg(h + q);
-    const float2 m = __ldg(h + ni * n + nj);
-    const float2 b = make_float2(m.x, -m.y);  // conj(h0(-k))
+    const float2 a = h[q], m = h[ni * n + nj];
+    h0p[idx] = make_float4(a.x, a.y, m.x, -m.y);
     const double dk = gc[c].dk;
     const double kx = dk * (i - n / 2), kz = dk * (j - n / 2);
-    const double omega = sqrt(gc[c].p.gravity * sqrt(kx * kx + kz * kz));
-    double ph = omega * t;
+    omega[idx] = sqrt(gc[c].p.gravity * sqrt(kx * kx + kz * kz));
+  }
+}
+
+// h~ = h0 e^{iwt} + conj(h0(-k)) e^{-iwt} -> spec_h, and (velocity plans)
+// G = h0 e^{iwt} - conj(h0(-k)) e^{-iwt} -> spec_g (surface.cpp:49-50;
+// velocity.cpp:16-20); the fp64 phase is reduced mod 2 pi before the fp32 sincos.
+template <bool WITH_G>
+__global__ void __launch_bounds__(256) k_evolve(size_t total, const double* d_time,
+                                                const float4* __restrict__ h0p,
+                                                const double* __restrict__ omega, float2* spec_h,
+                                                float2* spec_g) {
+  const double t = *d_time;
+  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    const float4 hp = __ldg(h0p + idx);
+    double ph = __ldg(omega + idx) * t;
     ph -= 6.283185307179586476925 * rint(ph * 0.15915494309189533577);
     float s, cs;
     sincosf((float)ph, &s, &cs);
     // A = a e^{i ph}, B = b e^{-i ph}
-    const float ar = a.x * cs - a.y * s, ai = a.x * s + a.y * cs;
-    const float br = b.x * cs + b.y * s, bi = b.y * cs - b.x * s;
-    spec[idx] = make_float4(ar + br, ai + bi, ar - br, ai - bi);
+    const float ar = hp.x * cs - hp.y * s, ai = hp.x * s + hp.y * cs;
+    const float br = hp.z * cs + hp.w * s, bi = hp.w * cs - hp.z * s;
+    __stcg(spec_h + idx, make_float2(ar + br, ai + bi));
+    if constexpr (WITH_G) __stcg(spec_g + idx, make_float2(ar - br, ai - bi));
   }
 }
 
@@ -224,7 +242,8 @@ struct RowArgs {
   int rpc = 1;  // warp kernel, surface family: rows per CTA
   const XformDesc* desc;   // group descriptors
   const GroupSeg* segs;    // per-grid segments of the group (warp kernel)
-  const float4* spec;      // (h~, G) of every grid, [grid][N][N]
+  const float2* spec_h;    // h~ of every grid, [grid][N][N]
+  const float2* spec_g;    // G of every grid (velocity plans)
   const GridConst* gc;     // per-grid constants
   float chop;
   const float2* src;  // plain mode: [G][N][N] complex input
@@ -233,7 +252,7 @@ struct RowArgs {
 };
 
 // packed coefficient X + iY of transform `d` at mode (i, j)
-__device__ __forceinline__ float2 packed_coef(const XformDesc& d, float4 s, int i, int j, int n,
+__device__ __forceinline__ float2 packed_coef(const XformDesc& d, float2 s, int i, int j, int n,
                                               float dk, float g, float chop) {
   const float kx = dk * (float)(i - n / 2);
   const float kz = dk * (float)(j - n / 2);
@@ -247,26 +266,26 @@ __device__ __forceinline__ float2 packed_coef(const XformDesc& d, float4 s, int 
     case kSurfHDx: {  // h~ (1 - ux chop)
       mr = 1.0f - kx * inv_k * chop;
       mi = 0.f;
-      base = make_float2(s.x, s.y);
+      base = s;
       break;
     }
     case kSurfDzDxDx: {  // i chop (uz + kx ux) h~
       mr = 0.f;
       mi = chop * (kz * inv_k + kx * kx * inv_k);
-      base = make_float2(s.x, s.y);
+      base = s;
       break;
     }
     case kSurfDzDxDzDz: {  // chop uz (kx + i kz) h~
       const float f = chop * kz * inv_k;
       mr = f * kx;
       mi = f * kz;
-      base = make_float2(s.x, s.y);
+      base = s;
       break;
     }
     case kSurfHxHz: {  // (-kz + i kx) h~
       mr = -kz;
       mi = kx;
-      base = make_float2(s.x, s.y);
+      base = s;
       break;
     }
     case kVelXZ: {  // -(g/w) E(y0) (kx + i kz) G
@@ -275,7 +294,7 @@ __device__ __forceinline__ float2 packed_coef(const XformDesc& d, float4 s, int 
       const float f = -(g / w) * e;
       mr = f * kx;
       mi = f * kz;
-      base = make_float2(s.z, s.w);
+      base = s;
       break;
     }
     case kVelYPair: {  // w (-E(y1) + i E(y0)) G
@@ -284,7 +303,7 @@ __device__ __forceinline__ float2 packed_coef(const XformDesc& d, float4 s, int 
       const float e1 = d.y1 > 0.f ? 1.0f + k * d.y1 : expf(k * d.y1);
       mr = -w * e1;
       mi = w * e0;
-      base = make_float2(s.z, s.w);
+      base = s;
       break;
     }
     default: {  // kVelYSingle: i w E(y0) G
@@ -292,7 +311,7 @@ __device__ __forceinline__ float2 packed_coef(const XformDesc& d, float4 s, int 
       const float e0 = d.y0 > 0.f ? 1.0f + k * d.y0 : expf(k * d.y0);
       mr = 0.f;
       mi = w * e0;
-      base = make_float2(s.z, s.w);
+      base = s;
       break;
     }
   }
@@ -321,7 +340,8 @@ __global__ void __launch_bounds__(Launch<N>::THREADS) k_rows(const RowArgs a) {
         });
   } else {
     const XformDesc d = a.desc[gi];
-    const float4* srow = a.spec + ((size_t)d.cascade * N + row) * N;
+    const float2* srow =
+        (d.kind <= kSurfHxHz ? a.spec_h : a.spec_g) + ((size_t)d.cascade * N + row) * N;
     const float dk = (float)a.gc[d.cascade].dk, g = (float)a.gc[d.cascade].p.gravity;
     fft::cta_fft<N>(
         t, sm, a.tw,
@@ -373,8 +393,11 @@ __device__ __forceinline__ float ex2_approx(float x) {
 
 enum RowMode : int { kRowPlain = 0, kRowSurface = 1, kRowVelocity = 2 };
 
+#ifndef OCN_ROWS_MINB_SMALL
+#define OCN_ROWS_MINB_SMALL 2
+#endif
 template <int N, int MODE>
-__global__ void __launch_bounds__(256, 2) k_rows_w(const RowArgs a) {
+__global__ void __launch_bounds__(256, N >= 1024 ? 2 : OCN_ROWS_MINB_SMALL) k_rows_w(const RowArgs a) {
   constexpr bool PLAIN = MODE == kRowPlain;
   using W = WarpLaunch<N>;
   constexpr int T = W::T, E = fft::Plan<N>::E;
@@ -408,13 +431,14 @@ __global__ void __launch_bounds__(256, 2) k_rows_w(const RowArgs a) {
   }
   const float dkf = PLAIN ? 0.f : (float)a.gc[grid].dk;
   if constexpr (!PLAIN) {
-    const float4* srow = a.spec + ((size_t)grid * N + row0) * N;
+    const float2* srow =
+        (MODE == kRowSurface ? a.spec_h : a.spec_g) + ((size_t)grid * N + row0) * N;
     const float g = (float)a.gc[grid].p.gravity;
     // MUFU reciprocal square roots (no IEEE slow-path calls, so the row's
     // loads issue back to back); only the arrays this family reads
 #pragma unroll 4
     for (int j = threadIdx.x; j < rpc * N; j += blockDim.x) {
-      const float4 sp = __ldg(srow + j);  // (h~, G)
+      const float2 sp = __ldg(srow + j);  // h~ (surface) or G (velocity)
       const float kx = dkf * (float)(row0 + j / N - N / 2);
       const float kz = dkf * (float)((j & (N - 1)) - N / 2);
       const float k2 = kx * kx + kz * kz;
@@ -422,13 +446,13 @@ __global__ void __launch_bounds__(256, 2) k_rows_w(const RowArgs a) {
       const float inv = zero ? 0.f : rsqrtf(k2);
       const float k = k2 * inv;
       if constexpr (MODE == kRowSurface) {
-        sht[j] = make_float2(sp.x, sp.y);
+        sht[j] = sp;
         sinv[j] = inv;
       } else {
         const float rw = zero ? 0.f : rsqrtf(g * k);  // 1 / w
         const float w = g * k * rw, f = -g * rw;     // w, -g / w
-        sv0[j] = make_float2(f * (sp.z * kx - sp.w * kz), f * (sp.z * kz + sp.w * kx));
-        sw0[j] = make_float2(sp.z * w, sp.w * w);
+        sv0[j] = make_float2(f * (sp.x * kx - sp.y * kz), f * (sp.x * kz + sp.y * kx));
+        sw0[j] = make_float2(sp.x * w, sp.y * w);
         sk[j] = k;
       }
     }
@@ -1182,8 +1206,12 @@ static void enqueue_spectral(ocn_cascades* cas, SpectralPlan* plan, double chopp
   };
   {
     ProfWindow pw(ctx, OCN_PROF_EVOLVE);  // every grid in one launch
-    k_evolve<<<grid_for(ctx, nn * cas->count), 256, 0, A>>>(n, cas->count, cas->gconst.p,
-                                                            cas->d_time.p, cas->h0.p, cas->spec.p);
+    if (plan->need_velocity)
+      k_evolve<true><<<grid_for(ctx, nn * cas->count), 256, 0, A>>>(
+          nn * cas->count, cas->d_time.p, cas->h0p.p, cas->omega.p, cas->spec_h.p, cas->spec_g.p);
+    else
+      k_evolve<false><<<grid_for(ctx, nn * cas->count), 256, 0, A>>>(
+          nn * cas->count, cas->d_time.p, cas->h0p.p, cas->omega.p, cas->spec_h.p, nullptr);
     OCN_LAUNCHED(ctx);
   }
   if (plan->fused) {
@@ -1195,7 +1223,8 @@ static void enqueue_spectral(ocn_cascades* cas, SpectralPlan* plan, double chopp
       attr = true;
     }
     FusedArgs fa{};
-    fa.spec = cas->spec.p;
+    fa.spec_h = cas->spec_h.p;
+    fa.spec_g = cas->spec_g.p;
     fa.gc = cas->gconst.p;
     fa.chop = (float)choppiness;
     fa.desc = plan->desc.p;
@@ -1221,7 +1250,8 @@ static void enqueue_spectral(ocn_cascades* cas, SpectralPlan* plan, double chopp
     ra.G = gr.count;
     ra.desc = plan->desc.p + gr.first;
     ra.segs = plan->segs.p + gr.seg0;
-    ra.spec = cas->spec.p;
+    ra.spec_h = cas->spec_h.p;
+    ra.spec_g = cas->spec_g.p;
     ra.gc = cas->gconst.p;
     ra.chop = (float)choppiness;
     ra.scratch = scratch;
@@ -1550,7 +1580,10 @@ int ocn_cascades_create_multi(ocn_ctx* ctx, int resolution, int count, const dou
     cas->h0_f64.alloc(nn * count);
     cas->h0.alloc(nn * count);
     cas->in_band.alloc(nn * count);
-    cas->spec.alloc(nn * count);
+    cas->h0p.alloc(nn * count);
+    cas->omega.alloc(nn * count);
+    cas->spec_h.alloc(nn * count);
+    cas->spec_g.alloc(nn * count);
     std::vector<GridConst> gc(count);
     for (int c = 0; c < count; ++c) {
       gc[c].dk = 2.0 * kPi / lengths[c];
@@ -1565,6 +1598,9 @@ int ocn_cascades_create_multi(ocn_ctx* ctx, int resolution, int count, const dou
                              cudaMemcpyHostToDevice, ctx->stream));
     k_spectrum_init<<<grid_for(ctx, nn * count), 256, 0, ctx->stream>>>(
         resolution, count, cas->gconst.p, cas->h0_f64.p, cas->h0.p, cas->in_band.p);
+    OCN_LAUNCHED(ctx);
+    k_evolve_tables<<<grid_for(ctx, nn * count), 256, 0, ctx->stream>>>(
+        resolution, count, cas->gconst.p, cas->h0.p, cas->h0p.p, cas->omega.p);
     OCN_LAUNCHED(ctx);
     std::vector<float2> tw = make_twiddles(resolution);
     cas->twiddle.alloc(tw.size());

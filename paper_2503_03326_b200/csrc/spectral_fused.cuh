@@ -47,7 +47,8 @@ struct FusedWave {
 };
 
 struct FusedArgs {
-  const float4* spec;  // (h~, G) of every grid, [grid][N][N]
+  const float2* spec_h;  // h~ of every grid, [grid][N][N]
+  const float2* spec_g;  // G of every grid
   const GridConst* gc;
   float chop;
   const XformDesc* desc;   // plan descriptors
@@ -145,23 +146,23 @@ __global__ void __launch_bounds__(Fused<N>::THREADS, 1)
       const GridConst& gcv = a.gc[wv.grid];
       const float dk = (float)gcv.dk, g = (float)gcv.p.gravity;
       const float kx = dk * (float)(row - N / 2);
-      const float4* srow = a.spec + ((size_t)wv.grid * N + row) * N;
+      const float2* srow = (wv.family == 0 ? a.spec_h : a.spec_g) + ((size_t)wv.grid * N + row) * N;
 #pragma unroll 4
       for (int j = tid; j < N; j += F::ROW_THREADS) {
-        const float4 sp = __ldg(srow + j);  // (h~, G)
+        const float2 sp = __ldg(srow + j);  // h~ (surface) or G (velocity)
         const float kz = dk * (float)(j - N / 2);
         const float k2 = kx * kx + kz * kz;
         const bool zero = k2 == 0.f;
         const float inv = zero ? 0.f : rsqrtf(k2);
         const float k = k2 * inv;
         if (wv.family == 0) {
-          sht[j] = make_float2(sp.x, sp.y);
+          sht[j] = sp;
           sinv[j] = inv;
         } else {
           const float rw = zero ? 0.f : rsqrtf(g * k);
           const float wq = g * k * rw, f = -g * rw;
-          sv0[j] = make_float2(f * (sp.z * kx - sp.w * kz), f * (sp.z * kz + sp.w * kx));
-          sw0[j] = make_float2(sp.z * wq, sp.w * wq);
+          sv0[j] = make_float2(f * (sp.x * kx - sp.y * kz), f * (sp.x * kz + sp.y * kx));
+          sw0[j] = make_float2(sp.x * wq, sp.y * wq);
           sk[j] = k;
         }
       }
