@@ -53,6 +53,7 @@ struct XformDesc {
 
 struct SpectralPlan {
   DevBuf<XformDesc> desc;
+  DevBuf<CUtensorMap> out_maps;  // TMA-store column pass: Re / Im maps per transform
   // transform groups (G consecutive transforms, possibly spanning grids) and
   // their per-grid segments
   struct Group {

@@ -360,6 +360,7 @@ struct ColArgs {
   const XformDesc* desc;  // split outputs per transform
   float2* out_c;          // complex mode: [G][N][N]
   const float2* tw;
+  const CUtensorMap* out_maps;  // TMA-store column pass: Re / Im store maps per transform
 };
 
 // ------------------------------------------------------------------ rows (N <= 1024)
@@ -680,7 +681,9 @@ struct ColTma {
   static constexpr int TW = PL::tw_size();
   static constexpr int STAGES = (227 * 1024 - TW * 8 - 64) / (STAGE * 8) >= 3 ? 3 : 2;
   static constexpr uint32_t TILE_BYTES = (uint32_t)DENSE * 8;
-  static constexpr size_t smem(int stages) { return ((size_t)stages * STAGE + TW) * 8 + stages * 8; }
+  static constexpr size_t smem(int stages, bool tma_store = false) {
+    return ((size_t)stages * STAGE + (tma_store ? DENSE : 0) + TW) * 8 + stages * 8;
+  }
   static constexpr size_t SMEM = smem(STAGES);
   static constexpr int BR = N < 256 ? N : 256;  // rows per box dimension
   static constexpr bool OK = PL::P > 1 && N >= 128 && N <= 4096 && SMEM <= 227 * 1024;
@@ -689,13 +692,19 @@ struct ColTma {
 // columns per tile of the TMA column kernel, 0 outside its range
 int cols_tma_pc(int n) { return n >= 128 && n <= 4096 ? 8192 / n : 0; }
 
-template <int N, bool COMPLEX_OUT, int S>
+// TMA_STORE (split mode): the final pass writes Re / Im into fp32 staging
+// planes and one elected thread stores them with two tiled TMA stores (no STG
+// from the warps); the staging is reused once the previous tile's stores have
+// read it (cp.async.bulk.wait_group.read in the refill point).
+template <int N, bool COMPLEX_OUT, int S, bool TMA_STORE = false>
 __global__ void __launch_bounds__(ColTma<N>::THREADS, 1)
     k_cols_tma(const __grid_constant__ CUtensorMap src, const ColArgs a, int tiles_x, int ntiles) {
   using CT = ColTma<N>;
   constexpr int PC = CT::PC;
   extern __shared__ __align__(128) float2 smem[];
-  float2* stw = smem + S * CT::STAGE;
+  float* sre = reinterpret_cast<float*>(smem + S * CT::STAGE);  // TMA_STORE staging
+  float* sim = sre + CT::DENSE;
+  float2* stw = smem + S * CT::STAGE + (TMA_STORE ? CT::DENSE : 0);
   const uint32_t bar0 = tma::smem_u32(stw + CT::TW);
   const int c = threadIdx.x % PC, t = threadIdx.x / PC;
   auto issue = [&](int tile, int s) {
@@ -721,6 +730,7 @@ __global__ void __launch_bounds__(ColTma<N>::THREADS, 1)
     float2* buf = smem + s * CT::STAGE;
     tma::mbar_wait(bar0 + 8 * s, phase);
     auto refill = [&] {
+      if (TMA_STORE && threadIdx.x == 0) tma::bulk_wait_read();  // staging free again
       __syncthreads();  // every thread's shared reads of this buffer are done
       if (threadIdx.x == 0) {
         const int next = tile + S * gridDim.x;
@@ -739,6 +749,22 @@ __global__ void __launch_bounds__(ColTma<N>::THREADS, 1)
             out[(size_t)r * N + col] = x;
           },
           refill);
+    } else if constexpr (TMA_STORE) {
+      fft::cta_fft<N, false, true, false, true>(
+          t, buf + c * CT::STRIDE, stw, [&](int i) { return dense[i * PC + c]; },
+          [&](int r, float2 x) {
+            sre[r * PC + c] = x.x;  // fft.cpp:93-99 split
+            sim[r * PC + c] = x.y;
+          },
+          refill);
+      tma::fence_proxy_async_smem();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const int col0 = col - c;
+        tma::store_3d(a.out_maps + 2 * xf, tma::smem_u32(sre), col0, 0, 0);
+        if (a.desc[xf].out_im) tma::store_3d(a.out_maps + 2 * xf + 1, tma::smem_u32(sim), col0, 0, 0);
+        tma::bulk_commit();
+      }
     } else {
       const XformDesc d = a.desc[xf];
       fft::cta_fft<N, false, true, false, true>(
@@ -751,6 +777,7 @@ __global__ void __launch_bounds__(ColTma<N>::THREADS, 1)
     }
     if (++s == S) s = 0, phase ^= 1;
   }
+  if (TMA_STORE && threadIdx.x == 0) tma::bulk_wait();
 }
 
 #include "spectral_fused.cuh"
@@ -891,12 +918,16 @@ void launch_cols(ocn_ctx* ctx, const ColArgs& a, int G, bool complex_out, cudaSt
         OCN_CUDA(cudaFuncSetAttribute(k_cols_tma<N, false, CT::STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CT::SMEM));
         OCN_CUDA(cudaFuncSetAttribute(k_cols_tma<N, true, CT::STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CT::SMEM));
         OCN_CUDA(cudaFuncSetAttribute(k_cols_tma<N, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CT::smem(2)));
+        if (CT::smem(2, true) <= 227 * 1024)
+          OCN_CUDA(cudaFuncSetAttribute(k_cols_tma<N, false, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CT::smem(2, true)));
         attr = true;
       }
       const int tiles_x = N / CT::PC, ntiles = tiles_x * G;
       const int grid = std::min(ntiles, ctx->sm_count);
       if (complex_out)
         k_cols_tma<N, true, CT::STAGES><<<grid, CT::THREADS, CT::SMEM, st>>>(*map, a, tiles_x, ntiles);
+      else if (a.out_maps && CT::smem(2, true) <= 227 * 1024)
+        k_cols_tma<N, false, 2, true><<<grid, CT::THREADS, CT::smem(2, true), st>>>(*map, a, tiles_x, ntiles);
       else if (lean)  // leaves room on each SM for a concurrent row pass
         k_cols_tma<N, false, 2><<<grid, CT::THREADS, CT::smem(2), st>>>(*map, a, tiles_x, ntiles);
       else
@@ -1035,6 +1066,39 @@ bool cols_map_for(int n, int G, const float2* scratch, CUtensorMap* map, int pc_
   return true;
 }
 
+// Store map of one fp32 output plane [N][N] viewed as [N / BR][BR][N]: box
+// {PC, BR, N / BR} is the plane's share of one column tile.
+static void plane_map_for(int n, float* plane, CUtensorMap* map) {
+  const int pc = cols_tma_pc(n), br = n < 256 ? n : 256;
+  const uint64_t dims[3] = {(uint64_t)n, (uint64_t)br, (uint64_t)(n / br)};
+  const uint64_t strides[2] = {(uint64_t)n * 4, (uint64_t)br * n * 4};
+  const uint32_t box[3] = {(uint32_t)pc, (uint32_t)br, (uint32_t)(n / br)};
+  *map = CUtensorMap{};
+  if (plane && !tma::encode_f32(map, 3, plane, dims, strides, box))
+    fail(OCN_ERR_CUDA, "cuTensorMapEncodeTiled failed for an output plane (N=%d)", n);
+}
+
+// TMA-store column pass (default; OCN_COLS_STG=1 selects direct evict-first
+// stores from the warps, 3 load stages): measured 1.122 vs 1.128 ms spectral
+// per frame (config 3); both sit at ~83% of the measured HBM copy bandwidth.
+static bool cols_tma_store() {
+  static const bool on = [] {
+    const char* e = getenv("OCN_COLS_STG");
+    return !(e && *e && *e != '0');
+  }();
+  return on;
+}
+
+static void build_out_maps(int n, const XformDesc* desc, int count, DevBuf<CUtensorMap>& out) {
+  std::vector<CUtensorMap> h((size_t)2 * count);
+  for (int i = 0; i < count; ++i) {
+    plane_map_for(n, desc[i].out_re, &h[2 * i]);
+    plane_map_for(n, desc[i].out_im, &h[2 * i + 1]);
+  }
+  out.alloc(h.size());
+  OCN_CUDA(cudaMemcpy(out.p, h.data(), h.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+}
+
 // The fused row + column step (spectral_fused.cuh, N = 1024) is opt-in
 // (OCN_FUSED=1): measured on B200 (config 3 spectral, ms / frame) 1.88-2.35
 // across wave sizes 8-24 and 2-4 slots, against 1.12 for the two-kernel step.
@@ -1105,6 +1169,8 @@ static SpectralPlan* get_plan(ocn_cascades* cas, ocn_maps* maps, ocn_slices* sli
       }
     }
   }
+  if (cas->cols_map_ok && cols_tma_store())
+    build_out_maps(cas->n, plan->host_desc.data(), (int)plan->host_desc.size(), plan->out_maps);
   plan->desc.alloc(plan->host_desc.size());
   OCN_CUDA(cudaMemcpy(plan->desc.p, plan->host_desc.data(),
                       plan->host_desc.size() * sizeof(XformDesc), cudaMemcpyHostToDevice));
@@ -1268,6 +1334,7 @@ static void enqueue_spectral(ocn_cascades* cas, SpectralPlan* plan, double chopp
     ca.scratch = scratch;
     ca.desc = plan->desc.p + gr.first;
     ca.tw = cas->twiddle.p;
+    ca.out_maps = plan->out_maps.p ? plan->out_maps.p + 2 * gr.first : nullptr;
     {
       ProfWindow pw(ctx, dual ? -1 : OCN_PROF_COLS);
       cols_dispatch(ctx, n, ca, gr.count, false, B,
