@@ -436,9 +436,15 @@ def run_ours(args):
         "config": cfg,
         "stages_ms": stages,
         "spectral_kernels_ms_eager": kernels,
-        "roofline": {"kernel": "spectral pipeline (k_evolve + k_rows_w + k_cols, one CUDA graph)",
+        "roofline": {"kernel": ("spectral pipeline (k_evolve + k_rows_w + k_cols_tma, one CUDA graph)"
+                                if not (c4 or c5) else
+                                "spectral pipeline (k_evolve + k_rows_w + k_cols_tma)" if c4 else
+                                "slab pipeline (k_slab_evolve + k_slab_rows + k_slab_cols)"),
                      "bound": "hbm", "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
-                     "unit": "GB/s", "frac": achieved / peak, "traffic": _traffic(),
+                     "unit": "GB/s", "frac": achieved / peak,
+                     # dram read + write bytes per frame of the same kernels (ncu
+                     # application replay, profiles/roofline_traffic.json; config 3)
+                     "traffic": _traffic() if not (c4 or c5) else None,
                      "algorithmic_bytes_per_frame": alg_bytes},
         "e2e": {"value": points / e2e_frame, "unit": "grid-points/s", "ms_per_frame": e2e_frame * 1e3,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
