@@ -1169,7 +1169,8 @@ static SpectralPlan* get_plan(ocn_cascades* cas, ocn_maps* maps, ocn_slices* sli
       }
     }
   }
-  if (cas->cols_map_ok && cols_tma_store())
+  // (16-byte store boxes: PC >= 4 columns, i.e. N <= 2048)
+  if (cas->cols_map_ok && cols_tma_store() && cols_tma_pc(cas->n) >= 4)
     build_out_maps(cas->n, plan->host_desc.data(), (int)plan->host_desc.size(), plan->out_maps);
   plan->desc.alloc(plan->host_desc.size());
   OCN_CUDA(cudaMemcpy(plan->desc.p, plan->host_desc.data(),

@@ -84,7 +84,14 @@ def test_generate_maps_config2_full(oc, port):
     _maps_case(oc, port, 1024, CONFIG2_LENGTHS, CONFIG2_CUTOFFS, config2_params(), 10.0)
 
 
-@pytest.mark.parametrize("n,count,dist", [(64, 7, 0), (128, 8, 1), (256, 32, 0)])
+@pytest.mark.parametrize("n", [2048, 4096])
+def test_generate_maps_large(oc, port, n):
+    """Large single grids: the TMA column pass at 8 / 4 / 2 columns per tile
+    and its store epilogues (TMA store up to 2048, direct stores at 4096)."""
+    _maps_case(oc, port, n, [float(n)], [], config2_params(seed=3), 4.0, 0.8)
+
+
+@pytest.mark.parametrize("n,count,dist", [(64, 7, 0), (128, 8, 1), (256, 32, 0), (1024, 3, 0)])
 def test_build_slices(oc, port, n, count, dist):
     p = config2_params(seed=5)
     cfg = SliceConfig.make(count=count, distribution=dist)
