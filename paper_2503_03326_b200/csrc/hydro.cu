@@ -6,13 +6,16 @@
 //
 // Pipeline (one stream, no host round trip until the report is read):
 //   k_vertices   world transform + Algorithm-1 height (+ other zones) -> depth
-//   k_classify   per triangle: 0 / 1 / 3 states, 0 / 1 waterline segment
-//   scan         order-preserving offsets (parent order, hydro.cpp:151-163)
+//   k_classify_scan  per triangle: 0 / 1 / 3 states, 0 / 1 waterline segment,
+//                and the block-local exclusive scan of those counts
+//   k_scan_blocks    the block totals -> order-preserving offsets (parent
+//                order, hydro.cpp:151-163)
 //   k_emit       TriangleStates and crossing segments at their offsets
 //   k_forces     per state: prism volume, immersion moment, drag (velocity_at
-//                at the centroid), dry area / moment -> fixed-tree block sums
-//   k_finalize   fixed-order reduction of the block sums, clamps, buoyancy,
-//                application points, composed force / torque (sim.cpp:114-122)
+//                at the centroid), dry area / moment -> fixed-tree block sums;
+//                the last block (ticket) reduces them in a fixed order, clamps,
+//                buoyancy, application points, composed force / torque
+//                (sim.cpp:114-122)
 //   k_chain      waterline chaining with the reference's visiting order
 //                (hydro.cpp:165-213): start at the lowest unused segment,
 //                enter through its first edge, last-writer crossing points.
@@ -67,76 +70,88 @@ __global__ void __launch_bounds__(128) k_vertices(int nv, const double* __restri
   }
 }
 
-// ---------------------------------------------------------------- K7: classify
-// counts.x = states emitted (0 degenerate, 1 whole, 3 split), counts.y = segment
-__global__ void __launch_bounds__(256) k_classify(int nt, const int3* __restrict__ tris,
-                                                  const double* __restrict__ areas,
-                                                  const double* __restrict__ depth, int2* counts) {
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
-    int2 c = make_int2(0, 0);
-    if (areas[t] > 0.0) {
-      const int3 v = tris[t];
-      const int above = (depth[v.x] >= 0.0) + (depth[v.y] >= 0.0) + (depth[v.z] >= 0.0);
-      if (above == 0 || above == 3) {
-        c.x = 1;
-      } else {
-        c.x = 3;
-        c.y = 1;  // keys (a,b) != (a,c) since a, b, c are distinct in a validated mesh
-      }
-    }
-    counts[t] = c;
-  }
-}
-
-// ---------------------------------------------------------------- scan (int2)
+// ---------------------------------------------------------------- K7: classify + scan
+// counts.x = states emitted (0 degenerate, 1 whole, 3 split), counts.y = segment.
+// One triangle per thread; each 1024-triangle block also scans its counts
+// (exclusive, parent order, hydro.cpp:151-163) and leaves its total for
+// k_scan_blocks; k_emit adds the block's offset.
 constexpr int kScanBlock = 1024;
 
 __device__ __forceinline__ int2 add2(int2 a, int2 b) { return make_int2(a.x + b.x, a.y + b.y); }
 
-__device__ int2 block_exclusive_scan(int2 v, int2* sh, int2* total) {
-  // Hillis-Steele in shared memory (blockDim = kScanBlock)
-  const int t = threadIdx.x;
-  sh[t] = v;
-  __syncthreads();
-  for (int off = 1; off < blockDim.x; off <<= 1) {
-    int2 a = t >= off ? sh[t - off] : make_int2(0, 0);
-    __syncthreads();
-    sh[t] = add2(sh[t], a);
-    __syncthreads();
+// exclusive scan of one int2 per thread over a block of kScanBlock threads
+// (warp shuffles, then the 32 warp totals by warp 0)
+__device__ int2 block_exclusive_scan(int2 v, int2* warp_tot, int2* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int2 incl = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int x = __shfl_up_sync(0xffffffffu, incl.x, off);
+    const int y = __shfl_up_sync(0xffffffffu, incl.y, off);
+    if (lane >= off) incl.x += x, incl.y += y;
   }
-  int2 incl = sh[t];
-  *total = sh[blockDim.x - 1];
+  if (lane == 31) warp_tot[warp] = incl;
   __syncthreads();
-  return make_int2(incl.x - v.x, incl.y - v.y);
+  if (warp == 0) {
+    int2 w = lane < (int)(blockDim.x >> 5) ? warp_tot[lane] : make_int2(0, 0);
+    int2 wi = w;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int x = __shfl_up_sync(0xffffffffu, wi.x, off);
+      const int y = __shfl_up_sync(0xffffffffu, wi.y, off);
+      if (lane >= off) wi.x += x, wi.y += y;
+    }
+    warp_tot[lane] = make_int2(wi.x - w.x, wi.y - w.y);  // exclusive warp offsets
+    if (lane == 31) *total = wi;
+  }
+  __syncthreads();
+  const int2 base = warp_tot[warp];
+  return make_int2(base.x + incl.x - v.x, base.y + incl.y - v.y);
 }
 
-__global__ void __launch_bounds__(kScanBlock) k_scan_local(int n, const int2* in, int2* out,
-                                                           int2* block_sums) {
-  __shared__ int2 sh[kScanBlock];
-  const int i = blockIdx.x * kScanBlock + threadIdx.x;
-  int2 v = i < n ? in[i] : make_int2(0, 0);
-  int2 tot;
-  int2 ex = block_exclusive_scan(v, sh, &tot);
-  if (i < n) out[i] = ex;
+__global__ void __launch_bounds__(kScanBlock) k_classify_scan(int nt, const int3* __restrict__ tris,
+                                                             const double* __restrict__ areas,
+                                                             const double* __restrict__ depth,
+                                                             int2* counts, int2* offsets,
+                                                             int2* block_sums) {
+  __shared__ int2 warp_tot[32];
+  __shared__ int2 tot;
+  const int t = blockIdx.x * kScanBlock + threadIdx.x;
+  int2 c = make_int2(0, 0);
+  if (t < nt && areas[t] > 0.0) {
+    const int3 v = tris[t];
+    const int above = (depth[v.x] >= 0.0) + (depth[v.y] >= 0.0) + (depth[v.z] >= 0.0);
+    if (above == 0 || above == 3) {
+      c.x = 1;
+    } else {
+      c.x = 3;
+      c.y = 1;  // keys (a,b) != (a,c) since a, b, c are distinct in a validated mesh
+    }
+  }
+  const int2 ex = block_exclusive_scan(c, warp_tot, &tot);
+  if (t < nt) {
+    counts[t] = c;
+    offsets[t] = ex;
+  }
+  __syncthreads();
   if (threadIdx.x == 0) block_sums[blockIdx.x] = tot;
 }
 
-// scans the block sums sequentially in one block (count <= a few hundred)
-__global__ void k_scan_blocks(int nb, int2* block_sums, int2* total) {
-  if (threadIdx.x == 0) {
-    int2 acc = make_int2(0, 0);
-    for (int b = 0; b < nb; ++b) {
-      int2 v = block_sums[b];
-      block_sums[b] = acc;
-      acc = add2(acc, v);
-    }
-    *total = acc;
+// exclusive scan of the per-block totals in one block (any count), total out
+__global__ void __launch_bounds__(kScanBlock) k_scan_blocks(int nb, int2* block_sums, int2* total) {
+  __shared__ int2 warp_tot[32];
+  __shared__ int2 tot;
+  int2 carry = make_int2(0, 0);
+  for (int base = 0; base < nb; base += kScanBlock) {
+    const int i = base + threadIdx.x;
+    const int2 v = i < nb ? block_sums[i] : make_int2(0, 0);
+    const int2 ex = block_exclusive_scan(v, warp_tot, &tot);
+    if (i < nb) block_sums[i] = add2(carry, ex);
+    __syncthreads();
+    carry = add2(carry, tot);
+    __syncthreads();
   }
-}
-
-__global__ void k_scan_add(int n, int2* out, const int2* block_sums) {
-  const int i = blockIdx.x * kScanBlock + threadIdx.x;
-  if (i < n) out[i] = add2(out[i], block_sums[blockIdx.x]);
+  if (threadIdx.x == 0) *total = carry;
 }
 
 // ---------------------------------------------------------------- K7: emit
@@ -158,12 +173,13 @@ __global__ void __launch_bounds__(256) k_emit(int nt, const int3* __restrict__ t
                                               const double* __restrict__ wpos,
                                               const double* __restrict__ depth, PoseDev P,
                                               const int2* __restrict__ counts,
-                                              const int2* __restrict__ offsets, StateDev* states,
+                                              const int2* __restrict__ offsets,
+                                              const int2* __restrict__ block_sums, StateDev* states,
                                               SegDev* segs) {
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
     const int2 c = counts[t];
     if (c.x == 0) continue;
-    const int2 off = offsets[t];
+    const int2 off = add2(offsets[t], block_sums[t / kScanBlock]);
     const int3 v = tris[t];
     const double3 n = qrot(P, ld3(normals + 3 * t));
     const double d0 = depth[v.x], d1 = depth[v.y], d2 = depth[v.z];
@@ -228,11 +244,20 @@ __device__ __forceinline__ double3 drag_dev(const StateDev& s, double3 medium, d
   return vrel * (-(0.5 * cd * rho * a_perp * speed));
 }
 
+__device__ void finalize_report(int nblocks, const double* block_out, PoseDev P, FluidDev F,
+                                double mesh_volume, const int2* total, int degenerate,
+                                ReportDev* rep);
+
+// Per-state loads (hydro.cpp:215-306) reduced per block in a fixed tree; the
+// last block to finish (ticket counter) reduces the block partials in a fixed
+// order and writes the report, so no separate finalize launch is needed.
 __global__ void __launch_bounds__(kForceThreads) k_forces(const StateDev* __restrict__ states,
                                                           const int2* total, PoseDev P,
                                                           SliceView vel, int have_vel, int clamp,
                                                           FluidDev F, double* block_out,
-                                                          int* domain_err) {
+                                                          int* domain_err, int* ticket,
+                                                          double mesh_volume, int degenerate,
+                                                          ReportDev* rep) {
   __shared__ double sh[kTerms][kForceThreads];
   const int ns = total->x;
   double acc[kTerms];
@@ -278,6 +303,15 @@ __global__ void __launch_bounds__(kForceThreads) k_forces(const StateDev* __rest
     __syncthreads();
   }
   if (threadIdx.x < kTerms) block_out[blockIdx.x * kTerms + threadIdx.x] = sh[threadIdx.x][0];
+  __threadfence();  // this block's partials, before its ticket
+  __syncthreads();
+  __shared__ bool last;
+  if (threadIdx.x == 0) last = atomicAdd(ticket, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  finalize_report(gridDim.x, block_out, P, F, mesh_volume, total, degenerate, rep);
+  if (threadIdx.x == 0) *ticket = 0;  // ready for the next evaluation
 }
 
 __device__ __forceinline__ double density_at_dev(const FluidDev& F, double y) {
@@ -300,22 +334,24 @@ __device__ __forceinline__ bool finite3(double3 v) {
 }
 
 // one block: fixed-order tree over the block partials, then the report
-__global__ void __launch_bounds__(256) k_finalize(int nblocks, const double* block_out, PoseDev P,
-                                                  FluidDev F, double mesh_volume, const int2* total,
-                                                  int degenerate, ReportDev* rep) {
-  __shared__ double sh[kTerms][256];
-  for (int k = 0; k < kTerms; ++k) {
+// Block partials -> totals (one warp per term: lane-strided sums in block
+// order, then a fixed xor tree), then the report (hydro.cpp:215-306,
+// sim.cpp:114-122). Called by the last k_forces block (kForceThreads threads).
+__device__ void finalize_report(int nblocks, const double* block_out, PoseDev P, FluidDev F,
+                                double mesh_volume, const int2* total, int degenerate,
+                                ReportDev* rep) {
+  __shared__ double tot[kTerms][1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
+  for (int k = warp; k < kTerms; k += warps) {
     double a = 0.0;
-    for (int b = threadIdx.x; b < nblocks; b += 256) a += block_out[b * kTerms + k];
-    sh[k][threadIdx.x] = a;
+    for (int b = lane; b < nblocks; b += 32) a += __ldcg(block_out + b * kTerms + k);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+    if (lane == 0) tot[k][0] = a;
   }
   __syncthreads();
-  for (int off = 128; off > 0; off >>= 1) {
-    if (threadIdx.x < off)
-      for (int k = 0; k < kTerms; ++k) sh[k][threadIdx.x] += sh[k][threadIdx.x + off];
-    __syncthreads();
-  }
   if (threadIdx.x != 0) return;
+  auto sh = tot;
   ocn_hydro_report r;
   memset(&r, 0, sizeof(r));
   double vw = sh[0][0];
@@ -753,27 +789,21 @@ void hydro_evaluate(ocn_mesh* m, const ocn_pose* pose, const ocn_fluid* fluid,
   k_vertices<<<grid_of(ctx, nv, 128), 128, 0, st>>>(nv, m->verts.p, P, sv, maps != nullptr, zl,
                                                    d_override, m->wpos.p, m->depth.p);
   OCN_LAUNCHED(ctx);
-  k_classify<<<grid_of(ctx, nt, 256), 256, 0, st>>>(nt, m->tris.p, m->areas.p, m->depth.p,
-                                                   m->counts.p);
-  OCN_LAUNCHED(ctx);
   const int nb = (nt + kScanBlock - 1) / kScanBlock;
-  k_scan_local<<<nb, kScanBlock, 0, st>>>(nt, m->counts.p, m->offsets.p, m->block_sums.p);
+  k_classify_scan<<<nb, kScanBlock, 0, st>>>(nt, m->tris.p, m->areas.p, m->depth.p, m->counts.p,
+                                             m->offsets.p, m->block_sums.p);
   OCN_LAUNCHED(ctx);
-  k_scan_blocks<<<1, 32, 0, st>>>(nb, m->block_sums.p, m->total.p);
-  OCN_LAUNCHED(ctx);
-  k_scan_add<<<nb, kScanBlock, 0, st>>>(nt, m->offsets.p, m->block_sums.p);
+  k_scan_blocks<<<1, kScanBlock, 0, st>>>(nb, m->block_sums.p, m->total.p);
   OCN_LAUNCHED(ctx);
   k_emit<<<grid_of(ctx, nt, 256), 256, 0, st>>>(nt, m->tris.p, m->normals.p, m->wpos.p, m->depth.p,
-                                               P, m->counts.p, m->offsets.p, m->states.p,
-                                               m->segs.p);
+                                               P, m->counts.p, m->offsets.p, m->block_sums.p,
+                                               m->states.p, m->segs.p);
   OCN_LAUNCHED(ctx);
   const int fblocks = ctx->sm_count * 2;
   k_forces<<<fblocks, kForceThreads, 0, st>>>(m->states.p, m->total.p, P, vv, slices != nullptr,
                                              fluid ? fluid->velocity_clamp : 1, F,
-                                             m->block_out.p, m->flags.p);
-  OCN_LAUNCHED(ctx);
-  k_finalize<<<1, 256, 0, st>>>(fblocks, m->block_out.p, P, F, m->volume, m->total.p,
-                                m->degenerate, m->report.p);
+                                             m->block_out.p, m->flags.p, m->ticket.p, m->volume,
+                                             m->degenerate, m->report.p);
   OCN_LAUNCHED(ctx);
   // waterline
   OCN_CUDA(cudaMemsetAsync(m->hkeys.p, 0, m->hkeys.bytes(), st));
@@ -853,6 +883,8 @@ int ocn_mesh_create(ocn_ctx* ctx, int nv, const double* verts, int nt, const int
     m->block_out.alloc((size_t)ctx->sm_count * 2 * kTerms);
     m->report.alloc(1);
     m->flags.alloc(4);
+    m->ticket.alloc(1);
+    OCN_CUDA(cudaMemset(m->ticket.p, 0, sizeof(int)));
     int hcap = 1;
     while (hcap < 4 * nt) hcap <<= 1;
     m->hcap = hcap;

@@ -53,6 +53,7 @@ struct ocn_mesh {
   ocn::DevBuf<double> block_out;
   ocn::DevBuf<ocn::ReportDev> report;
   ocn::DevBuf<int> flags;  // [0] velocity domain error, [1] non-manifold waterline
+  ocn::DevBuf<int> ticket;  // k_forces last-block counter (0 between evaluations)
   int hcap = 0;
   ocn::DevBuf<unsigned long long> hkeys;
   ocn::DevBuf<int> hvals, partner;
