@@ -420,14 +420,16 @@ OCN_API int ocn_zone_upload(ocn_zone* z, const double* host_curr, const double* 
  * complex64 (dev_send, exchange_bytes); the caller exchanges it (NCCL
  * all-to-all; dest tile d goes to rank d); ocn_slab_cols consumes the receive
  * buffer [src][4][R][R] and writes the 8 surface fields of the owned column
- * slab ([field][n][R] fp32, transposed-slab layout). Both are async. */
+ * slab ([field][n][R] fp32, transposed-slab layout). Both are async. For
+ * n >= 4096 the column pass is a four-step FFT that works in place in the
+ * receive buffer (its contents are overwritten). */
 OCN_API int ocn_slab_create(ocn_ctx* ctx, int n, int ranks, int rank, double length,
                             double band_min, double band_max, uint32_t cascade_index,
                             const ocn_spectrum_params* params, ocn_slab** out);
 OCN_API int ocn_slab_destroy(ocn_slab* s);
 OCN_API int ocn_slab_info(const ocn_slab* s, int* rows, int* cols, size_t* exchange_bytes);
 OCN_API int ocn_slab_rows(ocn_slab* s, double t, double choppiness, void* dev_send);
-OCN_API int ocn_slab_cols(ocn_slab* s, const void* dev_recv);
+OCN_API int ocn_slab_cols(ocn_slab* s, void* dev_recv);
 /* Column slab of one field: n x R doubles, row-major [i][column - rank R]. */
 OCN_API int ocn_slab_download(ocn_slab* s, int field, double* host_out);
 

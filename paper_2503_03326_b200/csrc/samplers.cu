@@ -87,6 +87,7 @@ __global__ void k_assemble(SurfView s, int64_t n, const double* xz, double* out)
     double px, pz, dx, dz;
     const double h = height_at_dev(s, xz[2 * i], xz[2 * i + 1], &px, &pz, &dx, &dz);
     double hx = 0, hz = 0, dxdx = 0, dzdx = 0, dzdz = 0;
+#pragma unroll 4
     for (int c = 0; c < s.C; ++c) {
       const Bilin w = bilin_setup(s.n, s.length[c], px, pz);
       hx += bilin_tap(w, s.f(c, OCN_FIELD_HX));

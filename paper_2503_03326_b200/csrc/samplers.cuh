@@ -79,6 +79,7 @@ __device__ __forceinline__ double bilin_tap(const Bilin& b, const float* __restr
 
 __device__ __forceinline__ double sample_field(const SurfView& s, int field, double x, double z) {
   double acc = 0.0;
+#pragma unroll 4  // the cascades' taps issue together (latency-bound gathers)
   for (int c = 0; c < s.C; ++c) acc += bilin_tap(bilin_setup(s.n, s.length[c], x, z), s.f(c, field));
   return acc;
 }
@@ -86,6 +87,7 @@ __device__ __forceinline__ double sample_field(const SurfView& s, int field, dou
 __device__ __forceinline__ void sample_disp(const SurfView& s, double x, double z, double* dx,
                                             double* h, double* dz) {
   double a = 0.0, b = 0.0, c2 = 0.0;
+#pragma unroll 4
   for (int c = 0; c < s.C; ++c) {
     const Bilin w = bilin_setup(s.n, s.length[c], x, z);
     a += bilin_tap(w, s.f(c, OCN_FIELD_DX));
@@ -134,6 +136,7 @@ __device__ __forceinline__ double zone_sample(const ZoneView& z, double x, doubl
 __device__ __forceinline__ void sample_slice_dev(const SliceView& s, int d, double x, double z,
                                                  double v[3]) {
   v[0] = v[1] = v[2] = 0.0;
+#pragma unroll 4
   for (int c = 0; c < s.C; ++c) {
     const Bilin w = bilin_setup(s.n, s.length[c], x, z);
     v[0] += bilin_tap(w, s.f(d, c, 0));

@@ -13,6 +13,14 @@
 //   ocn_slab_cols : column FFTs of the owned column slab from the receive
 //                   layout [src][pair][row][col], (-1)^(i+j), Re/Im split into
 //                   8 fp32 fields kept in the transposed (column-slab) layout.
+//                   For N >= 4096 a column (N x 8 B) is too long to stage
+//                   several of them in shared memory, and one column per CTA
+//                   reads one 8-byte element per 32-byte sector; the pass is
+//                   then a four-step FFT over N = N1 x 128 on 8-column tiles:
+//                   k_slab_colsA: length-N1 DFTs over rows i1 * 128 + i2
+//                   (fixed i2), twiddle w_N^(i2 k1), written back in place;
+//                   k_slab_colsB: length-128 DFTs over the contiguous rows
+//                   k1 * 128 + i2, output row k1 + N1 k2, sign and split.
 #include <algorithm>
 #include <cmath>
 #include <memory>
@@ -26,8 +34,9 @@ struct ocn_slab {
   int n = 0, ranks = 1, rank = 0, rows = 0, cols = 0;
   ocn::GridConst gc{};
   ocn::DevBuf<float2> h0, h0m;   // [rows][N]: h0 of owned rows, h0 of rows neg(i)
-  ocn::DevBuf<float4> spec;      // [rows][N]: (h~, G)
+  ocn::DevBuf<float2> spec;      // [rows][N]: h~ (the slab builds surface fields only)
   ocn::DevBuf<float2> twiddle;
+  ocn::DevBuf<float2> tw1, tw2, wn;  // four-step column pass: inner tables, w_N^m
   ocn::DevBuf<double> d_time;
   ocn::DevBuf<float> fields;     // [8][N][cols]
 };
@@ -68,7 +77,7 @@ __global__ void k_slab_init(int n, int row0, int rows, GridConst G, float2* h0, 
 // h~ (surface.cpp:49-50) of the owned rows; conj(h0(-k)) from the mirror rows
 __global__ void k_slab_evolve(int n, int row0, int rows, GridConst G, const double* d_time,
                               const float2* __restrict__ h0, const float2* __restrict__ h0m,
-                              float4* spec) {
+                              float2* spec) {
   const size_t total = (size_t)rows * n;
   const double t = *d_time;
   for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < total;
@@ -86,20 +95,20 @@ __global__ void k_slab_evolve(int n, int row0, int rows, GridConst G, const doub
     sincosf((float)ph, &s, &c);
     const float ar = a.x * c - a.y * s, ai = a.x * s + a.y * c;
     const float br = b.x * c + b.y * s, bi = b.y * c - b.x * s;
-    spec[q] = make_float4(ar + br, ai + bi, ar - br, ai - bi);
+    spec[q] = make_float2(ar + br, ai + bi);
   }
 }
 
 struct SlabRowArgs {
   int row0, rows, cols;
   float dk, chop;
-  const float4* spec;
+  const float2* spec;
   float2* send;  // [dest][4][rows][cols]
   const float2* tw;
 };
 
 // packed surface pair p at mode (i, j): h~ M_p (surface.cpp:77-80)
-__device__ __forceinline__ float2 surface_pair(int p, float4 s, float kx, float kz, float chop) {
+__device__ __forceinline__ float2 surface_pair(int p, float2 s, float kx, float kz, float chop) {
   const float k2 = kx * kx + kz * kz;
   if (k2 == 0.f) return make_float2(0.f, 0.f);
   const float inv = rsqrtf(k2);
@@ -120,7 +129,7 @@ __global__ void __launch_bounds__(SlabLaunch<N>::THREADS) k_slab_rows(const Slab
   const bool valid = item < a.rows * 4;
   const int li = valid ? item >> 2 : 0, p = item & 3;
   const float kx = a.dk * (float)(a.row0 + li - N / 2);
-  const float4* srow = a.spec + (size_t)li * N;
+  const float2* srow = a.spec + (size_t)li * N;
   fft::cta_fft<N>(
       t, smem + local * L::ROW_STRIDE, a.tw,
       [&](int j) {
@@ -136,6 +145,7 @@ __global__ void __launch_bounds__(SlabLaunch<N>::THREADS) k_slab_rows(const Slab
 
 struct SlabColArgs {
   int rows, cols, col0;
+  int rows_log2;  // rows = N / ranks is a power of two
   const float2* recv;  // [src][4][rows][cols]
   float* fields;       // [8][N][cols]
   const float2* tw;
@@ -156,7 +166,7 @@ __global__ void __launch_bounds__(SlabLaunch<N>::THREADS) k_slab_cols(const Slab
       t, smem + c * L::COL_STRIDE, a.tw,
       [&](int i) {
         if (!valid) return make_float2(0.f, 0.f);
-        const int src = i / a.rows, li = i - src * a.rows;
+        const int src = i >> a.rows_log2, li = i & (a.rows - 1);
         return __ldg(a.recv + (((size_t)src * 4 + p) * a.rows + li) * a.cols + kc);
       },
       [&](int i, float2 x) {
@@ -165,6 +175,108 @@ __global__ void __launch_bounds__(SlabLaunch<N>::THREADS) k_slab_cols(const Slab
         re[(size_t)i * a.cols + kc] = s * x.x;         // fft.cpp:93-99
         im[(size_t)i * a.cols + kc] = s * x.y;
       });
+}
+
+// ---------------------------------------------------------------- four-step columns
+constexpr int kFsN2 = 128;  // inner length of the second step
+constexpr int kFsPC = 32;   // columns per tile (256-byte row segments: DRAM page locality)
+constexpr int kFsB = 2;     // i2 (step A) or k1 (step B) values per CTA (64 transforms)
+
+__device__ __forceinline__ size_t recv_index(const SlabColArgs& a, int p, int i, int kc) {
+  const int src = i >> a.rows_log2, li = i & (a.rows - 1);
+  return (((size_t)src * 4 + p) * a.rows + li) * a.cols + kc;
+}
+
+// step A: for each i2 of the tile, Y[k1] = sum_i1 x[128 i1 + i2] w_N1^(i1 k1),
+// times w_N^(i2 k1), stored back at row 128 k1 + i2 (the same rows)
+template <int N>
+__global__ void __launch_bounds__(kFsB * kFsPC * (N / kFsN2) / 32) k_slab_colsA(const SlabColArgs a, float2* recv,
+                                                             const float2* __restrict__ tw1,
+                                                             const float2* __restrict__ wn) {
+  constexpr int N1 = N / kFsN2, NT = kFsB * kFsPC;
+  using PL = fft::Plan<N1>;
+  constexpr int T = PL::T, TPW = 32 / T, S = PL::SMEM;
+  extern __shared__ float2 smem[];  // [NT][S]
+  const int p = blockIdx.z, kc0 = blockIdx.x * kFsPC, i20 = blockIdx.y * kFsB;
+  for (int e = threadIdx.x; e < N1 * NT; e += blockDim.x) {
+    const int c = e % kFsPC, i2l = (e / kFsPC) % kFsB, i1 = e / NT;
+    smem[(i2l * kFsPC + c) * S + fft::pad32(i1)] =
+        __ldg(recv + recv_index(a, p, kFsN2 * i1 + i20 + i2l, kc0 + c));
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int tr = warp * TPW + lane / T, t = lane % T;
+  float2* buf = smem + tr * S;
+  const int i2 = i20 + tr / kFsPC;
+  fft::cta_fft<N1, true, true, true>(
+      t, buf, tw1, [&](int n) { return buf[fft::pad32(n)]; },
+      [&](int k1, float2 x) { buf[fft::pad32(k1)] = fft::cmul(x, __ldg(wn + i2 * k1)); });
+  __syncthreads();
+  for (int e = threadIdx.x; e < N1 * NT; e += blockDim.x) {
+    const int c = e % kFsPC, i2l = (e / kFsPC) % kFsB, k1 = e / NT;
+    recv[recv_index(a, p, kFsN2 * k1 + i20 + i2l, kc0 + c)] =
+        smem[(i2l * kFsPC + c) * S + fft::pad32(k1)];
+  }
+}
+
+// step B: for each k1 of the tile, X[k1 + N1 k2] = sum_i2 Y[128 k1 + i2] w_128^(i2 k2);
+// (-1)^(k + col) and the Re / Im split into the field planes
+template <int N>
+__global__ void __launch_bounds__(kFsB * kFsPC * kFsN2 / 32) k_slab_colsB(const SlabColArgs a, const float2* recv,
+                                                        const float2* __restrict__ tw2) {
+  constexpr int N1 = N / kFsN2, NT = kFsB * kFsPC;
+  using PL = fft::Plan<kFsN2>;
+  constexpr int T = PL::T, TPW = 32 / T, S = PL::SMEM;
+  extern __shared__ float2 smem[];  // [NT][S]
+  const int p = blockIdx.z, kc0 = blockIdx.x * kFsPC, k10 = blockIdx.y * kFsB;
+  for (int e = threadIdx.x; e < kFsN2 * NT; e += blockDim.x) {
+    const int c = e % kFsPC, k1l = (e / kFsPC) % kFsB, i2 = e / NT;
+    smem[(k1l * kFsPC + c) * S + fft::pad32(i2)] =
+        __ldg(recv + recv_index(a, p, kFsN2 * (k10 + k1l) + i2, kc0 + c));
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int tr = warp * TPW + lane / T, t = lane % T;
+  float2* buf = smem + tr * S;
+  fft::cta_fft<kFsN2, true, true, true>(
+      t, buf, tw2, [&](int n) { return buf[fft::pad32(n)]; },
+      [&](int k2, float2 x) { buf[fft::pad32(k2)] = x; });
+  __syncthreads();
+  float* re = a.fields + (size_t)(2 * p) * N * a.cols;
+  float* im = a.fields + (size_t)(2 * p + 1) * N * a.cols;
+  for (int e = threadIdx.x; e < kFsN2 * NT; e += blockDim.x) {
+    const int c = e % kFsPC, k1l = (e / kFsPC) % kFsB, k2 = e / NT;
+    const int k = k10 + k1l + N1 * k2, kc = kc0 + c;
+    const float2 x = smem[(k1l * kFsPC + c) * S + fft::pad32(k2)];
+    const float sg = ((k + a.col0 + kc) & 1) ? -1.f : 1.f;  // fft.cpp:73-75
+    __stcs(re + (size_t)k * a.cols + kc, sg * x.x);          // fft.cpp:93-99
+    __stcs(im + (size_t)k * a.cols + kc, sg * x.y);
+  }
+}
+
+template <int N>
+bool slab_fourstep(ocn_slab* sl, const SlabColArgs& a, float2* recv) {
+  if constexpr (N >= 4096) {
+    if (a.cols % kFsPC) return false;
+    constexpr int N1 = N / kFsN2;
+    const size_t smemA = (size_t)kFsB * kFsPC * fft::Plan<N1>::SMEM * sizeof(float2);
+    const size_t smemB = (size_t)kFsB * kFsPC * fft::Plan<kFsN2>::SMEM * sizeof(float2);
+    static bool attr = false;
+    if (!attr) {
+      OCN_CUDA(cudaFuncSetAttribute(k_slab_colsA<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemA));
+      OCN_CUDA(cudaFuncSetAttribute(k_slab_colsB<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemB));
+      attr = true;
+    }
+    const dim3 ga(a.cols / kFsPC, kFsN2 / kFsB, 4), gb(a.cols / kFsPC, N1 / kFsB, 4);
+    k_slab_colsA<N><<<ga, kFsB * kFsPC * N1 / 32, smemA, sl->ctx->stream>>>(a, recv, sl->tw1.p, sl->wn.p);
+    OCN_LAUNCHED(sl->ctx);
+    k_slab_colsB<N><<<gb, kFsB * kFsPC * kFsN2 / 32, smemB, sl->ctx->stream>>>(a, recv, sl->tw2.p);
+    OCN_LAUNCHED(sl->ctx);
+    return true;
+  } else {
+    (void)sl, (void)a, (void)recv;
+    return false;
+  }
 }
 
 template <int N>
@@ -184,7 +296,8 @@ void slab_rows_launch(ocn_slab* sl, const SlabRowArgs& a) {
 }
 
 template <int N>
-void slab_cols_launch(ocn_slab* sl, const SlabColArgs& a) {
+void slab_cols_launch(ocn_slab* sl, const SlabColArgs& a, float2* recv) {
+  if (slab_fourstep<N>(sl, a, recv)) return;
   using L = SlabLaunch<N>;
   static bool attr = false;
   if (!attr && L::SMEM_BYTES > 48 * 1024) {
@@ -274,6 +387,20 @@ int ocn_slab_create(ocn_ctx* ctx, int n, int ranks, int rank, double length, dou
     sl->twiddle.alloc(tw.size());
     OCN_CUDA(cudaMemcpyAsync(sl->twiddle.p, tw.data(), tw.size() * sizeof(float2),
                              cudaMemcpyHostToDevice, ctx->stream));
+    if (n >= 4096) {  // four-step column pass tables
+      auto up = [&](DevBuf<float2>& b, const std::vector<float2>& h) {
+        b.alloc(h.size());
+        OCN_CUDA(cudaMemcpy(b.p, h.data(), h.size() * sizeof(float2), cudaMemcpyHostToDevice));
+      };
+      up(sl->tw1, make_twiddles(n / kFsN2));
+      up(sl->tw2, make_twiddles(kFsN2));
+      std::vector<float2> w(n);
+      for (int m = 0; m < n; ++m) {
+        const double ang = 2.0 * kPi * m / n;  // synthesis sign, fft.hpp:10-17
+        w[m] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+      }
+      up(sl->wn, w);
+    }
     OCN_CUDA(cudaStreamSynchronize(ctx->stream));
     ctx_retain(ctx);
     *out = sl.release();
@@ -320,14 +447,16 @@ int ocn_slab_rows(ocn_slab* sl, double t, double choppiness, void* dev_send) {
   });
 }
 
-int ocn_slab_cols(ocn_slab* sl, const void* dev_recv) {
+int ocn_slab_cols(ocn_slab* sl, void* dev_recv) {
   return api_call(sl ? sl->ctx : nullptr, [&] {
     OCN_REQUIRE(sl && dev_recv, "null argument");
     DeviceScope ds(sl->ctx);
     ProfWindow pw(sl->ctx, OCN_PROF_COLS);
-    SlabColArgs a{sl->rows, sl->cols, sl->rank * sl->cols, (const float2*)dev_recv, sl->fields.p,
+    int lg = 0;
+    while ((1 << lg) < sl->rows) ++lg;
+    SlabColArgs a{sl->rows, sl->cols, sl->rank * sl->cols, lg, (const float2*)dev_recv, sl->fields.p,
                   sl->twiddle.p};
-#define OCN_SC(NN) slab_cols_launch<NN>(sl, a)
+#define OCN_SC(NN) slab_cols_launch<NN>(sl, a, (float2*)dev_recv)
     OCN_SLAB_DISPATCH(sl->n, OCN_SC)
 #undef OCN_SC
   });

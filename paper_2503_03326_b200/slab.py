@@ -48,6 +48,7 @@ class SlabSurface:
         check(lib().ocn_slab_rows(self.h, t, choppiness, C.c_void_p(send_ptr)), self.ctx.h, "rows")
 
     def cols_pass(self, recv_ptr: int):
+        """Column pass from the receive buffer (overwritten in place for n >= 4096)."""
         check(lib().ocn_slab_cols(self.h, C.c_void_p(recv_ptr)), self.ctx.h, "cols")
 
     def field(self, f: int) -> np.ndarray:

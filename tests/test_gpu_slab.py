@@ -18,3 +18,20 @@ def test_slab_matches_oracle(port, n, ranks):
     want = port.generate_maps(n, [L], [], p, 10.0)[0]
     for f in range(8):
         assert normwise_rel(got[f], want[f]) < 1e-4, f
+
+
+@pytest.mark.parametrize("n,ranks", [(4096, 1), (4096, 2), (8192, 4)])
+def test_slab_fourstep_matches_maps(n, ranks):
+    """n >= 4096: the four-step column pass (in place in the receive buffer)
+    against the single-grid spectral path at the same size, which
+    test_generate_maps_large pins to the oracle at 4096."""
+    from paper_2503_03326_b200 import ocean as oc
+    from paper_2503_03326_b200.slab import SlabSurface, emulated_frame
+    p = config2_params(seed=7)
+    L = 4096.0 * n / 16384
+    slabs = [SlabSurface(n, ranks, r, L, p) for r in range(ranks)]
+    got = emulated_frame(slabs, 10.0)
+    cs = oc.CascadeSet(oc.CascadeConfig(n, [L], []), p)
+    want = oc.generate_maps(cs, 10.0, oc.SurfaceGenOptions(choppiness=1.0)).all_fields()[0]
+    for f in range(8):
+        assert normwise_rel(got[f], want[f]) < 1e-4, f

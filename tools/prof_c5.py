@@ -1,0 +1,13 @@
+"""Run a few config-5 frames on one GPU (for ncu captures; not a benchmark)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+
+frames = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+fr = bench.Frame5(0, 0, 1, None)
+for _ in range(frames):
+    fr.step()
+fr.ctx.synchronize()
+print("ok", fr.ctx.kernel_launches())
