@@ -408,8 +408,12 @@ __global__ void __launch_bounds__(256, N >= 1024 ? 2 : OCN_ROWS_MINB_SMALL) k_ro
   //   sht = h~,  sv0 = V0 = G (-g / w)(kx + i kz),  sw0 = W0 = G w,  sk = |k|,
   //   sinv = 1/|k| (0 at k = 0). A velocity coefficient is then V0 E(y) or
   //   W0 (-E(y1) + i E(y0)), E(y) = exp(|k| y) (y <= 0) or 1 + |k| y.
-  // Surface CTAs may take a.rpc (<= 2) rows so that all 8 warps have work
-  // when a grid has only 4 surface transforms: sht [rpc][N], sinv [rpc][N].
+  // Surface CTAs take a.rpc rows: a grid has only 4 surface transforms, so
+  // one row keeps only 4 warps busy for a short CTA whose staging latency is
+  // then poorly hidden. N >= 1024: up to 4 rows with only h~ staged (1/|k|
+  // recomputed per element, MUFU); smaller N: up to 2 rows with h~ and 1/|k|
+  // staged (measured best for each: config 3 / config 4).
+  constexpr bool SURF_INV_INLINE = N >= 1024;
   const int rpc = MODE == kRowSurface ? a.rpc : 1;
   float2* sht = reinterpret_cast<float2*>(smem4);
   float* sinv = reinterpret_cast<float*>(sht + rpc * N);
@@ -448,7 +452,7 @@ __global__ void __launch_bounds__(256, N >= 1024 ? 2 : OCN_ROWS_MINB_SMALL) k_ro
       const float k = k2 * inv;
       if constexpr (MODE == kRowSurface) {
         sht[j] = sp;
-        sinv[j] = inv;
+        if constexpr (!SURF_INV_INLINE) sinv[j] = inv;
       } else {
         const float rw = zero ? 0.f : rsqrtf(g * k);  // 1 / w
         const float w = g * k * rw, f = -g * rw;     // w, -g / w
@@ -515,8 +519,14 @@ __global__ void __launch_bounds__(256, N >= 1024 ? 2 : OCN_ROWS_MINB_SMALL) k_ro
             [&](int j) {
               const int jj = j ^ H;
               const float2 h = sht[rr * N + jj];
-              const float inv = sinv[rr * N + jj];
               const float kz = dk * (float)(jj - N / 2);
+              float inv;
+              if constexpr (SURF_INV_INLINE) {
+                const float k2 = fmaf(kz, kz, kx2);
+                inv = k2 > 0.f ? rsqrtf(k2) : 0.f;
+              } else {
+                inv = sinv[rr * N + jj];
+              }
               const float mr = fmaf(inv * kx, fmaf(c2, kz, c1), fmaf(c3, kz, c0));
               const float mi = fmaf(inv, fmaf(c6 * kz, kz, c5 * (kz + kx2)), c4);
               return make_float2(h.x * mr - h.y * mi, h.x * mi + h.y * mr);
@@ -860,8 +870,13 @@ void launch_rows(ocn_ctx* ctx, const RowArgs& a, bool plain, cudaStream_t st, in
     const int slots = (max_seg + W::TPW - 1) / W::TPW;
     const int cap = lean ? 4 : 8;  // lean: co-resides with a column pass
     // surface grids have 4 transforms: two rows per CTA keep 8 warps busy
-    static const bool one_row = getenv("OCN_ROWS_RPC1") != nullptr;
-    const int rpc = (!one_row && !plain && family == 0 && 2 * slots <= cap) ? 2 : 1;
+    static const int max_rpc = [] {  // experiment override: OCN_ROWS_RPC=1|2|4
+      const char* e = getenv("OCN_ROWS_RPC");
+      return e && atoi(e) > 0 ? std::min(atoi(e), N >= 1024 ? 4 : 2) : (N >= 1024 ? 4 : 2);
+    }();
+    int rpc = 1;  // staging holds 4 rows of h~ (2 N float4 = 4 N float2)
+    if (!plain && family == 0)
+      while (2 * rpc <= max_rpc && 2 * rpc * slots <= 2 * cap) rpc *= 2;
     const int warps = slots * rpc < cap ? slots * rpc : cap;
     RowArgs ar = a;
     ar.rpc = rpc;
