@@ -34,24 +34,59 @@ namespace {
 // ---------------------------------------------------------------- K10 stencil
 // next[i][j] = d (a lap(curr @ (i+wx, j+wz)) + 2 curr(i+wx, j+wz) - prev(i+ox, j+oz))
 // (interactive.cpp:104-108); reads outside [0, n) are zero; margins stay zero.
+// Each thread computes 4 consecutive cells of one row; interior threads (every
+// read in range, the common case) take one branch-free path, the rest the
+// bounds-checked one. Same arithmetic order in both.
 __global__ void __launch_bounds__(256) k_fdm_step(int n, int m, int wx, int wz, int ox, int oz,
                                                   float a, float d, const float* __restrict__ curr,
                                                   const float* __restrict__ prev, float* next) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
   const int i = blockIdx.y;
-  if (j >= n) return;
-  float out = 0.f;
-  if (i >= m && i < n - m && j >= m && j < n - m) {
-    const int k = i + wx, l = j + wz;
+  if (j0 >= n) return;
+  const int k = i + wx;
+  const bool row_in = i >= m && i < n - m;
+  const bool fast = row_in && k >= 1 && k + 1 < n && j0 >= m && j0 + 3 < n - m &&
+                    j0 + wz >= 1 && j0 + 3 + wz + 1 < n && i + ox >= 0 && i + ox < n &&
+                    j0 + oz >= 0 && j0 + 3 + oz < n;
+  float out[4];
+  if (fast) {
+    const float* c0 = curr + (size_t)k * n + wz;
+    const float* cm = c0 - n;
+    const float* cp = c0 + n;
+    const float* pr = prev + (size_t)(i + ox) * n + oz;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int l = j0 + q;
+      const float ckl = __ldg(c0 + l);
+      const float lap = __ldg(cp + l) + __ldg(cm + l) + __ldg(c0 + l + 1) + __ldg(c0 + l - 1) -
+                        4.0f * ckl;
+      out[q] = d * (a * lap + 2.0f * ckl - __ldg(pr + l));
+    }
+  } else {
     auto rd = [&](const float* f, int r, int c) {
       return (r < 0 || c < 0 || r >= n || c >= n) ? 0.f : __ldg(f + (size_t)r * n + c);
     };
-    const float ckl = rd(curr, k, l);
-    const float lap = rd(curr, k + 1, l) + rd(curr, k - 1, l) + rd(curr, k, l + 1) +
-                      rd(curr, k, l - 1) - 4.0f * ckl;
-    out = d * (a * lap + 2.0f * ckl - rd(prev, i + ox, j + oz));
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = j0 + q;
+      out[q] = 0.f;
+      if (row_in && j >= m && j < n - m) {
+        const int l = j + wz;
+        const float ckl = rd(curr, k, l);
+        const float lap = rd(curr, k + 1, l) + rd(curr, k - 1, l) + rd(curr, k, l + 1) +
+                          rd(curr, k, l - 1) - 4.0f * ckl;
+        out[q] = d * (a * lap + 2.0f * ckl - rd(prev, i + ox, j + oz));
+      }
+    }
   }
-  next[(size_t)i * n + j] = out;
+  float* dst = next + (size_t)i * n + j0;
+  if ((n & 3) == 0) {  // rows start 16-byte aligned: one vector store
+    *reinterpret_cast<float4*>(dst) = make_float4(out[0], out[1], out[2], out[3]);
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (j0 + q < n) dst[q] = out[q];
+  }
 }
 
 __global__ void k_apply_cells(int n, int m, int count, const int* ij, const double* h, float* curr) {
@@ -121,7 +156,8 @@ __global__ void __launch_bounds__(1024) k_mask_prepare(MaskArgs A, const int* nl
                                                        int bin_cap) {
   __shared__ int s_cnt[kMaskBins + 1];
   __shared__ int s_kept;
-  __shared__ double s_lo[2][1024], s_hi[2][1024];
+  __shared__ double s_lo[2][32], s_hi[2][32];
+  __shared__ int s_wsum[32];
   const int nl = nloops_dev ? nloops_dev[0] : nloops_host;
   if (threadIdx.x == 0) {
     int kept = 0, np = 0;
@@ -155,19 +191,32 @@ __global__ void __launch_bounds__(1024) k_mask_prepare(MaskArgs A, const int* nl
     }
     ++k;
   }
-  s_lo[0][threadIdx.x] = lox;
-  s_lo[1][threadIdx.x] = loz;
-  s_hi[0][threadIdx.x] = hix;
-  s_hi[1][threadIdx.x] = hiz;
-  __syncthreads();
-  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-    if (threadIdx.x < o)
-      for (int a = 0; a < 2; ++a) {
-        s_lo[a][threadIdx.x] = fmin(s_lo[a][threadIdx.x], s_lo[a][threadIdx.x + o]);
-        s_hi[a][threadIdx.x] = fmax(s_hi[a][threadIdx.x], s_hi[a][threadIdx.x + o]);
-      }
-    __syncthreads();
+  // bbox: warp min / max, then across the warps (min / max are order-free)
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lox = fmin(lox, __shfl_xor_sync(0xffffffffu, lox, o));
+    loz = fmin(loz, __shfl_xor_sync(0xffffffffu, loz, o));
+    hix = fmax(hix, __shfl_xor_sync(0xffffffffu, hix, o));
+    hiz = fmax(hiz, __shfl_xor_sync(0xffffffffu, hiz, o));
   }
+  if (lane == 0) s_lo[0][wid] = lox, s_lo[1][wid] = loz, s_hi[0][wid] = hix, s_hi[1][wid] = hiz;
+  __syncthreads();
+  if (wid == 0) {
+    lox = lane < nw ? s_lo[0][lane] : 1e300;
+    loz = lane < nw ? s_lo[1][lane] : 1e300;
+    hix = lane < nw ? s_hi[0][lane] : -1e300;
+    hiz = lane < nw ? s_hi[1][lane] : -1e300;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lox = fmin(lox, __shfl_xor_sync(0xffffffffu, lox, o));
+      loz = fmin(loz, __shfl_xor_sync(0xffffffffu, loz, o));
+      hix = fmax(hix, __shfl_xor_sync(0xffffffffu, hix, o));
+      hiz = fmax(hiz, __shfl_xor_sync(0xffffffffu, hiz, o));
+    }
+    if (lane == 0) s_lo[0][0] = lox, s_lo[1][0] = loz, s_hi[0][0] = hix, s_hi[1][0] = hiz;
+  }
+  __syncthreads();
   const double lo_x = s_lo[0][0], hi_x = s_hi[0][0];
   double w = __ddiv_rn(__dsub_rn(hi_x, lo_x), (double)kMaskBins);
   if (!(w > 0.0)) w = 1.0;
@@ -187,16 +236,32 @@ __global__ void __launch_bounds__(1024) k_mask_prepare(MaskArgs A, const int* nl
     for (int b = b0; b <= b1; ++b) atomicAdd(&s_cnt[b], 1);
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int acc = 0;
-    for (int b = 0; b < kMaskBins; ++b) {
-      const int c = s_cnt[b];
-      s_cnt[b] = acc;
-      bin_off[b] = acc;
-      acc += c;
+  {  // exclusive scan of the bin counts (blockDim == kMaskBins == 1024)
+    static_assert(kMaskBins == 1024, "one thread per bin");
+    const int c = s_cnt[threadIdx.x];
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
     }
-    bin_off[kMaskBins] = acc;
-    s_cnt[kMaskBins] = acc;
+    if (lane == 31) s_wsum[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      const int wv = s_wsum[lane];
+      int wi = wv;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= o) wi += y;
+      }
+      s_wsum[lane] = wi - wv;
+      if (lane == 31) s_cnt[kMaskBins] = wi, bin_off[kMaskBins] = wi;
+    }
+    __syncthreads();
+    const int ex = s_wsum[wid] + incl - c;
+    s_cnt[threadIdx.x] = ex;
+    bin_off[threadIdx.x] = ex;
   }
   __syncthreads();
   const bool fits = s_cnt[kMaskBins] <= bin_cap;
@@ -473,7 +538,7 @@ int ocn_zone_step(ocn_zone* z, double dt, double bx, double bz) {
     const int ox = wx + z->last_shift[0], oz = wz + z->last_shift[1];
     const double a = z->c * z->c * dt * dt / (z->delta * z->delta);
     const int inext = 3 - z->icurr - z->iprev;
-    dim3 grid((z->n + 255) / 256, z->n);
+    dim3 grid(((z->n + 3) / 4 + 255) / 256, z->n);
     ProfWindow pw(ctx, OCN_PROF_FDM);
     k_fdm_step<<<grid, 256, 0, ctx->stream>>>(z->n, z->margin, wx, wz, ox, oz, (float)a,
                                               (float)z->damping, z->curr(), z->prev(),

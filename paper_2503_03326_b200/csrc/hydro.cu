@@ -50,23 +50,57 @@ __device__ __forceinline__ double3 qrot(const PoseDev& P, double3 v) {
 }
 
 // ---------------------------------------------------------------- K5: vertices
+// Four lanes per vertex: lane q sums the cascades c = q, q + 4, ... of each
+// Algorithm-1 iteration (surface.cpp:141-151, 4 iterations) and the four
+// partials are combined by a fixed xor tree, so the 48 taps of an iteration
+// are in flight together and 4x more threads hide the gather latency.
 __global__ void __launch_bounds__(128) k_vertices(int nv, const double* __restrict__ verts,
                                                   PoseDev P, SurfView surf, int have_surf,
                                                   ZoneList zones, const double* override_depth,
                                                   double* wpos, double* depth) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31, q = lane & 3;
+  const int per_warp = 8;  // vertices per warp pass
+  const int warp_g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int base = warp_g * per_warp; base < nv; base += warps * per_warp) {
+    const int iv = base + (lane >> 2);
+    const bool valid = iv < nv;
+    const int i = valid ? iv : nv - 1;  // every lane takes part in the shuffles
     const double3 b = ld3(verts + 3 * i);
     const double3 w = d3(P.p[0], P.p[1], P.p[2]) + qrot(P, b - d3(P.com[0], P.com[1], P.com[2]));
-    st3(wpos + 3 * i, w);
     double d;
     if (override_depth) {
       d = override_depth[i];
     } else {
-      double h = have_surf ? height_at_dev(surf, w.x, w.z) : 0.0;
+      double h = 0.0;
+      if (have_surf) {
+        double wx = 0.0, wz = 0.0;
+#pragma unroll 1
+        for (int it = 0; it < 4; ++it) {
+          const double qx = w.x - wx, qz = w.z - wz;
+          double sx = 0.0, sh = 0.0, sz = 0.0;
+          for (int c = q; c < surf.C; c += 4) {
+            const Bilin bl = bilin_setup(surf.n, surf.length[c], qx, qz);
+            sx += bilin_tap(bl, surf.f(c, OCN_FIELD_DX));
+            sh += bilin_tap(bl, surf.f(c, OCN_FIELD_H));
+            sz += bilin_tap(bl, surf.f(c, OCN_FIELD_DZ));
+          }
+#pragma unroll
+          for (int o = 1; o < 4; o <<= 1) {
+            sx += __shfl_xor_sync(0xffffffffu, sx, o);
+            sh += __shfl_xor_sync(0xffffffffu, sh, o);
+            sz += __shfl_xor_sync(0xffffffffu, sz, o);
+          }
+          wx = sx, wz = sz, h = sh;
+        }
+      }
       for (int z = 0; z < zones.count; ++z) h += zone_sample(zones.z[z], w.x, w.z);
       d = w.y - h;
     }
-    depth[i] = d;
+    if (valid && q == 0) {
+      st3(wpos + 3 * i, w);
+      depth[i] = d;
+    }
   }
 }
 
@@ -258,7 +292,7 @@ __global__ void __launch_bounds__(kForceThreads) k_forces(const StateDev* __rest
                                                           int* domain_err, int* ticket,
                                                           double mesh_volume, int degenerate,
                                                           ReportDev* rep) {
-  __shared__ double sh[kTerms][kForceThreads];
+  __shared__ double wsum[kForceThreads / 32][kTerms];
   const int ns = total->x;
   double acc[kTerms];
 #pragma unroll
@@ -293,16 +327,22 @@ __global__ void __launch_bounds__(kForceThreads) k_forces(const StateDev* __rest
       acc[14] += s.centroid.z * s.area;
     }
   }
+  // fixed tree: xor shuffles within each warp, then the warps in order
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-  for (int k = 0; k < kTerms - 1; ++k) sh[k][threadIdx.x] = acc[k];
-  sh[kTerms - 1][threadIdx.x] = 0.0;
-  __syncthreads();
-  for (int off = kForceThreads / 2; off > 0; off >>= 1) {
-    if (threadIdx.x < off)
-      for (int k = 0; k < kTerms; ++k) sh[k][threadIdx.x] += sh[k][threadIdx.x + off];
-    __syncthreads();
+  for (int k = 0; k < kTerms - 1; ++k) {
+    double v = acc[k];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if (lane == 0) wsum[warp][k] = v;
   }
-  if (threadIdx.x < kTerms) block_out[blockIdx.x * kTerms + threadIdx.x] = sh[threadIdx.x][0];
+  if (lane == 0) wsum[warp][kTerms - 1] = 0.0;
+  __syncthreads();
+  if (threadIdx.x < kTerms) {
+    double v = 0.0;
+    for (int w = 0; w < kForceThreads / 32; ++w) v += wsum[w][threadIdx.x];
+    block_out[blockIdx.x * kTerms + threadIdx.x] = v;
+  }
   __threadfence();  // this block's partials, before its ticket
   __syncthreads();
   __shared__ bool last;
@@ -786,7 +826,7 @@ void hydro_evaluate(ocn_mesh* m, const ocn_pose* pose, const ocn_fluid* fluid,
   }
   ProfWindow pw(ctx, OCN_PROF_HYDRO);
   OCN_CUDA(cudaMemsetAsync(m->flags.p, 0, 4 * sizeof(int), st));
-  k_vertices<<<grid_of(ctx, nv, 128), 128, 0, st>>>(nv, m->verts.p, P, sv, maps != nullptr, zl,
+  k_vertices<<<grid_of(ctx, 4 * (size_t)nv, 128), 128, 0, st>>>(nv, m->verts.p, P, sv, maps != nullptr, zl,
                                                    d_override, m->wpos.p, m->depth.p);
   OCN_LAUNCHED(ctx);
   const int nb = (nt + kScanBlock - 1) / kScanBlock;
