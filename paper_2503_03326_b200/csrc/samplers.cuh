@@ -165,29 +165,29 @@ __device__ __forceinline__ double wrap_angle_dev(double a) {
 
 // velocity_at (velocity.cpp:213-265). Returns false for y outside
 // [y_min, y_max] (DomainError) unless clamp (Simulation::water_velocity).
-__device__ __forceinline__ bool velocity_at_dev(const SliceView& s, double x, double z, double y,
-                                                int interp, int clamp, double out[3]) {
+// velocity_at split for lane-parallel callers: the depth bracket, the partial
+// slice sums over cascades c = c0, c0 + cstep, ..., and the combination.
+struct VelBracket {
+  int kind;  // 0 out of range, 1 below the first slice, 2 above the last, 3 interior
+  int il, ih;
+  double u;  // kinds 1 / 2: the linear weight
+};
+
+__device__ __forceinline__ VelBracket velocity_bracket(const SliceView& s, double& y, int clamp) {
+  VelBracket r{0, 0, 0, 0.0};
   if (clamp) y = y < s.y_min ? s.y_min : (s.y_max < y ? s.y_max : y);
-  if (y < s.y_min || y > s.y_max) {
-    out[0] = out[1] = out[2] = 0.0;
-    return false;
-  }
+  if (y < s.y_min || y > s.y_max) return r;
   const double* dep = s.depths;
   const int D = s.D;
-  double va[3], vb[3];
   if (y <= dep[0]) {
-    sample_slice_dev(s, 0, x, z, vb);
-    const double u = (y - s.y_min) / (dep[0] - s.y_min);
-    out[0] = vb[0] * u, out[1] = vb[1] * u, out[2] = vb[2] * u;
-    return true;
+    r.kind = 1, r.il = r.ih = 0;
+    r.u = (y - s.y_min) / (dep[0] - s.y_min);
+    return r;
   }
   if (y >= dep[D - 1]) {
-    const int last = D - 1;
-    sample_slice_dev(s, last - 1, x, z, va);
-    sample_slice_dev(s, last, x, z, vb);
-    const double u = (y - dep[last - 1]) / (dep[last] - dep[last - 1]);
-    for (int m = 0; m < 3; ++m) out[m] = va[m] + (vb[m] - va[m]) * u;
-    return true;
+    r.kind = 2, r.il = D - 2, r.ih = D - 1;
+    r.u = (y - dep[D - 2]) / (dep[D - 1] - dep[D - 2]);
+    return r;
   }
   int lo = 0, hi = D;  // upper_bound
   while (lo < hi) {
@@ -195,14 +195,55 @@ __device__ __forceinline__ bool velocity_at_dev(const SliceView& s, double x, do
     if (y < dep[mid]) hi = mid;
     else lo = mid + 1;
   }
-  const int ih = lo, il = lo - 1;
-  const double a = dep[il], b = dep[ih];
-  sample_slice_dev(s, il, x, z, va);
-  sample_slice_dev(s, ih, x, z, vb);
+  r.kind = 3, r.il = lo - 1, r.ih = lo;
+  return r;
+}
+
+__device__ __forceinline__ void sample_slice_part(const SliceView& s, int d, double x, double z,
+                                                  int c0, int cstep, double v[3]) {
+  v[0] = v[1] = v[2] = 0.0;
+  for (int c = c0; c < s.C; c += cstep) {
+    const Bilin w = bilin_setup(s.n, s.length[c], x, z);
+    v[0] += bilin_tap(w, s.f(d, c, 0));
+    v[1] += bilin_tap(w, s.f(d, c, 1));
+    v[2] += bilin_tap(w, s.f(d, c, 2));
+  }
+}
+
+static __device__ void velocity_combine(const SliceView& s, const VelBracket& br, double y,
+                                        int interp, const double va[3], const double vb[3],
+                                        double out[3]);
+
+__device__ __forceinline__ bool velocity_at_dev(const SliceView& s, double x, double z, double y,
+                                                int interp, int clamp, double out[3]) {
+  const VelBracket br = velocity_bracket(s, y, clamp);
+  if (br.kind == 0) {
+    out[0] = out[1] = out[2] = 0.0;
+    return false;
+  }
+  double va[3] = {0.0, 0.0, 0.0}, vb[3];
+  if (br.kind != 1) sample_slice_dev(s, br.il, x, z, va);
+  sample_slice_dev(s, br.ih, x, z, vb);
+  velocity_combine(s, br, y, interp, va, vb, out);
+  return true;
+}
+
+static __device__ __noinline__ void velocity_combine(const SliceView& s, const VelBracket& br,
+                                                     double y, int interp, const double va[3],
+                                                     const double vb[3], double out[3]) {
+  if (br.kind == 1) {
+    out[0] = vb[0] * br.u, out[1] = vb[1] * br.u, out[2] = vb[2] * br.u;
+    return;
+  }
+  if (br.kind == 2) {
+    for (int m = 0; m < 3; ++m) out[m] = va[m] + (vb[m] - va[m]) * br.u;
+    return;
+  }
+  const double a = s.depths[br.il], b = s.depths[br.ih];
   const double u_lin = (y - a) / (b - a);
   if (interp == OCN_INTERP_LINEAR) {
     for (int m = 0; m < 3; ++m) out[m] = va[m] + (vb[m] - va[m]) * u_lin;
-    return true;
+    return;
   }
   const double mag_a = hypot(va[0], va[2]);
   const double mag_b = hypot(vb[0], vb[2]);
@@ -228,7 +269,7 @@ __device__ __forceinline__ bool velocity_at_dev(const SliceView& s, double x, do
     hz = mag * sp;
   }
   out[0] = hx, out[1] = vy, out[2] = hz;
-  return true;
 }
+
 
 }  // namespace ocn
