@@ -36,8 +36,7 @@ struct ocn_slab {
   ocn::DevBuf<float2> h0, h0m;   // [rows][N]: h0 of owned rows, h0 of rows neg(i)
   ocn::DevBuf<float2> spec;      // [rows][N]: h~ (the slab builds surface fields only)
   ocn::DevBuf<float2> twiddle;
-  ocn::DevBuf<float2> tw1, tw2, wn;  // four-step passes: inner tables, w_N^m
-  ocn::DevBuf<float2> ytmp;          // four-step row pass: [4][rows][N] after step A
+  ocn::DevBuf<float2> tw1, tw2, wn;  // four-step column pass: inner tables, w_N^m
   ocn::DevBuf<double> d_time;
   ocn::DevBuf<float> fields;     // [8][N][cols]
 };
@@ -280,109 +279,8 @@ bool slab_fourstep(ocn_slab* sl, const SlabColArgs& a, float2* recv) {
   }
 }
 
-// ---------------------------------------------------------------- four-step rows
-// Row transform over j = 128 j1 + j2 (N1 = N / 128 values of j1), k = k1 + N1 k2:
-//   k_slab_rowsA: per (row, 32 consecutive j2): one h~ tile read serves the 4
-//     pairs; for each pair, length-N1 DFTs over j1 of the packed coefficients,
-//     times w_N^(j2 k1), into ytmp[pair][row][128 k1 + j2];
-//   k_slab_rowsB: per (row, pair, 32 consecutive k1): length-128 DFTs over the
-//     contiguous j2, written to the send layout at k = k1 + N1 k2.
-constexpr int kFrBJ = 32;  // j2 (step A) / k1 (step B) values per CTA
-
-template <int N>
-__global__ void __launch_bounds__(kFrBJ * (N / kFsN2) / 32) k_slab_rowsA(const SlabRowArgs a,
-                                                                      float2* ytmp,
-                                                                      const float2* __restrict__ tw1,
-                                                                      const float2* __restrict__ wn) {
-  constexpr int N1 = N / kFsN2;
-  using PL = fft::Plan<N1>;
-  constexpr int T = PL::T, TPW = 32 / T, S = PL::SMEM;
-  extern __shared__ float2 smem[];
-  float2* sh = smem;                        // [N1][kFrBJ] h~ tile
-  float2* bufs = smem + N1 * kFrBJ;         // [kFrBJ][S]
-  const int li = blockIdx.y, j20 = blockIdx.x * kFrBJ;
-  const float2* hrow = a.spec + (size_t)li * N;
-  for (int e = threadIdx.x; e < N1 * kFrBJ; e += blockDim.x)
-    sh[e] = __ldg(hrow + kFsN2 * (e / kFrBJ) + j20 + (e % kFrBJ));
-  __syncthreads();
-  const float kx = a.dk * (float)(a.row0 + li - N / 2);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int tr = warp * TPW + lane / T, t = lane % T;  // transform = j2 - j20
-  float2* buf = bufs + tr * S;
-  const int j2 = j20 + tr;
-  for (int p = 0; p < 4; ++p) {
-    fft::cta_fft<N1, true, false, true>(
-        t, buf, tw1,
-        [&](int j1) {
-          const int j = kFsN2 * j1 + j2;
-          return surface_pair(p, sh[j1 * kFrBJ + tr], kx, a.dk * (float)(j - N / 2), a.chop);
-        },
-        [&](int k1, float2 x) { buf[fft::pad32(k1)] = fft::cmul(x, __ldg(wn + j2 * k1)); });
-    __syncthreads();
-    float2* yrow = ytmp + ((size_t)p * a.rows + li) * N;
-    for (int e = threadIdx.x; e < N1 * kFrBJ; e += blockDim.x) {
-      const int k1 = e / kFrBJ, jj = e % kFrBJ;
-      yrow[kFsN2 * k1 + j20 + jj] = bufs[jj * S + fft::pad32(k1)];
-    }
-    __syncthreads();
-  }
-}
-
-template <int N>
-__global__ void __launch_bounds__(kFrBJ * kFsN2 / 32) k_slab_rowsB(const SlabRowArgs a,
-                                                                 const float2* __restrict__ ytmp,
-                                                                 const float2* __restrict__ tw2) {
-  constexpr int N1 = N / kFsN2;
-  using PL = fft::Plan<kFsN2>;
-  constexpr int T = PL::T, TPW = 32 / T, S = PL::SMEM;
-  extern __shared__ float2 smem[];  // [kFrBJ][S]
-  const int li = blockIdx.y, p = blockIdx.z, k10 = blockIdx.x * kFrBJ;
-  const float2* yrow = ytmp + ((size_t)p * a.rows + li) * N + kFsN2 * k10;  // contiguous tile
-  for (int e = threadIdx.x; e < kFsN2 * kFrBJ; e += blockDim.x)
-    smem[(e / kFsN2) * S + fft::pad32(e % kFsN2)] = __ldg(yrow + e);
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int tr = warp * TPW + lane / T, t = lane % T;  // transform = k1 - k10
-  float2* buf = smem + tr * S;
-  fft::cta_fft<kFsN2, true, true, true>(
-      t, buf, tw2, [&](int n) { return buf[fft::pad32(n)]; },
-      [&](int k2, float2 x) { buf[fft::pad32(k2)] = x; });
-  __syncthreads();
-  for (int e = threadIdx.x; e < kFsN2 * kFrBJ; e += blockDim.x) {
-    const int k2 = e / kFrBJ, kk = e % kFrBJ;
-    const int k = k10 + kk + N1 * k2;
-    const int dest = k / a.cols, kc = k - dest * a.cols;
-    a.send[(((size_t)dest * 4 + p) * a.rows + li) * a.cols + kc] = smem[kk * S + fft::pad32(k2)];
-  }
-}
-
-template <int N>
-bool slab_rows_fourstep(ocn_slab* sl, const SlabRowArgs& a) {
-  if constexpr (N >= 4096) {
-    constexpr int N1 = N / kFsN2;
-    const size_t smemA = ((size_t)N1 * kFrBJ + (size_t)kFrBJ * fft::Plan<N1>::SMEM) * sizeof(float2);
-    const size_t smemB = (size_t)kFrBJ * fft::Plan<kFsN2>::SMEM * sizeof(float2);
-    static bool attr = false;
-    if (!attr) {
-      OCN_CUDA(cudaFuncSetAttribute(k_slab_rowsA<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemA));
-      OCN_CUDA(cudaFuncSetAttribute(k_slab_rowsB<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemB));
-      attr = true;
-    }
-    const dim3 ga(kFsN2 / kFrBJ, a.rows), gb(N1 / kFrBJ, a.rows, 4);
-    k_slab_rowsA<N><<<ga, kFrBJ * N1 / 32, smemA, sl->ctx->stream>>>(a, sl->ytmp.p, sl->tw1.p, sl->wn.p);
-    OCN_LAUNCHED(sl->ctx);
-    k_slab_rowsB<N><<<gb, kFrBJ * kFsN2 / 32, smemB, sl->ctx->stream>>>(a, sl->ytmp.p, sl->tw2.p);
-    OCN_LAUNCHED(sl->ctx);
-    return true;
-  } else {
-    (void)sl, (void)a;
-    return false;
-  }
-}
-
 template <int N>
 void slab_rows_launch(ocn_slab* sl, const SlabRowArgs& a) {
-  if (slab_rows_fourstep<N>(sl, a)) return;
   using L = SlabLaunch<N>;
   static bool attr = false;
   if (!attr && L::SMEM_BYTES > 48 * 1024) {
@@ -480,7 +378,6 @@ int ocn_slab_create(ocn_ctx* ctx, int n, int ranks, int rank, double length, dou
     sl->h0.alloc(slab);
     sl->h0m.alloc(slab);
     sl->spec.alloc(slab);
-    if (n >= 4096) sl->ytmp.alloc(4 * slab);
     sl->fields.alloc(8 * slab);
     sl->d_time.alloc(1);
     k_slab_init<<<grid_cap(ctx, slab), 256, 0, ctx->stream>>>(n, rank * sl->rows, sl->rows, sl->gc,
