@@ -124,24 +124,57 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------- our arm
-class Frame:
-    """One frame of the hot path through the C-ABI (device-resident state)."""
+class _SingleStream:
+    """Frames whose work is all on one context stream."""
 
-    def __init__(self, device: int):
+    def contexts(self):
+        return [self.ctx]
+
+    def sync(self):
+        self.ctx.synchronize()
+
+    def timed_begin(self, ev):
+        import torch
+        ev.record(torch.cuda.ExternalStream(self.ctx.stream, device=f"cuda:{self.ctx.device}"))
+
+    def timed_end(self, ev):
+        self.timed_begin(ev)
+
+    def finish(self, read_report: bool = False):
+        pass
+
+
+class Frame:
+    """One config-3 frame of the hot path through the C-ABI (device-resident state).
+
+    Frames are pipelined: the spectral step runs on a low-priority context
+    (stream) into double-buffered maps / slices, forces, mask and FDM on a
+    high-priority one, so frame f's latency-bound forces / mask / FDM kernels
+    fill the SMs beside frame f+1's spectral kernels. Dependencies are CUDA
+    events on the two ocn_ctx_stream streams (ready: spectral done; consumed:
+    the last reader of a buffer done). pipelined=False runs everything in order
+    on one context."""
+
+    def __init__(self, device: int, pipelined: bool = True):
         from paper_2503_03326_b200 import ocean as oc
         from paper_2503_03326_b200._types import FdmConfig, MaskFrame, MaskParams, SliceConfig
         from paper_2503_03326_b200.meshgen import uv_ellipsoid
+        import torch
         self.oc = oc
         self.L = oc.lib()
-        self.ctx = oc.Context(device)
-        self.cs = oc.CascadeSet(oc.CascadeConfig(N_GRID, LENGTHS, CUTOFFS), _params(), ctx=self.ctx)
-        self.maps = oc.SurfaceMaps(self.cs)
-        self.slices = oc.VelocitySlices(self.cs, SliceConfig.make(count=DEPTHS))
+        self.pipelined = pipelined
+        self.sctx = oc.Context(device, priority=-1 if pipelined else 0)  # spectral
+        self.ctx = oc.Context(device, priority=1) if pipelined else self.sctx  # the rest
+        self.cs = oc.CascadeSet(oc.CascadeConfig(N_GRID, LENGTHS, CUTOFFS), _params(), ctx=self.sctx)
+        nbuf = 2 if pipelined else 1
+        self.maps = [oc.SurfaceMaps(self.cs) for _ in range(nbuf)]
+        self.slices = [oc.VelocitySlices(self.cs, SliceConfig.make(count=DEPTHS)) for _ in range(nbuf)]
         v, t = uv_ellipsoid()
         self.mesh = oc.TriMesh(v, t, ctx=self.ctx)
         self.pose = _pose(self.mesh.centroid)
-        self.fluid, self._keep = oc._fluid_struct(oc.FluidQuery(maps=self.maps, slices=self.slices,
-                                                                wind=WIND), oc.DragCoefficients())
+        self.fluids = [oc._fluid_struct(oc.FluidQuery(maps=self.maps[k], slices=self.slices[k],
+                                                      wind=WIND), oc.DragCoefficients())
+                       for k in range(nbuf)]
         self.zone = oc.FdmZone(FdmConfig.make(grid_size=FDM_N, margin=FDM_MARGIN), BODY_SIZE,
                                (self.pose.position[0], self.pose.position[2]), DT, ctx=self.ctx)
         ext = self.mesh.bbox_max - self.mesh.bbox_min
@@ -150,29 +183,75 @@ class Frame:
         self.mparams = MaskParams.make()
         self.speed = float(np.linalg.norm(list(self.pose.linear_velocity)))
         self.t = 0.0
+        self.f = 0
         from paper_2503_03326_b200._types import HydroReport
         self.report = HydroReport()
+        self.S = torch.cuda.ExternalStream(self.sctx.stream, device=f"cuda:{device}")
+        self.H = torch.cuda.ExternalStream(self.ctx.stream, device=f"cuda:{device}")
+        self.ready = [torch.cuda.Event() for _ in range(nbuf)]
+        self.consumed = [torch.cuda.Event() for _ in range(nbuf)]
+        self.pending_report = False
+        self.serialize = False  # profiling passes: no cross-frame overlap
+
+    def contexts(self):
+        return [self.sctx, self.ctx] if self.pipelined else [self.ctx]
+
+    def sync(self):
+        for c in self.contexts():
+            c.synchronize()
+
+    def timed_begin(self, ev):
+        ev.record(self.S)
+        self.H.wait_event(ev)
+
+    def timed_end(self, ev):
+        self.S.wait_event(self.consumed[(self.f - 1) % len(self.consumed)])
+        ev.record(self.S)
+
+    def _read_report(self):
+        self.oc.check(self.L.ocn_hydro_report_get(self.mesh.h, C.byref(self.report)), self.ctx.h,
+                      "report")
 
     def step(self, read_report: bool = False):
         """sim.cpp:59-109 minus the rigid integrator: spectral step, forces,
-        stability, mask from the device waterline, FDM step (all async)."""
+        stability, mask from the device waterline, FDM step (all async). With
+        read_report, the previous frame's report is read (its forces are what
+        an integrator needs before this frame's forces); finish() reads the last."""
         L, oc = self.L, self.oc
+        k = self.f % len(self.maps)
         self.t += DT
-        oc.check(L.ocn_spectral_step(self.maps.h, self.slices.h, self.t, 1.0), self.ctx.h, "spectral")
-        oc.check(L.ocn_hydro_aggregate(self.mesh.h, C.byref(self.pose), C.byref(self.fluid), None,
-                                       None), self.ctx.h, "aggregate")
+        # the buffer's previous readers are done (serialize: the previous frame is)
+        self.S.wait_event(self.consumed[(self.f - 1) % len(self.maps) if self.serialize else k])
+        oc.check(L.ocn_spectral_step(self.maps[k].h, self.slices[k].h, self.t, 1.0), self.sctx.h,
+                 "spectral")
+        self.ready[k].record(self.S)
+        if read_report and self.pending_report:
+            self._read_report()
+        self.H.wait_event(self.ready[k])
+        fluid, _ = self.fluids[k]
+        oc.check(L.ocn_hydro_aggregate(self.mesh.h, C.byref(self.pose), C.byref(fluid), None, None),
+                 self.ctx.h, "aggregate")
         oc.check(L.ocn_zone_update_stability(self.zone.h, self.speed, DT), self.ctx.h, "stability")
         px, pz = self.pose.position[0], self.pose.position[2]
         oc.check(L.ocn_zone_mask_from_hydro(self.zone.h, self.mesh.h, YAW, px, pz, self.speed,
                                             C.byref(self.frame), C.byref(self.mparams)), self.ctx.h,
                  "mask")
         # the body advances with its velocity (the rigid integrator is out of scope)
-        for k in range(3):
-            self.pose.position[k] += self.pose.linear_velocity[k] * DT
+        for q in range(3):
+            self.pose.position[q] += self.pose.linear_velocity[q] * DT
         oc.check(L.ocn_zone_step(self.zone.h, DT, self.pose.position[0], self.pose.position[2]),
                  self.ctx.h, "fdm")
-        if read_report:
-            oc.check(L.ocn_hydro_report_get(self.mesh.h, C.byref(self.report)), self.ctx.h, "report")
+        self.consumed[k].record(self.H)
+        self.pending_report = True
+        self.f += 1
+        if read_report and not self.pipelined:
+            self._read_report()
+            self.pending_report = False
+
+    def finish(self, read_report: bool = False):
+        if read_report and self.pending_report:
+            self._read_report()
+        self.pending_report = False
 
 
 # ---------------------------------------------------------------- config 4
@@ -184,7 +263,7 @@ C4_WORKLOAD = ("config4: 64 independent instances x 3 cascades x 512^2 (8 surfac
                "instances sharded across ranks, no collective")
 
 
-class Frame4:
+class Frame4(_SingleStream):
     """This rank's share of the 64 instances as one batched spectral set."""
 
     def __init__(self, device: int, rank: int, world: int):
@@ -225,7 +304,7 @@ C5_WORKLOAD = ("config5: single 16384^2 surface (8 fields, 4 packed transforms),
                "rank, NCCL all-to-all tile transpose between the row and column passes")
 
 
-class Frame5:
+class Frame5(_SingleStream):
     """This rank's slab of the 16384^2 grid; the transpose is an NCCL all-to-all."""
 
     def __init__(self, device: int, rank: int, world: int, dist):
@@ -314,43 +393,55 @@ def run_ours(args):
     dist, rank, world, local = _dist()
     c4 = args.config == 4
     c5 = args.config == 5
-    fr = Frame5(local, rank, world, dist) if c5 else (Frame4(local, rank, world) if c4 else Frame(local))
-    L, ctx = fr.L, fr.ctx
+    fr = (Frame5(local, rank, world, dist) if c5 else
+          (Frame4(local, rank, world) if c4 else Frame(local, pipelined=not args.no_pipeline)))
+    L = fr.L
+    ctxs = fr.contexts()
     for _ in range(max(args.warmup, 3)):
         fr.step()
-    ctx.synchronize()
-    # ---- timed region: device time with CUDA events on the library stream
+    fr.sync()
+    # ---- timed region: device time with CUDA events on the library stream(s)
     import torch
-    stream = torch.cuda.ExternalStream(ctx.stream, device=f"cuda:{local}")
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    launches0 = ctx.kernel_launches()
+
+    def n_launches():
+        return sum(c.kernel_launches() for c in ctxs)
+    launches0 = n_launches()
     with ClockSampler(local) as clk:
         _barrier(dist)
-        ctx.synchronize()
-        ev0.record(stream)
+        fr.sync()
+        fr.timed_begin(ev0)
         for _ in range(args.steps):
             fr.step()
-        ev1.record(stream)
-        ctx.synchronize()
+        fr.timed_end(ev1)
+        fr.sync()
         _barrier(dist)
         ms_total = ev0.elapsed_time(ev1)
-        launches = ctx.kernel_launches() - launches0
+        launches = n_launches() - launches0
 
         # ---- roofline pass: same K frames with CUDA-event windows per stage
-        # (mode 2: the spectral step still replays its graph) ...
+        # (mode 2: the spectral step still replays its graph), frames not
+        # overlapped so that each window times its own stage ...
+        fr.serialize = True
+
         def profiled(mode, names):
-            L.ocn_ctx_profile(ctx.h, mode)
-            L.ocn_ctx_profile_reset(ctx.h)
+            for c in ctxs:
+                L.ocn_ctx_profile(c.h, mode)
+                L.ocn_ctx_profile_reset(c.h)
             for _ in range(args.steps):
                 fr.step()
-            ctx.synchronize()
+            fr.sync()
             out = {}
             for name, cat in names:
-                ms, cnt = C.c_double(), C.c_uint64()
-                L.ocn_ctx_profile_read(ctx.h, cat, C.byref(ms), C.byref(cnt))
-                out[name] = ms.value / args.steps
-            L.ocn_ctx_profile(ctx.h, 0)
+                tot = 0.0
+                for c in ctxs:  # each category runs on one of the contexts
+                    ms, cnt = C.c_double(), C.c_uint64()
+                    L.ocn_ctx_profile_read(c.h, cat, C.byref(ms), C.byref(cnt))
+                    tot += ms.value
+                out[name] = tot / args.steps
+            for c in ctxs:
+                L.ocn_ctx_profile(c.h, 0)
             return out
         if c5:
             fr.timing = True
@@ -366,14 +457,16 @@ def run_ours(args):
             stages = {"spectral": stages["spectral"]}
         # ... and the kernel split of the spectral step (mode 1: eager launches)
         kernels = profiled(1, [("evolve", 0), ("fft_rows", 1), ("fft_cols", 2), ("spectral_eager", 6)])
+        fr.serialize = False
         # ---- e2e: through the C-ABI with host inputs (t, pose) and the host
         # read of each frame's result, wall clock
         _barrier(dist)
-        ctx.synchronize()
+        fr.sync()
         t0 = time.perf_counter()
         for _ in range(args.steps):
             fr.step(read_report=True)
-        ctx.synchronize()
+        fr.finish(read_report=True)
+        fr.sync()
         e2e_s = time.perf_counter() - t0
     ms_frame = _max_over_ranks(dist, ms_total / args.steps)
     e2e_frame = _max_over_ranks(dist, e2e_s / args.steps)
@@ -410,6 +503,10 @@ def run_ours(args):
         cfg = {"workload": workload, "grid": N_GRID, "cascades": len(LENGTHS),
                "depth_slices": DEPTHS, "hull_triangles": int(fr.mesh.triangles.shape[0]),
                "fdm_grid": FDM_N, "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+               "frame_pipeline": ("frame f forces/mask/FDM (high-priority stream) overlap frame "
+                                  "f+1 spectral step (low-priority stream), double-buffered "
+                                  "maps/slices; stages_ms timed without overlap"
+                                  if not args.no_pipeline else "off"),
                "l2": "per-frame working set 1.8 GB of outputs > 126 MB L2 (no explicit flush)"}
         scaling = "weak"
     value = points / (ms_frame / 1e3)
@@ -608,6 +705,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-pipeline", action="store_true",
+                    help="config 3: run every frame's stages in order on one stream")
     ap.add_argument("--config", type=int, default=3, choices=[3, 4, 5],
                     help="3: the BASELINE metric frame (default); 4: 64 batched 512^2 instances; "
                          "5: single 16384^2 grid, slab FFT + all-to-all across ranks")

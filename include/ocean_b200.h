@@ -209,6 +209,13 @@ typedef struct ocn_slab ocn_slab;
 /* ================================ context ================================ */
 OCN_API int ocn_abi_version(void);
 OCN_API int ocn_ctx_create(int device, ocn_ctx** out);
+/* As ocn_ctx_create with a stream priority: 1 highest, -1 lowest, 0 default.
+ * Objects of contexts on the same device may be passed to each other's calls
+ * (device memory is shared); ordering between two contexts is the caller's,
+ * with events on their ocn_ctx_stream streams. That is how bench.py overlaps
+ * frame f's forces / mask / FDM (high priority) with frame f+1's spectral
+ * step (low priority) on double-buffered maps and slices. */
+OCN_API int ocn_ctx_create_priority(int device, int priority, ocn_ctx** out);
 OCN_API int ocn_ctx_destroy(ocn_ctx* ctx);
 /* Last error message of this context (or the global one when ctx == NULL). */
 OCN_API const char* ocn_last_error(const ocn_ctx* ctx);

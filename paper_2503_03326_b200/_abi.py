@@ -71,6 +71,7 @@ pvp = C.POINTER(C.c_void_p)
 SIGNATURES = {
     "ocn_abi_version": (ci, []),
     "ocn_ctx_create": (ci, [ci, pvp]),
+    "ocn_ctx_create_priority": (ci, [ci, ci, pvp]),
     "ocn_ctx_destroy": (ci, [vp]),
     "ocn_last_error": (C.c_char_p, [vp]),
     "ocn_ctx_synchronize": (ci, [vp]),

@@ -1448,7 +1448,7 @@ extern "C" {
 
 int ocn_abi_version(void) { return OCN_ABI_VERSION; }
 
-int ocn_ctx_create(int device, ocn_ctx** out) {
+int ocn_ctx_create_priority(int device, int priority, ocn_ctx** out) {
   return api_call(nullptr, [&] {
     OCN_REQUIRE(out, "ocn_ctx_create: out is NULL");
     int ndev = 0;
@@ -1467,10 +1467,16 @@ int ocn_ctx_create(int device, ocn_ctx** out) {
       fail(OCN_ERR_CUDA, "libocean_b200 is built for sm_100a; device %d is sm_%d%d", device,
            prop.major, prop.minor);
     ctx->sm_count = prop.multiProcessorCount;
-    OCN_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    OCN_REQUIRE(priority >= -1 && priority <= 1, "ocn_ctx_create_priority: priority %d", priority);
+    int lo = 0, hi = 0;  // CUDA: lower numbers are higher priorities
+    OCN_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    const int prio = priority > 0 ? hi : (priority < 0 ? lo : 0);
+    OCN_CUDA(cudaStreamCreateWithPriority(&ctx->stream, cudaStreamNonBlocking, prio));
     *out = ctx.release();
   });
 }
+
+int ocn_ctx_create(int device, ocn_ctx** out) { return ocn_ctx_create_priority(device, 0, out); }
 
 int ocn_ctx_destroy(ocn_ctx* ctx) {
   ocn::ctx_release(ctx);

@@ -40,9 +40,10 @@ class Context:
 
     _default: dict[int, "Context"] = {}
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, priority: int = 0):
+        """priority: 1 highest, -1 lowest, 0 default stream priority."""
         h = C.c_void_p()
-        check(lib().ocn_ctx_create(device, C.byref(h)), None, "ocn_ctx_create")
+        check(lib().ocn_ctx_create_priority(device, priority, C.byref(h)), None, "ocn_ctx_create")
         self.h = h
         self.device = device
 

@@ -9,5 +9,5 @@ frames = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 fr = bench.Frame4(0, 0, 1)
 for _ in range(frames):
     fr.step()
-fr.ctx.synchronize()
+fr.sync()
 print("ok", fr.ctx.kernel_launches())

@@ -9,5 +9,5 @@ frames = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 fr = bench.Frame5(0, 0, 1, None)
 for _ in range(frames):
     fr.step()
-fr.ctx.synchronize()
+fr.sync()
 print("ok", fr.ctx.kernel_launches())

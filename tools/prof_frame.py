@@ -9,5 +9,5 @@ frames = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 fr = bench.Frame(0)
 for _ in range(frames):
     fr.step()
-fr.ctx.synchronize()
-print("ok", fr.ctx.kernel_launches())
+fr.sync()
+print("ok", sum(c.kernel_launches() for c in fr.contexts()))
