@@ -17,8 +17,8 @@
 //   k_cols_tma<N>: persistent column FFT of scratch fed by TMA (k_cols<N>
 //                  with direct loads outside 128 <= N <= 4096), Re -> field X,
 //                  Im -> field Y (fp32, row-major [i][j])
-// Transforms run in groups sharing one scratch buffer (group * N^2 * 8 B, 1 GB
-// budget; see group_for).
+// Transforms run in groups sharing one scratch buffer (group * N^2 * 8 B, 768 MB
+// budget, equal-sized groups per family; see group_for / get_plan).
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -1132,11 +1132,13 @@ size_t group_for(int n, int total) {
   // Scratch budget of the transform groups. Larger groups amortise the row
   // kernel's per-row staging over more transforms and keep the persistent
   // column kernel's tile ring full: measured on B200 at N = 1024 (config 3,
-  // spectral ms / frame) 64 MB 1.75, 256 MB 1.46, 512 MB 1.39, 1 GB 1.36,
-  // 2 GB 1.33 -> 1 GB default (0.6% of HBM). OCN_SCRATCH_MB overrides.
+  // spectral ms / frame, first TMA column kernel) 64 MB 1.75, 256 MB 1.46,
+  // 512 MB 1.39, 1 GB 1.36, 2 GB 1.33; with balanced family groups (get_plan)
+  // 384 MB 1.100, 512 MB 1.123, 768 MB 1.095, 1 GB 1.124 -> 768 MB default
+  // (96-transform groups at N = 1024). OCN_SCRATCH_MB overrides.
   static const size_t budget = [] {
     const char* e = getenv("OCN_SCRATCH_MB");
-    return (size_t)(e && atoi(e) > 0 ? atoi(e) : 1024) << 20;
+    return (size_t)(e && atoi(e) > 0 ? atoi(e) : 768) << 20;
   }();
   size_t per = (size_t)n * n * sizeof(float2);
   size_t g = budget / per;
@@ -1195,12 +1197,12 @@ static SpectralPlan* get_plan(ocn_cascades* cas, ocn_maps* maps, ocn_slices* sli
   const int total = (int)plan->host_desc.size();
   auto family = [&](int i) { return plan->host_desc[i].kind <= kSurfHxHz ? 0 : 1; };
   for (int g0 = 0; g0 < total;) {
-    int cnt = std::min(cas->group, total - g0);
-    for (int i = 1; i < cnt; ++i)
-      if (family(g0 + i) != family(g0)) {
-        cnt = i;  // keep groups single-family
-        break;
-      }
+    // the family's remaining run, split into equal groups of <= cas->group
+    // (balanced groups: 96 + 96 beat 128 + 64 at config 3, 1.11 vs 1.16 ms)
+    int run = 1;
+    while (g0 + run < total && family(g0 + run) == family(g0)) ++run;
+    const int ngroups = (run + cas->group - 1) / cas->group;
+    const int cnt = (run + ngroups - 1) / ngroups;
     SpectralPlan::Group gr{g0, cnt, (int)segs.size(), 0, 0, family(g0)};
     for (int i = 0; i < gr.count; ++i) {
       const int c = plan->host_desc[g0 + i].cascade;
