@@ -120,12 +120,6 @@ struct ocn_ctx {
   std::atomic<uint64_t> launches{0};
   ocn::PinnedBuf pinned;
   ocn::DevBuf<unsigned char> scratch;  // generic per-call device scratch
-  cudaStream_t aux = nullptr;          // second stream (column passes overlap row passes)
-  std::vector<cudaEvent_t> sync_events;
-  cudaStream_t aux_stream() {
-    if (!aux) cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking);
-    return aux;
-  }
 };
 
 namespace ocn {

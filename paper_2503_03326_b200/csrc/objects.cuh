@@ -105,8 +105,7 @@ struct ocn_cascades {
   ocn::DevBuf<float2> scratch;  // row-pass intermediates of one transform group
   ocn::DevBuf<double> d_time;   // frame time read by k_evolve (set per frame)
   int group = 1;                // transforms per group
-  int nbuf = 1;                 // scratch buffers (2: row/column passes overlap)
-  CUtensorMap cols_map[2];      // TMA source map of each scratch buffer (column pass)
+  CUtensorMap cols_map;         // TMA source map of the scratch (column pass)
   bool cols_map_ok = false;
   CUtensorMap fused_map;        // TMA source map of the fused step's column tiles
   bool fused_ok = false;

@@ -43,8 +43,6 @@ void ctx_release(ocn_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   cudaStreamDestroy(ctx->stream);
-  if (ctx->aux) cudaStreamSynchronize(ctx->aux), cudaStreamDestroy(ctx->aux);
-  for (cudaEvent_t e : ctx->sync_events) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->prof_pool) cudaEventDestroy(e);
   delete ctx;
 }
@@ -574,64 +572,6 @@ __global__ void __launch_bounds__(256, N >= 1024 ? 2 : OCN_ROWS_MINB_SMALL) k_ro
   }
 }
 
-// Column pass, warp per column: the tile [N][CC] is loaded with coalesced row
-// segments into per-column shared buffers, each warp transforms its columns,
-// the results go back through shared memory and leave as coalesced row
-// segments with the (-1)^(i+j) sign and the Re / Im split fused in.
-template <int N, bool COMPLEX_OUT>
-__global__ void __launch_bounds__(256) k_cols_w(const ColArgs a) {
-  using W = WarpLaunch<N>;
-  constexpr int T = W::T, CC = W::CC;
-  extern __shared__ float2 tile[];  // [CC][STRIDE]
-  const int col0 = blockIdx.x * CC;
-  const int xf = blockIdx.y;
-  const float2* in = a.scratch + (size_t)xf * N * N;
-  constexpr int NT = 32 * W::COLS_WARPS;
-  constexpr int ITER = N * CC / NT;
-  static_assert(ITER * NT == N * CC, "tile must split evenly");
-  {
-    float2 v[ITER];  // all loads in flight before the shared-memory stores
-#pragma unroll
-    for (int it = 0; it < ITER; ++it) {
-      const int idx = threadIdx.x + it * NT;
-      const int row = idx / CC, c = idx - row * CC;
-      v[it] = __ldg(in + (size_t)row * N + col0 + c);
-    }
-#pragma unroll
-    for (int it = 0; it < ITER; ++it) {
-      const int idx = threadIdx.x + it * NT;
-      const int row = idx / CC, c = idx - row * CC;
-      tile[c * W::STRIDE + fft::pad32(row)] = v[it];
-    }
-  }
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int sub = lane / T, t = lane - sub * T;
-  const int c = warp * W::TPW + sub;
-  float2* buf = tile + c * W::STRIDE;
-  fft::cta_fft<N, true, true, true>(
-      t, buf, a.tw, [&](int n) { return buf[fft::pad32(n)]; },
-      [&](int k, float2 x) { buf[fft::pad32(k)] = x; });
-  __syncthreads();
-  if constexpr (COMPLEX_OUT) {
-    float2* out = a.out_c + (size_t)xf * N * N;
-    for (int idx = threadIdx.x; idx < N * CC; idx += blockDim.x) {
-      const int row = idx / CC, cc = idx - row * CC, col = col0 + cc;
-      const float2 x = tile[cc * W::STRIDE + fft::pad32(row)];
-      out[(size_t)row * N + col] = x;
-    }
-  } else {
-    const XformDesc d = a.desc[xf];
-#pragma unroll 8
-    for (int idx = threadIdx.x; idx < N * CC; idx += NT) {
-      const int row = idx / CC, cc = idx - row * CC, col = col0 + cc;
-      const float2 x = tile[cc * W::STRIDE + fft::pad32(row)];
-      d.out_re[(size_t)row * N + col] = x.x;  // fft.cpp:93-99
-      if (d.out_im) d.out_im[(size_t)row * N + col] = x.y;
-    }
-  }
-}
-
 // ------------------------------------------------------------------ columns
 
 template <int N, bool COMPLEX_OUT>
@@ -864,11 +804,11 @@ constexpr bool use_warp_kernels() {
 
 template <int N>
 void launch_rows(ocn_ctx* ctx, const RowArgs& a, bool plain, cudaStream_t st, int nseg,
-                 int max_seg, int family, bool lean) {
+                 int max_seg, int family) {
   if constexpr (use_warp_kernels<N>()) {
     using W = WarpLaunch<N>;
     const int slots = (max_seg + W::TPW - 1) / W::TPW;
-    const int cap = lean ? 4 : 8;  // lean: co-resides with a column pass
+    const int cap = 8;
     // surface grids have 4 transforms: two rows per CTA keep 8 warps busy
     static const int max_rpc = [] {  // experiment override: OCN_ROWS_RPC=1|2|4
       const char* e = getenv("OCN_ROWS_RPC");
@@ -911,20 +851,9 @@ void launch_rows(ocn_ctx* ctx, const RowArgs& a, bool plain, cudaStream_t st, in
   OCN_LAUNCHED(ctx);
 }
 
-// The CTA-synchronous column kernel (direct coalesced global loads / stores,
-// no tile round trips) measured faster than the warp-per-column one at
-// N = 1024 on B200 (0.98 vs 1.17 ms / frame); OCN_COLS_WARP=1 selects the latter.
-static bool cols_generic() {
-  static const bool on = [] {
-    const char* e = getenv("OCN_COLS_WARP");
-    return !(e && *e && *e != '0');
-  }();
-  return on;
-}
-
 template <int N>
 void launch_cols(ocn_ctx* ctx, const ColArgs& a, int G, bool complex_out, cudaStream_t st,
-                 const CUtensorMap* map, bool lean) {
+                 const CUtensorMap* map) {
   if constexpr (ColTma<N>::OK) {
     if (map) {
       using CT = ColTma<N>;
@@ -932,7 +861,6 @@ void launch_cols(ocn_ctx* ctx, const ColArgs& a, int G, bool complex_out, cudaSt
       if (!attr) {
         OCN_CUDA(cudaFuncSetAttribute(k_cols_tma<N, false, CT::STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CT::SMEM));
         OCN_CUDA(cudaFuncSetAttribute(k_cols_tma<N, true, CT::STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CT::SMEM));
-        OCN_CUDA(cudaFuncSetAttribute(k_cols_tma<N, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CT::smem(2)));
         if (CT::smem(2, true) <= 227 * 1024)
           OCN_CUDA(cudaFuncSetAttribute(k_cols_tma<N, false, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CT::smem(2, true)));
         attr = true;
@@ -943,32 +871,11 @@ void launch_cols(ocn_ctx* ctx, const ColArgs& a, int G, bool complex_out, cudaSt
         k_cols_tma<N, true, CT::STAGES><<<grid, CT::THREADS, CT::SMEM, st>>>(*map, a, tiles_x, ntiles);
       else if (a.out_maps && CT::smem(2, true) <= 227 * 1024)
         k_cols_tma<N, false, 2, true><<<grid, CT::THREADS, CT::smem(2, true), st>>>(*map, a, tiles_x, ntiles);
-      else if (lean)  // leaves room on each SM for a concurrent row pass
-        k_cols_tma<N, false, 2><<<grid, CT::THREADS, CT::smem(2), st>>>(*map, a, tiles_x, ntiles);
       else
         k_cols_tma<N, false, CT::STAGES><<<grid, CT::THREADS, CT::SMEM, st>>>(*map, a, tiles_x, ntiles);
       OCN_LAUNCHED(ctx);
       return;
     }
-  }
-  if constexpr (use_warp_kernels<N>()) {
-   if (!cols_generic()) {
-    using W = WarpLaunch<N>;
-    const size_t smem = (size_t)W::CC * W::STRIDE * sizeof(float2);
-    static bool attr = false;
-    if (!attr) {
-      OCN_CUDA(cudaFuncSetAttribute(k_cols_w<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      OCN_CUDA(cudaFuncSetAttribute(k_cols_w<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = true;
-    }
-    dim3 grid(N / W::CC > 0 ? N / W::CC : 1, G);
-    if (complex_out)
-      k_cols_w<N, true><<<grid, 32 * W::COLS_WARPS, smem, st>>>(a);
-    else
-      k_cols_w<N, false><<<grid, 32 * W::COLS_WARPS, smem, st>>>(a);
-    OCN_LAUNCHED(ctx);
-    return;
-   }
   }
   using L = Launch<N>;
   set_smem_attrs<N>();
@@ -981,15 +888,15 @@ void launch_cols(ocn_ctx* ctx, const ColArgs& a, int G, bool complex_out, cudaSt
 }
 
 void rows_dispatch(ocn_ctx* ctx, int n, const RowArgs& a, bool plain, cudaStream_t st,
-                   int nseg = 1, int max_seg = 0, int family = 0, bool lean = false) {
+                   int nseg = 1, int max_seg = 0, int family = 0) {
   if (max_seg <= 0) max_seg = a.G;
-#define OCN_ROWS(NN) launch_rows<NN>(ctx, a, plain, st, nseg, max_seg, family, lean)
+#define OCN_ROWS(NN) launch_rows<NN>(ctx, a, plain, st, nseg, max_seg, family)
   OCN_DISPATCH_N(n, OCN_ROWS)
 #undef OCN_ROWS
 }
 void cols_dispatch(ocn_ctx* ctx, int n, const ColArgs& a, int G, bool complex_out, cudaStream_t st,
-                   const CUtensorMap* map = nullptr, bool lean = false) {
-#define OCN_COLS(NN) launch_cols<NN>(ctx, a, G, complex_out, st, map, lean)
+                   const CUtensorMap* map = nullptr) {
+#define OCN_COLS(NN) launch_cols<NN>(ctx, a, G, complex_out, st, map)
   OCN_DISPATCH_N(n, OCN_COLS)
 #undef OCN_COLS
 }
@@ -1029,34 +936,6 @@ std::vector<float2> make_twiddles(int n) {
 
 namespace {
 
-// Keep the row-pass scratch resident in L2 (126 MB): persisting access window
-// on the context stream (captured into the spectral graph's kernel nodes).
-void set_l2_window(ocn_ctx* ctx, void* base, size_t bytes) {
-  // opt-in: measured slower on B200 (spectral 2.04 vs 1.88 ms / frame)
-  static const bool on = [] {
-    const char* e = getenv("OCN_L2_WINDOW");
-    return e && *e && *e != '0';
-  }();
-  if (!on || bytes == 0) return;
-  int max_persist = 0, max_window = 0;
-  cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, ctx->device);
-  cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, ctx->device);
-  if (max_persist <= 0 || max_window <= 0) return;
-  const size_t win = std::min(bytes, (size_t)max_window);
-  const size_t limit = std::min(win, (size_t)max_persist);
-  if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, limit) != cudaSuccess) {
-    cudaGetLastError();
-    return;
-  }
-  cudaStreamAttrValue attr{};
-  attr.accessPolicyWindow.base_ptr = base;
-  attr.accessPolicyWindow.num_bytes = win;
-  attr.accessPolicyWindow.hitRatio = std::min(1.0f, (float)limit / (float)win);
-  attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-  attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-  if (cudaStreamSetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &attr) != cudaSuccess)
-    cudaGetLastError();
-}
 
 // Column-pass source map over a scratch buffer [G][N][N] complex64, viewed as
 // fp32 [G][N / BR][BR][2N] so one box {2 PC, BR, N / BR, 1} is a whole column
@@ -1258,36 +1137,12 @@ static void forget_plans(ocn_cascades* cas, const void* obj) {
   }
 }
 
-// Row pass of group g+1 overlaps the column pass of group g: rows on the
-// context stream, columns on the auxiliary stream, two scratch buffers
-// (dependencies by events; captured into the graph as two branches).
-// Off by default: measured no gain on B200 (2.38 vs 2.40 ms with half-size
-// groups, both slower than one 8-transform buffer); OCN_DUAL_STREAM=1 enables it.
-static bool dual_stream(const ocn_ctx* ctx) {
-  static const bool on = [] {
-    const char* e = getenv("OCN_DUAL_STREAM");
-    return e && *e && *e != '0';
-  }();
-  (void)ctx;
-  return on;
-}
-
 static void enqueue_spectral(ocn_cascades* cas, SpectralPlan* plan, double choppiness) {
   ocn_ctx* ctx = cas->ctx;
   const int n = cas->n;
   const size_t nn = (size_t)n * n;
-  const bool dual = dual_stream(ctx) && cas->nbuf == 2;
-  cudaStream_t A = ctx->stream, B = dual ? ctx->aux_stream() : ctx->stream;
+  cudaStream_t A = ctx->stream;
   ProfWindow whole(ctx, OCN_PROF_SPECTRAL);
-  std::vector<cudaEvent_t>& ev = ctx->sync_events;
-  auto event = [&](int k) {
-    while ((int)ev.size() <= k) {
-      cudaEvent_t e;
-      OCN_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      ev.push_back(e);
-    }
-    return ev[k];
-  };
   {
     ProfWindow pw(ctx, OCN_PROF_EVOLVE);  // every grid in one launch
     if (plan->need_velocity)
@@ -1324,11 +1179,9 @@ static void enqueue_spectral(ocn_cascades* cas, SpectralPlan* plan, double chopp
     OCN_LAUNCHED(ctx);
     return;
   }
-  const int G = cas->group;
   for (size_t gidx = 0; gidx < plan->groups.size(); ++gidx) {
     const SpectralPlan::Group& gr = plan->groups[gidx];
-    float2* scratch = cas->scratch.p + (size_t)(dual ? gidx % 2 : 0) * G * nn;
-    if (dual && gidx >= 2) OCN_CUDA(cudaStreamWaitEvent(A, event(2 * (int)gidx - 3), 0));
+    float2* scratch = cas->scratch.p;
     RowArgs ra{};
     ra.items = n * gr.count;
     ra.G = gr.count;
@@ -1341,12 +1194,8 @@ static void enqueue_spectral(ocn_cascades* cas, SpectralPlan* plan, double chopp
     ra.scratch = scratch;
     ra.tw = cas->twiddle.p;
     {
-      ProfWindow pw(ctx, dual ? -1 : OCN_PROF_ROWS);
-      rows_dispatch(ctx, n, ra, false, A, gr.nseg, gr.max_seg, gr.family, dual);
-    }
-    if (dual) {
-      OCN_CUDA(cudaEventRecord(event(2 * (int)gidx), A));
-      OCN_CUDA(cudaStreamWaitEvent(B, event(2 * (int)gidx), 0));
+      ProfWindow pw(ctx, OCN_PROF_ROWS);
+      rows_dispatch(ctx, n, ra, false, A, gr.nseg, gr.max_seg, gr.family);
     }
     ColArgs ca{};
     ca.scratch = scratch;
@@ -1354,14 +1203,10 @@ static void enqueue_spectral(ocn_cascades* cas, SpectralPlan* plan, double chopp
     ca.tw = cas->twiddle.p;
     ca.out_maps = plan->out_maps.p ? plan->out_maps.p + 2 * gr.first : nullptr;
     {
-      ProfWindow pw(ctx, dual ? -1 : OCN_PROF_COLS);
-      cols_dispatch(ctx, n, ca, gr.count, false, B,
-                    cas->cols_map_ok ? &cas->cols_map[dual ? gidx % 2 : 0] : nullptr, dual);
+      ProfWindow pw(ctx, OCN_PROF_COLS);
+      cols_dispatch(ctx, n, ca, gr.count, false, A, cas->cols_map_ok ? &cas->cols_map : nullptr);
     }
-    if (dual) OCN_CUDA(cudaEventRecord(event(2 * (int)gidx + 1), B));
   }
-  if (dual && !plan->groups.empty())
-    OCN_CUDA(cudaStreamWaitEvent(A, event(2 * (int)plan->groups.size() - 1), 0));
 }
 
 static bool graphs_enabled() {
@@ -1698,15 +1543,10 @@ int ocn_cascades_create_multi(ocn_ctx* ctx, int resolution, int count, const dou
     OCN_CUDA(cudaMemcpyAsync(cas->twiddle.p, tw.data(), tw.size() * sizeof(float2),
                              cudaMemcpyHostToDevice, ctx->stream));
     cas->group = (int)group_for(resolution, 1 << 30);
-    cas->nbuf = dual_stream(ctx) && cas->group >= 2 ? 2 : 1;
-    if (cas->nbuf == 2) cas->group /= 2;
     cas->d_time.alloc(1);
-    cas->scratch.alloc((size_t)cas->nbuf * cas->group * nn);
-    set_l2_window(ctx, cas->scratch.p, cas->scratch.bytes());
-    for (int b = 0; b < cas->nbuf; ++b)
-      cas->cols_map_ok = cols_map_for(resolution, cas->group,
-                                      cas->scratch.p + (size_t)b * cas->group * nn, &cas->cols_map[b]);
-    if (resolution == 1024 && fused_enabled() && cas->nbuf == 1 &&
+    cas->scratch.alloc((size_t)cas->group * nn);
+    cas->cols_map_ok = cols_map_for(resolution, cas->group, cas->scratch.p, &cas->cols_map);
+    if (resolution == 1024 && fused_enabled() &&
         cas->group >= kFuseSlots * kFuseW)
       cas->fused_ok = cols_map_for(1024, kFuseSlots * kFuseW, cas->scratch.p, &cas->fused_map,
                                    Fused<1024>::PC);
