@@ -45,3 +45,14 @@ def test_pipelined_frames_match_serial():
         assert x == y, f"frame {f}: pipelined {x} != serial {y}"
     if fa is not None:
         np.testing.assert_array_equal(fa, fb)
+
+
+def test_context_priority_arguments():
+    """ocn_ctx_create_priority: -1 / 0 / 1 accepted, anything else is a bad argument."""
+    from paper_2503_03326_b200 import ocean as oc
+    from paper_2503_03326_b200._abi import lib
+    for p in (-1, 0, 1):
+        c = oc.Context(0, priority=p)
+        c.synchronize()
+    h = C.c_void_p()
+    assert lib().ocn_ctx_create_priority(0, 2, C.byref(h)) == 8  # OCN_ERR_ARG
