@@ -376,13 +376,7 @@ struct WarpLaunch {
   static constexpr int TPW = 32 / T;  // transforms per warp
   static constexpr int STRIDE = Launch<N>::ROW_STRIDE;
   static constexpr int TWN = (PL::tw_size() + 15) / 16 * 16;  // shared twiddle slots
-  static constexpr int COLS_WARPS = 8;
-  static constexpr int CC = COLS_WARPS * TPW;  // columns per column-CTA
 };
-
-__device__ __forceinline__ float atten_f(float k, float y) {
-  return y > 0.f ? 1.0f + k * y : __expf(k * y);
-}
 
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
@@ -399,7 +393,7 @@ template <int N, int MODE>
 __global__ void __launch_bounds__(256, N >= 1024 ? 2 : OCN_ROWS_MINB_SMALL) k_rows_w(const RowArgs a) {
   constexpr bool PLAIN = MODE == kRowPlain;
   using W = WarpLaunch<N>;
-  constexpr int T = W::T, E = fft::Plan<N>::E;
+  constexpr int T = W::T;
   constexpr int H = N / 2;  // centring half-shift (see kCentreByShift)
   extern __shared__ float4 smem4[];
   // Per mode of this row, shared by every transform of the group (SoA):
