@@ -130,15 +130,30 @@ __global__ void __launch_bounds__(SlabLaunch<N>::THREADS) k_slab_rows(const Slab
   const int li = valid ? item >> 2 : 0, p = item & 3;
   const float kx = a.dk * (float)(a.row0 + li - N / 2);
   const float2* srow = a.spec + (size_t)li * N;
+  // surface_pair as one branch-free form with per-pair constants (as k_rows_w):
+  //   Re M = c0 + c3 kz + kx / |k| (c1 + c2 kz),  Im M = c4 + (c5 (kz + kx^2) + c6 kz^2) / |k|
+  const float chop = a.chop, kx2 = kx * kx;
+  float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f, c4 = 0.f, c5 = 0.f, c6 = 0.f;
+  if (p == 0) c0 = 1.f, c1 = -chop;
+  else if (p == 1) c5 = chop;
+  else if (p == 2) c2 = chop, c6 = chop;
+  else c3 = -1.f, c4 = kx;
+  const int cols_log2 = __ffs(a.cols) - 1;  // cols = N / ranks, a power of two
   fft::cta_fft<N>(
       t, smem + local * L::ROW_STRIDE, a.tw,
       [&](int j) {
         if (!valid) return make_float2(0.f, 0.f);
-        return surface_pair(p, __ldg(srow + j), kx, a.dk * (float)(j - N / 2), a.chop);
+        const float2 h = __ldg(srow + j);
+        const float kz = a.dk * (float)(j - N / 2);
+        const float k2 = fmaf(kz, kz, kx2);
+        const float inv = k2 > 0.f ? rsqrtf(k2) : 0.f;
+        const float mr = fmaf(inv * kx, fmaf(c2, kz, c1), fmaf(c3, kz, c0));
+        const float mi = fmaf(inv, fmaf(c6 * kz, kz, c5 * (kz + kx2)), c4);
+        return make_float2(h.x * mr - h.y * mi, h.x * mi + h.y * mr);
       },
       [&](int k, float2 x) {
         if (!valid) return;
-        const int dest = k / a.cols, kc = k - dest * a.cols;
+        const int dest = k >> cols_log2, kc = k & (a.cols - 1);
         a.send[(((size_t)dest * 4 + p) * a.rows + li) * a.cols + kc] = x;
       });
 }
