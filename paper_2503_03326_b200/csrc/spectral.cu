@@ -6,14 +6,16 @@
 // (surface.cpp:39-103), build_slices (velocity.cpp:104-179),
 // ifft2_centered / ifft2_hermitian_pair (fft.cpp:39-101).
 //
-// Per frame and cascade:
+// Per frame, for every grid of the set:
 //   k_evolve     : h~(k,t) = h0 e^{iwt} + conj(h0(-k)) e^{-iwt} and
 //                  G(k,t) = h0 e^{iwt} - conj(h0(-k)) e^{-iwt}  (fp64 phase,
-//                  reduced mod 2pi before the fp32 sincos) -> spec[c] (L2)
-//   k_rows<N>    : per (row, transform of the group): the packed coefficient
-//                  X + iY = spec * multiplier(k) generated in registers (no
-//                  coefficient arrays in HBM), then the row FFT -> scratch
-//                  (input half-shifted: the (-1)^(i+j) centring, kCentreByShift)
+//                  reduced mod 2pi before the fp32 sincos) -> spec_h / spec_g
+//   k_rows_w<N>  : (128 <= N <= 1024; k_rows<N> otherwise) per (row, grid
+//                  segment of a transform group): the row's h~ or G-derived
+//                  arrays staged in shared memory, each packed coefficient
+//                  X + iY generated in the FFT's pass-0 load (no coefficient
+//                  arrays in HBM), then the row FFT -> scratch (input
+//                  half-shifted: the (-1)^(i+j) centring, kCentreByShift)
 //   k_cols_tma<N>: persistent column FFT of scratch fed by TMA (k_cols<N>
 //                  with direct loads outside 128 <= N <= 4096), Re -> field X,
 //                  Im -> field Y (fp32, row-major [i][j])
@@ -607,11 +609,11 @@ __global__ void __launch_bounds__(Launch<N>::THREADS) k_cols(const ColArgs a) {
 // mbarrier) while the CTA transforms the landed tile in place (dense
 // [row][column] layout read by pass 0, padded per-column layout for the
 // exchange) and refills the buffer as soon as its last shared reads are done.
-// Twiddles live in shared memory, so the warps' only global accesses are the
-// output stores ((-1)^(i+j) sign and Re / Im split fused, evict-first).
-// Measured on B200 (config 3): this ring of 3 x 8-column tiles beat a
-// 2 x 4-column ring with TMA-store epilogue and 2 CTAs / SM (1.36 vs 2.06 ms
-// spectral per frame: the store drain serialised the ring).
+// Twiddles live in shared memory. The epilogue splits Re / Im: by default into
+// shared staging planes written out by TMA stores (2 load stages fit beside
+// them), otherwise with evict-first stores from the warps (3 load stages).
+// Measured on B200 (config 3): 8-column tiles with one CTA per SM beat a
+// 4-column ring with 2 CTAs / SM (1.36 vs 2.06 ms spectral per frame).
 template <int N>
 struct ColTma {
   using PL = fft::Plan<N>;
@@ -968,7 +970,8 @@ static void plane_map_for(int n, float* plane, CUtensorMap* map) {
 
 // TMA-store column pass (default; OCN_COLS_STG=1 selects direct evict-first
 // stores from the warps, 3 load stages): measured 1.122 vs 1.128 ms spectral
-// per frame (config 3); both sit at ~83% of the measured HBM copy bandwidth.
+// per frame (config 3); the column pass then runs at ~94% of the measured HBM
+// copy bandwidth on its real traffic (ncu, 96-transform groups).
 static bool cols_tma_store() {
   static const bool on = [] {
     const char* e = getenv("OCN_COLS_STG");
