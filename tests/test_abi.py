@@ -91,3 +91,40 @@ int main(){ const double kPi=3.14159265358979323846; long bad=0;
                         f, "-o", exe], check=True)
         out = subprocess.run([exe], capture_output=True, text=True, check=True).stdout.strip()
     assert out == "0"
+
+
+def test_struct_layouts_match_header():
+    """Every POD struct of include/ocean_b200.h has the same size and field
+    offsets in the C compiler's layout and in the ctypes mirror."""
+    import os
+    import subprocess
+    import tempfile
+    from paper_2503_03326_b200 import _types as T
+    pairs = {"ocn_spectrum_params": T.SpectrumParams, "ocn_slice_config": T.SliceConfig,
+             "ocn_pose": T.Pose, "ocn_fluid": T.Fluid, "ocn_hydro_report": T.HydroReport,
+             "ocn_triangle_state": T.TriangleState, "ocn_fdm_config": T.FdmConfig,
+             "ocn_mask_params": T.MaskParams, "ocn_mask_frame": T.MaskFrame,
+             "ocn_zone_state": T.ZoneState}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "ocean_b200.h"', 'int main(void){']
+    for cname, py in pairs.items():
+        lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
+        for fname, _ in py._fields_:
+            lines.append(f'printf("{cname} {fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines.append("return 0;}")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with tempfile.TemporaryDirectory() as d:
+        src = os.path.join(d, "layout.c")
+        open(src, "w").write("\n".join(lines))
+        exe = os.path.join(d, "layout")
+        subprocess.run(["gcc", "-std=c99", "-I", os.path.join(root, "include"), src, "-o", exe],
+                       check=True)
+        out = subprocess.run([exe], capture_output=True, text=True, check=True).stdout.split("\n")
+    got = {}
+    for ln in out:
+        if ln:
+            parts = ln.split()
+            got[tuple(parts[:-1])] = int(parts[-1])
+    for cname, py in pairs.items():
+        assert got[(cname, "size")] == C.sizeof(py), cname
+        for fname, _ in py._fields_:
+            assert got[(cname, fname)] == getattr(py, fname).offset, (cname, fname)
