@@ -20,7 +20,10 @@ constexpr int kMaxGrids = 1 << 16;  // grids of one spectral set (cascades x ins
 struct GridConst {
   double dk, length, band_min, band_max;
   uint32_t cindex;
-  int32_t pad;
+  // spectrum rows i with |i - N/2| >= row_half hold no mode of the band
+  // (|k| >= |kx| >= band_max): exactly zero h0, so their row transforms are
+  // exactly zero. N/2 + 1 when every row can carry the band.
+  int32_t row_half;
   ocn_spectrum_params p;
 };
 
@@ -106,6 +109,7 @@ struct ocn_cascades {
   ocn::DevBuf<double> d_time;   // frame time read by k_evolve (set per frame)
   int group = 1;                // transforms per group
   CUtensorMap cols_map;         // TMA source map of the scratch (column pass)
+  CUtensorMap cols_chunk_map;   // same, 32-row chunks (band-limited loads)
   bool cols_map_ok = false;
   CUtensorMap fused_map;        // TMA source map of the fused step's column tiles
   bool fused_ok = false;

@@ -187,7 +187,7 @@ void launch_rows(ocn_ctx* ctx, const RowArgs& a, bool plain, cudaStream_t st, in
 
 template <int N>
 void launch_cols(ocn_ctx* ctx, const ColArgs& a, int G, bool complex_out, cudaStream_t st,
-                 const CUtensorMap* map) {
+                 const CUtensorMap* map, const CUtensorMap* chunk_map) {
   if constexpr (ColTma<N>::OK) {
     if (map) {
       using CT = ColTma<N>;
@@ -202,11 +202,11 @@ void launch_cols(ocn_ctx* ctx, const ColArgs& a, int G, bool complex_out, cudaSt
       const int tiles_x = N / CT::PC, ntiles = tiles_x * G;
       const int grid = std::min(ntiles, ctx->sm_count);
       if (complex_out)
-        k_cols_tma<N, true, CT::STAGES><<<grid, CT::THREADS, CT::SMEM, st>>>(*map, a, tiles_x, ntiles);
+        k_cols_tma<N, true, CT::STAGES><<<grid, CT::THREADS, CT::SMEM, st>>>(*map, *chunk_map, a, tiles_x, ntiles);
       else if (a.out_maps && CT::smem(2, true) <= 227 * 1024)
-        k_cols_tma<N, false, 2, true><<<grid, CT::THREADS, CT::smem(2, true), st>>>(*map, a, tiles_x, ntiles);
+        k_cols_tma<N, false, 2, true><<<grid, CT::THREADS, CT::smem(2, true), st>>>(*map, *chunk_map, a, tiles_x, ntiles);
       else
-        k_cols_tma<N, false, CT::STAGES><<<grid, CT::THREADS, CT::SMEM, st>>>(*map, a, tiles_x, ntiles);
+        k_cols_tma<N, false, CT::STAGES><<<grid, CT::THREADS, CT::SMEM, st>>>(*map, *chunk_map, a, tiles_x, ntiles);
       OCN_LAUNCHED(ctx);
       return;
     }
@@ -229,8 +229,8 @@ void rows_dispatch(ocn_ctx* ctx, int n, const RowArgs& a, bool plain, cudaStream
 #undef OCN_ROWS
 }
 void cols_dispatch(ocn_ctx* ctx, int n, const ColArgs& a, int G, bool complex_out, cudaStream_t st,
-                   const CUtensorMap* map = nullptr) {
-#define OCN_COLS(NN) launch_cols<NN>(ctx, a, G, complex_out, st, map)
+                   const CUtensorMap* map = nullptr, const CUtensorMap* chunk_map = nullptr) {
+#define OCN_COLS(NN) launch_cols<NN>(ctx, a, G, complex_out, st, map, chunk_map ? chunk_map : map)
   OCN_DISPATCH_N(n, OCN_COLS)
 #undef OCN_COLS
 }
@@ -283,12 +283,15 @@ static bool cols_ldg() {
   return on;
 }
 
-bool cols_map_for(int n, int G, const float2* scratch, CUtensorMap* map, int pc_fused = 0) {
-  const int pc = pc_fused ? pc_fused : cols_tma_pc(n), br = n < 256 ? n : 256;
+// chunk: the 32-row chunk map of the band-limited loads (box {2 PC, 32, 1, 1})
+bool cols_map_for(int n, int G, const float2* scratch, CUtensorMap* map, int pc_fused = 0,
+                  bool chunk = false) {
+  const int pc = pc_fused ? pc_fused : cols_tma_pc(n);
+  const int br = chunk ? std::min(32, n) : (n < 256 ? n : 256);
   if (!pc || (!pc_fused && cols_ldg())) return false;
   const uint64_t dims[4] = {2ull * n, (uint64_t)br, (uint64_t)(n / br), (uint64_t)G};
   const uint64_t strides[3] = {2ull * n * 4, (uint64_t)br * 2 * n * 4, (uint64_t)n * n * 8};
-  const uint32_t box[4] = {2u * pc, (uint32_t)br, (uint32_t)(n / br), 1u};
+  const uint32_t box[4] = {2u * pc, (uint32_t)br, chunk ? 1u : (uint32_t)(n / br), 1u};
   if (!tma::encode_f32(map, 4, const_cast<float2*>(scratch), dims, strides, box))
     fail(OCN_ERR_CUDA, "cuTensorMapEncodeTiled failed for the column pass (N=%d, G=%d)", n, G);
   return true;
@@ -334,6 +337,14 @@ static void build_out_maps(int n, const XformDesc* desc, int count, DevBuf<CUten
 // With one 12-warp CTA per SM each row task and column tile exposes its load
 // latency and barrier waits, and the scratch still round-trips HBM
 // (1.7 GB read + 3.4 GB written per frame in the capture).
+static bool band_skip_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("OCN_NO_BAND_SKIP");
+    return !(e && *e && *e != '0');
+  }();
+  return on;
+}
+
 static bool fused_enabled() {
   static const bool on = [] {
     const char* e = getenv("OCN_FUSED");
@@ -528,6 +539,10 @@ static void enqueue_spectral(ocn_cascades* cas, SpectralPlan* plan, double chopp
     ra.chop = (float)choppiness;
     ra.scratch = scratch;
     ra.tw = cas->twiddle.p;
+    // band-limited grids: the row pass skips the exactly-zero rows and the
+    // TMA column pass reads only the band rows (off with OCN_NO_BAND_SKIP=1)
+    const bool band = cas->cols_map_ok && band_skip_enabled();
+    ra.skip_zero_rows = band ? 1 : 0;
     {
       ProfWindow pw(ctx, OCN_PROF_ROWS);
       rows_dispatch(ctx, n, ra, false, A, gr.nseg, gr.max_seg, gr.family);
@@ -537,9 +552,11 @@ static void enqueue_spectral(ocn_cascades* cas, SpectralPlan* plan, double chopp
     ca.desc = plan->desc.p + gr.first;
     ca.tw = cas->twiddle.p;
     ca.out_maps = plan->out_maps.p ? plan->out_maps.p + 2 * gr.first : nullptr;
+    ca.gc = band ? cas->gconst.p : nullptr;
     {
       ProfWindow pw(ctx, OCN_PROF_COLS);
-      cols_dispatch(ctx, n, ca, gr.count, false, A, cas->cols_map_ok ? &cas->cols_map : nullptr);
+      cols_dispatch(ctx, n, ca, gr.count, false, A, cas->cols_map_ok ? &cas->cols_map : nullptr,
+                    cas->cols_map_ok ? &cas->cols_chunk_map : nullptr);
     }
   }
 }
@@ -863,6 +880,10 @@ int ocn_cascades_create_multi(ocn_ctx* ctx, int resolution, int count, const dou
       gc[c].band_max = band_max[c];
       gc[c].cindex = cas->cascade_index[c];
       gc[c].p = params[c];
+      // rows with |kx| >= band_max (1 + 1e-9) are outside the band whatever kz
+      // (hypot(kx, kz) >= |kx|; the margin covers rounding)
+      const double rh = std::ceil(band_max[c] * (1.0 + 1e-9) / gc[c].dk);
+      gc[c].row_half = rh > resolution / 2 ? resolution / 2 + 1 : (int)rh;
     }
     cas->gconst.alloc(count);
     OCN_CUDA(cudaMemcpyAsync(cas->gconst.p, gc.data(), count * sizeof(GridConst),
@@ -881,6 +902,8 @@ int ocn_cascades_create_multi(ocn_ctx* ctx, int resolution, int count, const dou
     cas->d_time.alloc(1);
     cas->scratch.alloc((size_t)cas->group * nn);
     cas->cols_map_ok = cols_map_for(resolution, cas->group, cas->scratch.p, &cas->cols_map);
+    if (cas->cols_map_ok)
+      cols_map_for(resolution, cas->group, cas->scratch.p, &cas->cols_chunk_map, 0, true);
     if (resolution == 1024 && fused_enabled() &&
         cas->group >= kFuseSlots * kFuseW)
       cas->fused_ok = cols_map_for(1024, kFuseSlots * kFuseW, cas->scratch.p, &cas->fused_map,

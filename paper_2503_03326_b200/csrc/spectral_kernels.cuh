@@ -170,6 +170,9 @@ struct RowArgs {
   const float2* src;  // plain mode: [G][N][N] complex input
   float2* scratch;    // [G][N][N]
   const float2* tw;
+  // rows outside a grid's band (GridConst::row_half) are exactly zero: skip
+  // them (set only when the column pass treats them as zero without reading)
+  int skip_zero_rows;
 };
 
 // packed coefficient X + iY of transform `d` at mode (i, j)
@@ -279,6 +282,7 @@ __global__ void __launch_bounds__(Launch<N>::THREADS) k_rows(const RowArgs a) {
 struct ColArgs {
   const float2* scratch;  // [G][N][N]
   const XformDesc* desc;  // split outputs per transform
+  const GridConst* gc;    // band-limited skipping (nullptr: every row is read)
   float2* out_c;          // complex mode: [G][N][N]
   const float2* tw;
   const CUtensorMap* out_maps;  // TMA-store column pass: Re / Im store maps per transform
@@ -350,6 +354,15 @@ __global__ void __launch_bounds__(256, N >= 1024 ? 2 : OCN_ROWS_MINB_SMALL) k_ro
     seg_first = sg.first, seg_count = sg.count, grid = sg.grid;
   }
   const float dkf = PLAIN ? 0.f : (float)a.gc[grid].dk;
+  int row_half = N;  // |row - N/2| < row_half may be nonzero
+  if constexpr (!PLAIN) {
+    if (a.skip_zero_rows) {
+      row_half = a.gc[grid].row_half;
+      if (abs(row0 - N / 2) >= row_half && abs(row0 + rpc - 1 - N / 2) >= row_half &&
+          (row0 - N / 2) * (row0 + rpc - 1 - N / 2) > 0)
+        return;  // every row of this CTA is outside the band (uniform exit)
+    }
+  }
   if constexpr (!PLAIN) {
     const float2* srow =
         (MODE == kRowSurface ? a.spec_h : a.spec_g) + ((size_t)grid * N + row0) * N;
@@ -399,6 +412,7 @@ __global__ void __launch_bounds__(256, N >= 1024 ? 2 : OCN_ROWS_MINB_SMALL) k_ro
     const float3 dcur = dnext;
     if constexpr (!PLAIN)
       if (item + warps < items) dnext = desc_of(item + warps);
+    if (abs(row - N / 2) >= row_half) continue;  // exactly zero: not written, not read
     float2* out = a.scratch + ((size_t)gi * N + (row ^ H)) * N;
     auto store = [&](int k, float2 x) {
       if (valid) out[k] = x;
@@ -563,11 +577,21 @@ int cols_tma_pc(int n) { return n >= 128 && n <= 4096 ? 8192 / n : 0; }
 // planes and one elected thread stores them with two tiled TMA stores (no STG
 // from the warps); the staging is reused once the previous tile's stores have
 // read it (cp.async.bulk.wait_group.read in the refill point).
+// Band-limited grids (GridConst::row_half, a.gc != nullptr): only the scratch
+// rows that can be nonzero are loaded, as 32-row chunks through `src_chunk`;
+// the others are exactly zero (the row pass skipped them) and pass 0 reads
+// them as zero. Scratch row r holds spectrum row r ^ N/2, so the nonzero rows
+// are [0, row_half) and (N - row_half, N).
 template <int N, bool COMPLEX_OUT, int S, bool TMA_STORE = false>
 __global__ void __launch_bounds__(ColTma<N>::THREADS, 1)
-    k_cols_tma(const __grid_constant__ CUtensorMap src, const ColArgs a, int tiles_x, int ntiles) {
+    k_cols_tma(const __grid_constant__ CUtensorMap src, const __grid_constant__ CUtensorMap src_chunk,
+               const ColArgs a, int tiles_x, int ntiles) {
   using CT = ColTma<N>;
   constexpr int PC = CT::PC;
+  constexpr int H = N / 2, CH = 32, NCH = N / CH;  // 32-row chunks
+  auto row_half_of = [&](int xf) {
+    return a.gc ? __ldg(&a.gc[__ldg(&a.desc[xf].cascade)].row_half) : H + 1;
+  };
   extern __shared__ __align__(128) float2 smem[];
   float* sre = reinterpret_cast<float*>(smem + S * CT::STAGE);  // TMA_STORE staging
   float* sim = sre + CT::DENSE;
@@ -576,8 +600,21 @@ __global__ void __launch_bounds__(ColTma<N>::THREADS, 1)
   const int c = threadIdx.x % PC, t = threadIdx.x / PC;
   auto issue = [&](int tile, int s) {
     const int xf = tile / tiles_x, col0 = (tile - xf * tiles_x) * PC;
-    tma::mbar_arrive_expect_tx(bar0 + 8 * s, CT::TILE_BYTES);
-    tma::load_4d(tma::smem_u32(smem + s * CT::STAGE), &src, 2 * col0, 0, 0, xf, bar0 + 8 * s);
+    const int rh = row_half_of(xf);
+    const int lo = (rh + CH - 1) / CH;        // chunks [0, lo) hold rows [0, rh)
+    const int hi = (N - rh + 1) / CH;         // chunks [hi, NCH) hold rows (N - rh, N)
+    if (rh > H || lo >= hi) {
+      tma::mbar_arrive_expect_tx(bar0 + 8 * s, CT::TILE_BYTES);
+      tma::load_4d(tma::smem_u32(smem + s * CT::STAGE), &src, 2 * col0, 0, 0, xf, bar0 + 8 * s);
+    } else {
+      const int nch = lo + (NCH - hi);
+      tma::mbar_arrive_expect_tx(bar0 + 8 * s, (uint32_t)nch * CH * PC * 8);
+      for (int k = 0; k < NCH; ++k) {
+        if (k >= lo && k < hi) continue;
+        tma::load_4d(tma::smem_u32(smem + s * CT::STAGE + k * CH * PC), &src_chunk, 2 * col0, 0, k,
+                     xf, bar0 + 8 * s);
+      }
+    }
   };
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) tma::mbar_init(bar0 + 8 * s, 1);
@@ -608,17 +645,22 @@ __global__ void __launch_bounds__(ColTma<N>::THREADS, 1)
       }
     };
     const float2* dense = buf;
+    const int rh = row_half_of(xf);
+    // pass-0 element i of column `col`: zero outside the band rows
+    auto load_band = [&](int i) {
+      return abs((i ^ H) - H) < rh ? dense[i * PC + c] : make_float2(0.f, 0.f);
+    };
     if constexpr (COMPLEX_OUT) {
       float2* out = a.out_c + (size_t)xf * N * N;
       fft::cta_fft<N, false, true, false, true>(
-          t, buf + c * CT::STRIDE, stw, [&](int i) { return dense[i * PC + c]; },
+          t, buf + c * CT::STRIDE, stw, load_band,
           [&](int r, float2 x) {
             out[(size_t)r * N + col] = x;
           },
           refill);
     } else if constexpr (TMA_STORE) {
       fft::cta_fft<N, false, true, false, true>(
-          t, buf + c * CT::STRIDE, stw, [&](int i) { return dense[i * PC + c]; },
+          t, buf + c * CT::STRIDE, stw, load_band,
           [&](int r, float2 x) {
             sre[r * PC + c] = x.x;  // fft.cpp:93-99 split
             sim[r * PC + c] = x.y;
@@ -635,7 +677,7 @@ __global__ void __launch_bounds__(ColTma<N>::THREADS, 1)
     } else {
       const XformDesc d = a.desc[xf];
       fft::cta_fft<N, false, true, false, true>(
-          t, buf + c * CT::STRIDE, stw, [&](int i) { return dense[i * PC + c]; },
+          t, buf + c * CT::STRIDE, stw, load_band,
           [&](int r, float2 x) {
             __stcs(d.out_re + (size_t)r * N + col, x.x);  // fft.cpp:93-99 split
             if (d.out_im) __stcs(d.out_im + (size_t)r * N + col, x.y);
