@@ -217,19 +217,40 @@ struct NoHook {
 //   TW_SM    : `tw` points to shared memory (plain loads instead of __ldg)
 //   BAR, BAR_THREADS : (!WARP) synchronise on named barrier BAR of BAR_THREADS
 //              threads instead of __syncthreads (warp-specialised kernels)
+//   SPARSE   : (P > 1) with `edge_only` set at run time, only inputs n < T
+//              and n >= N - T (r = 0 and r = E - 1 of every thread) may be
+//              nonzero: pass 0 is then the 2-term DFT x_0 + x_{E-1} w^{-m}
+//              (a band-limited column: rows [0, R) and (N - R, N), R <= T)
 template <int N, bool WARP = false, bool LOAD_SM = false, bool STORE_SM = false, bool TW_SM = false,
-          int BAR = 0, int BAR_THREADS = 0, class Load, class Store, class Free = NoHook>
+          int BAR = 0, int BAR_THREADS = 0, bool SPARSE = false, class Load, class Store,
+          class Free = NoHook>
 __device__ __forceinline__ void cta_fft(int t, float2* sm, const float2* __restrict__ tw,
-                                        Load&& load, Store&& store, Free&& on_free = Free{}) {
+                                        Load&& load, Store&& store, Free&& on_free = Free{},
+                                        bool edge_only = false) {
   using PL = Plan<N>;
   constexpr int E = PL::E, T = PL::T, P = PL::P;
   static_assert(!WARP || T <= 32, "warp-synchronous FFT needs T <= 32");
+  static_assert(!SPARSE || P > 1, "the sparse pass 0 writes the exchange buffer");
   float2 v[E];
+  bool pass0_done = false;
+  if constexpr (SPARSE) {
+    if (edge_only) {
+      const float2 x0 = load(t), xl = load(t + (E - 1) * T);
+      if constexpr (LOAD_SM) fft_sync<WARP, BAR, BAR_THREADS>();
+      static_for<0, E>([&](auto mi) {
+        constexpr int m = decltype(mi)::value;
+        sm[pad32(t * E + m)] = cadd(x0, twiddle_c<E, ((E - 1) * m) % E>(xl));
+      });
+      pass0_done = true;
+    }
+  }
+  if (!pass0_done) {
   // ---- pass 0: radix E, Ns = 1, no twiddles
 #pragma unroll
   for (int r = 0; r < E; ++r) v[r] = load(t + r * T);
   if constexpr (LOAD_SM) fft_sync<WARP, BAR, BAR_THREADS>();
   dft_dif<E>(v);
+  }
   if constexpr (P == 1) {
     if constexpr (STORE_SM && !LOAD_SM) fft_sync<WARP, BAR, BAR_THREADS>();
     static_for<0, E>([&](auto ri) {
@@ -237,10 +258,11 @@ __device__ __forceinline__ void cta_fft(int t, float2* sm, const float2* __restr
       store(r, v[bitrev(r, PL::LOGE)]);
     });
   } else {
-    static_for<0, E>([&](auto ri) {
-      constexpr int r = decltype(ri)::value;
-      sm[pad32(t * E + r)] = v[bitrev(r, PL::LOGE)];
-    });
+    if (!pass0_done)
+      static_for<0, E>([&](auto ri) {
+        constexpr int r = decltype(ri)::value;
+        sm[pad32(t * E + r)] = v[bitrev(r, PL::LOGE)];
+      });
     fft_sync<WARP, BAR, BAR_THREADS>();
     static_for<1, P>([&](auto pi) {
       constexpr int p = decltype(pi)::value;

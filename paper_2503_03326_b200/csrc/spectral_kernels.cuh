@@ -646,26 +646,27 @@ __global__ void __launch_bounds__(ColTma<N>::THREADS, 1)
     };
     const float2* dense = buf;
     const int rh = row_half_of(xf);
+    const bool edge_only = rh <= N / 32;  // band within the first / last T rows
     // pass-0 element i of column `col`: zero outside the band rows
     auto load_band = [&](int i) {
       return abs((i ^ H) - H) < rh ? dense[i * PC + c] : make_float2(0.f, 0.f);
     };
     if constexpr (COMPLEX_OUT) {
       float2* out = a.out_c + (size_t)xf * N * N;
-      fft::cta_fft<N, false, true, false, true>(
+      fft::cta_fft<N, false, true, false, true, 0, 0, true>(
           t, buf + c * CT::STRIDE, stw, load_band,
           [&](int r, float2 x) {
             out[(size_t)r * N + col] = x;
           },
-          refill);
+          refill, edge_only);
     } else if constexpr (TMA_STORE) {
-      fft::cta_fft<N, false, true, false, true>(
+      fft::cta_fft<N, false, true, false, true, 0, 0, true>(
           t, buf + c * CT::STRIDE, stw, load_band,
           [&](int r, float2 x) {
             sre[r * PC + c] = x.x;  // fft.cpp:93-99 split
             sim[r * PC + c] = x.y;
           },
-          refill);
+          refill, edge_only);
       tma::fence_proxy_async_smem();
       __syncthreads();
       if (threadIdx.x == 0) {
@@ -676,13 +677,13 @@ __global__ void __launch_bounds__(ColTma<N>::THREADS, 1)
       }
     } else {
       const XformDesc d = a.desc[xf];
-      fft::cta_fft<N, false, true, false, true>(
+      fft::cta_fft<N, false, true, false, true, 0, 0, true>(
           t, buf + c * CT::STRIDE, stw, load_band,
           [&](int r, float2 x) {
             __stcs(d.out_re + (size_t)r * N + col, x.x);  // fft.cpp:93-99 split
             if (d.out_im) __stcs(d.out_im + (size_t)r * N + col, x.y);
           },
-          refill);
+          refill, edge_only);
     }
     if (++s == S) s = 0, phase ^= 1;
   }
