@@ -84,6 +84,7 @@ struct SpectralPlan {
   std::vector<int> first;  // per cascade: first transform index
   std::vector<int> count;  // per cascade: number of transforms
   bool need_surface = false, need_velocity = false;
+  int zero_transforms = 0;  // velocity transforms dropped as exactly zero (planes zeroed once)
 };
 
 }  // namespace ocn

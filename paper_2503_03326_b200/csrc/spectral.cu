@@ -411,6 +411,40 @@ static SpectralPlan* get_plan(ocn_cascades* cas, ocn_maps* maps, ocn_slices* sli
       }
     }
   }
+  // Depth-attenuated velocity transforms that are exactly zero: every mode of
+  // grid c has |k| >= band_min (others have h0 = 0), so at depth y < 0 the
+  // attenuation 2^(|k| y log2 e) of every mode is at most 2^(band_min y log2 e);
+  // below 2^-132 the row pass's ex2.approx.ftz returns 0 for all of them and
+  // the whole transform is 0. Such transforms are dropped from the step and
+  // their output planes zeroed once here (OCN_NO_DEPTH_SKIP=1 keeps them).
+  // At config 3 this drops 31 of the 48 velocity transforms of the 4 m grid
+  // and 13 of the 16 m grid.
+  {
+    static const bool skip = [] {
+      const char* e = getenv("OCN_NO_DEPTH_SKIP");
+      return !(e && *e && *e != '0');
+    }();
+    auto dead = [&](int c, float y) {
+      const double bmin = cas->band_min[c] * (1.0 - 1e-5);
+      return y < 0.f && bmin * (-(double)y) * 1.4426950408889634 >= 132.0;
+    };
+    std::vector<XformDesc> keep;
+    for (const XformDesc& d : plan->host_desc) {
+      bool zero = false;
+      if (skip && d.kind == kVelXZ) zero = dead(d.cascade, d.y0);
+      else if (skip && d.kind == kVelYPair) zero = dead(d.cascade, d.y0) && dead(d.cascade, d.y1);
+      else if (skip && d.kind == kVelYSingle) zero = dead(d.cascade, d.y0);
+      if (!zero) {
+        keep.push_back(d);
+        continue;
+      }
+      const size_t bytes = (size_t)cas->n * cas->n * sizeof(float);
+      OCN_CUDA(cudaMemsetAsync(d.out_re, 0, bytes, cas->ctx->stream));
+      if (d.out_im) OCN_CUDA(cudaMemsetAsync(d.out_im, 0, bytes, cas->ctx->stream));
+      ++plan->zero_transforms;
+    }
+    plan->host_desc.swap(keep);
+  }
   // (16-byte store boxes: PC >= 4 columns, i.e. N <= 2048)
   if (cas->cols_map_ok && cols_tma_store() && cols_tma_pc(cas->n) >= 4)
     build_out_maps(cas->n, plan->host_desc.data(), (int)plan->host_desc.size(), plan->out_maps);
