@@ -52,6 +52,10 @@ struct XformDesc {
   float y0, y1;   // slice depths for the velocity kinds
   float* out_re;  // fp32 plane [N][N] receiving Re
   float* out_im;  // fp32 plane receiving Im (nullptr: dropped)
+  // spectrum rows i with |i - N/2| >= row_half have an exactly zero
+  // coefficient row: outside the grid's band, or (velocity) attenuated below
+  // fp32 at this depth. <= 0: unknown (every row is transformed).
+  int row_half = 0;
 };
 
 struct SpectralPlan {

@@ -428,8 +428,27 @@ static SpectralPlan* get_plan(ocn_cascades* cas, ocn_maps* maps, ocn_slices* sli
       const double bmin = cas->band_min[c] * (1.0 - 1e-5);
       return y < 0.f && bmin * (-(double)y) * 1.4426950408889634 >= 132.0;
     };
+    // Per-transform row band: the grid's, narrowed at depth y < 0 to the modes
+    // whose attenuation survives fp32: |kx| < 132 / (|y| log2 e) (the pair
+    // transforms take the shallower of their two depths).
+    auto depth_rows = [&](int c, float y) {
+      if (!(y < 0.f)) return cas->n / 2 + 1;
+      const double kmax = 132.0 / ((-(double)y) * 1.4426950408889634) * (1.0 + 1e-5);
+      const double rh = std::ceil(kmax / (2.0 * kPi / cas->lengths[c]));
+      return rh > cas->n / 2 ? cas->n / 2 + 1 : (int)rh;
+    };
     std::vector<XformDesc> keep;
-    for (const XformDesc& d : plan->host_desc) {
+    for (XformDesc d : plan->host_desc) {
+      {
+        const double rg = std::ceil(cas->band_max[d.cascade] * (1.0 + 1e-9) /
+                                    (2.0 * kPi / cas->lengths[d.cascade]));
+        d.row_half = rg > cas->n / 2 ? cas->n / 2 + 1 : (int)rg;  // = GridConst::row_half
+        if (d.kind == kVelXZ || d.kind == kVelYSingle)
+          d.row_half = std::min(d.row_half, depth_rows(d.cascade, d.y0));
+        else if (d.kind == kVelYPair)
+          d.row_half = std::min(d.row_half, std::max(depth_rows(d.cascade, d.y0),
+                                                     depth_rows(d.cascade, d.y1)));
+      }
       bool zero = false;
       if (skip && d.kind == kVelXZ) zero = dead(d.cascade, d.y0);
       else if (skip && d.kind == kVelYPair) zero = dead(d.cascade, d.y0) && dead(d.cascade, d.y1);

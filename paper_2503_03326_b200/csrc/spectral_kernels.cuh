@@ -398,9 +398,10 @@ __global__ void __launch_bounds__(256, N >= 1024 ? 2 : OCN_ROWS_MINB_SMALL) k_ro
   auto desc_of = [&](int item) {
     const int li = (item % slots) * W::TPW + sub;
     const XformDesc* d = a.desc + seg_first + (li < seg_count ? li : 0);
-    return make_float3(__int_as_float(__ldg(&d->kind)), __ldg(&d->y0), __ldg(&d->y1));
+    return make_float4(__int_as_float(__ldg(&d->kind)), __ldg(&d->y0), __ldg(&d->y1),
+                       __int_as_float(__ldg(&d->row_half)));
   };
-  float3 dnext = make_float3(0.f, 0.f, 0.f);
+  float4 dnext = make_float4(0.f, 0.f, 0.f, 0.f);
   if constexpr (!PLAIN) dnext = desc_of(warp < items ? warp : 0);
   for (int item = warp; item < items; item += warps) {
     const int rr = item / slots, slot = item - rr * slots;
@@ -409,10 +410,15 @@ __global__ void __launch_bounds__(256, N >= 1024 ? 2 : OCN_ROWS_MINB_SMALL) k_ro
     const int li = slot * W::TPW + sub;
     const bool valid = li < seg_count;
     const int gi = seg_first + (valid ? li : 0);  // transform index within the group
-    const float3 dcur = dnext;
+    const float4 dcur = dnext;
     if constexpr (!PLAIN)
       if (item + warps < items) dnext = desc_of(item + warps);
     if (abs(row - N / 2) >= row_half) continue;  // exactly zero: not written, not read
+    if constexpr (!PLAIN)
+      if (a.skip_zero_rows) {  // this transform's own band (depth attenuation)
+        const int rt = __float_as_int(dcur.w);
+        if (rt > 0 && abs(row - N / 2) >= rt) continue;
+      }
     float2* out = a.scratch + ((size_t)gi * N + (row ^ H)) * N;
     auto store = [&](int k, float2 x) {
       if (valid) out[k] = x;
@@ -590,7 +596,8 @@ __global__ void __launch_bounds__(ColTma<N>::THREADS, 1)
   constexpr int PC = CT::PC;
   constexpr int H = N / 2, CH = 32, NCH = N / CH;  // 32-row chunks
   auto row_half_of = [&](int xf) {
-    return a.gc ? __ldg(&a.gc[__ldg(&a.desc[xf].cascade)].row_half) : H + 1;
+    const int rh = a.gc ? __ldg(&a.desc[xf].row_half) : 0;
+    return rh > 0 ? rh : H + 1;
   };
   extern __shared__ __align__(128) float2 smem[];
   float* sre = reinterpret_cast<float*>(smem + S * CT::STAGE);  // TMA_STORE staging
