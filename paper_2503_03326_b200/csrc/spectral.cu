@@ -544,12 +544,18 @@ static void enqueue_spectral(ocn_cascades* cas, SpectralPlan* plan, double chopp
   ProfWindow whole(ctx, OCN_PROF_SPECTRAL);
   {
     ProfWindow pw(ctx, OCN_PROF_EVOLVE);  // every grid in one launch
+    // skip never-read rows only where every reader is a band-aware warp row kernel
+    const GridConst* gcs = (n >= 128 && n <= 1024 && !plan->fused && cas->cols_map_ok &&
+                            band_skip_enabled())
+                               ? cas->gconst.p
+                               : nullptr;
     if (plan->need_velocity)
       k_evolve<true><<<grid_for(ctx, nn * cas->count), 256, 0, A>>>(
-          nn * cas->count, cas->d_time.p, cas->h0p.p, cas->omega.p, cas->spec_h.p, cas->spec_g.p);
+          nn * cas->count, cas->d_time.p, cas->h0p.p, cas->omega.p, cas->spec_h.p, cas->spec_g.p,
+          n, gcs);
     else
       k_evolve<false><<<grid_for(ctx, nn * cas->count), 256, 0, A>>>(
-          nn * cas->count, cas->d_time.p, cas->h0p.p, cas->omega.p, cas->spec_h.p, nullptr);
+          nn * cas->count, cas->d_time.p, cas->h0p.p, cas->omega.p, cas->spec_h.p, nullptr, n, gcs);
     OCN_LAUNCHED(ctx);
   }
   if (plan->fused) {

@@ -128,14 +128,22 @@ __global__ void __launch_bounds__(256) k_evolve_tables(int n, int count, const G
 // h~ = h0 e^{iwt} + conj(h0(-k)) e^{-iwt} -> spec_h, and (velocity plans)
 // G = h0 e^{iwt} - conj(h0(-k)) e^{-iwt} -> spec_g (surface.cpp:49-50;
 // velocity.cpp:16-20); the fp64 phase is reduced mod 2 pi before the fp32 sincos.
+// With `gc` (band skipping), only the rows a row pass can read are evolved:
+// |i - N/2| < GridConst::row_half (the others are never staged).
 template <bool WITH_G>
 __global__ void __launch_bounds__(256) k_evolve(size_t total, const double* d_time,
                                                 const float4* __restrict__ h0p,
                                                 const double* __restrict__ omega, float2* spec_h,
-                                                float2* spec_g) {
+                                                float2* spec_g, int n, const GridConst* gc) {
   const double t = *d_time;
+  const size_t nn = (size_t)n * n;
   for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
        idx += (size_t)gridDim.x * blockDim.x) {
+    if (gc) {
+      const int c = (int)(idx / nn);
+      const int i = (int)((idx - (size_t)c * nn) / n);
+      if (abs(i - n / 2) >= __ldg(&gc[c].row_half)) continue;
+    }
     const float4 hp = __ldg(h0p + idx);
     double ph = __ldg(omega + idx) * t;
     ph -= 6.283185307179586476925 * rint(ph * 0.15915494309189533577);
