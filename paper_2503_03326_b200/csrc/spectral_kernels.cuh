@@ -422,10 +422,13 @@ __global__ void __launch_bounds__(256, N >= 1024 ? 2 : OCN_ROWS_MINB_SMALL) k_ro
     if constexpr (!PLAIN)
       if (item + warps < items) dnext = desc_of(item + warps);
     if (abs(row - N / 2) >= row_half) continue;  // exactly zero: not written, not read
+    bool edge_row = false;  // the row's nonzero inputs are j < T and j >= N - T
     if constexpr (!PLAIN)
       if (a.skip_zero_rows) {  // this transform's own band (depth attenuation)
         const int rt = __float_as_int(dcur.w);
         if (rt > 0 && abs(row - N / 2) >= rt) continue;
+        // |kz| < band as well: input j (mode j ^ N/2) is zero unless j < rt or j > N - rt
+        edge_row = rt > 0 && rt <= fft::Plan<N>::T;
       }
     float2* out = a.scratch + ((size_t)gi * N + (row ^ H)) * N;
     auto store = [&](int k, float2 x) {
@@ -457,7 +460,7 @@ __global__ void __launch_bounds__(256, N >= 1024 ? 2 : OCN_ROWS_MINB_SMALL) k_ro
         else if (dkind == kSurfDzDxDzDz) c2 = chop, c6 = chop;    // chop kz (kx + i kz) / k
         else c3 = -1.f, c4 = kx;                                  // -kz + i kx
         const float kx2 = kx * kx;
-        fft::cta_fft<N, true, false, false, true>(
+        fft::cta_fft<N, true, false, false, true, 0, 0, (fft::Plan<N>::P > 1)>(
             t, buf, stw,
             [&](int j) {
               const int jj = j ^ H;
@@ -474,7 +477,7 @@ __global__ void __launch_bounds__(256, N >= 1024 ? 2 : OCN_ROWS_MINB_SMALL) k_ro
               const float mi = fmaf(inv, fmaf(c6 * kz, kz, c5 * (kz + kx2)), c4);
               return make_float2(h.x * mr - h.y * mi, h.x * mi + h.y * mr);
             },
-            store);
+            store, fft::NoHook{}, edge_row);
       } else {
         static_assert(MODE == kRowVelocity, "row mode");
         // velocity: Z (re + i im) with Z = V0 (x/z pair) or W0 (vy pair);
@@ -486,7 +489,7 @@ __global__ void __launch_bounds__(256, N >= 1024 ? 2 : OCN_ROWS_MINB_SMALL) k_ro
         const bool up0 = y0 > 0.f, up1 = y1 > 0.f;
         auto run = [&](auto kind_c) {
           constexpr int KIND = decltype(kind_c)::value;
-          fft::cta_fft<N, true, false, false, true>(
+          fft::cta_fft<N, true, false, false, true, 0, 0, (fft::Plan<N>::P > 1)>(
               t, buf, stw,
               [&](int j) {
                 const int jj = j ^ H;
@@ -504,7 +507,7 @@ __global__ void __launch_bounds__(256, N >= 1024 ? 2 : OCN_ROWS_MINB_SMALL) k_ro
                   return make_float2(-z.y * e0, z.x * e0);
                 }
               },
-              store);
+              store, fft::NoHook{}, edge_row);
         };
         switch (dkind) {
           case kVelXZ: run(std::integral_constant<int, kVelXZ>{}); break;
