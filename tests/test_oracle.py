@@ -201,3 +201,25 @@ def test_port_matches_reference_live(port, ref, n):
     assert a[0] == b[0]
     assert np.array_equal(a[1], b[1])
     assert all(np.array_equal(x, y) for x, y in zip(a[2], b[2]))
+
+
+@pytest.mark.parametrize("n", [256, 1024])
+def test_band_rows_outside_row_half_are_zero(port, n):
+    """The premise of the device's band skipping: for every
+    cascade, spectrum rows and columns with |i - N/2| >= row_half carry no mode
+    of the band, so h0 there is exactly zero in the reference algorithm."""
+    import math
+    from helpers import CONFIG2_CUTOFFS, CONFIG2_LENGTHS, config2_params
+    p = config2_params()
+    for c, L in enumerate(CONFIG2_LENGTHS):
+        bmin = 0.0 if c == 0 else CONFIG2_CUTOFFS[c - 1]
+        bmax = CONFIG2_CUTOFFS[c] if c < len(CONFIG2_CUTOFFS) else 1e300
+        h0, h0cn, band, _ = port.generate_h0(n, L, bmin, bmax, p, c)
+        dk = 2 * math.pi / L
+        rh = math.ceil(bmax * (1 + 1e-9) / dk)
+        if rh > n // 2:
+            continue  # every row may carry the band
+        far = np.abs(np.arange(n) - n // 2) >= rh
+        assert not band[far, :].any() and not band[:, far].any(), c
+        assert np.all(h0[far, :] == 0) and np.all(h0[:, far] == 0), c
+        assert np.all(h0cn[far, :] == 0), c
