@@ -440,6 +440,27 @@ OCN_API int ocn_slab_cols(ocn_slab* s, void* dev_recv);
 /* Column slab of one field: n x R doubles, row-major [i][column - rank R]. */
 OCN_API int ocn_slab_download(ocn_slab* s, int field, double* host_out);
 
+/* ================= composed surface and ABHF heightfields ================== */
+/* Simulation::compose_height (sim.cpp:44-51) in bulk: height_at over the maps
+ * plus FdmZone::sample of each listed zone (pass every body's zone except the
+ * excluded one). xz / out may be host or device pointers. */
+OCN_API int ocn_compose_height(ocn_maps* m, int n_zones, ocn_zone* const* zones, int64_t n,
+                               const double* xz, double* out);
+/* dump_fields' composed grid (main.cpp:62-67): out[i*res + j] =
+ * compose_height(extent*i/res, extent*j/res); points generated on the device. */
+OCN_API int ocn_compose_grid(ocn_maps* m, int n_zones, ocn_zone* const* zones, int resolution,
+                             double extent, double* out);
+/* write_heightfield_file (heightfield_io.hpp:11-16, heightfield_io.cpp:30-45,
+ * 73-78) of one device field, header {N, cascade, time}; OCN_ERR_IO when the
+ * file cannot be written (IoError). */
+OCN_API int ocn_heightfield_write_field(ocn_maps* m, int cascade, int field, float time,
+                                        const char* path);
+/* The composed-surface file of dump_fields (main.cpp:68-75): header
+ * {resolution, -1, time}, samples rounded to fp32 on the device. */
+OCN_API int ocn_heightfield_write_composed(ocn_maps* m, int n_zones, ocn_zone* const* zones,
+                                           int resolution, double extent, float time,
+                                           const char* path);
+
 #ifdef __cplusplus
 }
 #endif

@@ -31,6 +31,7 @@
 #define private public
 #include "ocean/bench.hpp"
 #include "ocean/fft.hpp"
+#include "ocean/heightfield_io.hpp"
 #include "ocean/hydro.hpp"
 #include "ocean/interactive.hpp"
 #include "ocean/mesh.hpp"
@@ -719,5 +720,25 @@ extern "C" int ref_generate_maps_timed(int n, int C, const double* lengths, cons
       (void)m;
     }
     *seconds = (now_s() - t0) / frames;
+  });
+}
+
+// heightfield_io.cpp:73-78, 98-103 (ABHF / CSV writers) on a row-major n x n field.
+extern "C" int ref_write_heightfield(const char* path, int n, int cascade, float time,
+                                     const double* data) {
+  return guard([&] {
+    RealField f(n);
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) f.at(i, j) = data[(size_t)i * n + j];
+    write_heightfield_file(path, {static_cast<uint32_t>(n), cascade, time}, f);
+  });
+}
+
+extern "C" int ref_write_heightfield_csv(const char* path, int n, const double* data) {
+  return guard([&] {
+    RealField f(n);
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) f.at(i, j) = data[(size_t)i * n + j];
+    write_heightfield_csv_file(path, f);
   });
 }

@@ -156,6 +156,10 @@ SIGNATURES = {
     "ocn_slab_rows": (ci, [vp, cd, cd, vp]),
     "ocn_slab_cols": (ci, [vp, vp]),
     "ocn_slab_download": (ci, [vp, ci, d]),
+    "ocn_compose_height": (ci, [vp, ci, pvp, i64, d, d]),
+    "ocn_compose_grid": (ci, [vp, ci, pvp, ci, cd, d]),
+    "ocn_heightfield_write_field": (ci, [vp, ci, ci, C.c_float, C.c_char_p]),
+    "ocn_heightfield_write_composed": (ci, [vp, ci, pvp, ci, cd, C.c_float, C.c_char_p]),
 }
 
 _lib = None

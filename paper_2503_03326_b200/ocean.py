@@ -20,7 +20,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 from . import _abi
-from ._abi import (ArgumentError, ConfigError, DomainError, MeshError, NumericError,  # noqa: F401
+from ._abi import (ArgumentError, ConfigError, DomainError, IoError, MeshError, NumericError,  # noqa: F401
                    OceanCudaError, OceanError, check, lib)
 from ._types import (FdmConfig, Fluid, HydroReport, MaskFrame, MaskParams, Pose, SliceConfig,
                      SpectrumParams, TriangleState, ZoneState)
@@ -735,3 +735,130 @@ def mask_from_hydro(zone: FdmZone, mesh: TriMesh, body_yaw, body_position, body_
     check(lib().ocn_zone_mask_from_hydro(zone.h, mesh.h, body_yaw, float(body_position[0]),
                                          float(body_position[1]), body_speed, C.byref(frame),
                                          C.byref(params)), zone.ctx.h, "mask_from_hydro")
+
+
+# ============== composed surface and ABHF heightfields ==============
+
+_FIELD_FILE_NAMES = ("h", "dx", "dz", "ddx_dx", "ddz_dx", "ddz_dz", "dh_dx", "dh_dz")  # main.cpp:76-77
+
+
+def _zone_array(zones):
+    zones = list(zones or ())
+    arr = (C.c_void_p * max(1, len(zones)))(*[z.h.value for z in zones])
+    return len(zones), C.cast(arr, _abi.pvp), arr
+
+
+def compose_height(maps: SurfaceMaps, xz, zones: Sequence["FdmZone"] = ()) -> np.ndarray:
+    """Simulation::compose_height (sim.cpp:44-51), batched over points (N, 2) -> (N,).
+
+    `zones` are the other bodies' FdmZones (the excluded body's zone left out)."""
+    xz = np.ascontiguousarray(np.atleast_2d(xz), np.float64)
+    out = np.zeros(xz.shape[0])
+    nz, zp, _keep = _zone_array(zones)
+    check(lib().ocn_compose_height(maps.h, nz, zp, xz.shape[0], _dp(xz), _dp(out)), maps.ctx.h,
+          "compose_height")
+    return out
+
+
+def compose_grid(maps: SurfaceMaps, resolution: int, extent: float,
+                 zones: Sequence["FdmZone"] = ()) -> np.ndarray:
+    """The composed grid of dump_fields (main.cpp:62-67): [i][j] = compose_height(extent*i/res,
+    extent*j/res), evaluated on the device -> (res, res) float64."""
+    out = np.zeros((resolution, resolution))
+    nz, zp, _keep = _zone_array(zones)
+    check(lib().ocn_compose_grid(maps.h, nz, zp, int(resolution), float(extent), _dp(out)),
+          maps.ctx.h, "compose_grid")
+    return out
+
+
+def write_field_heightfield(path: str, maps: SurfaceMaps, cascade: int, field: int, t: float):
+    """write_heightfield_file (heightfield_io.cpp:73-78) of one device field, header
+    {N, cascade, float(t)} (main.cpp:80-85)."""
+    check(lib().ocn_heightfield_write_field(maps.h, int(cascade), int(field), float(t),
+                                            str(path).encode()), maps.ctx.h, "write_heightfield")
+
+
+def write_composed_heightfield(path: str, maps: SurfaceMaps, resolution: int, extent: float,
+                               t: float, zones: Sequence["FdmZone"] = ()):
+    """The composed-surface ABHF file of dump_fields (main.cpp:68-75), computed on the device."""
+    nz, zp, _keep = _zone_array(zones)
+    check(lib().ocn_heightfield_write_composed(maps.h, nz, zp, int(resolution), float(extent),
+                                               float(t), str(path).encode()),
+          maps.ctx.h, "write_heightfield")
+
+
+def write_heightfield(path: str, field, resolution: int = None, cascade: int = -1, t: float = 0.0):
+    """write_heightfield_file for a host field (heightfield_io.cpp:30-45, 73-78): "ABHF", u32 N,
+    i32 cascade, f32 time, N*N f32 little-endian row-major. IoError on a header / field size
+    mismatch or an unwritable path, as the reference."""
+    a = np.asarray(field, np.float64)
+    res = a.shape[0] if resolution is None else int(resolution)
+    if a.ndim != 2 or a.shape[0] != a.shape[1] or a.shape[0] != res:
+        raise IoError("heightfield: header resolution does not match field")
+    hdr = (b"ABHF" + np.uint32(res).astype("<u4").tobytes() + np.int32(cascade).astype("<i4").tobytes()
+           + np.float32(t).astype("<f4").tobytes())
+    try:
+        with open(path, "wb") as f:
+            f.write(hdr)
+            f.write(a.astype("<f4").tobytes())
+    except OSError:
+        raise IoError(f"cannot open for writing: {path}") from None
+
+
+def read_heightfield(path: str):
+    """read_heightfield_file (heightfield_io.cpp:47-63, 80-84) -> (field float64 (N, N),
+    {"resolution", "cascade", "time"}). IoError on bad magic, bad resolution or truncation."""
+    try:
+        with open(path, "rb") as f:
+            buf = f.read()
+    except OSError:
+        raise IoError(f"cannot open: {path}") from None
+    if len(buf) < 4 or buf[:4] != b"ABHF":
+        raise IoError("heightfield: bad magic, not an ABHF file")
+    if len(buf) < 16:
+        raise IoError("heightfield: truncated stream")
+    res = int(np.frombuffer(buf, "<u4", 1, 4)[0])
+    cascade = int(np.frombuffer(buf, "<i4", 1, 8)[0])
+    t = float(np.frombuffer(buf, "<f4", 1, 12)[0])
+    if res == 0 or res > 1 << 16:
+        raise IoError("heightfield: bad resolution")
+    if len(buf) < 16 + 4 * res * res:
+        raise IoError("heightfield: truncated stream")
+    data = np.frombuffer(buf, "<f4", res * res, 16).astype(np.float64).reshape(res, res)
+    return data, {"resolution": res, "cascade": cascade, "time": t}
+
+
+def write_heightfield_csv(path: str, field):
+    """write_heightfield_csv_file (heightfield_io.cpp:86-103): one row per grid row, 9 significant
+    digits (ostream precision 9, default float format)."""
+    a = np.asarray(field, np.float64)
+    try:
+        with open(path, "w") as f:
+            for row in a:
+                f.write(",".join(format(float(v), ".9g") for v in row) + "\n")
+    except OSError:
+        raise IoError(f"cannot open for writing: {path}") from None
+
+
+def dump_fields(maps: SurfaceMaps, directory: str, t: float, resolution: int,
+                zones: Sequence["FdmZone"] = (), fmt: str = "abhf"):
+    """dump_fields (main.cpp:59-90): the composed surface over the first cascade's tile plus
+    every cascade field, named as the reference CLI names them. Fields come straight from the
+    device; only the CSV format formats on the host."""
+    import os
+    os.makedirs(directory, exist_ok=True)
+    tb = "%.3f" % t
+    lengths = maps.cascade_set.config.lengths
+    extent = lengths[0]
+    name = os.path.join(directory, f"surface_composed_t{tb}")
+    if fmt == "csv":
+        write_heightfield_csv(name + ".csv", compose_grid(maps, resolution, extent, zones))
+    else:
+        write_composed_heightfield(name + ".abhf", maps, resolution, extent, t, zones)
+    for c in range(len(lengths)):
+        for f in range(8):
+            base = os.path.join(directory, f"cascade{c}_{_FIELD_FILE_NAMES[f]}_t{tb}")
+            if fmt == "csv":
+                write_heightfield_csv(base + ".csv", maps.field(c, f))
+            else:
+                write_field_heightfield(base + ".abhf", maps, c, f, t)

@@ -8,6 +8,7 @@
 #include <sstream>
 #include <string>
 
+#include "ocean/heightfield_io.hpp"
 #include "ocean/hydro.hpp"
 #include "ocean/interactive.hpp"
 #include "ocean/surface.hpp"
@@ -160,6 +161,38 @@ int main(int argc, char** argv) {
   double energy = 0.0;
   for (double x : fld) energy += x * x;
   CHECK(std::isfinite(energy) && energy > 0.0);
+  // ---- heightfields (heightfield_io.hpp) and the composed surface (sim.cpp:44-51)
+  {
+    const std::string hf = out + "/h_dev.abhf", hh = out + "/h_host.abhf";
+    write_heightfield_file(hf, maps, 1, kFieldH, 1.5);
+    write_heightfield_file(hh, {64u, 1, 1.5f}, maps.cascades[1].fields[kFieldH]);
+    std::ifstream a(hf, std::ios::binary), b(hh, std::ios::binary);
+    std::stringstream sa, sb;
+    sa << a.rdbuf();
+    sb << b.rdbuf();
+    CHECK(sa.str().size() == 16 + 4 * 64 * 64 && sa.str() == sb.str());  // device fp32 == host f64->f32
+    HeightfieldHeader hdr;
+    RealField back = read_heightfield_file(hf, &hdr);
+    CHECK(hdr.resolution == 64 && hdr.cascade == 1 && hdr.time == 1.5f);
+    CHECK(back.at(5, 9) == maps.cascades[1].fields[kFieldH].at(5, 9));
+    bool io_threw = false;
+    try {
+      read_heightfield_file(out + "/missing.abhf");
+    } catch (const IoError&) {
+      io_threw = true;
+    }
+    CHECK(io_threw);
+    std::vector<Vec2> pts = {{3.5, 7.25}, {10.0, 2.0}, {-4.0, 30.0}};
+    auto ch = compose_height(maps, {&zone}, pts);
+    for (size_t i = 0; i < pts.size(); ++i)
+      CHECK(std::fabs(ch[i] - (height_at(maps, pts[i]) + zone.sample(pts[i]))) <= 1e-9);
+    write_composed_heightfield_file(out + "/composed.abhf", maps, {&zone}, 32, 1024.0, 1.5);
+    RealField comp = read_heightfield_file(out + "/composed.abhf", &hdr);
+    CHECK(hdr.resolution == 32 && hdr.cascade == -1 && comp.size() == 32);
+    const double want = height_at(maps, Vec2{1024.0 * 3 / 32, 1024.0 * 5 / 32}) +
+                        zone.sample(Vec2{1024.0 * 3 / 32, 1024.0 * 5 / 32});
+    CHECK(std::fabs(comp.at(3, 5) - want) <= 1e-6 * (1.0 + std::fabs(want)));
+  }
   std::printf("cpp api: %d failures (cells %zu, v_w %.6f)\n", failures, cells.size(),
               wave.submerged_volume);
   return failures ? 1 : 0;
