@@ -12,6 +12,7 @@
 #include "ocean/surface.hpp"
 
 struct ocn_slices;
+struct ocn_direct;
 
 namespace ocean {
 
@@ -32,6 +33,24 @@ struct SliceConfig {
 };
 
 std::vector<double> slice_depths(const SliceConfig& config);
+
+// Precomputed time-rotated coefficients for repeated direct evaluations at
+// one instant (velocity.hpp:24-37). The mode list lives on the device
+// (ocn_direct_*); a single-point call is one launch, the batched overload
+// (B200 extension) evaluates every point in one launch.
+class DirectVelocityEvaluator {
+ public:
+  DirectVelocityEvaluator(const CascadeSet& cascades, double t);
+  Vec3 operator()(Vec2 x, double y) const;
+  // B200 extension: points packed (x, z, y) as the batched velocity_at
+  std::vector<Vec3> operator()(const std::vector<Vec3>& xzy) const;
+  long long mode_count() const;                                      // B200 extension
+
+ private:
+  std::shared_ptr<ocn_direct> dev_;
+};
+
+Vec3 velocity_direct(const CascadeSet& cascades, Vec2 x, double y, double t);
 
 namespace detail {
 struct SlicesHandle;

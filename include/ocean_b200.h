@@ -205,6 +205,7 @@ typedef struct ocn_slices ocn_slices;
 typedef struct ocn_mesh ocn_mesh;
 typedef struct ocn_zone ocn_zone;
 typedef struct ocn_slab ocn_slab;
+typedef struct ocn_direct ocn_direct;
 
 /* ================================ context ================================ */
 OCN_API int ocn_abi_version(void);
@@ -460,6 +461,19 @@ OCN_API int ocn_heightfield_write_field(ocn_maps* m, int cascade, int field, flo
 OCN_API int ocn_heightfield_write_composed(ocn_maps* m, int n_zones, ocn_zone* const* zones,
                                            int resolution, double extent, float time,
                                            const char* path);
+
+/* ===================== direct spectral velocity (K11) ====================== */
+/* DirectVelocityEvaluator (velocity.hpp:24-37, velocity.cpp:24-59): the mode
+ * list of the cascade set at time t (every in-band mode with G != 0, in
+ * (cascade, i, j) order, fp64 coefficients), kept on the device. */
+OCN_API int ocn_direct_create(ocn_cascades* c, double t, ocn_direct** out);
+OCN_API int ocn_direct_destroy(ocn_direct* d);
+OCN_API int ocn_direct_modes(const ocn_direct* d, int64_t* count);
+/* operator()(x, y) at n points: xzy = (x, z, y) per point, out = (vx, vy, vz)
+ * per point (host or device pointers). fp64 phases and sums, fp32 sin / cos /
+ * exp of the reduced phase and attenuation (max relative error <= 1e-6 of the
+ * summed magnitude, tests/test_gpu_direct.py). */
+OCN_API int ocn_direct_evaluate(ocn_direct* d, int64_t n, const double* xzy, double* out);
 
 #ifdef __cplusplus
 }

@@ -160,6 +160,10 @@ SIGNATURES = {
     "ocn_compose_grid": (ci, [vp, ci, pvp, ci, cd, d]),
     "ocn_heightfield_write_field": (ci, [vp, ci, ci, C.c_float, C.c_char_p]),
     "ocn_heightfield_write_composed": (ci, [vp, ci, pvp, ci, cd, C.c_float, C.c_char_p]),
+    "ocn_direct_create": (ci, [vp, cd, pvp]),
+    "ocn_direct_destroy": (ci, [vp]),
+    "ocn_direct_modes": (ci, [vp, C.POINTER(C.c_int64)]),
+    "ocn_direct_evaluate": (ci, [vp, i64, d, d]),
 }
 
 _lib = None

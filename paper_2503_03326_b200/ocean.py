@@ -862,3 +862,46 @@ def dump_fields(maps: SurfaceMaps, directory: str, t: float, resolution: int,
                 write_heightfield_csv(base + ".csv", maps.field(c, f))
             else:
                 write_field_heightfield(base + ".abhf", maps, c, f, t)
+
+
+# ===================== direct spectral velocity =====================
+
+class DirectVelocityEvaluator:
+    """velocity.hpp:24-37 — the exact spectral velocity sum at time t, on the device."""
+
+    def __init__(self, cascades: CascadeSet, t: float):
+        self.ctx = cascades.ctx
+        h = C.c_void_p()
+        check(lib().ocn_direct_create(cascades.h, float(t), C.byref(h)), self.ctx.h,
+              "DirectVelocityEvaluator")
+        self.h = h
+        self.time = t
+
+    @property
+    def mode_count(self) -> int:
+        n = C.c_int64()
+        check(lib().ocn_direct_modes(self.h, C.byref(n)), self.ctx.h, "modes")
+        return n.value
+
+    def __call__(self, xz, y) -> np.ndarray:
+        """operator()(x, y) batched: xz (N, 2), y scalar or (N,) -> (N, 3)."""
+        xz = np.atleast_2d(np.asarray(xz, np.float64))
+        xzy = np.ascontiguousarray(np.column_stack([xz, np.broadcast_to(np.asarray(y, np.float64),
+                                                                        (xz.shape[0],))]))
+        out = np.zeros((xzy.shape[0], 3))
+        check(lib().ocn_direct_evaluate(self.h, xzy.shape[0], _dp(xzy), _dp(out)), self.ctx.h,
+              "direct velocity")
+        return out
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().ocn_direct_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+def velocity_direct(cascades: CascadeSet, xz, y, t: float) -> np.ndarray:
+    """velocity_direct (velocity.cpp:61-63), batched."""
+    return DirectVelocityEvaluator(cascades, t)(xz, y)

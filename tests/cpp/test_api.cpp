@@ -193,6 +193,17 @@ int main(int argc, char** argv) {
                         zone.sample(Vec2{1024.0 * 3 / 32, 1024.0 * 5 / 32});
     CHECK(std::fabs(comp.at(3, 5) - want) <= 1e-6 * (1.0 + std::fabs(want)));
   }
+  // ---- DirectVelocityEvaluator (velocity.hpp:24-37) on the device
+  {
+    DirectVelocityEvaluator dv(cs, 1.5);
+    CHECK(dv.mode_count() > 0);
+    Vec3 a = dv(Vec2{3.0, 7.0}, -2.0);
+    auto batch = dv(std::vector<Vec3>{{3.0, 7.0, -2.0}, {10.0, -4.0, 1.0}});
+    CHECK(batch.size() == 2 && std::fabs(batch[0].x - a.x) <= 1e-12 * (1 + std::fabs(a.x)));
+    Vec3 b = velocity_direct(cs, Vec2{3.0, 7.0}, -2.0, 1.5);
+    CHECK(std::fabs(b.y - a.y) <= 1e-12 * (1 + std::fabs(a.y)));
+    dump(out + "/direct.bin", &a.x, 3);
+  }
   std::printf("cpp api: %d failures (cells %zu, v_w %.6f)\n", failures, cells.size(),
               wave.submerged_volume);
   return failures ? 1 : 0;

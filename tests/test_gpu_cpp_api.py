@@ -37,3 +37,6 @@ def test_cpp_api(tmp_path, port):
     v = np.fromfile(tmp_path / "velocity.bin")
     v_ref = port.velocity_at_port(64, CONFIG2_LENGTHS, d_ref, cfg, s_ref, np.array([[3.0, 7.0, -2.0]]))[0]
     assert np.linalg.norm(v - v_ref) <= 1e-4 * np.linalg.norm(v_ref)
+    dv = np.fromfile(tmp_path / "direct.bin")
+    dv_ref = port.direct_velocity(64, CONFIG2_LENGTHS, CONFIG2_CUTOFFS, p, 1.5, np.array([[3.0, 7.0, -2.0]]))[0]
+    assert np.linalg.norm(dv - dv_ref) <= 1e-4 * np.linalg.norm(dv_ref)
