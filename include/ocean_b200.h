@@ -412,6 +412,14 @@ OCN_API int ocn_zone_compute_mask(ocn_zone* z, int n_loops, const int32_t* host_
 OCN_API int ocn_zone_mask_from_hydro(ocn_zone* z, ocn_mesh* mesh, double body_yaw, double body_x,
                              double body_z, double body_speed, const ocn_mask_frame* frame,
                              const ocn_mask_params* params);
+/* As ocn_zone_mask_from_hydro without apply_mask: Simulation::step computes
+ * every body's mask before any is applied (sim.cpp:73-109), since other bodies'
+ * hull depths read this zone. ocn_zone_apply_last_mask applies it (async). */
+OCN_API int ocn_zone_mask_from_hydro_deferred(ocn_zone* z, ocn_mesh* mesh, double body_yaw,
+                                              double body_x, double body_z, double body_speed,
+                                              const ocn_mask_frame* frame,
+                                              const ocn_mask_params* params);
+OCN_API int ocn_zone_apply_last_mask(ocn_zone* z);
 /* Cells of the last mask in row-major order (MaskCell, interactive.hpp:56-59). */
 OCN_API int ocn_zone_mask_download(ocn_zone* z, int capacity, int32_t* host_ij, double* host_h,
                            int* n_cells);

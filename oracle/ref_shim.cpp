@@ -36,6 +36,7 @@
 #include "ocean/interactive.hpp"
 #include "ocean/mesh.hpp"
 #include "ocean/parallel.hpp"
+#include "ocean/rigid_body.hpp"
 #include "ocean/rng.hpp"
 #include "ocean/spectra.hpp"
 #include "ocean/surface.hpp"
@@ -740,5 +741,112 @@ extern "C" int ref_write_heightfield_csv(const char* path, int n, const double* 
     for (int i = 0; i < n; ++i)
       for (int j = 0; j < n; ++j) f.at(i, j) = data[(size_t)i * n + j];
     write_heightfield_csv_file(path, f);
+  });
+}
+
+// Simulation (sim.cpp:16-131) for nb bodies sharing one hull, driven through
+// the reference library's own pieces (the Scenario loader is not built). Per
+// body b: cfg[b*8 + 0..7] = position xyz, yaw, initial velocity xyz, density.
+// Bodies use cd_water = cd_air = 1, no thrust, MaskParams{}, polyhedral
+// inertia. out_pose[(step*nb + b)*13 + ..] = position, orientation (w x y z),
+// linear velocity, angular velocity after each step; out_vw[step*nb + b] =
+// the submerged volume of that step's report.
+extern "C" int ref_sim_run(int n, int C, const double* lengths, const double* cutoffs,
+                           const ocn_spectrum_params* p, const ocn_slice_config* sc, int nv,
+                           const double* verts, int nt, const int32_t* tris, int nb,
+                           const double* cfg, const ocn_fdm_config* fc, double angular_damping,
+                           const double* wind, double dt, int steps, double* out_pose,
+                           double* out_vw) {
+  return guard([&] {
+    CascadeSet cascades(to_cascades(n, C, lengths, cutoffs), to_params(p));
+    SliceConfig slc = to_slices(sc);
+    FdmConfig f;
+    f.grid_size = fc->grid_size;
+    f.margin = fc->margin;
+    f.delta_min = fc->delta_min;
+    f.delta_max = fc->delta_max;
+    f.delta_rate_limit = fc->delta_rate_limit;
+    f.damping = {fc->d0, fc->d_max, fc->v_max};
+    struct B {
+      TriMesh mesh;
+      RigidBody rigid;
+      FdmZone zone;
+      HydroReport report;
+      std::vector<MaskCell> mask;
+    };
+    std::vector<std::unique_ptr<B>> bodies;
+    SurfaceMaps maps = generate_maps(cascades, 0.0, {});
+    VelocitySlices slices = build_slices(cascades, 0.0, slc);
+    for (int b = 0; b < nb; ++b) {
+      const double* c = cfg + 8 * b;
+      TriMesh mesh = mesh_from(nv, verts, nt, tris);
+      BodyPose pose;
+      pose.orientation = Quat::yaw(c[3]);
+      pose.com_body = mesh.centroid();
+      pose.position = Vec3{c[0], c[1], c[2]} + pose.orientation.rotate(mesh.centroid());
+      pose.linear_velocity = {c[4], c[5], c[6]};
+      RigidBody rigid = RigidBody::from_mesh(mesh, c[7], pose, false);
+      Vec3 ext = mesh.bbox_max() - mesh.bbox_min();
+      FdmZone zone(f, std::max(ext.x, ext.z), pose.position.xz(), dt);
+      bodies.push_back(std::unique_ptr<B>(new B{std::move(mesh), std::move(rigid), std::move(zone), {}, {}}));
+    }
+    const Vec3 w{wind[0], wind[1], wind[2]};
+    double time = 0.0;
+    for (int s = 0; s < steps; ++s) {
+      const double t_next = time + dt;
+      maps = generate_maps(cascades, t_next, {});
+      slices = build_slices(cascades, t_next, slc);
+      for (int i = 0; i < nb; ++i) {
+        B& body = *bodies[i];
+        FluidQuery fluid;
+        fluid.surface_height = [&, i](Vec2 x) {
+          double h = height_at(maps, x);
+          for (int k = 0; k < nb; ++k)
+            if (k != i) h += bodies[k]->zone.sample(x);
+          return h;
+        };
+        fluid.water_velocity = [&](Vec2 x, double y) {
+          return velocity_at(slices, x, std::clamp(y, slices.y_min(), slices.y_max()),
+                             DepthInterp::Exponential);
+        };
+        fluid.wind = w;
+        body.report = aggregate(body.mesh, body.rigid.pose(), fluid, {1.0, 1.0});
+        double speed = body.rigid.pose().linear_velocity.norm();
+        body.zone.update_stability(speed, dt);
+        Vec3 ext = body.mesh.bbox_max() - body.mesh.bbox_min();
+        MaskFrame frame;
+        frame.center_x = 0.0;
+        frame.half_beam = ext.x;
+        frame.z_min = body.mesh.bbox_min().z;
+        frame.z_max = body.mesh.bbox_max().z;
+        frame.mesh_height = body.mesh.height();
+        frame.volume_ratio = body.mesh.volume() > 0.0 ? body.report.submerged_volume / body.mesh.volume() : 0.0;
+        body.mask = compute_mask(body.zone, body.report.waterline, body.rigid.pose().yaw(),
+                                 body.rigid.pose().position.xz(), speed, frame, {});
+      }
+      for (auto& bp : bodies) {
+        bp->zone.apply_mask(bp->mask);
+        bp->zone.step(dt, bp->rigid.pose().position.xz());
+      }
+      for (int i = 0; i < nb; ++i) {
+        B& body = *bodies[i];
+        const HydroReport& r = body.report;
+        if (r.center_of_immersion) {
+          body.rigid.apply_force_at(r.buoyancy_force, r.water_center);
+          body.rigid.apply_force_at(r.water_drag, r.water_center);
+        }
+        body.rigid.apply_force_at(r.air_drag, r.air_center);
+        body.rigid.integrate({0.0, -p->gravity, 0.0}, dt, angular_damping);
+        const BodyPose& q = body.rigid.pose();
+        double* o = out_pose + ((size_t)s * nb + i) * 13;
+        const double v[13] = {q.position.x, q.position.y, q.position.z, q.orientation.w,
+                              q.orientation.x, q.orientation.y, q.orientation.z,
+                              q.linear_velocity.x, q.linear_velocity.y, q.linear_velocity.z,
+                              q.angular_velocity.x, q.angular_velocity.y, q.angular_velocity.z};
+        std::memcpy(o, v, sizeof v);
+        out_vw[(size_t)s * nb + i] = r.submerged_volume;
+      }
+      time = t_next;
+    }
   });
 }

@@ -160,6 +160,8 @@ SIGNATURES = {
     "ocn_compose_grid": (ci, [vp, ci, pvp, ci, cd, d]),
     "ocn_heightfield_write_field": (ci, [vp, ci, ci, C.c_float, C.c_char_p]),
     "ocn_heightfield_write_composed": (ci, [vp, ci, pvp, ci, cd, C.c_float, C.c_char_p]),
+    "ocn_zone_mask_from_hydro_deferred": (ci, [vp, vp, cd, cd, cd, cd, C.POINTER(MaskFrame), C.POINTER(MaskParams)]),
+    "ocn_zone_apply_last_mask": (ci, [vp]),
     "ocn_direct_create": (ci, [vp, cd, pvp]),
     "ocn_direct_destroy": (ci, [vp]),
     "ocn_direct_modes": (ci, [vp, C.POINTER(C.c_int64)]),

@@ -97,6 +97,24 @@ __global__ void k_apply_cells(int n, int m, int count, const int* ij, const doub
   }
 }
 
+// apply_mask (interactive.cpp:113-118) of the cell set the last mask pass
+// left on the device (box [i0, i1) x [j0, j1), flags, heights).
+__global__ void k_apply_box(const int* box, const unsigned char* mask_f, const double* mask_h,
+                            size_t cap, int n, int m, float* curr) {
+  const int i0 = box[0], i1 = box[1], j0 = box[2], j1 = box[3];
+  if (box[4] <= 0 || i1 <= i0 || j1 <= j0) return;
+  const int bw = j1 - j0;
+  size_t cells = (size_t)(i1 - i0) * bw;
+  if (cells > cap) cells = cap;
+  for (size_t c = blockIdx.x * (size_t)blockDim.x + threadIdx.x; c < cells;
+       c += (size_t)gridDim.x * blockDim.x) {
+    if (!mask_f[c]) continue;
+    const int i = i0 + (int)(c / bw), j = j0 + (int)(c % bw);
+    if (i < m || j < m || i >= n - m || j >= n - m) continue;
+    curr[(size_t)i * n + j] = (float)mask_h[c];
+  }
+}
+
 __global__ void k_zone_sample(ZoneView z, int64_t count, const double* xz, double* out) {
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < count;
        q += (int64_t)gridDim.x * blockDim.x)
@@ -617,6 +635,34 @@ int ocn_zone_mask_from_hydro(ocn_zone* z, ocn_mesh* mesh, double yaw, double bx,
     A.mesh_volume = mesh->volume;
     mask_launch(z, A, mesh->loop_counts.p, 0, mesh->loop_off.p, mesh->loop_points.p,
                 2 * mesh->nt + 2, 1);
+  });
+}
+
+int ocn_zone_mask_from_hydro_deferred(ocn_zone* z, ocn_mesh* mesh, double yaw, double bx, double bz,
+                                      double speed, const ocn_mask_frame* frame,
+                                      const ocn_mask_params* params) {
+  return api_call(z ? z->ctx : nullptr, [&] {
+    OCN_REQUIRE(z && mesh && frame && params, "bad arguments");
+    OCN_REQUIRE(mesh->evaluated, "mesh has no hydro evaluation");
+    OCN_REQUIRE(mesh->ctx == z->ctx, "mesh and zone use different contexts");
+    check_mask_frame(frame);
+    DeviceScope ds(z->ctx);
+    MaskArgs A = mask_args(z, yaw, bx, bz, speed, frame, params);
+    A.vw = &mesh->report.p->r.submerged_volume;
+    A.mesh_volume = mesh->volume;
+    mask_launch(z, A, mesh->loop_counts.p, 0, mesh->loop_off.p, mesh->loop_points.p,
+                2 * mesh->nt + 2, 0);
+  });
+}
+
+int ocn_zone_apply_last_mask(ocn_zone* z) {
+  return api_call(z ? z->ctx : nullptr, [&] {
+    OCN_REQUIRE(z, "null zone");
+    ocn_ctx* ctx = z->ctx;
+    DeviceScope ds(ctx);
+    k_apply_box<<<ctx->sm_count * 2, 256, 0, ctx->stream>>>(z->mask_box.p, z->mask_f.p, z->mask_h.p,
+                                                           z->mask_f.n, z->n, z->margin, z->curr());
+    OCN_LAUNCHED(ctx);
   });
 }
 

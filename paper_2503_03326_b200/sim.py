@@ -1,0 +1,258 @@
+"""Simulation::step over the device hot path (sim.cpp:16-131).
+
+The caller of the per-frame path: surface maps and velocity slices from one
+spectral step, then per body the hull forces against the composed surface
+(height_at plus every OTHER body's FDM zone, sim.cpp:44-51), the stability
+update and the wake mask, then all masks applied and every zone stepped, then
+the rigid-body integration. Every field-sized stage runs on the device
+(ocn_spectral_step, ocn_hydro_aggregate with the zone list,
+ocn_zone_mask_from_hydro_deferred / ocn_zone_apply_last_mask, ocn_zone_step);
+the rigid body (13 doubles per body, rigid_body.cpp:6-61) is host scalar code,
+as in the reference. Only the hydro report (forces, centres, volume) crosses
+to the host per body and step.
+
+Ordering matches sim.cpp exactly: body i's aggregate sees the zones of bodies
+< i after their update_stability (the spacing changes immediately) but before
+any mask is applied, so masks are computed deferred and applied after every
+body's aggregate (sim.cpp:73-109).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import ocean as oc
+from ._abi import DomainError, NumericError, check, lib
+from ._types import FdmConfig, MaskFrame, MaskParams, Pose, SliceConfig, SpectrumParams
+
+import ctypes as C
+
+
+# ---------------------------------------------------------------- quaternions (core.hpp:142-186)
+def quat_axis_angle(axis, angle):
+    n = math.sqrt(axis[0] ** 2 + axis[1] ** 2 + axis[2] ** 2)
+    if n < 1e-300:
+        return np.array([1.0, 0.0, 0.0, 0.0])
+    h = 0.5 * angle
+    s = math.sin(h) / n
+    return np.array([math.cos(h), axis[0] * s, axis[1] * s, axis[2] * s])
+
+
+def quat_mul(a, b):
+    w, x, y, z = a
+    ow, ox, oy, oz = b
+    return np.array([w * ow - x * ox - y * oy - z * oz, w * ox + x * ow + y * oz - z * oy,
+                     w * oy - x * oz + y * ow + z * ox, w * oz + x * oy - y * ox + z * ow])
+
+
+def quat_normalized(q):
+    return q / math.sqrt(float(q @ q))
+
+
+def quat_rotate(q, v):
+    u = q[1:]
+    t = np.cross(u, v) * 2.0
+    return v + t * q[0] + np.cross(u, t)
+
+
+def quat_matrix(q):
+    w, x, y, z = q
+    return np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)],
+                     [2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)],
+                     [2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)]])
+
+
+def pose_yaw(q):
+    """BodyPose::yaw, hydro.hpp:31-34."""
+    bow = quat_rotate(q, np.array([0.0, 0.0, 1.0]))
+    return math.atan2(bow[0], bow[2])
+
+
+# ---------------------------------------------------------------- rigid body (rigid_body.cpp)
+class RigidBody:
+    """rigid_body.cpp:6-61: mass, body inertia, pose, angular momentum, force / torque accumulators."""
+
+    def __init__(self, mass, inertia_body, position, orientation, linear_velocity, angular_velocity,
+                 com_body):
+        if not mass > 0.0:
+            raise oc.ConfigError("rigid body mass must be > 0")
+        self.mass = float(mass)
+        self.inertia_body = np.asarray(inertia_body, np.float64)
+        self.inertia_body_inv = np.linalg.inv(self.inertia_body)
+        self.position = np.asarray(position, np.float64)
+        self.orientation = quat_normalized(np.asarray(orientation, np.float64))
+        self.linear_velocity = np.asarray(linear_velocity, np.float64)
+        self.angular_velocity = np.asarray(angular_velocity, np.float64)
+        self.com_body = np.asarray(com_body, np.float64)
+        r = quat_matrix(self.orientation)
+        self.angular_momentum = (r @ self.inertia_body @ r.T) @ self.angular_velocity
+        self.force = np.zeros(3)
+        self.torque = np.zeros(3)
+
+    @classmethod
+    def from_mesh(cls, mesh: "oc.TriMesh", density, position, orientation, linear_velocity,
+                  box_inertia=False):
+        """RigidBody::from_mesh, rigid_body.cpp:16-34."""
+        mass = density * mesh.volume
+        if box_inertia:
+            s = mesh.bbox_max - mesh.bbox_min
+            inertia = np.diag([mass / 12.0 * (s[1] ** 2 + s[2] ** 2), mass / 12.0 * (s[0] ** 2 + s[2] ** 2),
+                               mass / 12.0 * (s[0] ** 2 + s[1] ** 2)])
+        else:
+            inertia = mesh.unit_inertia * density
+        return cls(mass, inertia, position, orientation, linear_velocity, np.zeros(3), mesh.centroid)
+
+    def pose(self) -> Pose:
+        return Pose.make(position=tuple(self.position), orientation=tuple(self.orientation),
+                         linear_velocity=tuple(self.linear_velocity),
+                         angular_velocity=tuple(self.angular_velocity), com_body=tuple(self.com_body))
+
+    def apply_force(self, f):
+        self.force = self.force + f
+
+    def apply_force_at(self, f, world_point):
+        """rigid_body.cpp:36-39."""
+        self.force = self.force + f
+        self.torque = self.torque + np.cross(np.asarray(world_point) - self.position, f)
+
+    def integrate(self, gravity, dt, angular_damping):
+        """Semi-implicit Euler, rigid_body.cpp:41-61."""
+        if not dt > 0.0:
+            raise DomainError("integrate: dt must be > 0")
+        self.linear_velocity = self.linear_velocity + (self.force / self.mass + gravity) * dt
+        self.angular_momentum = self.angular_momentum + self.torque * dt
+        if angular_damping > 0.0:
+            self.angular_momentum = self.angular_momentum * (1.0 - angular_damping * dt)
+        r = quat_matrix(self.orientation)
+        self.angular_velocity = (r @ self.inertia_body_inv @ r.T) @ self.angular_momentum
+        self.position = self.position + self.linear_velocity * dt
+        w = float(np.linalg.norm(self.angular_velocity))
+        if w > 1e-300:
+            dq = quat_axis_angle(self.angular_velocity / w, w * dt)
+            self.orientation = quat_normalized(quat_mul(dq, self.orientation))
+        self.force = np.zeros(3)
+        self.torque = np.zeros(3)
+
+
+# ---------------------------------------------------------------- scene
+@dataclass
+class BodyConfig:
+    """The per-body part of the scenario (scenario.hpp BodyConfig) this path uses."""
+    vertices: np.ndarray
+    triangles: np.ndarray
+    position: Sequence[float] = (0.0, 0.0, 0.0)
+    yaw: float = 0.0
+    initial_velocity: Sequence[float] = (0.0, 0.0, 0.0)
+    density: float = 500.0
+    cd_water: float = 1.0
+    cd_air: float = 1.0
+    angular_damping: float = 0.0
+    box_inertia: bool = False
+    fdm: FdmConfig = field(default_factory=lambda: FdmConfig.make())
+    mask: MaskParams = field(default_factory=lambda: MaskParams.make())
+    thrust: Sequence = ()  # [(until, (fx, fy, fz))], body-frame force (sim.cpp:53-57)
+
+
+class _Body:
+    def __init__(self, cfg: BodyConfig, dt: float, ctx):
+        self.config = cfg
+        self.mesh = oc.TriMesh(cfg.vertices, cfg.triangles, ctx=ctx)
+        q = quat_axis_angle((0.0, 1.0, 0.0), cfg.yaw)
+        pos = np.asarray(cfg.position, np.float64) + quat_rotate(q, self.mesh.centroid)
+        self.rigid = RigidBody.from_mesh(self.mesh, cfg.density, pos, q, cfg.initial_velocity,
+                                         cfg.box_inertia)
+        ext = self.mesh.bbox_max - self.mesh.bbox_min
+        self.zone = oc.FdmZone(cfg.fdm, max(ext[0], ext[2]), (pos[0], pos[2]), dt, ctx=ctx)
+        self.report: Optional[oc.HydroResult] = None
+
+
+class Simulation:
+    """sim.cpp:16-131 over the device path. Spectrum, cascades and slice config as
+    CascadeSet / SliceConfig; gravity from the spectrum parameters."""
+
+    def __init__(self, cascade_config: "oc.CascadeConfig", spectrum: SpectrumParams,
+                 slices: SliceConfig, bodies: Sequence[BodyConfig], dt: float = 1.0 / 60.0,
+                 wind=(0.0, 0.0, 0.0), choppiness: float = 1.0, rebuild_stride: int = 1,
+                 ctx=None):
+        if not dt > 0.0:
+            raise oc.ConfigError("dt must be > 0")
+        self.ctx = ctx or oc.Context.default()
+        self.dt = dt
+        self.wind = tuple(float(w) for w in wind)
+        self.choppiness = choppiness
+        self.rebuild_stride = max(1, int(rebuild_stride))
+        self.gravity = spectrum.gravity
+        self.cascades = oc.CascadeSet(cascade_config, spectrum, ctx=self.ctx)
+        self.maps = oc.SurfaceMaps(self.cascades)
+        self.slices = oc.VelocitySlices(self.cascades, slices)
+        oc.spectral_step(self.maps, self.slices, 0.0, choppiness)  # sim.cpp:18-20
+        self.bodies: List[_Body] = [_Body(b, dt, self.ctx) for b in bodies]
+        self.time = 0.0
+        self.step_index = 0
+
+    def compose_height(self, xz, exclude_body: int = -1):
+        """sim.cpp:44-51, batched on the device."""
+        zones = [b.zone for i, b in enumerate(self.bodies) if i != exclude_body]
+        return oc.compose_height(self.maps, xz, zones)
+
+    def thrust_force(self, body: _Body):
+        for until, f in body.config.thrust:
+            if self.time < until:
+                return quat_rotate(body.rigid.orientation, np.asarray(f, np.float64))
+        return np.zeros(3)
+
+    def step(self):
+        """sim.cpp:59-124."""
+        dt = self.dt
+        t_next = self.time + dt
+        if self.step_index % self.rebuild_stride == 0:
+            oc.spectral_step(self.maps, self.slices, t_next, self.choppiness)
+        else:
+            oc.spectral_step(self.maps, None, t_next, self.choppiness)
+        L = lib()
+        for i, body in enumerate(self.bodies):
+            others = [b.zone for k, b in enumerate(self.bodies) if k != i]
+            fluid = oc.FluidQuery(maps=self.maps, slices=self.slices, zones=others, wind=self.wind)
+            pose = body.rigid.pose()
+            body.report = oc.aggregate(body.mesh, pose, fluid,
+                                       oc.DragCoefficients(body.config.cd_water, body.config.cd_air))
+            speed = float(np.linalg.norm(body.rigid.linear_velocity))
+            body.zone.update_stability(speed, dt)
+            m = body.mesh
+            frame = MaskFrame.make(half_beam=float(m.bbox_max[0] - m.bbox_min[0]),
+                                   z_min=float(m.bbox_min[2]), z_max=float(m.bbox_max[2]),
+                                   mesh_height=m.height())
+            check(L.ocn_zone_mask_from_hydro_deferred(body.zone.h, m.h, pose_yaw(body.rigid.orientation),
+                                                      float(body.rigid.position[0]),
+                                                      float(body.rigid.position[2]), speed,
+                                                      C.byref(frame), C.byref(body.config.mask)),
+                  self.ctx.h, "mask")
+        for body in self.bodies:
+            check(L.ocn_zone_apply_last_mask(body.zone.h), self.ctx.h, "apply_mask")
+            body.zone.step(dt, (body.rigid.position[0], body.rigid.position[2]))
+        for body in self.bodies:
+            r = body.report
+            if r.center_of_immersion is not None:
+                body.rigid.apply_force_at(r.buoyancy_force, r.water_center)
+                body.rigid.apply_force_at(r.water_drag, r.water_center)
+            body.rigid.apply_force_at(r.air_drag, r.air_center)
+            body.rigid.apply_force(self.thrust_force(body))
+            body.rigid.integrate(np.array([0.0, -self.gravity, 0.0]), dt, body.config.angular_damping)
+        self.time = t_next
+        self.step_index += 1
+        self.check_finite()
+
+    def check_finite(self):
+        """sim.cpp:126-135."""
+        for i, b in enumerate(self.bodies):
+            probe = float(b.rigid.position.sum() + b.rigid.linear_velocity.sum())
+            if not math.isfinite(probe):
+                raise NumericError(f"non-finite body state (body {i}, step {self.step_index})")
+
+    def poses(self) -> np.ndarray:
+        """(bodies, 13): position, orientation (w x y z), linear, angular velocity."""
+        return np.array([np.concatenate([b.rigid.position, b.rigid.orientation, b.rigid.linear_velocity,
+                                         b.rigid.angular_velocity]) for b in self.bodies])
