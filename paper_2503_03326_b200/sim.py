@@ -9,7 +9,8 @@ the rigid-body integration. Every field-sized stage runs on the device
 ocn_zone_mask_from_hydro_deferred / ocn_zone_apply_last_mask, ocn_zone_step);
 the rigid body (13 doubles per body, rigid_body.cpp:6-61) is host scalar code,
 as in the reference. Only the hydro report (forces, centres, volume) crosses
-to the host per body and step.
+to the host per body and step, read after every body's device stages are
+enqueued (one stream synchronisation per step).
 
 Ordering matches sim.cpp exactly: body i's aggregate sees the zones of bodies
 < i after their update_stability (the spacing changes immediately) but before
@@ -26,7 +27,7 @@ import numpy as np
 
 from . import ocean as oc
 from ._abi import DomainError, NumericError, check, lib
-from ._types import FdmConfig, MaskFrame, MaskParams, Pose, SliceConfig, SpectrumParams
+from ._types import FdmConfig, HydroReport, MaskFrame, MaskParams, Pose, SliceConfig, SpectrumParams
 
 import ctypes as C
 
@@ -217,8 +218,9 @@ class Simulation:
             others = [b.zone for k, b in enumerate(self.bodies) if k != i]
             fluid = oc.FluidQuery(maps=self.maps, slices=self.slices, zones=others, wind=self.wind)
             pose = body.rigid.pose()
-            body.report = oc.aggregate(body.mesh, pose, fluid,
-                                       oc.DragCoefficients(body.config.cd_water, body.config.cd_air))
+            # enqueued only: the report is read once after every body's stages (below)
+            oc.aggregate(body.mesh, pose, fluid,
+                         oc.DragCoefficients(body.config.cd_water, body.config.cd_air), sync=False)
             speed = float(np.linalg.norm(body.rigid.linear_velocity))
             body.zone.update_stability(speed, dt)
             m = body.mesh
@@ -234,7 +236,9 @@ class Simulation:
             check(L.ocn_zone_apply_last_mask(body.zone.h), self.ctx.h, "apply_mask")
             body.zone.step(dt, (body.rigid.position[0], body.rigid.position[2]))
         for body in self.bodies:
-            r = body.report
+            rep = HydroReport()
+            check(L.ocn_hydro_report_get(body.mesh.h, C.byref(rep)), self.ctx.h, "report")
+            body.report = r = oc.HydroResult(body.mesh, rep)
             if r.center_of_immersion is not None:
                 body.rigid.apply_force_at(r.buoyancy_force, r.water_center)
                 body.rigid.apply_force_at(r.water_drag, r.water_center)
