@@ -11,9 +11,9 @@
 //
 // Evaluation: points × modes, one thread per point, modes streamed through
 // shared memory in tiles (every warp reads the same mode: broadcast). The
-// phase kx x + kz z is fp64 and reduced mod 2π in fp64; cos / sin of the
-// reduced phase and the e^{ky} attenuation are fp32 SFU ops; the sums are
-// fp64. When there are too few points to fill the GPU, the mode list is split
+// phase kx x + kz z is fp64 (in turns) and reduced to [-1/2, 1/2] in fp64;
+// cos / sin of the reduced phase and the e^{ky} attenuation are fp32 SFU ops;
+// the sums are fp64. When there are too few points to fill the GPU, the mode list is split
 // into chunks whose partial sums are added in chunk order by a second kernel
 // (deterministic for a given device).
 #include <vector>
@@ -115,44 +115,57 @@ __global__ void k_direct_emit(const GridConst* gc, int n, int C, const double2* 
 }
 
 // Sum over modes [m0, m1) at each point; out[p*3 + comp] (+ chunk offset).
+// Staging converts each mode once per CTA into the form the inner loop wants:
+// wave numbers in turns (kx / 2π, fp64) so the phase reduction is one rint,
+// and k log2 e as fp32 for the attenuation. Per mode-point the inner loop is
+// then phase (DMUL + DFMA), reduction (rint + DADD), fp32 sin / cos / ex2 with
+// the attenuation folded into sin and cos, and 6 DFMA accumulations.
 __global__ void __launch_bounds__(kEvalThreads) k_direct_eval(const double* __restrict__ m,
                                                               int64_t stride, int64_t modes,
                                                               int64_t chunk, int64_t n,
                                                               const double* __restrict__ xzy,
                                                               double* __restrict__ out) {
-  __shared__ double sm_m[kModeFields][kTile];
+  __shared__ double s_kt[2][kTile];  // kx / 2π, kz / 2π
+  __shared__ double s_c[6][kTile];   // cx, cy, cz (re, im)
+  __shared__ float s_kl[kTile];      // k log2 e
   const int64_t p = blockIdx.x * (int64_t)kEvalThreads + threadIdx.x;
   const int64_t m0 = blockIdx.y * chunk;
   const int64_t m1 = min(modes, m0 + chunk);
   double x = 0.0, z = 0.0, y = 0.0;
   if (p < n) x = xzy[3 * p], z = xzy[3 * p + 1], y = xzy[3 * p + 2];
+  // attenuation (velocity.cpp:10): e^{ky} = 2^{(k log2e) y} below, 1 + ky = 1 + (k log2e)(y ln 2) above
   const bool above = y > 0.0;
-  const float ylog2e = (float)(y * 1.4426950408889634);
+  const float ya = above ? (float)(y * 0.6931471805599453) : (float)y;
   double vx = 0.0, vy = 0.0, vz = 0.0;
-  constexpr double kTwoPi = 6.283185307179586;
   constexpr double kInvTwoPi = 0.15915494309189535;
-  constexpr double kTwoPiLo = 2.4492935982947064e-16;  // 2π − fl(2π)
+  constexpr float kTwoPiF = 6.28318530717958648f;
   for (int64_t t0 = m0; t0 < m1; t0 += kTile) {
     const int cnt = (int)min((int64_t)kTile, m1 - t0);
     __syncthreads();
-    for (int q = threadIdx.x; q < kModeFields * kTile; q += kEvalThreads) {
+    for (int e = threadIdx.x; e < cnt; e += kEvalThreads) {
+      const int64_t q = t0 + e;
+      s_kt[0][e] = m[q] * kInvTwoPi;
+      s_kt[1][e] = m[stride + q] * kInvTwoPi;
+      s_kl[e] = (float)(m[2 * stride + q] * 1.4426950408889634);
+    }
+    for (int q = threadIdx.x; q < 6 * kTile; q += kEvalThreads) {
       const int f = q / kTile, e = q % kTile;
-      if (e < cnt) sm_m[f][e] = m[f * stride + t0 + e];
+      if (e < cnt) s_c[f][e] = m[(3 + f) * stride + t0 + e];
     }
     __syncthreads();
-#pragma unroll 2
+#pragma unroll 4
     for (int e = 0; e < cnt; ++e) {
-      const double kx = sm_m[0][e], kz = sm_m[1][e], k = sm_m[2][e];
-      const double ph = fma(kx, x, kz * z);
-      const double r = rint(ph * kInvTwoPi);
-      const double red = fma(-r, kTwoPiLo, fma(-r, kTwoPi, ph));  // |red| <= π (+ulp)
+      const double u = fma(s_kt[0][e], x, s_kt[1][e] * z);  // phase in turns
+      const float r = (float)(u - rint(u));                 // |r| <= 1/2
       float sf, cf;
-      __sincosf((float)red, &sf, &cf);
-      const double s = sf, c = cf;
-      const double att = above ? fma(k, y, 1.0) : (double)exp2f((float)k * ylog2e);
-      vx = fma(att, fma(sm_m[3][e], c, -sm_m[4][e] * s), vx);
-      vy = fma(att, fma(sm_m[5][e], c, -sm_m[6][e] * s), vy);
-      vz = fma(att, fma(sm_m[7][e], c, -sm_m[8][e] * s), vz);
+      __sincosf(r * kTwoPiF, &sf, &cf);
+      const float kl = s_kl[e];
+      const float att = above ? fmaf(kl, ya, 1.0f) : exp2f(kl * ya);
+      const double s = (double)(sf * att), c = (double)(cf * att);
+      // Re((a + i b)(c + i s)) = a c - b s, velocity.cpp:51-55
+      vx = fma(s_c[0][e], c, fma(-s_c[1][e], s, vx));
+      vy = fma(s_c[2][e], c, fma(-s_c[3][e], s, vy));
+      vz = fma(s_c[4][e], c, fma(-s_c[5][e], s, vz));
     }
   }
   if (p < n) {
@@ -243,11 +256,24 @@ int ocn_direct_evaluate(ocn_direct* d, int64_t n, const double* xzy, double* out
     InStage si(ctx, xzy, (size_t)n * 3 * sizeof(double));
     OutStage so(ctx, out, (size_t)n * 3 * sizeof(double));
     const int64_t pblocks = (n + kEvalThreads - 1) / kEvalThreads;
-    // split the mode list until ~4 CTAs per SM, keeping >= 16 tiles per chunk
-    const int64_t want = (int64_t)ctx->sm_count * 4;
-    int64_t chunks = pblocks >= want ? 1 : (want + pblocks - 1) / pblocks;
-    chunks = std::min<int64_t>(chunks, std::max<int64_t>(1, d->modes / (16 * kTile)));
-    chunks = std::min<int64_t>(chunks, 65535);
+    // Split the mode list into ordered chunks so that points x chunks fills whole
+    // waves of resident CTAs (few points: many chunks; a ragged last wave costs
+    // up to half the time otherwise).
+    static int per_sm = 0;
+    if (!per_sm) {
+      OCN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_direct_eval, kEvalThreads, 0));
+      per_sm = std::max(per_sm, 1);
+    }
+    const int64_t slots = (int64_t)ctx->sm_count * per_sm;
+    const int64_t max_chunks = std::min<int64_t>(65535, std::max<int64_t>(1, d->modes / (16 * kTile)));
+    int64_t chunks = 1;
+    double best = -1.0;
+    for (int64_t c = 1; c <= std::min<int64_t>(max_chunks, 4 * slots); ++c) {
+      const int64_t ctas = pblocks * c;
+      const double eff = (double)ctas / (double)(((ctas + slots - 1) / slots) * slots);
+      if (eff > best + 1e-3) best = eff, chunks = c;
+      if (ctas >= 4 * slots) break;
+    }
     const int64_t chunk = chunks > 1 ? (d->modes + chunks - 1) / chunks : std::max<int64_t>(d->modes, 1);
     chunks = chunks > 1 ? (d->modes + chunk - 1) / chunk : 1;
     double* dst = (double*)so.dev;
