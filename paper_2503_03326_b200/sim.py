@@ -177,22 +177,54 @@ class Simulation:
     def __init__(self, cascade_config: "oc.CascadeConfig", spectrum: SpectrumParams,
                  slices: SliceConfig, bodies: Sequence[BodyConfig], dt: float = 1.0 / 60.0,
                  wind=(0.0, 0.0, 0.0), choppiness: float = 1.0, rebuild_stride: int = 1,
-                 ctx=None):
+                 ctx=None, pipelined: bool = False, device: int = 0):
+        """pipelined: the spectral step of step f+1 (a pure function of time) runs on a
+        low-priority context into the other of two map / slice buffers while step f's
+        bodies run on a high-priority one; CUDA events order the buffers (the bench.py
+        frame pipeline). Results are identical to the serial order."""
         if not dt > 0.0:
             raise oc.ConfigError("dt must be > 0")
-        self.ctx = ctx or oc.Context.default()
+        if pipelined and rebuild_stride != 1:
+            raise oc.ConfigError("pipelined Simulation rebuilds the slices every step (rebuild_stride 1)")
         self.dt = dt
         self.wind = tuple(float(w) for w in wind)
         self.choppiness = choppiness
         self.rebuild_stride = max(1, int(rebuild_stride))
         self.gravity = spectrum.gravity
-        self.cascades = oc.CascadeSet(cascade_config, spectrum, ctx=self.ctx)
-        self.maps = oc.SurfaceMaps(self.cascades)
-        self.slices = oc.VelocitySlices(self.cascades, slices)
-        oc.spectral_step(self.maps, self.slices, 0.0, choppiness)  # sim.cpp:18-20
+        self.pipelined = pipelined
+        if pipelined:
+            import torch
+            self.sctx = oc.Context(device, priority=-1)  # spectral steps
+            self.ctx = oc.Context(device, priority=1)    # bodies
+            self._S = torch.cuda.ExternalStream(self.sctx.stream, device=f"cuda:{device}")
+            self._H = torch.cuda.ExternalStream(self.ctx.stream, device=f"cuda:{device}")
+            self._ready = [torch.cuda.Event(), torch.cuda.Event()]
+            self._consumed = [torch.cuda.Event(), torch.cuda.Event()]
+        else:
+            self.ctx = self.sctx = ctx or oc.Context.default()
+        nbuf = 2 if pipelined else 1
+        self.cascades = oc.CascadeSet(cascade_config, spectrum, ctx=self.sctx)
+        self._maps = [oc.SurfaceMaps(self.cascades) for _ in range(nbuf)]
+        self._slices = [oc.VelocitySlices(self.cascades, slices) for _ in range(nbuf)]
+        self._cur = 0
+        oc.spectral_step(self._maps[0], self._slices[0], 0.0, choppiness)  # sim.cpp:18-20
         self.bodies: List[_Body] = [_Body(b, dt, self.ctx) for b in bodies]
         self.time = 0.0
         self.step_index = 0
+        self._prefetched = False
+        if pipelined:
+            self._ready[0].record(self._S)
+
+    @property
+    def maps(self) -> "oc.SurfaceMaps":
+        return self._maps[self._cur]
+
+    @property
+    def slices(self) -> "oc.VelocitySlices":
+        return self._slices[self._cur]
+
+    def _spectral(self, k: int, t: float, with_slices: bool):
+        oc.spectral_step(self._maps[k], self._slices[k] if with_slices else None, t, self.choppiness)
 
     def compose_height(self, xz, exclude_body: int = -1):
         """sim.cpp:44-51, batched on the device."""
@@ -209,10 +241,16 @@ class Simulation:
         """sim.cpp:59-124."""
         dt = self.dt
         t_next = self.time + dt
-        if self.step_index % self.rebuild_stride == 0:
-            oc.spectral_step(self.maps, self.slices, t_next, self.choppiness)
+        if not self.pipelined:
+            self._spectral(0, t_next, self.step_index % self.rebuild_stride == 0)
         else:
-            oc.spectral_step(self.maps, None, t_next, self.choppiness)
+            k = 1 - self._cur
+            if not self._prefetched:  # first step: nothing prefetched yet
+                self._S.wait_event(self._consumed[k])
+                self._spectral(k, t_next, True)
+                self._ready[k].record(self._S)
+            self._cur = k
+            self._H.wait_event(self._ready[k])
         L = lib()
         for i, body in enumerate(self.bodies):
             others = [b.zone for k, b in enumerate(self.bodies) if k != i]
@@ -235,6 +273,15 @@ class Simulation:
         for body in self.bodies:
             check(L.ocn_zone_apply_last_mask(body.zone.h), self.ctx.h, "apply_mask")
             body.zone.step(dt, (body.rigid.position[0], body.rigid.position[2]))
+        if self.pipelined:
+            # buffer _cur is free once the bodies' stages are done; prefetch the next
+            # step's spectral step into the other buffer on the low-priority stream
+            self._consumed[self._cur].record(self._H)
+            k = 1 - self._cur
+            self._S.wait_event(self._consumed[k])
+            self._spectral(k, t_next + dt, True)
+            self._ready[k].record(self._S)
+            self._prefetched = True
         for body in self.bodies:
             rep = HydroReport()
             check(L.ocn_hydro_report_get(body.mesh.h, C.byref(rep)), self.ctx.h, "report")

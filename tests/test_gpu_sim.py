@@ -17,8 +17,8 @@ from make_golden_sim import sim_scene  # noqa: E402
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module")
-def run():
+@pytest.fixture(scope="module", params=[False, True], ids=["serial", "pipelined"])
+def run(request):
     from paper_2503_03326_b200 import ocean as oc
     from paper_2503_03326_b200.sim import BodyConfig, Simulation
     s = sim_scene()
@@ -26,7 +26,7 @@ def run():
                          yaw=b["yaw"], initial_velocity=b["velocity"], density=b["density"],
                          angular_damping=s["angular_damping"], fdm=s["fdm"]) for b in s["bodies"]]
     sim = Simulation(oc.CascadeConfig(s["n"], s["lengths"], s["cutoffs"]), s["params"], s["slices"],
-                     bodies, dt=s["dt"], wind=s["wind"])
+                     bodies, dt=s["dt"], wind=s["wind"], pipelined=request.param)
     v0 = sim.poses()[:, 7:10].copy()
     poses, vw = [], []
     for _ in range(s["steps"]):
