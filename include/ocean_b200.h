@@ -420,6 +420,25 @@ OCN_API int ocn_zone_mask_from_hydro_deferred(ocn_zone* z, ocn_mesh* mesh, doubl
                                               const ocn_mask_frame* frame,
                                               const ocn_mask_params* params);
 OCN_API int ocn_zone_apply_last_mask(ocn_zone* z);
+/* One body of a Simulation step (sim.cpp:73-109): its mesh and zone handles,
+ * pose, drag coefficients, speed |v|, yaw (BodyPose::yaw) and mask inputs. */
+typedef struct ocn_body_frame {
+  void* mesh; /* ocn_mesh* */
+  void* zone; /* ocn_zone* */
+  ocn_pose pose;
+  double cd_water, cd_air;
+  double speed, yaw;
+  ocn_mask_frame frame;
+  ocn_mask_params mask;
+} ocn_body_frame;
+/* The per-body stages of Simulation::step for every body, in sim.cpp's order:
+ * per body aggregate (fluid = maps / slices / medium; the zone list is every
+ * OTHER body's zone), update_stability, deferred mask; then per body
+ * apply_mask + FdmZone::step at the given position; then the reports
+ * (reports[n_bodies], synchronous). reports == NULL leaves the stages
+ * enqueued (async); read them with ocn_hydro_report_get. */
+OCN_API int ocn_bodies_step(int n_bodies, const ocn_body_frame* bodies, const ocn_fluid* fluid,
+                            double dt, ocn_hydro_report* reports);
 /* Cells of the last mask in row-major order (MaskCell, interactive.hpp:56-59). */
 OCN_API int ocn_zone_mask_download(ocn_zone* z, int capacity, int32_t* host_ij, double* host_h,
                            int* n_cells);

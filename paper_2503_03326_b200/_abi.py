@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 from ._types import (Fluid, FdmConfig, HydroReport, MaskFrame, MaskParams, Pose, SliceConfig,
-                     SpectrumParams, TriangleState, ZoneState)
+                     SpectrumParams, TriangleState, ZoneState, BodyFrame)
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 # OCN_LIB: an alternative build of the same library (kernel-variant experiments)
@@ -162,6 +162,7 @@ SIGNATURES = {
     "ocn_heightfield_write_composed": (ci, [vp, ci, pvp, ci, cd, C.c_float, C.c_char_p]),
     "ocn_zone_mask_from_hydro_deferred": (ci, [vp, vp, cd, cd, cd, cd, C.POINTER(MaskFrame), C.POINTER(MaskParams)]),
     "ocn_zone_apply_last_mask": (ci, [vp]),
+    "ocn_bodies_step": (ci, [ci, C.POINTER(BodyFrame), C.POINTER(Fluid), cd, C.POINTER(HydroReport)]),
     "ocn_direct_create": (ci, [vp, cd, pvp]),
     "ocn_direct_destroy": (ci, [vp]),
     "ocn_direct_modes": (ci, [vp, C.POINTER(C.c_int64)]),

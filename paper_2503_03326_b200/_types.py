@@ -216,3 +216,19 @@ class ZoneState(C.Structure):
         ("delta_min", C.c_double),
         ("delta_max", C.c_double),
     ]
+
+
+class BodyFrame(C.Structure):
+    """ocn_body_frame — one body of a Simulation step (sim.cpp:73-109)."""
+
+    _fields_ = [
+        ("mesh", C.c_void_p),
+        ("zone", C.c_void_p),
+        ("pose", Pose),
+        ("cd_water", C.c_double),
+        ("cd_air", C.c_double),
+        ("speed", C.c_double),
+        ("yaw", C.c_double),
+        ("frame", MaskFrame),
+        ("mask", MaskParams),
+    ]

@@ -27,7 +27,7 @@ import numpy as np
 
 from . import ocean as oc
 from ._abi import DomainError, NumericError, check, lib
-from ._types import FdmConfig, HydroReport, MaskFrame, MaskParams, Pose, SliceConfig, SpectrumParams
+from ._types import BodyFrame, FdmConfig, HydroReport, MaskFrame, MaskParams, Pose, SliceConfig, SpectrumParams
 
 import ctypes as C
 
@@ -177,11 +177,17 @@ class Simulation:
     def __init__(self, cascade_config: "oc.CascadeConfig", spectrum: SpectrumParams,
                  slices: SliceConfig, bodies: Sequence[BodyConfig], dt: float = 1.0 / 60.0,
                  wind=(0.0, 0.0, 0.0), choppiness: float = 1.0, rebuild_stride: int = 1,
-                 ctx=None, pipelined: bool = False, device: int = 0):
+                 ctx=None, pipelined: bool = False, device: int = 0, native: bool = False,
+                 concurrent: bool = False):
         """pipelined: the spectral step of step f+1 (a pure function of time) runs on a
         low-priority context into the other of two map / slice buffers while step f's
         bodies run on a high-priority one; CUDA events order the buffers (the bench.py
-        frame pipeline). Results are identical to the serial order."""
+        frame pipeline). Results are identical to the serial order.
+        native: the per-body stages go through one ocn_bodies_step call.
+        concurrent (implies pipelined): every body gets its own high-priority context, so
+        the bodies' latency-bound hull chains overlap; CUDA events keep sim.cpp's order
+        (every aggregate after every zone's previous step, every zone's mask / step after
+        every other body's aggregate)."""
         if not dt > 0.0:
             raise oc.ConfigError("dt must be > 0")
         if pipelined and rebuild_stride != 1:
@@ -191,7 +197,10 @@ class Simulation:
         self.choppiness = choppiness
         self.rebuild_stride = max(1, int(rebuild_stride))
         self.gravity = spectrum.gravity
+        pipelined = pipelined or concurrent
         self.pipelined = pipelined
+        self.concurrent = concurrent
+        self.native = native  # per-body stages in one ocn_bodies_step call
         if pipelined:
             import torch
             self.sctx = oc.Context(device, priority=-1)  # spectral steps
@@ -208,7 +217,15 @@ class Simulation:
         self._slices = [oc.VelocitySlices(self.cascades, slices) for _ in range(nbuf)]
         self._cur = 0
         oc.spectral_step(self._maps[0], self._slices[0], 0.0, choppiness)  # sim.cpp:18-20
-        self.bodies: List[_Body] = [_Body(b, dt, self.ctx) for b in bodies]
+        if concurrent:
+            import torch
+            self._bctx = [oc.Context(device, priority=1) for _ in bodies]
+            self._B = [torch.cuda.ExternalStream(c.stream, device=f"cuda:{device}") for c in self._bctx]
+            self._agg = [torch.cuda.Event() for _ in bodies]
+            self._zdone = [torch.cuda.Event() for _ in bodies]
+            self.bodies: List[_Body] = [_Body(b, dt, c) for b, c in zip(bodies, self._bctx)]
+        else:
+            self.bodies = [_Body(b, dt, self.ctx) for b in bodies]
         self.time = 0.0
         self.step_index = 0
         self._prefetched = False
@@ -237,6 +254,79 @@ class Simulation:
                 return quat_rotate(body.rigid.orientation, np.asarray(f, np.float64))
         return np.zeros(3)
 
+    def _mask_frame(self, body: _Body) -> MaskFrame:
+        m = body.mesh
+        return MaskFrame.make(half_beam=float(m.bbox_max[0] - m.bbox_min[0]), z_min=float(m.bbox_min[2]),
+                              z_max=float(m.bbox_max[2]), mesh_height=m.height())
+
+    def _bodies_native(self, speeds, dt):
+        """sim.cpp:73-109 for every body in one library call (ocn_bodies_step)."""
+        nb = len(self.bodies)
+        frames = (BodyFrame * max(nb, 1))()
+        for i, body in enumerate(self.bodies):
+            f = frames[i]
+            f.mesh, f.zone = body.mesh.h.value, body.zone.h.value
+            f.pose = body.rigid.pose()
+            f.cd_water, f.cd_air = body.config.cd_water, body.config.cd_air
+            f.speed, f.yaw = speeds[i], pose_yaw(body.rigid.orientation)
+            f.frame = self._mask_frame(body)
+            f.mask = body.config.mask
+        fluid, _keep = oc._fluid_struct(oc.FluidQuery(maps=self.maps, slices=self.slices, wind=self.wind),
+                                        oc.DragCoefficients())
+        check(lib().ocn_bodies_step(nb, frames, C.byref(fluid), dt, None), self.ctx.h, "bodies_step")
+
+    def _bodies_calls(self, speeds, dt):
+        """The same stages as separate library calls per body."""
+        L = lib()
+        for i, body in enumerate(self.bodies):
+            others = [b.zone for k, b in enumerate(self.bodies) if k != i]
+            fluid = oc.FluidQuery(maps=self.maps, slices=self.slices, zones=others, wind=self.wind)
+            # enqueued only: the reports are read once after every body's stages
+            oc.aggregate(body.mesh, body.rigid.pose(), fluid,
+                         oc.DragCoefficients(body.config.cd_water, body.config.cd_air), sync=False)
+            body.zone.update_stability(speeds[i], dt)
+            frame = self._mask_frame(body)
+            check(L.ocn_zone_mask_from_hydro_deferred(body.zone.h, body.mesh.h,
+                                                      pose_yaw(body.rigid.orientation),
+                                                      float(body.rigid.position[0]),
+                                                      float(body.rigid.position[2]), speeds[i],
+                                                      C.byref(frame), C.byref(body.config.mask)),
+                  self.ctx.h, "mask")
+        for body in self.bodies:
+            check(L.ocn_zone_apply_last_mask(body.zone.h), self.ctx.h, "apply_mask")
+            body.zone.step(dt, (body.rigid.position[0], body.rigid.position[2]))
+
+    def _bodies_concurrent(self, speeds, dt):
+        """_bodies_calls with one stream per body and events for sim.cpp's order."""
+        L = lib()
+        nb = len(self.bodies)
+        for i, body in enumerate(self.bodies):
+            B = self._B[i]
+            for k in range(nb):
+                if k != i:
+                    B.wait_event(self._zdone[k])  # zone k's previous step (no-op before the first)
+            others = [b.zone for k, b in enumerate(self.bodies) if k != i]
+            fluid = oc.FluidQuery(maps=self.maps, slices=self.slices, zones=others, wind=self.wind)
+            oc.aggregate(body.mesh, body.rigid.pose(), fluid,
+                         oc.DragCoefficients(body.config.cd_water, body.config.cd_air), sync=False)
+            body.zone.update_stability(speeds[i], dt)
+            frame = self._mask_frame(body)
+            check(L.ocn_zone_mask_from_hydro_deferred(body.zone.h, body.mesh.h,
+                                                      pose_yaw(body.rigid.orientation),
+                                                      float(body.rigid.position[0]),
+                                                      float(body.rigid.position[2]), speeds[i],
+                                                      C.byref(frame), C.byref(body.config.mask)),
+                  body.zone.ctx.h, "mask")
+            self._agg[i].record(B)
+        for k, body in enumerate(self.bodies):
+            B = self._B[k]
+            for i in range(nb):
+                if i != k:
+                    B.wait_event(self._agg[i])  # every aggregate that read zone k
+            check(L.ocn_zone_apply_last_mask(body.zone.h), body.zone.ctx.h, "apply_mask")
+            body.zone.step(dt, (body.rigid.position[0], body.rigid.position[2]))
+            self._zdone[k].record(B)
+
     def step(self):
         """sim.cpp:59-124."""
         dt = self.dt
@@ -250,41 +340,34 @@ class Simulation:
                 self._spectral(k, t_next, True)
                 self._ready[k].record(self._S)
             self._cur = k
-            self._H.wait_event(self._ready[k])
-        L = lib()
-        for i, body in enumerate(self.bodies):
-            others = [b.zone for k, b in enumerate(self.bodies) if k != i]
-            fluid = oc.FluidQuery(maps=self.maps, slices=self.slices, zones=others, wind=self.wind)
-            pose = body.rigid.pose()
-            # enqueued only: the report is read once after every body's stages (below)
-            oc.aggregate(body.mesh, pose, fluid,
-                         oc.DragCoefficients(body.config.cd_water, body.config.cd_air), sync=False)
-            speed = float(np.linalg.norm(body.rigid.linear_velocity))
-            body.zone.update_stability(speed, dt)
-            m = body.mesh
-            frame = MaskFrame.make(half_beam=float(m.bbox_max[0] - m.bbox_min[0]),
-                                   z_min=float(m.bbox_min[2]), z_max=float(m.bbox_max[2]),
-                                   mesh_height=m.height())
-            check(L.ocn_zone_mask_from_hydro_deferred(body.zone.h, m.h, pose_yaw(body.rigid.orientation),
-                                                      float(body.rigid.position[0]),
-                                                      float(body.rigid.position[2]), speed,
-                                                      C.byref(frame), C.byref(body.config.mask)),
-                  self.ctx.h, "mask")
-        for body in self.bodies:
-            check(L.ocn_zone_apply_last_mask(body.zone.h), self.ctx.h, "apply_mask")
-            body.zone.step(dt, (body.rigid.position[0], body.rigid.position[2]))
+            for st in (self._B if self.concurrent else [self._H]):
+                st.wait_event(self._ready[k])
+        speeds = [float(np.linalg.norm(b.rigid.linear_velocity)) for b in self.bodies]
+        if self.concurrent:
+            self._bodies_concurrent(speeds, dt)
+        elif self.native:
+            self._bodies_native(speeds, dt)
+        else:
+            self._bodies_calls(speeds, dt)
         if self.pipelined:
-            # buffer _cur is free once the bodies' stages are done; prefetch the next
-            # step's spectral step into the other buffer on the low-priority stream
-            self._consumed[self._cur].record(self._H)
+            # the bodies' stages are enqueued; the next step's spectral step (a function of
+            # time only) goes into the other buffer once this step's map readers are done
+            if self.concurrent:
+                for ev in self._agg:
+                    self._S.wait_event(ev)
+            else:
+                self._consumed[self._cur].record(self._H)
+                self._S.wait_event(self._consumed[self._cur])
             k = 1 - self._cur
-            self._S.wait_event(self._consumed[k])
             self._spectral(k, t_next + dt, True)
             self._ready[k].record(self._S)
             self._prefetched = True
+        reports = []
         for body in self.bodies:
             rep = HydroReport()
-            check(L.ocn_hydro_report_get(body.mesh.h, C.byref(rep)), self.ctx.h, "report")
+            check(lib().ocn_hydro_report_get(body.mesh.h, C.byref(rep)), body.mesh.ctx.h, "report")
+            reports.append(rep)
+        for body, rep in zip(self.bodies, reports):
             body.report = r = oc.HydroResult(body.mesh, rep)
             if r.center_of_immersion is not None:
                 body.rigid.apply_force_at(r.buoyancy_force, r.water_center)

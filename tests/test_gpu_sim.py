@@ -17,7 +17,9 @@ from make_golden_sim import sim_scene  # noqa: E402
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module", params=[False, True], ids=["serial", "pipelined"])
+@pytest.fixture(scope="module", params=[(False, False, False), (False, True, False),
+                                        (True, True, False), (True, False, True)],
+                ids=["serial-calls", "serial-native", "pipelined-native", "concurrent"])
 def run(request):
     from paper_2503_03326_b200 import ocean as oc
     from paper_2503_03326_b200.sim import BodyConfig, Simulation
@@ -26,7 +28,8 @@ def run(request):
                          yaw=b["yaw"], initial_velocity=b["velocity"], density=b["density"],
                          angular_damping=s["angular_damping"], fdm=s["fdm"]) for b in s["bodies"]]
     sim = Simulation(oc.CascadeConfig(s["n"], s["lengths"], s["cutoffs"]), s["params"], s["slices"],
-                     bodies, dt=s["dt"], wind=s["wind"], pipelined=request.param)
+                     bodies, dt=s["dt"], wind=s["wind"], pipelined=request.param[0], native=request.param[1],
+                     concurrent=request.param[2])
     v0 = sim.poses()[:, 7:10].copy()
     poses, vw = [], []
     for _ in range(s["steps"]):
