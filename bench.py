@@ -1,19 +1,29 @@
 #!/usr/bin/env python
 """bench.py — per-frame Arc Blanc hot path on B200 (BASELINE.json metric).
 
-Workload (one "step" = one frame): the 4-cascade 1024^2
-spectrum (U=20, F=1e5, theta0=0.4, xi=0.5, delta=0.5, standard peak, seed 42;
-lengths 1024/256/16/4 m) evolved to t, its 8 surface maps + 32 logarithmic
-velocity-at-depth slices (208 packed 1024^2 inverse FFTs), fluid-to-solid
-forces on the 100,352-triangle UV-ellipsoid hull (height_at + velocity_at
-samplers, deterministic reductions, waterline), the waterline mask and one
-2048^2 Cords-Staadt FDM step. Metric: ocean grid points / s (= 4 * 1024^2 per
-frame / frame time) and ms / frame.
+Headline workload (one "step" = one frame): the 4-cascade
+1024^2 spectrum (U=20, F=1e5, theta0=0.4, xi=0.5, delta=0.5, standard peak,
+seed 42; lengths 1024/256/16/4 m) evolved to t, its 8 surface maps + 32
+logarithmic velocity-at-depth slices (208 packed 1024^2 inverse FFTs in the
+reference; 164 run per frame here, the other 44 are exactly zero in fp32 at
+their depth and their planes are zeroed once), fluid-to-solid forces on the
+100,352-triangle UV-ellipsoid hull (height_at + velocity_at samplers,
+deterministic reductions, waterline), the waterline mask and one 2048^2
+Cords-Staadt FDM step. Metric: ocean grid points / s (= 4 * 1024^2 per frame /
+frame time) and ms / frame.
 
-    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+The same run also measures the other SURVEY 8d configurations (the "configs"
+object of the line; skip with --no-extra-configs):
+  1: 600 frames of the reference-default 256^2 cascade in one batched step
+     (frames f mod G across ranks), plus the single-frame latency;
+  4: 64 independent 3 x 512^2 instances (64/G per rank);
+  5: one 16384^2 grid, row slabs per rank, NCCL all-to-all transpose.
 
-N > 1 (torchrun, one rank per GPU): independent replicas of the frame on every
-GPU (configs 2/3 do not shard), weak scaling, max over ranks.
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config 1|3|4|5]
+
+N > 1 (torchrun, one rank per GPU): config 3 runs independent replicas (configs
+2/3 do not shard), weak scaling; configs 1/4/5 split their fixed
+work across the ranks (strong scaling); every time is the max over ranks.
 """
 from __future__ import annotations
 
@@ -46,8 +56,9 @@ POINTS_PER_FRAME = len(LENGTHS) * N_GRID * N_GRID
 # h0 read once (8 B / cascade-point) + every output field written once in fp32
 SPECTRAL_FIELDS = 8 + 3 * DEPTHS
 SPECTRAL_BYTES = POINTS_PER_FRAME * (8 + 4 * SPECTRAL_FIELDS)
-WORKLOAD = ("config3: 4 cascades x 1024^2 (8 surface maps + 32 velocity slices, 208 packed "
-            "2D iFFTs) + 100,352-tri hull forces + waterline mask + 2048^2 FDM step")
+WORKLOAD = ("config3: 4 cascades x 1024^2 (8 surface maps + 32 velocity slices: 208 packed "
+            "2D iFFTs in the reference, 164 executed per frame + 44 exactly zero in fp32 at their "
+            "depth, planes zeroed once) + 100,352-tri hull forces + waterline mask + 2048^2 FDM step")
 
 
 def _params():
@@ -254,6 +265,62 @@ class Frame:
         self.pending_report = False
 
 
+# ---------------------------------------------------------------- config 1
+C1_FRAMES, C1_N, C1_L = 600, 256, 256.0
+C1_WORKLOAD = ("config1: reference-default spectrum (U=5, F=1e5, seed 0), one 256^2 cascade "
+               "(band [0, inf)), 8 surface maps per frame, 600 frames t_f = (f+1)/60 batched in "
+               "one spectral step (one 10 s clip per step); frames f mod G per rank")
+
+
+class Frame1(_SingleStream):
+    """This rank's frames of the 600-frame clip as one time-batched set: rank r
+    owns frames f = r, r + G, ... (t_f = (f + 1) / 60), i.e. t0 = (r + 1) / 60
+    and spacing G / 60 (no collective)."""
+
+    def __init__(self, device: int, rank: int, world: int):
+        from paper_2503_03326_b200 import ocean as oc
+        from paper_2503_03326_b200._types import SpectrumParams
+        self.oc, self.L = oc, oc.lib()
+        self.ctx = oc.Context(device)
+        self.per = C1_FRAMES // world
+        self.p = SpectrumParams.make()
+        self.cfg = oc.CascadeConfig(C1_N, [C1_L], [])
+        self.frames = oc.CascadeFrames(self.cfg, self.p, self.per, world * DT, ctx=self.ctx)
+        self.maps = oc.SurfaceMaps(self.frames)
+        self.t0 = (rank + 1) * DT
+        self.dt = world * DT
+        self.clip = 0
+        self.points = self.per * C1_N * C1_N
+        self._h = np.zeros(C1_N * C1_N, np.float32)
+
+    def step(self, read_report: bool = False):
+        t0 = self.t0 + self.clip * C1_FRAMES * DT  # successive 10 s clips
+        self.clip += 1
+        self.oc.check(self.L.ocn_surface_generate_batch(self.maps.h, t0, self.dt, 1.0), self.ctx.h,
+                      "generate_batch")
+        if read_report:  # the step's result probe: the clip's last frame height map -> host
+            self.oc.check(self.L.ocn_maps_download_f32(self.maps.h, self.per - 1, 0,
+                                                       self._h.ctypes.data_as(C.POINTER(C.c_float))),
+                          self.ctx.h, "download")
+
+    def single_frame_latency(self, reps: int = 50) -> float:
+        """One frame through the C-ABI, launch to completion (host wall clock,
+        median): ocn_surface_generate on a one-frame set + synchronize."""
+        oc = self.oc
+        cs = oc.CascadeSet(self.cfg, self.p, ctx=self.ctx)
+        m = oc.SurfaceMaps(cs)
+        for k in range(5):
+            m.generate(DT * (k + 1))
+        self.ctx.synchronize()
+        ts = []
+        for k in range(reps):
+            t0 = time.perf_counter()
+            self.oc.check(self.L.ocn_surface_generate(m.h, DT * (k + 1), 1.0), self.ctx.h, "gen")
+            self.ctx.synchronize()
+            ts.append(time.perf_counter() - t0)
+        return float(np.median(ts) * 1e3)
+
+
 # ---------------------------------------------------------------- config 4
 C4_INSTANCES, C4_N = 64, 512
 C4_LENGTHS = [256.0, 16.0, 4.0]
@@ -389,19 +456,15 @@ def _traffic():
         return None
 
 
-def run_ours(args):
-    dist, rank, world, local = _dist()
-    c4 = args.config == 4
-    c5 = args.config == 5
-    fr = (Frame5(local, rank, world, dist) if c5 else
-          (Frame4(local, rank, world) if c4 else Frame(local, pipelined=not args.no_pipeline)))
+def _measure(fr, dist, local, steps, warmup, stage_names, kernel_names=None, c5=False):
+    """Warm-up, then K timed steps (CUDA events on the frame's streams, barrier +
+    synchronize on both sides), a profiled pass per stage, and the e2e pass."""
+    import torch
     L = fr.L
     ctxs = fr.contexts()
-    for _ in range(max(args.warmup, 3)):
+    for _ in range(max(warmup, 3)):
         fr.step()
     fr.sync()
-    # ---- timed region: device time with CUDA events on the library stream(s)
-    import torch
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
 
@@ -412,7 +475,7 @@ def run_ours(args):
         _barrier(dist)
         fr.sync()
         fr.timed_begin(ev0)
-        for _ in range(args.steps):
+        for _ in range(steps):
             fr.step()
         fr.timed_end(ev1)
         fr.sync()
@@ -420,8 +483,8 @@ def run_ours(args):
         ms_total = ev0.elapsed_time(ev1)
         launches = n_launches() - launches0
 
-        # ---- roofline pass: same K frames with CUDA-event windows per stage
-        # (mode 2: the spectral step still replays its graph), frames not
+        # ---- roofline pass: same K steps with CUDA-event windows per stage
+        # (mode 2: the spectral step still replays its graph), steps not
         # overlapped so that each window times its own stage ...
         fr.serialize = True
 
@@ -429,7 +492,7 @@ def run_ours(args):
             for c in ctxs:
                 L.ocn_ctx_profile(c.h, mode)
                 L.ocn_ctx_profile_reset(c.h)
-            for _ in range(args.steps):
+            for _ in range(steps):
                 fr.step()
             fr.sync()
             out = {}
@@ -439,7 +502,7 @@ def run_ours(args):
                     ms, cnt = C.c_double(), C.c_uint64()
                     L.ocn_ctx_profile_read(c.h, cat, C.byref(ms), C.byref(cnt))
                     tot += ms.value
-                out[name] = tot / args.steps
+                out[name] = tot / steps
             for c in ctxs:
                 L.ocn_ctx_profile(c.h, 0)
             return out
@@ -452,55 +515,112 @@ def run_ours(args):
             stages["all_to_all"] = float(np.mean(a2a)) if a2a else 0.0
             stages["spectral"] = stages["slab_rows"] + stages["slab_cols"]
         else:
-            stages = profiled(2, [("spectral", 6), ("hydro", 3), ("mask", 4), ("fdm", 5)])
-        if c4:
-            stages = {"spectral": stages["spectral"]}
+            stages = profiled(2, stage_names)
         # ... and the kernel split of the spectral step (mode 1: eager launches)
-        kernels = profiled(1, [("evolve", 0), ("fft_rows", 1), ("fft_cols", 2), ("spectral_eager", 6)])
+        kernels = profiled(1, kernel_names) if kernel_names else None
         fr.serialize = False
         # ---- e2e: through the C-ABI with host inputs (t, pose) and the host
-        # read of each frame's result, wall clock
+        # read of each step's result, wall clock
         _barrier(dist)
         fr.sync()
         t0 = time.perf_counter()
-        for _ in range(args.steps):
+        for _ in range(steps):
             fr.step(read_report=True)
         fr.finish(read_report=True)
         fr.sync()
         e2e_s = time.perf_counter() - t0
-    ms_frame = _max_over_ranks(dist, ms_total / args.steps)
-    e2e_frame = _max_over_ranks(dist, e2e_s / args.steps)
+    return {"ms_step": _max_over_ranks(dist, ms_total / steps),
+            "e2e_step": _max_over_ranks(dist, e2e_s / steps),
+            "spectral_ms": _max_over_ranks(dist, stages["spectral"]),
+            "stages": stages, "kernels": kernels, "launches": int(launches),
+            "clocks": clk.summary()}
+
+
+def _produced_bytes(fr):
+    """Bytes the config-3 spectral step actually moves by definition per frame:
+    h0 read once (8 B / point) + the output planes of the transforms it executes
+    (the 44 exactly-zero transforms' planes are written once, at plan build)."""
+    plan = fr.oc.spectral_plan(fr.maps[0], fr.slices[0])
+    planes = sum((2 if x["index1"] >= 0 else 1) for x in plan if x["executed"])
+    return POINTS_PER_FRAME * 8 + planes * N_GRID * N_GRID * 4, plan
+
+
+def _roofline(kernel, alg_bytes, spec_ms, peak, peak_kind, traffic=None):
+    achieved = alg_bytes / (spec_ms / 1e3) / 1e9
+    return {"kernel": kernel, "bound": "hbm", "achieved": achieved, "peak": peak,
+            "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+            "algorithmic_bytes_per_frame": alg_bytes}
+
+
+def _config_line(args, cfgno, dist, rank, world, local, steps, warmup, peak, peak_kind,
+                 headline: bool):
+    """Measure one SURVEY 8d configuration; returns its line (rank 0) or None."""
+    c1, c4, c5 = cfgno == 1, cfgno == 4, cfgno == 5
+    if c5:
+        fr = Frame5(local, rank, world, dist)
+    elif c4:
+        fr = Frame4(local, rank, world)
+    elif c1:
+        fr = Frame1(local, rank, world)
+    else:
+        fr = Frame(local, pipelined=not args.no_pipeline)
+    stage_names = ([("spectral", 6)] if (c1 or c4) else
+                   [("spectral", 6), ("hydro", 3), ("mask", 4), ("fdm", 5)])
+    kernel_names = None if c5 else [("evolve", 0), ("fft_rows", 1), ("fft_cols", 2),
+                                    ("spectral_eager", 6)]
+    m = _measure(fr, dist, local, steps, warmup, stage_names, kernel_names, c5=c5)
+    extra = {}
+    if c1:
+        extra["single_frame_latency_ms"] = fr.single_frame_latency()
     if rank != 0:
-        if dist:
-            dist.destroy_process_group()
-        return
-    peak, peak_kind = _peaks()
+        return None
+    spec_ms = m["spectral_ms"]
     if c5:
         points = C5_N * C5_N
         alg_bytes = fr.points * (16 + 4 * 8)  # h0 + h0 mirror slab read, 8 fp32 fields written
         metric = "ocean grid points/sec (single 16384^2 surface, slab FFT + all-to-all)"
-        workload, h2d, d2h = C5_WORKLOAD, 8, 0
+        h2d, d2h = 8, 0
         sent = fr.slab.exchange_bytes * (world - 1) / world
-        cfg = {"workload": workload, "grid": C5_N, "ranks": world, "parallelism": f"row slabs x{world}",
-               "exchange_bytes_per_gpu": sent,
+        cfg = {"workload": C5_WORKLOAD, "grid": C5_N, "ranks": world,
+               "parallelism": f"row slabs x{world}", "exchange_bytes_per_gpu": sent,
                "l2": "per-frame slabs 4-8 GB > 126 MB L2 (no explicit flush)"}
         scaling = "strong"
+        roof = _roofline("slab pipeline (k_slab_evolve + k_slab_rows + k_slab_cols)", alg_bytes,
+                         spec_ms, peak, peak_kind)
+        if world > 1 and m["stages"].get("all_to_all", 0) > 0:
+            gbs = sent / (m["stages"]["all_to_all"] / 1e3) / 1e9
+            cfg["all_to_all_GBps_per_gpu"] = gbs
+            cfg["nvlink_efficiency_vs_900GBps"] = gbs / 900.0
+            cfg["nvlink_efficiency_vs_770GBps_measured_peer_copy"] = gbs / 770.0
     elif c4:
-        points = C4_POINTS if world > 1 else fr.points * world
+        points = C4_POINTS
         alg_bytes = fr.points * (8 + 4 * 8)  # per rank and frame
         metric = "ocean grid points/sec (64 x 3 x 512^2 instances, surface synthesis)"
-        workload, h2d, d2h = C4_WORKLOAD, 8, C4_N * C4_N * 4
-        cfg = {"workload": workload, "grid": C4_N, "instances": C4_INSTANCES,
+        h2d, d2h = 8, C4_N * C4_N * 4
+        cfg = {"workload": C4_WORKLOAD, "grid": C4_N, "instances": C4_INSTANCES,
                "cascades_per_instance": len(C4_LENGTHS),
                "parallelism": f"instances sharded {C4_INSTANCES // world}/rank x {world}",
                "l2": "per-frame outputs 1.6 GB / world > 126 MB L2 (no explicit flush)"}
         scaling = "strong"
+        roof = _roofline("spectral pipeline (k_evolve + k_rows_w + k_cols_tma)", alg_bytes, spec_ms,
+                         peak, peak_kind)
+    elif c1:
+        points = C1_FRAMES * C1_N * C1_N
+        alg_bytes = fr.points * (8 + 4 * 8)
+        metric = "ocean grid points/sec (600 frames of a 256^2 cascade, batched)"
+        h2d, d2h = 16, C1_N * C1_N * 4
+        cfg = {"workload": C1_WORKLOAD, "grid": C1_N, "frames": C1_FRAMES,
+               "parallelism": f"frames f mod {world} x {world}" if world > 1 else "1 GPU",
+               "l2": "per-step outputs 1.26 GB / world > 126 MB L2 (no explicit flush)"}
+        scaling = "strong"
+        roof = _roofline("spectral pipeline (k_evolve + k_rows_w + k_cols_tma, one CUDA graph)",
+                         alg_bytes, spec_ms, peak, peak_kind)
     else:
         points = world * POINTS_PER_FRAME
         alg_bytes = SPECTRAL_BYTES
         metric = "ocean grid points/sec (spectrum+iFFT+forces) at 1024^2 x 4 cascades"
-        workload, h2d, d2h = WORKLOAD, C.sizeof(fr.pose) + 8, C.sizeof(fr.report)
-        cfg = {"workload": workload, "grid": N_GRID, "cascades": len(LENGTHS),
+        h2d, d2h = C.sizeof(fr.pose) + 8, C.sizeof(fr.report)
+        cfg = {"workload": WORKLOAD, "grid": N_GRID, "cascades": len(LENGTHS),
                "depth_slices": DEPTHS, "hull_triangles": int(fr.mesh.triangles.shape[0]),
                "fdm_grid": FDM_N, "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
                "frame_pipeline": ("frame f forces/mask/FDM (high-priority stream) overlap frame "
@@ -509,57 +629,94 @@ def run_ours(args):
                                   if not args.no_pipeline else "off"),
                "l2": "per-frame working set 1.8 GB of outputs > 126 MB L2 (no explicit flush)"}
         scaling = "weak"
-    value = points / (ms_frame / 1e3)
-    spec_ms = stages["spectral"]
-    if c5 and world > 1 and stages.get("all_to_all", 0) > 0:
-        gbs = cfg["exchange_bytes_per_gpu"] / (stages["all_to_all"] / 1e3) / 1e9
-        cfg["all_to_all_GBps_per_gpu"] = gbs
-        cfg["nvlink_efficiency_vs_900GBps"] = gbs / 900.0
-    achieved = alg_bytes / (spec_ms / 1e3) / 1e9
+        roof = _roofline("spectral pipeline (k_evolve + k_rows_w + k_cols_tma, one CUDA graph)",
+                         alg_bytes, spec_ms, peak, peak_kind, _traffic())
+        produced, plan = _produced_bytes(fr)
+        roof["produced_bytes_per_frame"] = produced
+        roof["achieved_produced"] = produced / (spec_ms / 1e3) / 1e9
+        roof["frac_produced"] = roof["achieved_produced"] / peak
+        roof["transforms"] = {"reference": len(plan),
+                              "executed_per_frame": sum(x["executed"] for x in plan),
+                              "exactly_zero_planes_written_once": sum(1 - x["executed"] for x in plan)}
+        roof["note"] = ("frac: SURVEY 8d algorithmic bytes (h0 + all 104 output fields, 424 B/pt); "
+                        "frac_produced: h0 + the planes of the executed transforms only")
+    ms = m["ms_step"]
     line = {
         "metric": metric,
-        "value": value,
+        "value": points / (ms / 1e3),
         "unit": "grid-points/s",
         "n_gpus": world,
-        "steps": args.steps,
-        "warmup": max(args.warmup, 3),
-        "ms_per_step": ms_frame,
-        "ms_per_frame": ms_frame,
+        "steps": steps,
+        "warmup": max(warmup, 3),
+        "ms_per_step": ms,
+        "ms_per_frame": ms if not c1 else ms / C1_FRAMES * world,
         "higher_is_better": True,
         "scaling": scaling,
         "vs_baseline": None,
         "dtype": "f32 (fields, FFT) / f64 (spectrum init, phases, samplers, forces)",
         "data": "synthetic (SURVEY 8d spectrum presets; UV-ellipsoid hull)",
         "config": cfg,
-        "stages_ms": stages,
-        "spectral_kernels_ms_eager": kernels,
-        "roofline": {"kernel": ("spectral pipeline (k_evolve + k_rows_w + k_cols_tma, one CUDA graph)"
-                                if not (c4 or c5) else
-                                "spectral pipeline (k_evolve + k_rows_w + k_cols_tma)" if c4 else
-                                "slab pipeline (k_slab_evolve + k_slab_rows + k_slab_cols)"),
-                     "bound": "hbm", "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
-                     "unit": "GB/s", "frac": achieved / peak,
-                     # dram read + write bytes per frame of the same kernels (ncu
-                     # application replay, profiles/roofline_traffic.json; config 3)
-                     "traffic": _traffic() if not (c4 or c5) else None,
-                     "algorithmic_bytes_per_frame": alg_bytes},
-        "e2e": {"value": points / e2e_frame, "unit": "grid-points/s", "ms_per_frame": e2e_frame * 1e3,
-                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-        "gpu_launches": int(launches),
-        "clocks": clk.summary(),
+        "stages_ms": m["stages"],
+        "roofline": roof,
+        "e2e": {"value": points / m["e2e_step"], "unit": "grid-points/s",
+                "ms_per_step": m["e2e_step"] * 1e3, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": m["launches"],
+        "clocks": m["clocks"],
     }
-    if world == 1 and not args.no_cpu_baseline and not c5:
-        line["cpu_baseline"] = cpu_baseline_c4() if c4 else cpu_baseline(frames=1, warmup=0)
-    print(json.dumps(line), flush=True)
+    if m["kernels"]:
+        line["spectral_kernels_ms_eager"] = m["kernels"]
+    line.update(extra)
+    if world == 1 and not args.no_cpu_baseline:
+        if c4:
+            line["cpu_baseline"] = cpu_baseline_c4()
+        elif c1:
+            line["cpu_baseline"] = cpu_baseline_c1()
+        elif not c5 and headline:
+            line["cpu_baseline"] = cpu_baseline(frames=1, warmup=0, one_worker=True)
+    del fr
+    return line
+
+
+def run_ours(args):
+    dist, rank, world, local = _dist()
+    peak, peak_kind = _peaks()
+    line = _config_line(args, args.config, dist, rank, world, local, args.steps, args.warmup, peak,
+                        peak_kind, headline=True)
+    if args.config == 3 and not args.no_extra_configs:
+        import gc
+        import torch
+        extra = {}
+        for cfgno in (1, 4, 5):
+            gc.collect()
+            torch.cuda.empty_cache()
+            sub = _config_line(args, cfgno, dist, rank, world, local, min(args.steps, 10),
+                               args.warmup, peak, peak_kind, headline=False)
+            if sub is not None:
+                extra[str(cfgno)] = sub
+        if line is not None:
+            line["configs"] = extra
+    if line is not None:
+        print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
 
 
 def cpu_baseline_c4(sample_instances: int = 2):
     """Reference generate_maps per instance (3 x 512^2, no batch API in the
     reference), `sample_instances` of the 64 timed and scaled."""
     from oracle.oracle import P
-    from paper_2503_03326_b200._types import SpectrumParams  # noqa: F401
     lib = _ref_lib()
     ncpu = os.cpu_count() or 1
     lib.ref_set_worker_count.argtypes = [C.c_int]
@@ -578,9 +735,35 @@ def cpu_baseline_c4(sample_instances: int = 2):
         per.append(sec.value)
     dt = float(np.mean(per)) * C4_INSTANCES
     return {"value": C4_POINTS / dt, "unit": "grid-points/s", "ms_per_frame": dt * 1e3, "cores": ncpu,
-            "kind": "reference",
+            "cpu_model": _cpu_model(), "kind": "reference",
             "sample": f"{sample_instances} of 64 instances: reference generate_maps (3 x 512^2, "
                       f"CascadeSet built outside the timing), scaled x{C4_INSTANCES // sample_instances}"}
+
+
+def cpu_baseline_c1(sample_frames: int = 60):
+    """Reference generate_maps of the config-1 cascade, `sample_frames` of the
+    600 frames timed (CascadeSet built outside the timing)."""
+    from oracle.oracle import P
+    from paper_2503_03326_b200._types import SpectrumParams
+    lib = _ref_lib()
+    ncpu = os.cpu_count() or 1
+    lib.ref_set_worker_count.argtypes = [C.c_int]
+    lib.ref_set_worker_count(ncpu)
+    f = lib.ref_generate_maps_timed
+    f.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int,
+                  C.POINTER(C.c_double)]
+    la = np.ascontiguousarray([C1_L])
+    cu = np.ascontiguousarray([0.0])
+    p = SpectrumParams.make()
+    sec = C.c_double()
+    f(C1_N, 1, P(la), P(cu), C.byref(p), DT, sample_frames, C.byref(sec))
+    per_clip = sec.value * C1_FRAMES
+    return {"value": C1_FRAMES * C1_N * C1_N / per_clip, "unit": "grid-points/s",
+            "ms_per_frame": sec.value * 1e3, "cores": ncpu, "cpu_model": _cpu_model(),
+            "kind": "reference",
+            "sample": f"{sample_frames} of the 600 frames: reference generate_maps (1 x 256^2), "
+                      f"set_worker_count({ncpu}) (its 4 transforms run as one 256-item chunk, "
+                      f"i.e. on one thread, parallel.cpp:29)"}
 
 
 # ---------------------------------------------------------- reference (CPU)
@@ -592,18 +775,21 @@ def _ref_lib():
     return lib
 
 
-def cpu_baseline(frames: int = 1, warmup: int = 0, budget_s: float = 1e9):
+def cpu_baseline(frames: int = 1, warmup: int = 0, budget_s: float = 1e9, workers: int = 0,
+                 one_worker: bool = False):
     """The reference's own CPU implementation (oracle/_ref: the unmodified
-    reference library compiled from its sources) on this host, all threads
-    (set_worker_count(nproc)); spectral stages stay single-threaded in the
-    reference (256-item chunks, parallel.cpp:29). Sample: full generate_maps
-    (4 x 1024^2), build_slices at 2 of the 32 depths (scaled x16: its cost is
-    linear in the depth count), full aggregate / compute_mask / FDM step."""
+    reference library compiled from its sources) on this host: full config-3
+    frames (generate_maps 4 x 1024^2, build_slices at all 32 depths, aggregate,
+    compute_mask, FdmZone::step), set_worker_count(workers or nproc). Its
+    spectral stages stay single-threaded whatever the worker count (4 C and
+    D C jobs <= 256 run as one chunk, parallel.cpp:29). Frames run until
+    `budget_s` is spent; `frames` reports how many ran. one_worker: also one
+    frame with set_worker_count(1)."""
     from paper_2503_03326_b200._types import FdmConfig, SliceConfig
     from paper_2503_03326_b200.meshgen import uv_ellipsoid
     from oracle.oracle import P
     lib = _ref_lib()
-    ncpu = os.cpu_count() or 1
+    ncpu = workers or os.cpu_count() or 1
     lib.ref_set_worker_count.argtypes = [C.c_int]
     lib.ref_set_worker_count(ncpu)
     v, t = uv_ellipsoid()
@@ -632,37 +818,46 @@ def cpu_baseline(frames: int = 1, warmup: int = 0, budget_s: float = 1e9):
     t_init = time.perf_counter() - t_init
     if st.value != 0:
         raise RuntimeError("reference bench setup failed")
-    sample_depths = 2
     stage = np.zeros(5)
     for _ in range(warmup):
-        lib.ref_bench_frame(b, DT, sample_depths, P(stage))
-    ests, done = [], 0
+        lib.ref_bench_frame(b, DT, DEPTHS, P(stage))
+    walls, stages = [], []
     t_start = time.perf_counter()
-    for _ in range(frames):
-        lib.ref_bench_frame(b, DT, sample_depths, P(stage))
-        est = stage[0] + stage[1] * (DEPTHS / sample_depths) + stage[2] + stage[3] + stage[4]
-        ests.append((est, stage.copy()))
-        done += 1
+    for _ in range(max(frames, 1)):
+        w0 = time.perf_counter()
+        lib.ref_bench_frame(b, DT, DEPTHS, P(stage))
+        walls.append(time.perf_counter() - w0)
+        stages.append(stage.copy())
         if time.perf_counter() - t_start > budget_s:
             break
+    one = None
+    if one_worker:
+        lib.ref_set_worker_count(1)
+        w0 = time.perf_counter()
+        lib.ref_bench_frame(b, DT, DEPTHS, P(stage))
+        one = time.perf_counter() - w0
+        lib.ref_set_worker_count(ncpu)
     lib.ref_bench_destroy(b)
-    est = float(np.mean([e for e, _ in ests]))
-    st_mean = np.mean([s for _, s in ests], axis=0)
-    return {
-        "value": POINTS_PER_FRAME / est,
+    wall = float(np.mean(walls))
+    st_mean = np.mean(stages, axis=0)
+    out = {
+        "value": POINTS_PER_FRAME / wall,
         "unit": "grid-points/s",
-        "ms_per_frame": est * 1e3,
+        "ms_per_frame": wall * 1e3,
         "cores": ncpu,
+        "cpu_model": _cpu_model(),
         "kind": "reference",
-        "frames": done,
-        "stage_s": {"generate_maps": st_mean[0], "build_slices_32_est": st_mean[1] * DEPTHS / sample_depths,
-                    "aggregate": st_mean[2], "stability_mask": st_mean[3], "fdm": st_mean[4],
-                    "cascade_init_once": t_init},
-        "sample": (f"{done} frame(s) of config 3 through the reference library (oracle/_ref, g++ -O2): "
-                   f"full generate_maps + aggregate + compute_mask + FdmZone::step, build_slices at "
-                   f"{sample_depths} of {DEPTHS} depths scaled x{DEPTHS // sample_depths}; "
-                   f"set_worker_count({ncpu})"),
+        "frames": len(walls),
+        "warmup_frames": warmup,
+        "stage_s": {"generate_maps": st_mean[0], "build_slices": st_mean[1], "aggregate": st_mean[2],
+                    "stability_mask": st_mean[3], "fdm": st_mean[4], "cascade_init_once": t_init},
+        "sample": (f"{len(walls)} full config-3 frame(s) through the reference library (oracle/_ref, "
+                   f"g++ -O2): generate_maps + build_slices (all {DEPTHS} depths) + aggregate + "
+                   f"compute_mask + FdmZone::step; set_worker_count({ncpu})"),
     }
+    if one is not None:
+        out["one_worker"] = {"value": POINTS_PER_FRAME / one, "ms_per_frame": one * 1e3, "cores": 1}
+    return out
 
 
 def run_reference(args):
@@ -670,8 +865,9 @@ def run_reference(args):
     if rank != 0:
         return
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    budget = 150.0
-    cb = cpu_baseline(frames=args.steps, warmup=min(args.warmup, 1), budget_s=budget)
+    warmup = max(args.warmup, 3) if not args.reference_fast_warmup else 1
+    # bounded: the warm-up frames plus timed frames until ~100 s are spent
+    cb = cpu_baseline(frames=args.steps, warmup=warmup, budget_s=100.0)
     line = {
         "impl": "reference",
         "metric": "ocean grid points/sec (spectrum+iFFT+forces) at 1024^2 x 4 cascades",
@@ -680,17 +876,20 @@ def run_reference(args):
         "n_gpus": world,
         "steps": cb["frames"],
         "steps_requested": args.steps,
-        "warmup": min(args.warmup, 1),
+        "warmup": warmup,
         "ms_per_step": cb["ms_per_frame"],
         "ms_per_frame": cb["ms_per_frame"],
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic (SURVEY 8d config 3)",
+        "data": "synthetic (SURVEY 8d spectrum presets; UV-ellipsoid hull)",
         "config": {"workload": WORKLOAD, "grid": N_GRID, "cascades": len(LENGTHS),
-                   "depth_slices": DEPTHS, "fdm_grid": FDM_N, "parallelism": "host CPU"},
-        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                   "depth_slices": DEPTHS, "hull_triangles": 100352, "fdm_grid": FDM_N,
+                   "parallelism": "host CPU",
+                   "frame_pipeline": "off (the reference steps frames in order)",
+                   "l2": "n/a (CPU)"},
+        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "cpu_model", "kind", "sample")},
         "e2e": {"value": cb["value"], "unit": "grid-points/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "stage_s": cb["stage_s"],
@@ -707,9 +906,14 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pipeline", action="store_true",
                     help="config 3: run every frame's stages in order on one stream")
-    ap.add_argument("--config", type=int, default=3, choices=[3, 4, 5],
-                    help="3: the BASELINE metric frame (default); 4: 64 batched 512^2 instances; "
-                         "5: single 16384^2 grid, slab FFT + all-to-all across ranks")
+    ap.add_argument("--config", type=int, default=3, choices=[1, 3, 4, 5],
+                    help="3: the BASELINE metric frame (default); 1: 600 batched 256^2 frames; "
+                         "4: 64 batched 512^2 instances; 5: single 16384^2 grid, slab FFT + "
+                         "all-to-all across ranks")
+    ap.add_argument("--no-extra-configs", action="store_true",
+                    help="config 3: do not also measure configs 1, 4 and 5 in the same run")
+    ap.add_argument("--reference-fast-warmup", action="store_true",
+                    help="reference arm: one warm-up frame instead of our arm's warm-up count")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -288,6 +288,19 @@ OCN_API int ocn_cascades_create_multi(ocn_ctx* ctx, int resolution, int count,
                                       const double* host_band_max,
                                       const uint32_t* host_cascade_index,
                                       const ocn_spectrum_params* params, ocn_cascades** out);
+/* Time-batched spectral set (generate_maps is a pure function
+ * of t, surface.cpp:70-103): `frames` copies of a `count`-grid cascade set; grid
+ * f * count + c is grid c evaluated at t + f dt. The spectrum tables exist once
+ * per grid c. Maps of the set are laid out [frames][count][8][N][N]; dt is the
+ * spacing ocn_surface_generate / ocn_spectral_step use (ocn_surface_generate_batch
+ * passes its own). Info / download / assemble calls take any grid index
+ * (frame f's grid c downloads grid c's spectrum). Samplers reject such maps. */
+OCN_API int ocn_cascades_create_frames(ocn_ctx* ctx, int resolution, int count,
+                                       const double* host_lengths, const double* host_band_min,
+                                       const double* host_band_max,
+                                       const uint32_t* host_cascade_index,
+                                       const ocn_spectrum_params* params, int frames, double dt,
+                                       ocn_cascades** out);
 OCN_API int ocn_cascades_destroy(ocn_cascades* c);
 OCN_API int ocn_cascades_info(const ocn_cascades* c, int* resolution, int* count);
 /* WaveGrid accessors (spectra.hpp:95-104): h0 / h0_conj_neg as interleaved
@@ -310,6 +323,15 @@ OCN_API int ocn_maps_destroy(ocn_maps* m);
 /* generate_maps (surface.cpp:70-103), (async). Same pairing as
  * surface.cpp:77-80; each pair is one C2C inverse FFT of X + iY. */
 OCN_API int ocn_surface_generate(ocn_maps* m, double t, double choppiness);
+/* generate_maps of every frame of a time-batched set at t0 + f dt, (async). On an
+ * ordinary set it equals ocn_surface_generate(m, t0, choppiness). */
+OCN_API int ocn_surface_generate_batch(ocn_maps* m, double t0, double dt, double choppiness);
+/* North-star item 3 on the grid: with enable != 0 every
+ * spectral step of these maps also writes, per texel of every grid, the slope
+ * normal (-Hx, 1, -Hz)/|.| and the Jacobian J = (1 - DxDx)(1 - DzDz) - DzDx^2
+ * of X = p + D into fp32 planes [grid][4][N][N] (nx, ny, nz, J). */
+OCN_API int ocn_maps_set_assembly(ocn_maps* m, int enable);
+OCN_API int ocn_maps_download_assembly(ocn_maps* m, int cascade, int component, float* host_out);
 OCN_API int ocn_maps_time(const ocn_maps* m, double* t);
 OCN_API int ocn_maps_download(ocn_maps* m, int cascade, int field, double* host_out);
 OCN_API int ocn_maps_download_f32(ocn_maps* m, int cascade, int field, float* host_out);
@@ -334,6 +356,26 @@ OCN_API int ocn_slices_download(ocn_slices* s, int depth, int cascade, int compo
 /* Fused per-frame spectral step: maps and (optional) slices at time t in one
  * enqueued graph (async). Equivalent to ocn_surface_generate + ocn_velocity_build. */
 OCN_API int ocn_spectral_step(ocn_maps* m, ocn_slices* s, double t, double choppiness);
+
+/* One packed transform of the spectral step of (maps, slices), in plan order:
+ * the surface pairs of every grid (surface.cpp:77-80), then per grid the
+ * (vx, vz) transform of every depth and the vy transforms across adjacent
+ * depths (velocity.cpp:145-172). */
+typedef struct ocn_xform_info {
+  int32_t cascade;
+  int32_t kind;     /* 0..3 surface pairs; 4 (vx, vz)_d; 5 (vy_d, vy_d+1); 6 (vy_d, 0) */
+  int32_t index0;   /* surface: field of Re; velocity: depth index d of Re             */
+  int32_t index1;   /* surface: field of Im; velocity: depth index of Im (-1: none)     */
+  int32_t row_half; /* spectrum rows |i - N/2| >= row_half are exactly zero in fp32 and
+                       skipped (band edge, or attenuation below 2^-132 at the depth)    */
+  int32_t executed; /* 0: the whole transform is exactly zero at its depth(s): its
+                       planes are zeroed once when the plan is built, never per frame */
+  double y0, y1;    /* slice depths of the velocity kinds                              */
+} ocn_xform_info;
+/* The transform list of ocn_spectral_step(m, s) (builds the plan if needed).
+ * count = total transforms; the first min(capacity, count) are copied to out. */
+OCN_API int ocn_spectral_plan_info(ocn_maps* m, ocn_slices* s, int capacity, ocn_xform_info* out,
+                                   int* count);
 
 /* ============================= standalone FFT ============================= */
 /* ifft2_centered (fft.cpp:69-77) and ifft2_hermitian_pair (fft.cpp:79-101) on

@@ -1450,3 +1450,165 @@ int orc_aggregate(int nv, const double* verts, int nt, const int32_t* tris,
   vstore(r->torque, T);
   return OCN_OK;
 }
+
+/* ======================================================================== */
+/* Large single grids (16384^2 cannot hold CascadeSet + generate_maps
+ * in host memory). One packed surface pair of one grid, computed mode by mode:
+ * h0(i, j) is a pure function of (i, j) (counter-based Philox, spectra.cpp:150-169),
+ * so h0 and conj(h0(-k)) (spectra.cpp:171-177) are evaluated on the fly instead
+ * of being stored; the two coefficients of the pair follow surface.cpp:45-66
+ * exactly as orc_assemble_coefficients, are packed as fft.cpp:88-91, and the
+ * packed field goes through the same radix-2 ifft2_centered (fft.cpp:39-77) with
+ * rows / columns spread over `threads` OpenMP threads (each row / column
+ * transform is unchanged, so the result does not depend on the thread count).
+ * Before the transform, the packed spectrum is also summed directly at the
+ * grid nodes `ab` (npts pairs a, b): out[a, b] = sum_{i,j} P(i, j)
+ * e^{+2 pi i ((i - N/2) a + (j - N/2) b) / N}, the definition fft.hpp:10-17 the
+ * FFT implements (an independent check of the transform at spot points). */
+static void h0_mode_at(int n, double dk, double length, double bmin, double bmax,
+                       const ocn_spectrum_params* p, uint32_t cascade, int i, int j,
+                       int* banded_out, double out[2]) {
+  double kx = dk * (i - n / 2);
+  double kz = dk * (j - n / 2);
+  double k = hypot(kx, kz);
+  double omega = orc_dispersion(k, p->gravity);
+  int banded = k > 0.0 && k >= bmin && k < bmax;
+  if (banded_out) *banded_out = banded;
+  out[0] = out[1] = 0.0;
+  if (!banded) return;
+  double xi[2];
+  orc_gaussian_complex(p->rng_seed, cascade, (uint32_t)i, (uint32_t)j, xi);
+  double amp = sqrt(orc_h0_variance(kx, kz, k, omega, length, p));
+  out[0] = xi[0] * amp;
+  out[1] = xi[1] * amp;
+}
+
+static void ifft2_centered_mt(int n, double* f, int threads) {
+  double* tw = (double*)malloc(sizeof(double) * (size_t)n);
+  for (int j = 0; j < n / 2; ++j) {
+    tw[2 * j] = cos(2.0 * KPI * j / n);
+    tw[2 * j + 1] = sin(2.0 * KPI * j / n);
+  }
+#pragma omp parallel for schedule(dynamic, 16) num_threads(threads)
+  for (int i = 0; i < n; ++i) fft1d(f + 2 * (size_t)i * n, n, tw);
+  const int CB = 8; /* columns gathered together (same per-column arithmetic) */
+#pragma omp parallel num_threads(threads)
+  {
+    double* col = (double*)malloc(sizeof(double) * 2 * (size_t)n * CB);
+#pragma omp for schedule(dynamic, 1)
+    for (int j0 = 0; j0 < n; j0 += CB) {
+      int cb = n - j0 < CB ? n - j0 : CB;
+      for (int i = 0; i < n; ++i)
+        for (int c = 0; c < cb; ++c) {
+          col[2 * ((size_t)c * n + i)] = f[2 * ((size_t)i * n + j0 + c)];
+          col[2 * ((size_t)c * n + i) + 1] = f[2 * ((size_t)i * n + j0 + c) + 1];
+        }
+      for (int c = 0; c < cb; ++c) fft1d(col + 2 * (size_t)c * n, n, tw);
+      for (int i = 0; i < n; ++i)
+        for (int c = 0; c < cb; ++c) {
+          double sgn = ((i + j0 + c) & 1) ? -1.0 : 1.0;
+          f[2 * ((size_t)i * n + j0 + c)] = sgn * col[2 * ((size_t)c * n + i)];
+          f[2 * ((size_t)i * n + j0 + c) + 1] = sgn * col[2 * ((size_t)c * n + i) + 1];
+        }
+    }
+    free(col);
+  }
+  free(tw);
+}
+
+int orc_surface_pair_large(int n, double length, double band_min, double band_max,
+                           const ocn_spectrum_params* p, uint32_t cascade, double t, double chop,
+                           int pair, int threads, int npts, const int32_t* ab, double* direct,
+                           double* re, double* im) {
+  static const int pairs[4][2] = {{0, 1}, {2, 3}, {4, 5}, {6, 7}};
+  if (!is_pow2(n) || n < 2 || !(length > 0.0) || pair < 0 || pair > 3) return OCN_ERR_CONFIG;
+  int st = orc_spectrum_validate(p);
+  if (st) return st;
+  if (threads < 1) threads = 1;
+  size_t nn = (size_t)n * n;
+  double* packed = (double*)malloc(2 * nn * sizeof(double));
+  if (!packed) return OCN_ERR_ARG;
+  const double dk = 2.0 * KPI / length;
+  const double gravity = p->gravity;
+#pragma omp parallel for schedule(dynamic, 4) num_threads(threads)
+  for (int i = 0; i < n; ++i) {
+    const int ni = neg_index(i, n);
+    for (int j = 0; j < n; ++j) {
+      size_t q = (size_t)i * n + j;
+      double a[2], m[2];
+      int banded;
+      h0_mode_at(n, dk, length, band_min, band_max, p, cascade, i, j, &banded, a);
+      double f[8][2];
+      memset(f, 0, sizeof f);
+      if (banded) {
+        h0_mode_at(n, dk, length, band_min, band_max, p, cascade, ni, neg_index(j, n), NULL, m);
+        const double h0cr = m[0], h0ci = -m[1];
+        /* surface.cpp:45-66, operation order of orc_assemble_coefficients */
+        double kx = dk * (i - n / 2), kz = dk * (j - n / 2);
+        double k = hypot(kx, kz);
+        double omega = sqrt(gravity * k);
+        double cr = cos(omega * t), si = sin(omega * t);
+        double ar, ai, br, bi;
+        cmul(a[0], a[1], cr, si, &ar, &ai);
+        cmul(h0cr, h0ci, cr, -si, &br, &bi);
+        double htr = ar + br, hti = ai + bi;
+        double ux = kx / k, uz = kz / k;
+        double tr, ti, dxr, dxi, dzr, dzi;
+        cmul(0.0 * ux, 1.0 * ux, htr, hti, &tr, &ti);
+        dxr = tr * chop;
+        dxi = ti * chop;
+        cmul(0.0 * uz, 1.0 * uz, htr, hti, &tr, &ti);
+        dzr = tr * chop;
+        dzi = ti * chop;
+        f[0][0] = htr;
+        f[0][1] = hti;
+        f[1][0] = dxr;
+        f[1][1] = dxi;
+        f[2][0] = dzr;
+        f[2][1] = dzi;
+        cmul(0.0, -kx, dxr, dxi, &f[3][0], &f[3][1]);
+        cmul(0.0, -kx, dzr, dzi, &f[4][0], &f[4][1]);
+        cmul(0.0, -kz, dzr, dzi, &f[5][0], &f[5][1]);
+        cmul(0.0, kx, htr, hti, &f[6][0], &f[6][1]);
+        cmul(0.0, kz, htr, hti, &f[7][0], &f[7][1]);
+      }
+      const double* x = f[pairs[pair][0]];
+      const double* y = f[pairs[pair][1]];
+      packed[2 * q] = x[0] + (0.0 * y[0] - 1.0 * y[1]);
+      packed[2 * q + 1] = x[1] + (0.0 * y[1] + 1.0 * y[0]);
+    }
+  }
+  if (npts > 0 && direct) {
+    double* tw = (double*)malloc(2 * sizeof(double) * (size_t)n);
+    for (int q = 0; q < n; ++q) {
+      tw[2 * q] = cos(2.0 * KPI * q / n);
+      tw[2 * q + 1] = sin(2.0 * KPI * q / n);
+    }
+    for (int s = 0; s < npts; ++s) {
+      const long long a = ab[2 * s], b = ab[2 * s + 1];
+      double sr = 0.0, si = 0.0;
+#pragma omp parallel for reduction(+ : sr, si) schedule(static) num_threads(threads)
+      for (int i = 0; i < n; ++i) {
+        const long long pa = (long long)(i - n / 2) * a;
+        for (int j = 0; j < n; ++j) {
+          long long ph = (pa + (long long)(j - n / 2) * b) % n;
+          if (ph < 0) ph += n;
+          const double* w = tw + 2 * ph;
+          const double* v = packed + 2 * ((size_t)i * n + j);
+          sr += v[0] * w[0] - v[1] * w[1];
+          si += v[0] * w[1] + v[1] * w[0];
+        }
+      }
+      direct[2 * s] = sr;
+      direct[2 * s + 1] = si;
+    }
+    free(tw);
+  }
+  ifft2_centered_mt(n, packed, threads);
+  for (size_t q = 0; q < nn; ++q) {
+    if (re) re[q] = packed[2 * q];
+    if (im) im[q] = packed[2 * q + 1];
+  }
+  free(packed);
+  return OCN_OK;
+}

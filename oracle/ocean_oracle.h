@@ -61,6 +61,15 @@ int orc_assemble_coefficients(int n, double length, double gravity, const double
                               const double* h0cn, const uint8_t* in_band, double t,
                               double choppiness, double* out);
 /* generate_maps surface.cpp:70-103; maps = [C][8][n*n]. */
+/* One packed surface pair of a grid too large for generate_maps on the host
+ * (16384^2): h0 per mode on the fly, surface.cpp:45-66 coefficients of pair
+ * `pair` (surface.cpp:77-80 order), fft.cpp:79-101 packed transform with rows /
+ * columns over `threads` OpenMP threads; optional direct sums of the packed
+ * spectrum at npts grid nodes ab = (a, b) pairs -> direct (re, im). */
+int orc_surface_pair_large(int n, double length, double band_min, double band_max,
+                           const ocn_spectrum_params* p, uint32_t cascade, double t, double chop,
+                           int pair, int threads, int npts, const int32_t* ab, double* direct,
+                           double* re, double* im);
 int orc_generate_maps(int n, int C, const double* lengths, double gravity, const double* h0,
                       const double* h0cn, const uint8_t* in_band, double t, double choppiness,
                       int single_precision, double* maps);

@@ -224,6 +224,27 @@ class Oracle:
                    int(single_precision), P(maps)), "generate_maps")
         return maps
 
+    def surface_pair_large(self, n, length, band_min, band_max, params, t, pair, choppiness=1.0,
+                           cascade=0, threads=None, ab=None):
+        """Port only: one packed surface pair of a single large grid (fft.cpp:79-101
+        on the surface.cpp:45-66 coefficients, h0 per mode on the fly) -> (re, im)
+        [n, n] fp64, plus the direct sums of the packed spectrum at the grid
+        nodes ab ([k, 2] ints) -> complex [k] (None without ab)."""
+        assert self.kind == "port"
+        f = self.lib.orc_surface_pair_large
+        f.argtypes = [C.c_int, C.c_double, C.c_double, C.c_double, C.POINTER(SpectrumParams),
+                      C.c_uint32, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int, _i32, _d, _d,
+                      _d]
+        threads = threads or os.cpu_count() or 1
+        re = np.zeros((n, n))
+        im = np.zeros((n, n))
+        npts = 0 if ab is None else len(ab)
+        ab_a = np.ascontiguousarray(ab if ab is not None else np.zeros((0, 2)), np.int32)
+        direct = np.zeros(2 * max(npts, 1))
+        _chk(f(n, length, band_min, band_max, C.byref(params), cascade, t, choppiness, pair, threads,
+               npts, P(ab_a, _i32), P(direct), P(re), P(im)), "surface_pair_large")
+        return re, im, (direct[:2 * npts].view(np.complex128) if npts else None)
+
     def build_slices(self, n, lengths, cutoffs, params, t, cfg: SliceConfig, tables=None):
         """-> (depths [D], slices [D, C, 3, n, n])."""
         C_ = len(lengths)

@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 from ._types import (Fluid, FdmConfig, HydroReport, MaskFrame, MaskParams, Pose, SliceConfig,
-                     SpectrumParams, TriangleState, ZoneState, BodyFrame)
+                     SpectrumParams, TriangleState, ZoneState, BodyFrame, XformInfo)
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 # OCN_LIB: an alternative build of the same library (kernel-variant experiments)
@@ -101,6 +101,8 @@ SIGNATURES = {
     "ocn_slice_depths": (ci, [C.POINTER(SliceConfig), d]),
     "ocn_cascades_create": (ci, [vp, ci, ci, d, d, d, u32, C.POINTER(SpectrumParams), pvp]),
     "ocn_cascades_create_multi": (ci, [vp, ci, ci, d, d, d, u32, C.POINTER(SpectrumParams), pvp]),
+    "ocn_cascades_create_frames": (ci, [vp, ci, ci, d, d, d, u32, C.POINTER(SpectrumParams), ci, cd,
+                                        pvp]),
     "ocn_cascades_destroy": (ci, [vp]),
     "ocn_cascades_info": (ci, [vp, C.POINTER(ci), C.POINTER(ci)]),
     "ocn_cascades_download": (ci, [vp, ci, d, d, u8, d]),
@@ -111,6 +113,9 @@ SIGNATURES = {
     "ocn_maps_destroy": (ci, [vp]),
     "ocn_surface_generate": (ci, [vp, cd, cd]),
     "ocn_maps_time": (ci, [vp, d]),
+    "ocn_surface_generate_batch": (ci, [vp, cd, cd, cd]),
+    "ocn_maps_set_assembly": (ci, [vp, ci]),
+    "ocn_maps_download_assembly": (ci, [vp, ci, ci, f32]),
     "ocn_maps_download": (ci, [vp, ci, ci, d]),
     "ocn_maps_download_f32": (ci, [vp, ci, ci, f32]),
     "ocn_maps_device_field": (ci, [vp, ci, ci, C.POINTER(f32)]),
@@ -120,6 +125,7 @@ SIGNATURES = {
     "ocn_slices_depths": (ci, [vp, C.POINTER(ci), d]),
     "ocn_slices_download": (ci, [vp, ci, ci, ci, d]),
     "ocn_spectral_step": (ci, [vp, vp, cd, cd]),
+    "ocn_spectral_plan_info": (ci, [vp, vp, ci, C.POINTER(XformInfo), C.POINTER(ci)]),
     "ocn_ifft2_centered": (ci, [vp, ci, d, d]),
     "ocn_ifft2_pair": (ci, [vp, ci, d, d, d, d]),
     "ocn_maps_sample": (ci, [vp, ci, i64, d, d]),

@@ -232,3 +232,18 @@ class BodyFrame(C.Structure):
         ("frame", MaskFrame),
         ("mask", MaskParams),
     ]
+
+
+class XformInfo(C.Structure):
+    """ocn_xform_info — one packed transform of a spectral step's plan."""
+
+    _fields_ = [
+        ("cascade", C.c_int32),
+        ("kind", C.c_int32),
+        ("index0", C.c_int32),
+        ("index1", C.c_int32),
+        ("row_half", C.c_int32),
+        ("executed", C.c_int32),
+        ("y0", C.c_double),
+        ("y1", C.c_double),
+    ]

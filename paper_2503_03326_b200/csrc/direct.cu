@@ -194,6 +194,7 @@ extern "C" {
 int ocn_direct_create(ocn_cascades* cas, double t, ocn_direct** out) {
   return api_call(cas ? cas->ctx : nullptr, [&] {
     OCN_REQUIRE(cas && out, "null argument");
+    if (cas->frames > 1) fail(OCN_ERR_CONFIG, "the direct evaluator takes one frame's cascade set");
     ocn_ctx* ctx = cas->ctx;
     DeviceScope ds(ctx);
     const int n = cas->n, C = cas->count, rows = C * n;

@@ -25,6 +25,10 @@ struct GridConst {
   // exactly zero. N/2 + 1 when every row can carry the band.
   int32_t row_half;
   ocn_spectrum_params p;
+  // time-batched sets: grid g reads the h0 / w tables of
+  // grid `src` and is evaluated at t + frame dt (src = g, frame = 0 otherwise)
+  int32_t src;
+  int32_t frame;
 };
 
 // A run of consecutive transforms of one grid inside a transform group.
@@ -78,17 +82,13 @@ struct SpectralPlan {
   ~SpectralPlan() {
     if (exec) cudaGraphExecDestroy(exec);
   }
-  // fused row + column step (N = 1024): waves, column-tile prefix, counters
-  bool fused = false;
-  int nwaves = 0;
-  DevBuf<int> fused_waves;  // FusedWave[nwaves] (4 ints each)
-  DevBuf<int> fused_tile0;  // [nwaves + 1]
-  DevBuf<int> fused_ctr;    // [2 + 2 nwaves]
   std::vector<XformDesc> host_desc;
+  std::vector<ocn_xform_info> info;  // every transform of the step, incl. the dropped ones
   std::vector<int> first;  // per cascade: first transform index
   std::vector<int> count;  // per cascade: number of transforms
   bool need_surface = false, need_velocity = false;
   int zero_transforms = 0;  // velocity transforms dropped as exactly zero (planes zeroed once)
+  bool assembly = false;    // the captured graph includes the per-texel assembly
 };
 
 }  // namespace ocn
@@ -113,11 +113,12 @@ struct ocn_cascades {
   ocn::DevBuf<float2> scratch;  // row-pass intermediates of one transform group
   ocn::DevBuf<double> d_time;   // frame time read by k_evolve (set per frame)
   int group = 1;                // transforms per group
+  int base = 0;                 // grids holding tables (count / frames)
+  int frames = 1;               // time-batched set: count = base x frames
+  double frame_dt = 0.0;        // default frame spacing of a time-batched set
   CUtensorMap cols_map;         // TMA source map of the scratch (column pass)
   CUtensorMap cols_chunk_map;   // same, 32-row chunks (band-limited loads)
   bool cols_map_ok = false;
-  CUtensorMap fused_map;        // TMA source map of the fused step's column tiles
-  bool fused_ok = false;
   std::map<std::pair<const void*, const void*>, std::unique_ptr<ocn::SpectralPlan>> plans;
 };
 
@@ -127,6 +128,9 @@ struct ocn_maps {
   double choppiness = 1.0;
   ocn::DevBuf<float> fields;  // [C][8][N][N]
   float* field(int c, int f) { return fields.p + ((size_t)c * 8 + f) * (size_t)cas->n * cas->n; }
+  // per-texel normal + Jacobian planes [C][4][N][N] (ocn_maps_set_assembly)
+  bool assembly = false;
+  ocn::DevBuf<float> assembled;
 };
 
 struct ocn_slices {
@@ -176,7 +180,8 @@ void ctx_retain(ocn_ctx* ctx);
 void ctx_release(ocn_ctx* ctx);
 
 // Spectral engine (spectral.cu)
+// dt < 0: the set's own frame spacing (time-batched sets, ocn_cascades_create_frames)
 void spectral_step(ocn_cascades* cas, ocn_maps* maps, ocn_slices* slices, double t,
-                   double choppiness);
+                   double choppiness, double dt = -1.0);
 
 }  // namespace ocn

@@ -8,6 +8,9 @@
 namespace ocn {
 
 SurfView make_surf_view(ocn_maps* m) {
+  if (m->cas->frames > 1)
+    fail(OCN_ERR_CONFIG, "samplers need one frame's maps (this set batches %d frames)",
+         m->cas->frames);
   if (m->cas->count > kMaxCascades)
     fail(OCN_ERR_CONFIG, "samplers sum at most %d cascades (maps of a %d-grid set)", kMaxCascades,
          m->cas->count);
@@ -20,6 +23,9 @@ SurfView make_surf_view(ocn_maps* m) {
 }
 
 SliceView make_slice_view(ocn_slices* s) {
+  if (s->cas->frames > 1)
+    fail(OCN_ERR_CONFIG, "samplers need one frame's slices (this set batches %d frames)",
+         s->cas->frames);
   if (s->cas->count > kMaxCascades)
     fail(OCN_ERR_CONFIG, "samplers sum at most %d cascades (slices of a %d-grid set)", kMaxCascades,
          s->cas->count);

@@ -284,11 +284,10 @@ static bool cols_ldg() {
 }
 
 // chunk: the 32-row chunk map of the band-limited loads (box {2 PC, 32, 1, 1})
-bool cols_map_for(int n, int G, const float2* scratch, CUtensorMap* map, int pc_fused = 0,
-                  bool chunk = false) {
-  const int pc = pc_fused ? pc_fused : cols_tma_pc(n);
+bool cols_map_for(int n, int G, const float2* scratch, CUtensorMap* map, bool chunk = false) {
+  const int pc = cols_tma_pc(n);
   const int br = chunk ? std::min(32, n) : (n < 256 ? n : 256);
-  if (!pc || (!pc_fused && cols_ldg())) return false;
+  if (!pc || cols_ldg()) return false;
   const uint64_t dims[4] = {2ull * n, (uint64_t)br, (uint64_t)(n / br), (uint64_t)G};
   const uint64_t strides[3] = {2ull * n * 4, (uint64_t)br * 2 * n * 4, (uint64_t)n * n * 8};
   const uint32_t box[4] = {2u * pc, (uint32_t)br, chunk ? 1u : (uint32_t)(n / br), 1u};
@@ -331,24 +330,10 @@ static void build_out_maps(int n, const XformDesc* desc, int count, DevBuf<CUten
   OCN_CUDA(cudaMemcpy(out.p, h.data(), h.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
 }
 
-// The fused row + column step (spectral_fused.cuh, N = 1024) is opt-in
-// (OCN_FUSED=1): measured on B200 (config 3 spectral, ms / frame) 1.88-2.35
-// across wave sizes 8-24 and 2-4 slots, against 1.12 for the two-kernel step.
-// With one 12-warp CTA per SM each row task and column tile exposes its load
-// latency and barrier waits, and the scratch still round-trips HBM
-// (1.7 GB read + 3.4 GB written per frame in the capture).
 static bool band_skip_enabled() {
   static const bool on = [] {
     const char* e = getenv("OCN_NO_BAND_SKIP");
     return !(e && *e && *e != '0');
-  }();
-  return on;
-}
-
-static bool fused_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("OCN_FUSED");
-    return e && *e && *e != '0';
   }();
   return on;
 }
@@ -390,24 +375,32 @@ static SpectralPlan* get_plan(ocn_cascades* cas, ocn_maps* maps, ocn_slices* sli
                                     {OCN_FIELD_DZDX, OCN_FIELD_DZDZ},
                                     {OCN_FIELD_HX, OCN_FIELD_HZ}};
     for (int c = 0; c < cas->count; ++c)
-      for (int p = 0; p < 4; ++p)
+      for (int p = 0; p < 4; ++p) {
         plan->host_desc.push_back({c, p, 0.f, 0.f, maps->field(c, pairs[p][0]),
                                    maps->field(c, pairs[p][1])});
+        plan->info.push_back({c, p, pairs[p][0], pairs[p][1], 0, 1, 0.0, 0.0});
+      }
   }
   if (slices) {
     const int D = slices->cfg.count;
     for (int c = 0; c < cas->count; ++c) {
-      for (int d = 0; d < D; ++d)
+      for (int d = 0; d < D; ++d) {
         plan->host_desc.push_back({c, kVelXZ, (float)slices->depths[d], 0.f,
                                    slices->field(d, c, 0), slices->field(d, c, 2)});
+        plan->info.push_back({c, kVelXZ, d, d, 0, 1, slices->depths[d], 0.0});
+      }
       for (int d0 = 0; d0 < D; d0 += 2) {
-        if (d0 + 1 < D)
+        if (d0 + 1 < D) {
           plan->host_desc.push_back({c, kVelYPair, (float)slices->depths[d0],
                                      (float)slices->depths[d0 + 1], slices->field(d0, c, 1),
                                      slices->field(d0 + 1, c, 1)});
-        else
+          plan->info.push_back({c, kVelYPair, d0, d0 + 1, 0, 1, slices->depths[d0],
+                                slices->depths[d0 + 1]});
+        } else {
           plan->host_desc.push_back({c, kVelYSingle, (float)slices->depths[d0], 0.f,
                                      slices->field(d0, c, 1), nullptr});
+          plan->info.push_back({c, kVelYSingle, d0, -1, 0, 1, slices->depths[d0], 0.0});
+        }
       }
     }
   }
@@ -438,7 +431,8 @@ static SpectralPlan* get_plan(ocn_cascades* cas, ocn_maps* maps, ocn_slices* sli
       return rh > cas->n / 2 ? cas->n / 2 + 1 : (int)rh;
     };
     std::vector<XformDesc> keep;
-    for (XformDesc d : plan->host_desc) {
+    for (size_t xi = 0; xi < plan->host_desc.size(); ++xi) {
+      XformDesc d = plan->host_desc[xi];
       {
         const double rg = std::ceil(cas->band_max[d.cascade] * (1.0 + 1e-9) /
                                     (2.0 * kPi / cas->lengths[d.cascade]));
@@ -449,6 +443,7 @@ static SpectralPlan* get_plan(ocn_cascades* cas, ocn_maps* maps, ocn_slices* sli
           d.row_half = std::min(d.row_half, std::max(depth_rows(d.cascade, d.y0),
                                                      depth_rows(d.cascade, d.y1)));
       }
+      plan->info[xi].row_half = d.row_half;
       bool zero = false;
       if (skip && d.kind == kVelXZ) zero = dead(d.cascade, d.y0);
       else if (skip && d.kind == kVelYPair) zero = dead(d.cascade, d.y0) && dead(d.cascade, d.y1);
@@ -457,6 +452,7 @@ static SpectralPlan* get_plan(ocn_cascades* cas, ocn_maps* maps, ocn_slices* sli
         keep.push_back(d);
         continue;
       }
+      plan->info[xi].executed = 0;
       const size_t bytes = (size_t)cas->n * cas->n * sizeof(float);
       OCN_CUDA(cudaMemsetAsync(d.out_re, 0, bytes, cas->ctx->stream));
       if (d.out_im) OCN_CUDA(cudaMemsetAsync(d.out_im, 0, bytes, cas->ctx->stream));
@@ -494,30 +490,6 @@ static SpectralPlan* get_plan(ocn_cascades* cas, ocn_maps* maps, ocn_slices* sli
     plan->groups.push_back(gr);
     g0 += cnt;
   }
-  if (cas->fused_ok && total > 0) {
-    // waves: runs of <= kFuseW consecutive transforms of one grid and family
-    std::vector<FusedWave> waves;
-    std::vector<int> tile0{0};
-    for (int i = 0; i < total;) {
-      const int c = plan->host_desc[i].cascade, f = family(i);
-      int cnt = 1;
-      while (i + cnt < total && cnt < kFuseW && plan->host_desc[i + cnt].cascade == c &&
-             family(i + cnt) == f)
-        ++cnt;
-      waves.push_back({c, f, i, cnt});
-      tile0.push_back(tile0.back() + cnt * Fused<1024>::TILES_PER_XF);
-      i += cnt;
-    }
-    plan->nwaves = (int)waves.size();
-    plan->fused_waves.alloc(4 * waves.size());
-    OCN_CUDA(cudaMemcpy(plan->fused_waves.p, waves.data(), waves.size() * sizeof(FusedWave),
-                        cudaMemcpyHostToDevice));
-    plan->fused_tile0.alloc(tile0.size());
-    OCN_CUDA(cudaMemcpy(plan->fused_tile0.p, tile0.data(), tile0.size() * sizeof(int),
-                        cudaMemcpyHostToDevice));
-    plan->fused_ctr.alloc(2 + 2 * waves.size());
-    plan->fused = true;
-  }
   plan->segs.alloc(std::max<size_t>(segs.size(), 1));
   if (!segs.empty())
     OCN_CUDA(cudaMemcpy(plan->segs.p, segs.data(), segs.size() * sizeof(GroupSeg),
@@ -536,7 +508,17 @@ static void forget_plans(ocn_cascades* cas, const void* obj) {
   }
 }
 
-static void enqueue_spectral(ocn_cascades* cas, SpectralPlan* plan, double choppiness) {
+static void assemble_grids(ocn_maps* m, cudaStream_t st) {
+  ocn_ctx* ctx = m->cas->ctx;
+  const size_t nn = (size_t)m->cas->n * m->cas->n;
+  OCN_REQUIRE(nn % 4 == 0 && m->assembled.p, "assembly planes missing");
+  k_assemble_grid<<<grid_for(ctx, nn / 4 * m->cas->count), 256, 0, st>>>(m->cas->count, nn,
+                                                                         m->fields.p, m->assembled.p);
+  OCN_LAUNCHED(ctx);
+}
+
+static void enqueue_spectral(ocn_cascades* cas, SpectralPlan* plan, ocn_maps* maps,
+                             double choppiness) {
   ocn_ctx* ctx = cas->ctx;
   const int n = cas->n;
   const size_t nn = (size_t)n * n;
@@ -545,44 +527,17 @@ static void enqueue_spectral(ocn_cascades* cas, SpectralPlan* plan, double chopp
   {
     ProfWindow pw(ctx, OCN_PROF_EVOLVE);  // every grid in one launch
     // skip never-read rows only where every reader is a band-aware warp row kernel
-    const GridConst* gcs = (n >= 128 && n <= 1024 && !plan->fused && cas->cols_map_ok &&
-                            band_skip_enabled())
-                               ? cas->gconst.p
-                               : nullptr;
+    const int skip = n >= 128 && n <= 1024 && cas->cols_map_ok && band_skip_enabled() ? 1 : 0;
+    const size_t total = nn * cas->count;
     if (plan->need_velocity)
-      k_evolve<true><<<grid_for(ctx, nn * cas->count), 256, 0, A>>>(
-          nn * cas->count, cas->d_time.p, cas->h0p.p, cas->omega.p, cas->spec_h.p, cas->spec_g.p,
-          n, gcs);
+      k_evolve<true><<<grid_for(ctx, total), 256, 0, A>>>(total, ilog2(n), cas->d_time.p,
+                                                          cas->h0p.p, cas->omega.p, cas->spec_h.p,
+                                                          cas->spec_g.p, cas->gconst.p, skip);
     else
-      k_evolve<false><<<grid_for(ctx, nn * cas->count), 256, 0, A>>>(
-          nn * cas->count, cas->d_time.p, cas->h0p.p, cas->omega.p, cas->spec_h.p, nullptr, n, gcs);
+      k_evolve<false><<<grid_for(ctx, total), 256, 0, A>>>(total, ilog2(n), cas->d_time.p,
+                                                           cas->h0p.p, cas->omega.p, cas->spec_h.p,
+                                                           nullptr, cas->gconst.p, skip);
     OCN_LAUNCHED(ctx);
-  }
-  if (plan->fused) {
-    using F = Fused<1024>;
-    static bool attr = false;
-    if (!attr) {
-      OCN_CUDA(cudaFuncSetAttribute(k_spectral_fused<1024>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F::SMEM));
-      attr = true;
-    }
-    FusedArgs fa{};
-    fa.spec_h = cas->spec_h.p;
-    fa.spec_g = cas->spec_g.p;
-    fa.gc = cas->gconst.p;
-    fa.chop = (float)choppiness;
-    fa.desc = plan->desc.p;
-    fa.waves = reinterpret_cast<const FusedWave*>(plan->fused_waves.p);
-    fa.tile0 = plan->fused_tile0.p;
-    fa.nwaves = plan->nwaves;
-    fa.scratch = cas->scratch.p;
-    fa.tw = cas->twiddle.p;
-    fa.ctr = plan->fused_ctr.p;
-    ProfWindow pw(ctx, OCN_PROF_ROWS);  // rows and columns in one kernel
-    OCN_CUDA(cudaMemsetAsync(plan->fused_ctr.p, 0, plan->fused_ctr.bytes(), A));
-    k_spectral_fused<1024><<<ctx->sm_count, F::THREADS, F::SMEM, A>>>(cas->fused_map, fa);
-    OCN_LAUNCHED(ctx);
-    return;
   }
   for (size_t gidx = 0; gidx < plan->groups.size(); ++gidx) {
     const SpectralPlan::Group& gr = plan->groups[gidx];
@@ -618,6 +573,7 @@ static void enqueue_spectral(ocn_cascades* cas, SpectralPlan* plan, double chopp
                     cas->cols_map_ok ? &cas->cols_chunk_map : nullptr);
     }
   }
+  if (plan->assembly && maps) assemble_grids(maps, A);
 }
 
 static bool graphs_enabled() {
@@ -629,12 +585,17 @@ static bool graphs_enabled() {
 }
 
 void spectral_step(ocn_cascades* cas, ocn_maps* maps, ocn_slices* slices, double t,
-                   double choppiness) {
+                   double choppiness, double dt) {
   ocn_ctx* ctx = cas->ctx;
   DeviceScope ds(ctx);
   OCN_REQUIRE(cas->h0.p, "these maps carry no spectrum (ocn_maps_create_bare)");
   SpectralPlan* plan = get_plan(cas, maps, slices);
-  k_set_time<<<1, 1, 0, ctx->stream>>>(cas->d_time.p, t);
+  const bool assembly = maps && maps->assembly;
+  if (plan->assembly != assembly) {  // the captured graph has (or lacks) the assembly node
+    if (plan->exec) cudaGraphExecDestroy(plan->exec), plan->exec = nullptr;
+    plan->assembly = assembly;
+  }
+  k_set_time<<<1, 1, 0, ctx->stream>>>(cas->d_time.p, t, dt < 0.0 ? cas->frame_dt : dt);
   OCN_LAUNCHED(ctx);
   // profiling mode 1 = per-kernel windows (eager launches); mode 2 = stage
   // windows only, the step still replays its graph
@@ -647,7 +608,7 @@ void spectral_step(ocn_cascades* cas, ocn_maps* maps, ocn_slices* slices, double
     ctx->profiling = false;  // no event windows inside the captured graph
     OCN_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeRelaxed));
     try {
-      enqueue_spectral(cas, plan, choppiness);
+      enqueue_spectral(cas, plan, maps, choppiness);
       ctx->profiling = prof;
     } catch (...) {
       ctx->profiling = prof;
@@ -667,7 +628,7 @@ void spectral_step(ocn_cascades* cas, ocn_maps* maps, ocn_slices* slices, double
     OCN_CUDA(cudaGraphLaunch(plan->exec, ctx->stream));
     ctx->launches.fetch_add(plan->graph_kernels);
   } else {
-    enqueue_spectral(cas, plan, choppiness);
+    enqueue_spectral(cas, plan, maps, choppiness);
   }
   ++plan->uses;
   if (maps) {
@@ -894,82 +855,112 @@ int ocn_slice_depths(const ocn_slice_config* cfg, double* depths) {
 }
 
 // ---- cascades (K1)
+// `count` grids with tables (spectrum init, h0 / w tables), each repeated for
+// `frames` frames (time-batched sets; frames = 1 otherwise): grid f * count + c
+// evaluates grid c's spectrum at t + f dt.
+static void cascades_create(ocn_ctx* ctx, int resolution, int count, const double* lengths,
+                            const double* band_min, const double* band_max,
+                            const uint32_t* cascade_index, const ocn_spectrum_params* params,
+                            int frames, double frame_dt, ocn_cascades** out) {
+  OCN_REQUIRE(ctx && out && lengths && band_min && band_max && params, "null argument");
+  OCN_REQUIRE(count >= 1 && count <= kMaxGrids, "grid count %d out of range", count);
+  OCN_REQUIRE(frames >= 1 && (size_t)frames * count <= (size_t)kMaxGrids,
+              "frames x grids %d x %d out of range", frames, count);
+  if (!is_pow2(resolution) || resolution < 2)
+    fail(OCN_ERR_CONFIG, "grid resolution must be a power of two >= 2");
+  if (resolution > 16384) fail(OCN_ERR_CONFIG, "grid resolution above 16384 is not supported");
+  for (int c = 0; c < count; ++c) {
+    if (!(lengths[c] > 0.0)) fail(OCN_ERR_CONFIG, "cascade length must be > 0");
+    if (!(band_min[c] >= 0.0) || !(band_max[c] > band_min[c]))
+      fail(OCN_ERR_CONFIG, "cascade band must satisfy 0 <= band_min < band_max");
+    int st = ocn_spectrum_validate(params + c);
+    if (st) fail(st, "%s", global_error().c_str());
+  }
+  DeviceScope ds(ctx);
+  auto cas = std::make_unique<ocn_cascades>();
+  const int total = count * frames;
+  cas->ctx = ctx;
+  cas->n = resolution;
+  cas->count = total;
+  cas->base = count;
+  cas->frames = frames;
+  cas->frame_dt = frame_dt;
+  for (int f = 0; f < frames; ++f) {
+    cas->lengths.insert(cas->lengths.end(), lengths, lengths + count);
+    cas->band_min.insert(cas->band_min.end(), band_min, band_min + count);
+    cas->band_max.insert(cas->band_max.end(), band_max, band_max + count);
+    for (int c = 0; c < count; ++c)
+      cas->cascade_index.push_back(cascade_index ? cascade_index[c] : (uint32_t)c);
+    cas->grid_params.insert(cas->grid_params.end(), params, params + count);
+  }
+  cas->params = params[0];
+  const size_t nn = (size_t)resolution * resolution;
+  cas->h0_f64.alloc(nn * count);
+  cas->h0.alloc(nn * count);
+  cas->in_band.alloc(nn * count);
+  cas->h0p.alloc(nn * count);
+  cas->omega.alloc(nn * count);
+  cas->spec_h.alloc(nn * total);
+  cas->spec_g.alloc(nn * total);
+  std::vector<GridConst> gc(total);
+  for (int g = 0; g < total; ++g) {
+    const int c = g % count;
+    gc[g].dk = 2.0 * kPi / lengths[c];
+    gc[g].length = lengths[c];
+    gc[g].band_min = band_min[c];
+    gc[g].band_max = band_max[c];
+    gc[g].cindex = cas->cascade_index[c];
+    gc[g].p = params[c];
+    // rows with |kx| >= band_max (1 + 1e-9) are outside the band whatever kz
+    // (hypot(kx, kz) >= |kx|; the margin covers rounding)
+    const double rh = std::ceil(band_max[c] * (1.0 + 1e-9) / gc[g].dk);
+    gc[g].row_half = rh > resolution / 2 ? resolution / 2 + 1 : (int)rh;
+    gc[g].src = c;
+    gc[g].frame = g / count;
+  }
+  cas->gconst.alloc(total);
+  OCN_CUDA(cudaMemcpyAsync(cas->gconst.p, gc.data(), total * sizeof(GridConst),
+                           cudaMemcpyHostToDevice, ctx->stream));
+  k_spectrum_init<<<grid_for(ctx, nn * count), 256, 0, ctx->stream>>>(
+      resolution, count, cas->gconst.p, cas->h0_f64.p, cas->h0.p, cas->in_band.p);
+  OCN_LAUNCHED(ctx);
+  k_evolve_tables<<<grid_for(ctx, nn * count), 256, 0, ctx->stream>>>(
+      resolution, count, cas->gconst.p, cas->h0.p, cas->h0p.p, cas->omega.p);
+  OCN_LAUNCHED(ctx);
+  std::vector<float2> tw = make_twiddles(resolution);
+  cas->twiddle.alloc(tw.size());
+  OCN_CUDA(cudaMemcpyAsync(cas->twiddle.p, tw.data(), tw.size() * sizeof(float2),
+                           cudaMemcpyHostToDevice, ctx->stream));
+  cas->group = (int)group_for(resolution, 1 << 30);
+  cas->d_time.alloc(2);
+  cas->scratch.alloc((size_t)cas->group * nn);
+  cas->cols_map_ok = cols_map_for(resolution, cas->group, cas->scratch.p, &cas->cols_map);
+  if (cas->cols_map_ok)
+    cols_map_for(resolution, cas->group, cas->scratch.p, &cas->cols_chunk_map, true);
+  OCN_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx_retain(ctx);
+  *out = cas.release();
+}
+
 int ocn_cascades_create_multi(ocn_ctx* ctx, int resolution, int count, const double* lengths,
                               const double* band_min, const double* band_max,
                               const uint32_t* cascade_index, const ocn_spectrum_params* params,
                               ocn_cascades** out) {
   return api_call(ctx, [&] {
-    OCN_REQUIRE(ctx && out && lengths && band_min && band_max && params, "null argument");
-    OCN_REQUIRE(count >= 1 && count <= kMaxGrids, "grid count %d out of range", count);
-    if (!is_pow2(resolution) || resolution < 2)
-      fail(OCN_ERR_CONFIG, "grid resolution must be a power of two >= 2");
-    if (resolution > 16384) fail(OCN_ERR_CONFIG, "grid resolution above 16384 is not supported");
-    for (int c = 0; c < count; ++c) {
-      if (!(lengths[c] > 0.0)) fail(OCN_ERR_CONFIG, "cascade length must be > 0");
-      if (!(band_min[c] >= 0.0) || !(band_max[c] > band_min[c]))
-        fail(OCN_ERR_CONFIG, "cascade band must satisfy 0 <= band_min < band_max");
-      int st = ocn_spectrum_validate(params + c);
-      if (st) fail(st, "%s", global_error().c_str());
-    }
-    DeviceScope ds(ctx);
-    auto cas = std::make_unique<ocn_cascades>();
-    cas->ctx = ctx;
-    cas->n = resolution;
-    cas->count = count;
-    cas->lengths.assign(lengths, lengths + count);
-    cas->band_min.assign(band_min, band_min + count);
-    cas->band_max.assign(band_max, band_max + count);
-    for (int c = 0; c < count; ++c)
-      cas->cascade_index.push_back(cascade_index ? cascade_index[c] : (uint32_t)c);
-    cas->params = params[0];
-    cas->grid_params.assign(params, params + count);
-    const size_t nn = (size_t)resolution * resolution;
-    cas->h0_f64.alloc(nn * count);
-    cas->h0.alloc(nn * count);
-    cas->in_band.alloc(nn * count);
-    cas->h0p.alloc(nn * count);
-    cas->omega.alloc(nn * count);
-    cas->spec_h.alloc(nn * count);
-    cas->spec_g.alloc(nn * count);
-    std::vector<GridConst> gc(count);
-    for (int c = 0; c < count; ++c) {
-      gc[c].dk = 2.0 * kPi / lengths[c];
-      gc[c].length = lengths[c];
-      gc[c].band_min = band_min[c];
-      gc[c].band_max = band_max[c];
-      gc[c].cindex = cas->cascade_index[c];
-      gc[c].p = params[c];
-      // rows with |kx| >= band_max (1 + 1e-9) are outside the band whatever kz
-      // (hypot(kx, kz) >= |kx|; the margin covers rounding)
-      const double rh = std::ceil(band_max[c] * (1.0 + 1e-9) / gc[c].dk);
-      gc[c].row_half = rh > resolution / 2 ? resolution / 2 + 1 : (int)rh;
-    }
-    cas->gconst.alloc(count);
-    OCN_CUDA(cudaMemcpyAsync(cas->gconst.p, gc.data(), count * sizeof(GridConst),
-                             cudaMemcpyHostToDevice, ctx->stream));
-    k_spectrum_init<<<grid_for(ctx, nn * count), 256, 0, ctx->stream>>>(
-        resolution, count, cas->gconst.p, cas->h0_f64.p, cas->h0.p, cas->in_band.p);
-    OCN_LAUNCHED(ctx);
-    k_evolve_tables<<<grid_for(ctx, nn * count), 256, 0, ctx->stream>>>(
-        resolution, count, cas->gconst.p, cas->h0.p, cas->h0p.p, cas->omega.p);
-    OCN_LAUNCHED(ctx);
-    std::vector<float2> tw = make_twiddles(resolution);
-    cas->twiddle.alloc(tw.size());
-    OCN_CUDA(cudaMemcpyAsync(cas->twiddle.p, tw.data(), tw.size() * sizeof(float2),
-                             cudaMemcpyHostToDevice, ctx->stream));
-    cas->group = (int)group_for(resolution, 1 << 30);
-    cas->d_time.alloc(1);
-    cas->scratch.alloc((size_t)cas->group * nn);
-    cas->cols_map_ok = cols_map_for(resolution, cas->group, cas->scratch.p, &cas->cols_map);
-    if (cas->cols_map_ok)
-      cols_map_for(resolution, cas->group, cas->scratch.p, &cas->cols_chunk_map, 0, true);
-    if (resolution == 1024 && fused_enabled() &&
-        cas->group >= kFuseSlots * kFuseW)
-      cas->fused_ok = cols_map_for(1024, kFuseSlots * kFuseW, cas->scratch.p, &cas->fused_map,
-                                   Fused<1024>::PC);
-    OCN_CUDA(cudaStreamSynchronize(ctx->stream));
-    ctx_retain(ctx);
-    *out = cas.release();
+    cascades_create(ctx, resolution, count, lengths, band_min, band_max, cascade_index, params, 1,
+                    0.0, out);
+  });
+}
+
+int ocn_cascades_create_frames(ocn_ctx* ctx, int resolution, int count, const double* lengths,
+                               const double* band_min, const double* band_max,
+                               const uint32_t* cascade_index, const ocn_spectrum_params* params,
+                               int frames, double dt, ocn_cascades** out) {
+  return api_call(ctx, [&] {
+    OCN_REQUIRE(params, "null argument");
+    std::vector<ocn_spectrum_params> ps(count > 0 ? count : 0, *params);
+    cascades_create(ctx, resolution, count, lengths, band_min, band_max, cascade_index, ps.data(),
+                    frames, dt, out);
   });
 }
 
@@ -1006,6 +997,7 @@ int ocn_cascades_download(ocn_cascades* c, int grid, double* h0, double* h0cn, u
     ocn_ctx* ctx = c->ctx;
     DeviceScope ds(ctx);
     const size_t nn = (size_t)c->n * c->n;
+    grid %= c->base;  // time-batched sets: one table per cascade
     const double2* src = c->h0_f64.p + (size_t)grid * nn;
     if (h0)
       OCN_CUDA(cudaMemcpyAsync(h0, src, nn * sizeof(double2), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1035,6 +1027,7 @@ int ocn_assemble_coefficients(ocn_cascades* c, int grid, double t, double chop, 
     OCN_REQUIRE(c && out && grid >= 0 && grid < c->count, "bad arguments");
     ocn_ctx* ctx = c->ctx;
     DeviceScope ds(ctx);
+    grid %= c->base;
     const size_t nn = (size_t)c->n * c->n;
     DevBuf<double2> d(8 * nn);
     k_assemble_coef<<<grid_for(ctx, nn), 256, 0, ctx->stream>>>(
@@ -1102,6 +1095,43 @@ int ocn_maps_download(ocn_maps* m, int cascade, int field, double* out) {
   });
 }
 
+int ocn_surface_generate_batch(ocn_maps* m, double t0, double dt, double choppiness) {
+  return api_call(m ? m->cas->ctx : nullptr, [&] {
+    OCN_REQUIRE(m, "ocn_surface_generate_batch: maps is NULL");
+    spectral_step(m->cas, m, nullptr, t0, choppiness, dt);
+  });
+}
+
+int ocn_maps_set_assembly(ocn_maps* m, int enable) {
+  return api_call(m ? m->cas->ctx : nullptr, [&] {
+    OCN_REQUIRE(m, "ocn_maps_set_assembly: maps is NULL");
+    const size_t nn = (size_t)m->cas->n * m->cas->n;
+    if (!m->cas->h0.p) fail(OCN_ERR_CONFIG, "maps without a spectrum have no spectral step");
+    if (nn % 4) fail(OCN_ERR_CONFIG, "per-texel assembly needs N >= 2");
+    m->assembly = enable != 0;
+    if (m->assembly && !m->assembled.p) {
+      DeviceScope ds(m->cas->ctx);
+      m->assembled.alloc(nn * 4 * m->cas->count);
+      OCN_CUDA(cudaMemsetAsync(m->assembled.p, 0, m->assembled.bytes(), m->cas->ctx->stream));
+    }
+  });
+}
+
+int ocn_maps_download_assembly(ocn_maps* m, int cascade, int component, float* out) {
+  return api_call(m ? m->cas->ctx : nullptr, [&] {
+    OCN_REQUIRE(m && out && cascade >= 0 && cascade < m->cas->count && component >= 0 &&
+                    component < 4,
+                "bad assembly download arguments");
+    if (!m->assembled.p) fail(OCN_ERR_CONFIG, "assembly is not enabled on these maps");
+    ocn_ctx* ctx = m->cas->ctx;
+    DeviceScope ds(ctx);
+    const size_t nn = (size_t)m->cas->n * m->cas->n;
+    OCN_CUDA(cudaMemcpyAsync(out, m->assembled.p + ((size_t)cascade * 4 + component) * nn,
+                             nn * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+    OCN_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
 int ocn_maps_download_f32(ocn_maps* m, int cascade, int field, float* out) {
   return api_call(m ? m->cas->ctx : nullptr, [&] {
     OCN_REQUIRE(m && out && cascade >= 0 && cascade < m->cas->count && field >= 0 && field < 8,
@@ -1132,6 +1162,7 @@ int ocn_maps_create_bare(ocn_ctx* ctx, int n, int count, const double* lengths, 
     cas->ctx = ctx;
     cas->n = n;
     cas->count = count;
+    cas->base = count;
     cas->lengths.assign(lengths, lengths + count);
     cas->band_min.assign(count, 0.0);
     cas->band_max.assign(count, 1e300);
@@ -1243,6 +1274,21 @@ int ocn_spectral_step(ocn_maps* m, ocn_slices* s, double t, double choppiness) {
     OCN_REQUIRE(cas, "ocn_spectral_step: maps and slices are both NULL");
     OCN_REQUIRE(!m || !s || m->cas == s->cas, "maps and slices belong to different cascades");
     spectral_step(cas, m, s, t, choppiness);
+  });
+}
+
+int ocn_spectral_plan_info(ocn_maps* m, ocn_slices* s, int capacity, ocn_xform_info* out,
+                           int* count) {
+  ocn_cascades* cas = m ? m->cas : (s ? s->cas : nullptr);
+  return api_call(cas ? cas->ctx : nullptr, [&] {
+    OCN_REQUIRE(cas, "ocn_spectral_plan_info: maps and slices are both NULL");
+    OCN_REQUIRE(!m || !s || m->cas == s->cas, "maps and slices belong to different cascades");
+    OCN_REQUIRE(count, "ocn_spectral_plan_info: count is NULL");
+    DeviceScope ds(cas->ctx);
+    const SpectralPlan* plan = get_plan(cas, m, s);
+    *count = (int)plan->info.size();
+    if (out)
+      for (int i = 0; i < capacity && i < *count; ++i) out[i] = plan->info[i];
   });
 }
 

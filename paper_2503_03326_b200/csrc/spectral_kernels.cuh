@@ -1,7 +1,7 @@
 // spectral_kernels.cuh — the device side of the spectral step: K1 (spectrum
 // init) and its tables, the time evolution, the row kernels (k_rows, the
 // warp-synchronous k_rows_w), the column kernels (k_cols, the persistent
-// TMA-fed k_cols_tma), the opt-in fused kernel and the small conversion
+// TMA-fed k_cols_tma) and the small conversion
 // kernels of the plain-FFT entry points. Included by spectral.cu inside
 // namespace ocn::{anonymous}; the host side (plans, groups, graphs, C-ABI)
 // stays in spectral.cu.
@@ -99,7 +99,12 @@ __global__ void k_assemble_coef(int n, double dk, double g, double t, double cho
 
 // ------------------------------------------------------------------ evolve
 // h~ and G (surface.cpp:49-50; velocity.cpp:16-20) at time t, one cascade.
-__global__ void k_set_time(double* d_time, double t) { *d_time = t; }
+// d_time = {t, dt}: grid g of a time-batched set (GridConst::frame) is
+// evaluated at t + frame dt.
+__global__ void k_set_time(double* d_time, double t, double dt) {
+  d_time[0] = t;
+  d_time[1] = dt;
+}
 
 // Per-frame tables built once at spectrum creation: h0p = (h0(k), conj(h0(-k)))
 // as one float4 (no mirror gather per frame, spectra.cpp:171-177) and the fp64
@@ -128,24 +133,30 @@ __global__ void __launch_bounds__(256) k_evolve_tables(int n, int count, const G
 // h~ = h0 e^{iwt} + conj(h0(-k)) e^{-iwt} -> spec_h, and (velocity plans)
 // G = h0 e^{iwt} - conj(h0(-k)) e^{-iwt} -> spec_g (surface.cpp:49-50;
 // velocity.cpp:16-20); the fp64 phase is reduced mod 2 pi before the fp32 sincos.
-// With `gc` (band skipping), only the rows a row pass can read are evolved:
-// |i - N/2| < GridConst::row_half (the others are never staged).
+// Grid g reads the tables of grid GridConst::src (time-batched sets share one
+// table per cascade). With skip_rows (band skipping), only the rows a row pass
+// can read are evolved: |i - N/2| < GridConst::row_half.
 template <bool WITH_G>
-__global__ void __launch_bounds__(256) k_evolve(size_t total, const double* d_time,
+__global__ void __launch_bounds__(256) k_evolve(size_t total, int logn, const double* d_time,
                                                 const float4* __restrict__ h0p,
                                                 const double* __restrict__ omega, float2* spec_h,
-                                                float2* spec_g, int n, const GridConst* gc) {
-  const double t = *d_time;
-  const size_t nn = (size_t)n * n;
+                                                float2* spec_g, const GridConst* gc, int skip_rows) {
+  const double t0 = d_time[0], dt = d_time[1];
+  const int n = 1 << logn, lognn = 2 * logn;
+  const size_t qmask = ((size_t)1 << lognn) - 1;
   for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
        idx += (size_t)gridDim.x * blockDim.x) {
-    if (gc) {
-      const int c = (int)(idx / nn);
-      const int i = (int)((idx - (size_t)c * nn) / n);
-      if (abs(i - n / 2) >= __ldg(&gc[c].row_half)) continue;
+    const int g = (int)(idx >> lognn);
+    const size_t q = idx & qmask;
+    const GridConst& G = gc[g];
+    if (skip_rows) {
+      const int i = (int)(q >> logn);
+      if (abs(i - n / 2) >= __ldg(&G.row_half)) continue;
     }
-    const float4 hp = __ldg(h0p + idx);
-    double ph = __ldg(omega + idx) * t;
+    const size_t src = ((size_t)__ldg(&G.src) << lognn) | q;
+    const float4 hp = __ldg(h0p + src);
+    const double t = t0 + (double)__ldg(&G.frame) * dt;
+    double ph = __ldg(omega + src) * t;
     ph -= 6.283185307179586476925 * rint(ph * 0.15915494309189533577);
     float s, cs;
     sincosf((float)ph, &s, &cs);
@@ -154,6 +165,42 @@ __global__ void __launch_bounds__(256) k_evolve(size_t total, const double* d_ti
     const float br = hp.z * cs + hp.w * s, bi = hp.w * cs - hp.z * s;
     __stcg(spec_h + idx, make_float2(ar + br, ai + bi));
     if constexpr (WITH_G) __stcg(spec_g + idx, make_float2(ar - br, ai - bi));
+  }
+}
+
+// North-star item 3 per texel of every grid: the slope
+// normal n = (-Hx, 1, -Hz) / |.| and the Jacobian of X = p + D,
+// J = (1 - DxDx)(1 - DzDz) - DzDx^2 (stored DxDx / DzDx / DzDz are -dD/d(.)),
+// from the grid's maps -> out [grid][4][N][N] (nx, ny, nz, J), 4 texels per thread.
+__global__ void __launch_bounds__(256) k_assemble_grid(int count, size_t nn, const float* maps,
+                                                       float* out) {
+  const size_t quads = nn / 4;
+  const size_t total = quads * count;
+  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    const size_t g = idx / quads, q = idx - g * quads;
+    const float4* f = reinterpret_cast<const float4*>(maps + g * 8 * nn) + q;
+    const float4 hx = __ldcs(f + OCN_FIELD_HX * quads), hz = __ldcs(f + OCN_FIELD_HZ * quads);
+    const float4 xx = __ldcs(f + OCN_FIELD_DXDX * quads), zx = __ldcs(f + OCN_FIELD_DZDX * quads);
+    const float4 zz = __ldcs(f + OCN_FIELD_DZDZ * quads);
+    float4 nx, ny, nz, jac;
+    auto one = [](float a, float b, float dxx, float dzx, float dzz, float& ox, float& oy, float& oz,
+                  float& oj) {
+      const float inv = 1.0f / sqrtf(fmaf(a, a, fmaf(b, b, 1.0f)));
+      ox = -a * inv;
+      oy = inv;
+      oz = -b * inv;
+      oj = (1.0f - dxx) * (1.0f - dzz) - dzx * dzx;
+    };
+    one(hx.x, hz.x, xx.x, zx.x, zz.x, nx.x, ny.x, nz.x, jac.x);
+    one(hx.y, hz.y, xx.y, zx.y, zz.y, nx.y, ny.y, nz.y, jac.y);
+    one(hx.z, hz.z, xx.z, zx.z, zz.z, nx.z, ny.z, nz.z, jac.z);
+    one(hx.w, hz.w, xx.w, zx.w, zz.w, nx.w, ny.w, nz.w, jac.w);
+    float4* o = reinterpret_cast<float4*>(out + g * 4 * nn) + q;
+    __stcs(o, nx);
+    __stcs(o + quads, ny);
+    __stcs(o + 2 * quads, nz);
+    __stcs(o + 3 * quads, jac);
   }
 }
 
@@ -707,8 +754,6 @@ __global__ void __launch_bounds__(ColTma<N>::THREADS, 1)
   }
   if (TMA_STORE && threadIdx.x == 0) tma::bulk_wait();
 }
-
-#include "spectral_fused.cuh"
 
 // fp64 interleaved pair -> fp32 X + iY (fft.cpp:88-91)
 __global__ void k_pack_pair(size_t nn, const double2* x, const double2* y, float2* out) {

@@ -248,6 +248,44 @@ class CascadeInstances:
             pass
 
 
+class CascadeFrames:
+    """Time-batched frames of one CascadeSet: frame f is the
+    cascade set at t0 + f dt, and one spectral step synthesises every frame
+    (ocn_cascades_create_frames; generate_maps is a pure function of t,
+    surface.cpp:70-103). Maps of it are [frames][C][8][N][N]."""
+
+    def __init__(self, config: CascadeConfig, params: SpectrumParams, frames: int,
+                 dt: float = 1.0 / 60.0, ctx: Context = None):
+        config.validate()
+        self.config = config
+        self.params = params
+        self.frames = frames
+        self.dt = dt
+        C_ = len(config.lengths)
+        bmin = [0.0 if c == 0 else config.cutoffs[c - 1] for c in range(C_)]
+        bmax = [config.cutoffs[c] if c + 1 < C_ else 1e300 for c in range(C_)]
+        self.ctx = ctx or Context.default()
+        la = np.ascontiguousarray(config.lengths, np.float64)
+        bl = np.ascontiguousarray(bmin, np.float64)
+        bh = np.ascontiguousarray(bmax, np.float64)
+        ci = np.ascontiguousarray(list(range(C_)), np.uint32)
+        h = C.c_void_p()
+        check(lib().ocn_cascades_create_frames(self.ctx.h, config.resolution, C_, _dp(la), _dp(bl),
+                                               _dp(bh), ci.ctypes.data_as(_abi.u32), C.byref(params),
+                                               frames, dt, C.byref(h)),
+              self.ctx.h, "cascade frames")
+        self.h = h
+        self.grids = frames * C_
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().ocn_cascades_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
 # --------------------------------------------------------------------- surface
 @dataclass
 class SurfaceGenOptions:
@@ -284,6 +322,28 @@ class SurfaceMaps:
         check(lib().ocn_surface_generate(self.h, t, choppiness), self.ctx.h, "generate_maps")
         self.time = t
         return self
+
+    def generate_batch(self, t0, dt, choppiness=1.0):
+        """Every frame of a CascadeFrames set: frame f at t0 + f dt (async)."""
+        check(lib().ocn_surface_generate_batch(self.h, t0, dt, choppiness), self.ctx.h,
+              "generate_batch")
+        self.time = t0
+        return self
+
+    def set_assembly(self, enable: bool = True):
+        """Per-texel normal + Jacobian planes written by every spectral step."""
+        check(lib().ocn_maps_set_assembly(self.h, int(enable)), self.ctx.h, "set_assembly")
+        return self
+
+    def assembly(self, grid) -> np.ndarray:
+        """[4][N][N] fp32: nx, ny, nz, J of grid `grid`."""
+        n = self.cascade_set.config.resolution
+        out = np.zeros((4, n, n), np.float32)
+        for k in range(4):
+            check(lib().ocn_maps_download_assembly(self.h, grid, k,
+                                                   out[k].ctypes.data_as(_abi.f32)),
+                  self.ctx.h, "assembly")
+        return out
 
     def field(self, cascade, f) -> np.ndarray:
         n = self.cascade_set.config.resolution
@@ -431,6 +491,21 @@ def spectral_step(maps: Optional[SurfaceMaps], slices: Optional[VelocitySlices],
     check(lib().ocn_spectral_step(maps.h if maps else None, slices.h if slices else None, t,
                                   choppiness),
           (maps or slices).ctx.h, "spectral_step")
+
+
+def spectral_plan(maps: Optional[SurfaceMaps], slices: Optional[VelocitySlices]) -> list:
+    """The packed transforms of spectral_step(maps, slices) in plan order
+    (ocn_spectral_plan_info): kind, grid, depth / field indices, the skipped
+    row band and whether the transform runs per frame."""
+    from ._types import XformInfo
+    L = lib()
+    ctx = (maps or slices).ctx
+    n = C.c_int()
+    args = (maps.h if maps else None, slices.h if slices else None)
+    check(L.ocn_spectral_plan_info(*args, 0, None, C.byref(n)), ctx.h, "plan_info")
+    arr = (XformInfo * max(n.value, 1))()
+    check(L.ocn_spectral_plan_info(*args, n.value, arr, C.byref(n)), ctx.h, "plan_info")
+    return [{k: getattr(x, k) for k, _ in XformInfo._fields_} for x in arr[:n.value]]
 
 
 # ------------------------------------------------------------------------- fft

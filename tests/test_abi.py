@@ -104,7 +104,8 @@ def test_struct_layouts_match_header():
              "ocn_pose": T.Pose, "ocn_fluid": T.Fluid, "ocn_hydro_report": T.HydroReport,
              "ocn_triangle_state": T.TriangleState, "ocn_fdm_config": T.FdmConfig,
              "ocn_mask_params": T.MaskParams, "ocn_mask_frame": T.MaskFrame,
-             "ocn_zone_state": T.ZoneState, "ocn_body_frame": T.BodyFrame}
+             "ocn_zone_state": T.ZoneState, "ocn_body_frame": T.BodyFrame,
+             "ocn_xform_info": T.XformInfo}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "ocean_b200.h"', 'int main(void){']
     for cname, py in pairs.items():
         lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')

@@ -204,3 +204,38 @@ def test_instances_batched(oc, port):
             for f in range(8):
                 got = maps.field(3 * k + c, f)
                 assert normwise_rel(got, want[c, f]) < TOL, (k, c, f)
+
+
+def test_frames_batch_small(oc, port):
+    """Time-batched set (config 1 shape, 3 cascades): frame f at t0 + f dt."""
+    p = config2_params(seed=2)
+    cfg = oc.CascadeConfig(64, CONFIG2_LENGTHS[1:], CONFIG2_CUTOFFS[1:])
+    frames = oc.CascadeFrames(cfg, p, 5, 0.25)
+    maps = oc.SurfaceMaps(frames)
+    maps.generate_batch(1.0, 0.5)  # the call's dt overrides the set's
+    for f in range(5):
+        want = port.generate_maps(64, cfg.lengths, cfg.cutoffs, p, 1.0 + 0.5 * f)
+        for c in range(3):
+            for k in range(8):
+                assert normwise_rel(maps.field(3 * f + c, k), want[c, k]) < TOL, (f, c, k)
+    maps.generate(2.0)  # the set's own spacing
+    want = port.generate_maps(64, cfg.lengths, cfg.cutoffs, p, 2.0 + 0.25 * 4)
+    assert normwise_rel(maps.field(3 * 4 + 1, 0), want[1, 0]) < TOL
+    with pytest.raises(oc.ConfigError):
+        oc.height_at(maps, [[0.0, 0.0]])
+
+
+def test_assembly_grid_small(oc, port):
+    p = config2_params(seed=4)
+    cs = oc.CascadeSet(oc.CascadeConfig(128, CONFIG2_LENGTHS, CONFIG2_CUTOFFS), p)
+    maps = oc.SurfaceMaps(cs).set_assembly(True)
+    maps.generate(3.0, 0.9)
+    want = port.generate_maps(128, CONFIG2_LENGTHS, CONFIG2_CUTOFFS, p, 3.0, 0.9)
+    for c in range(4):
+        got = maps.assembly(c)
+        hx, hz = want[c, 6], want[c, 7]
+        inv = 1.0 / np.sqrt(hx * hx + 1.0 + hz * hz)
+        ref = [-hx * inv, inv, -hz * inv,
+               (1 - want[c, 3]) * (1 - want[c, 5]) - want[c, 4] ** 2]
+        for k in range(4):
+            assert normwise_rel(got[k], ref[k]) < TOL, (c, k)

@@ -223,3 +223,21 @@ def test_band_rows_outside_row_half_are_zero(port, n):
         assert not band[far, :].any() and not band[:, far].any(), c
         assert np.all(h0[far, :] == 0) and np.all(h0[:, far] == 0), c
         assert np.all(h0cn[far, :] == 0), c
+
+
+def test_surface_pair_large_equals_generate_maps(port):
+    """The large-grid pair (per-mode h0 on the fly, threaded row / column
+    transforms) used for the 16384^2 parity test is bit-identical to the
+    restatement's generate_maps on the same grid, and its direct sums at grid
+    nodes equal the transform to fp64 rounding."""
+    from helpers import config2_params
+    p = config2_params(seed=7)
+    n, L, t = 128, 32.0, 10.0
+    want = port.generate_maps(n, [L], [], p, t, 0.8)[0]
+    ab = np.array([[0, 0], [5, 77], [127, 64], [64, 1]])
+    for pair in range(4):
+        re, im, direct = port.surface_pair_large(n, L, 0.0, 1e300, p, t, pair, choppiness=0.8,
+                                                 threads=3, ab=ab)
+        assert np.array_equal(re, want[2 * pair]) and np.array_equal(im, want[2 * pair + 1])
+        at = re[ab[:, 0], ab[:, 1]] + 1j * im[ab[:, 0], ab[:, 1]]
+        assert np.abs(direct - at).max() <= 1e-12 * max(np.abs(re).max(), np.abs(im).max())
