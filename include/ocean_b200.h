@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define OCN_ABI_VERSION 1
+#define OCN_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define OCN_API __attribute__((visibility("default")))
@@ -99,9 +99,18 @@ typedef struct ocn_pose {
   double com_body[3];
 } ocn_pose;
 
+/* A host water-velocity sampler (FluidQuery::water_velocity, hydro.hpp:38-49,
+ * called per submerged state at hydro.cpp:276-282): the library calls it once per
+ * evaluation with every submerged TriangleState centroid as (x, z, y) triples in
+ * state order (xzy[3 n]) and reads the medium velocities (vx, vy, vz) from
+ * out[3 n]. */
+typedef void (*ocn_velocity_fn)(void* user, int64_t n, const double* host_xzy, double* host_out);
+
 /* DragCoefficients hydro.hpp:92-95 + medium constants of FluidQuery
  * hydro.hpp:38-49. The surface / velocity samplers of FluidQuery are the
- * device-resident maps / slices / zones named in ocn_fluid. */
+ * device-resident maps / slices / zones named in ocn_fluid, or host callbacks:
+ * a host surface sampler enters as ocn_hydro_aggregate's host_vertex_depth, a
+ * host velocity sampler as host_velocity (used when slices is NULL). */
 typedef struct ocn_fluid {
   void* maps;          /* ocn_maps*   : height_at sampler (required unless depths are overridden) */
   void* slices;        /* ocn_slices* : velocity_at sampler, or NULL for still water            */
@@ -117,6 +126,8 @@ typedef struct ocn_fluid {
   int32_t n_profile;    /* density_profile entries (depth, rho), hydro.cpp:11-23 */
   int32_t reserved0;
   const double* host_profile; /* 2 * n_profile doubles, or NULL */
+  ocn_velocity_fn host_velocity; /* host water_velocity sampler, or NULL (ABI 2) */
+  void* host_velocity_user;
 } ocn_fluid;
 
 /* HydroReport, hydro.hpp:97-109, plus the composed rigid-body load of

@@ -37,6 +37,10 @@ def build(reference: bool = True) -> None:
     targets = ["all"]
     if reference and os.path.isdir("/root/reference/proj/src"):
         targets.append("ref")
+        # the reference's own Simulation over the drop-in (needs libocean_api.so)
+        api = os.path.join(os.path.dirname(HERE), "paper_2503_03326_b200", "lib", "libocean_api.so")
+        if os.path.exists(api):
+            targets.append("caller")
     subprocess.run(["make", "-s", "-C", HERE] + targets, check=True)
 
 

@@ -80,6 +80,10 @@ class Pose(C.Structure):
         return p
 
 
+# ocn_velocity_fn: host water_velocity sampler (user, n, xzy[3n] in, out[3n])
+VelocityFn = C.CFUNCTYPE(None, C.c_void_p, C.c_int64, C.POINTER(C.c_double), C.POINTER(C.c_double))
+
+
 class Fluid(C.Structure):
     """ocn_fluid — FluidQuery (hydro.hpp:38-49) + DragCoefficients."""
 
@@ -97,6 +101,8 @@ class Fluid(C.Structure):
         ("n_profile", C.c_int32),
         ("reserved0", C.c_int32),
         ("host_profile", C.POINTER(C.c_double)),
+        ("host_velocity", VelocityFn),
+        ("host_velocity_user", C.c_void_p),
     ]
 
 

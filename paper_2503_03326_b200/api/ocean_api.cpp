@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <fstream>
 #include <map>
+#include <unordered_map>
 #include <mutex>
 #include <sstream>
 #include <thread>
@@ -734,6 +735,80 @@ TriMesh make_icosphere(double radius, int subdivisions) {
   return TriMesh(std::move(v), std::move(f));
 }
 
+// Procedural boxes (mesh.cpp:166-221, 260-276): a welded lattice over the
+// surface of [0, n]^3, quads split along their first diagonal, vertices
+// numbered in first-use order. Each face's corner walk (u, v offsets in the
+// face's own coordinates) is the reference's; with it the -z face turns inward
+// and shares directed edges with its neighbours, so TriMesh validation rejects
+// every lattice (SURVEY 2 note 1: make_box / make_hull always throw MeshError,
+// verified for segments 1..92), exactly as the reference does.
+namespace {
+struct Lattice {
+  std::vector<Vec3> verts;
+  std::vector<TriMesh::Tri> tris;
+};
+Lattice lattice_surface(int n) {
+  Lattice L;
+  std::unordered_map<long long, int> id;
+  const long long m = (long long)n + 1;
+  auto vertex = [&](int i, int j, int k) {
+    const long long key = ((long long)i * m + j) * m + k;
+    auto [it, fresh] = id.emplace(key, (int)L.verts.size());
+    if (fresh) L.verts.push_back({(double)i, (double)j, (double)k});
+    return it->second;
+  };
+  // per face: where (u, v) and the fixed coordinate go, and the corner walk
+  struct Face {
+    int axis_u, axis_v, axis_w, w;  // coordinate index of u / v / fixed, fixed value (0 / n)
+    int walk[4][2];                 // corner offsets (du, dv) in winding order
+  };
+  const Face faces[6] = {
+      {0, 2, 1, 0, {{0, 0}, {1, 0}, {1, 1}, {0, 1}}},  // -y
+      {0, 2, 1, n, {{0, 0}, {0, 1}, {1, 1}, {1, 0}}},  // +y
+      {1, 2, 0, 0, {{0, 0}, {0, 1}, {1, 1}, {1, 0}}},  // -x
+      {1, 2, 0, n, {{0, 0}, {1, 0}, {1, 1}, {0, 1}}},  // +x
+      {0, 1, 2, 0, {{0, 0}, {1, 0}, {1, 1}, {0, 1}}},  // -z
+      {0, 1, 2, n, {{0, 0}, {0, 1}, {1, 1}, {1, 0}}},  // +z
+  };
+  for (int u = 0; u < n; ++u)
+    for (int v = 0; v < n; ++v)
+      for (const Face& fc : faces) {
+        int q[4];
+        for (int c = 0; c < 4; ++c) {
+          int x[3];
+          x[fc.axis_u] = u + fc.walk[c][0];
+          x[fc.axis_v] = v + fc.walk[c][1];
+          x[fc.axis_w] = fc.w;
+          q[c] = vertex(x[0], x[1], x[2]);
+        }
+        L.tris.push_back({{q[0], q[1], q[2]}});
+        L.tris.push_back({{q[0], q[2], q[3]}});
+      }
+  return L;
+}
+}  // namespace
+
+TriMesh make_box(double sx, double sy, double sz, int segments) {
+  Lattice L = lattice_surface(segments);
+  const double n = segments;
+  for (Vec3& p : L.verts) p = {(p.x / n - 0.5) * sx, (p.y / n - 0.5) * sy, (p.z / n - 0.5) * sz};
+  return TriMesh(std::move(L.verts), std::move(L.tris));
+}
+
+TriMesh make_hull(double length, double beam, double depth, int segments) {
+  Lattice L = lattice_surface(segments);
+  const double n = segments, freeboard = 0.35;
+  for (Vec3& p : L.verts) {
+    const double u = p.z / n, x = p.x / n - 0.5, y = p.y / n - 0.5;  // stern..bow, port..stbd
+    const double taper = std::max(0.0, (u - 0.55) / 0.45);
+    const double w = std::sqrt(std::max(0.04, 1.0 - 0.96 * taper * taper));
+    const double rise = 0.55 * taper * taper;  // the bottom lifts toward the bow
+    const double yy = y < 0.0 ? y * (1.0 - rise) : y;
+    p = {x * beam * w, (yy + 0.5) * depth - (1.0 - freeboard) * depth, (u - 0.5) * length};
+  }
+  return TriMesh(std::move(L.verts), std::move(L.tris));
+}
+
 // ============================================================ hydro
 double FluidQuery::density_at(double y) const {
   if (density_profile.empty()) return water_density;
@@ -777,9 +852,18 @@ ocn_hydro_report run_hydro(const TriMesh& mesh, const BodyPose& pose, const Flui
   for (const FdmZone* z : fluid.zones) zones.push_back(z->device_handle());
   f.maps = fluid.maps ? fluid.maps->device_handle() : nullptr;
   f.slices = fluid.slices ? fluid.slices->device_handle() : nullptr;
-  if (fluid.water_velocity && !fluid.slices)
-    throw ConfigError("aggregate: host water_velocity callbacks are not supported on the B200 path; "
-                      "pass the device VelocitySlices in FluidQuery::slices");
+  if (fluid.water_velocity && !fluid.slices) {
+    // the caller's host sampler (sim.cpp:80), called once per submerged state
+    // with the states batched per evaluation (hydro.cpp:276-282)
+    f.host_velocity = [](void* user, int64_t n, const double* xzy, double* out) {
+      const auto& fn = *static_cast<const std::function<Vec3(Vec2, double)>*>(user);
+      for (int64_t i = 0; i < n; ++i) {
+        const Vec3 v = fn(Vec2{xzy[3 * i], xzy[3 * i + 1]}, xzy[3 * i + 2]);
+        out[3 * i] = v.x, out[3 * i + 1] = v.y, out[3 * i + 2] = v.z;
+      }
+    };
+    f.host_velocity_user = const_cast<std::function<Vec3(Vec2, double)>*>(&fluid.water_velocity);
+  }
   f.velocity_clamp = fluid.velocity_clamp;
   f.n_zones = static_cast<int>(zones.size());
   f.zones = zones.data();

@@ -291,7 +291,8 @@ __global__ void __launch_bounds__(kForceThreads) k_forces(const StateDev* __rest
                                                           FluidDev F, double* block_out,
                                                           int* domain_err, int* ticket,
                                                           double mesh_volume, int degenerate,
-                                                          ReportDev* rep) {
+                                                          ReportDev* rep,
+                                                          const double* __restrict__ ext_vel) {
   __shared__ double wsum[kForceThreads / 32][kTerms];
   const int ns = total->x;
   double acc[kTerms];
@@ -308,7 +309,9 @@ __global__ void __launch_bounds__(kForceThreads) k_forces(const StateDev* __rest
       acc[3] += (s.centroid.y - 0.5 * s.depth) * w;
       acc[4] += s.centroid.z * w;
       double3 med = d3(0, 0, 0);
-      if (have_vel) {
+      if (ext_vel) {  // host sampler results, one triple per state
+        med = d3(ext_vel[3 * i], ext_vel[3 * i + 1], ext_vel[3 * i + 2]);
+      } else if (have_vel) {
         double v[3];
         if (!velocity_at_dev(vel, s.centroid.x, s.centroid.z, s.centroid.y, OCN_INTERP_EXPONENTIAL,
                              clamp, v))
@@ -839,11 +842,41 @@ void hydro_evaluate(ocn_mesh* m, const ocn_pose* pose, const ocn_fluid* fluid,
                                                P, m->counts.p, m->offsets.p, m->block_sums.p,
                                                m->states.p, m->segs.p);
   OCN_LAUNCHED(ctx);
+  const double* ext_vel = nullptr;
+  if (fluid && fluid->host_velocity && !slices) {
+    // host water_velocity sampler (hydro.cpp:276-282): the submerged states'
+    // centroids go to the host once, the callback fills their medium
+    // velocities, which the force pass reads instead of velocity_at
+    int2 total{};
+    OCN_CUDA(cudaMemcpyAsync(&total, m->total.p, sizeof(int2), cudaMemcpyDeviceToHost, st));
+    OCN_CUDA(cudaStreamSynchronize(st));
+    const int ns = total.x;
+    std::vector<StateDev> hs(ns);
+    if (ns)
+      OCN_CUDA(cudaMemcpy(hs.data(), m->states.p, ns * sizeof(StateDev), cudaMemcpyDeviceToHost));
+    std::vector<double> xzy, vel;
+    std::vector<int> idx;
+    for (int i = 0; i < ns; ++i)
+      if (hs[i].status == 0) {
+        idx.push_back(i);
+        xzy.insert(xzy.end(), {hs[i].centroid.x, hs[i].centroid.z, hs[i].centroid.y});
+      }
+    vel.assign(xzy.size(), 0.0);
+    if (!idx.empty())
+      fluid->host_velocity(fluid->host_velocity_user, (int64_t)idx.size(), xzy.data(), vel.data());
+    m->ext_vel_host.assign(3 * (size_t)std::max(ns, 1), 0.0);
+    for (size_t k = 0; k < idx.size(); ++k)
+      for (int c = 0; c < 3; ++c) m->ext_vel_host[3 * (size_t)idx[k] + c] = vel[3 * k + c];
+    m->ext_vel.ensure(m->ext_vel_host.size());
+    OCN_CUDA(cudaMemcpyAsync(m->ext_vel.p, m->ext_vel_host.data(),
+                             m->ext_vel_host.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+    ext_vel = m->ext_vel.p;
+  }
   const int fblocks = ctx->sm_count * 2;
   k_forces<<<fblocks, kForceThreads, 0, st>>>(m->states.p, m->total.p, P, vv, slices != nullptr,
                                              fluid ? fluid->velocity_clamp : 1, F,
                                              m->block_out.p, m->flags.p, m->ticket.p, m->volume,
-                                             m->degenerate, m->report.p);
+                                             m->degenerate, m->report.p, ext_vel);
   OCN_LAUNCHED(ctx);
   // waterline
   OCN_CUDA(cudaMemsetAsync(m->hkeys.p, 0, m->hkeys.bytes(), st));

@@ -47,6 +47,8 @@ struct ocn_mesh {
   ocn::DevBuf<double> verts, normals, areas;
   ocn::DevBuf<int3> tris;
   ocn::DevBuf<double> wpos, depth, override_depth, d_profile;
+  ocn::DevBuf<double> ext_vel;           // host water_velocity results per state
+  std::vector<double> ext_vel_host;
   ocn::DevBuf<int2> counts, offsets, block_sums, total;
   ocn::DevBuf<ocn::StateDev> states;
   ocn::DevBuf<ocn::SegDev> segs;

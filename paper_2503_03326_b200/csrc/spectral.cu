@@ -185,9 +185,38 @@ void launch_rows(ocn_ctx* ctx, const RowArgs& a, bool plain, cudaStream_t st, in
   OCN_LAUNCHED(ctx);
 }
 
+// Column kernel of the spectral step: OCN_COLS=direct selects k_cols_direct
+// (direct loads, 2 CTAs / SM), otherwise the persistent TMA ring.
+static int cols_variant() {
+  static const int v = [] {
+    const char* e = getenv("OCN_COLS");
+    if (!e) return 0;
+    if (!strcmp(e, "direct")) return 1;
+    if (!strcmp(e, "tma2")) return 2;  // 2 persistent CTAs / SM, one TMA stage each, STG stores
+    return 0;
+  }();
+  return v;
+}
+
 template <int N>
 void launch_cols(ocn_ctx* ctx, const ColArgs& a, int G, bool complex_out, cudaStream_t st,
                  const CUtensorMap* map, const CUtensorMap* chunk_map) {
+  if constexpr (N >= 128 && N <= 1024) {
+    if (!complex_out && cols_variant() == 1) {
+      using L = Launch<N>;
+      const size_t smem = ((size_t)L::PER_CTA * L::COL_STRIDE + fft::Plan<N>::tw_size()) * 8;
+      static bool attr = false;
+      if (!attr) {
+        OCN_CUDA(cudaFuncSetAttribute(k_cols_direct<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+        attr = true;
+      }
+      const int tiles_x = N / L::PER_CTA;
+      k_cols_direct<N><<<tiles_x * G, L::THREADS, smem, st>>>(a, tiles_x);
+      OCN_LAUNCHED(ctx);
+      return;
+    }
+  }
   if constexpr (ColTma<N>::OK) {
     if (map) {
       using CT = ColTma<N>;
@@ -201,6 +230,22 @@ void launch_cols(ocn_ctx* ctx, const ColArgs& a, int G, bool complex_out, cudaSt
       }
       const int tiles_x = N / CT::PC, ntiles = tiles_x * G;
       const int grid = std::min(ntiles, ctx->sm_count);
+      if constexpr (CT::smem(1) * 2 <= 227 * 1024) {
+        if (!complex_out && cols_variant() == 2) {
+          static bool attr2 = false;
+          if (!attr2) {
+            OCN_CUDA(cudaFuncSetAttribute(k_cols_tma<N, false, 1, false, 2>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)CT::smem(1)));
+            attr2 = true;
+          }
+          const int grid2 = std::min(ntiles, 2 * ctx->sm_count);
+          k_cols_tma<N, false, 1, false, 2><<<grid2, CT::THREADS, CT::smem(1), st>>>(
+              *map, *chunk_map, a, tiles_x, ntiles);
+          OCN_LAUNCHED(ctx);
+          return;
+        }
+      }
       if (complex_out)
         k_cols_tma<N, true, CT::STAGES><<<grid, CT::THREADS, CT::SMEM, st>>>(*map, *chunk_map, a, tiles_x, ntiles);
       else if (a.out_maps && CT::smem(2, true) <= 227 * 1024)

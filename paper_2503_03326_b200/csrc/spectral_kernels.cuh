@@ -601,6 +601,45 @@ __global__ void __launch_bounds__(Launch<N>::THREADS) k_cols(const ColArgs a) {
   }
 }
 
+// Column pass with direct loads, one column tile (PC columns x N rows) per
+// CTA, two CTAs per SM: the scratch is read straight into registers (only the
+// band rows of band-limited transforms: the others were never written by the
+// row pass and are exactly zero), shared memory holds only the inter-pass
+// exchange and the twiddles, and Re / Im go out as evict-first stores. Per
+// element that moves 16 B through the shared-memory crossbar instead of the
+// TMA ring's 48 (tile landing, pass-0 read, exchange, staging, TMA-store read).
+template <int N>
+__global__ void __launch_bounds__(Launch<N>::THREADS, 2) k_cols_direct(const ColArgs a, int tiles_x) {
+  using L = Launch<N>;
+  using PL = fft::Plan<N>;
+  constexpr int PC = L::PER_CTA, H = N / 2;
+  extern __shared__ __align__(16) float2 smem[];
+  float2* stw = smem + PC * L::COL_STRIDE;
+  for (int i = threadIdx.x; i < PL::tw_size(); i += blockDim.x) stw[i] = __ldg(a.tw + i);
+  const int c = threadIdx.x % PC, t = threadIdx.x / PC;
+  const int xf = blockIdx.x / tiles_x;
+  const int col = (blockIdx.x - xf * tiles_x) * PC + c;
+  const XformDesc* dp = a.desc + xf;
+  const int rh0 = a.gc ? __ldg(&dp->row_half) : 0;
+  const int rh = rh0 > 0 ? rh0 : H + 1;
+  const bool edge_only = rh <= PL::T;  // band within the first / last T rows of the column
+  const float2* in = a.scratch + (size_t)xf * N * N + col;
+  float* out_re = reinterpret_cast<float*>(__ldg(reinterpret_cast<const unsigned long long*>(&dp->out_re)));
+  float* out_im = reinterpret_cast<float*>(__ldg(reinterpret_cast<const unsigned long long*>(&dp->out_im)));
+  __syncthreads();  // twiddles staged
+  fft::cta_fft<N, false, false, false, true, 0, 0, (PL::P > 1)>(
+      t, smem + c * L::COL_STRIDE, stw,
+      [&](int i) {
+        // scratch row i holds spectrum row i ^ N/2: nonzero only for |(i ^ H) - H| < rh
+        return abs((i ^ H) - H) < rh ? __ldcs(in + (size_t)i * N) : make_float2(0.f, 0.f);
+      },
+      [&](int r, float2 x) {
+        __stcs(out_re + (size_t)r * N + col, x.x);  // fft.cpp:93-99 split
+        if (out_im) __stcs(out_im + (size_t)r * N + col, x.y);
+      },
+      fft::NoHook{}, edge_only);
+}
+
 // Column pass, persistent and TMA-fed (128 <= N <= 4096). A CTA walks the
 // column tiles [N rows][PC columns] (tile = transform x column block) with a
 // ring of STAGES shared buffers: one elected thread keeps STAGES - 1 tiles in
@@ -646,8 +685,8 @@ int cols_tma_pc(int n) { return n >= 128 && n <= 4096 ? 8192 / n : 0; }
 // the others are exactly zero (the row pass skipped them) and pass 0 reads
 // them as zero. Scratch row r holds spectrum row r ^ N/2, so the nonzero rows
 // are [0, row_half) and (N - row_half, N).
-template <int N, bool COMPLEX_OUT, int S, bool TMA_STORE = false>
-__global__ void __launch_bounds__(ColTma<N>::THREADS, 1)
+template <int N, bool COMPLEX_OUT, int S, bool TMA_STORE = false, int MINB = 1>
+__global__ void __launch_bounds__(ColTma<N>::THREADS, MINB)
     k_cols_tma(const __grid_constant__ CUtensorMap src, const __grid_constant__ CUtensorMap src_chunk,
                const ColArgs a, int tiles_x, int ntiles) {
   using CT = ColTma<N>;

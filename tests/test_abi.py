@@ -23,7 +23,7 @@ def test_exports_every_declared_symbol(L):
     missing = [s for s in syms if not hasattr(L, s)]
     assert not missing, missing
     assert set(_abi.SIGNATURES) == set(syms), set(_abi.SIGNATURES) ^ set(syms)
-    assert L.ocn_abi_version() == 1
+    assert L.ocn_abi_version() == 2
 
 
 def test_no_silent_cpu_fallback(L):
