@@ -521,6 +521,30 @@ OCN_API int ocn_slab_cols(ocn_slab* s, void* dev_recv);
 /* Column slab of one field: n x R doubles, row-major [i][column - rank R]. */
 OCN_API int ocn_slab_download(ocn_slab* s, int field, double* host_out);
 
+/* ------ the exchange over NVLink: an NCCL
+ * communicator of the library's own (NCCL is loaded at run time, sharing a copy
+ * the process already has). Rank 0 makes the unique id (128 bytes), the caller
+ * distributes it (MPI, torch.distributed, a file, ...), every rank creates its
+ * communicator on its context's device. */
+typedef struct ocn_comm ocn_comm;
+OCN_API int ocn_comm_unique_id(char* host_id_128);
+OCN_API int ocn_comm_create(ocn_ctx* ctx, const char* host_id_128, int nranks, int rank,
+                            ocn_comm** out);
+OCN_API int ocn_comm_destroy(ocn_comm* comm);
+OCN_API int ocn_comm_info(const ocn_comm* comm, int* nranks, int* rank);
+/* The all-to-all of the R x R tiles of packed pair `pair` (-1: all four) between
+ * dev_send ([dest][4][R][R]) and dev_recv ([src][4][R][R]) as grouped
+ * ncclSend / ncclRecv on the slab's stream (async); the rank's own tile is a
+ * device copy. */
+OCN_API int ocn_slab_exchange(ocn_slab* s, ocn_comm* comm, int pair, void* dev_send, void* dev_recv);
+/* One frame (async): per packed pair p, the row pass, then its exchange on the
+ * communicator's stream, then its column pass once its tiles arrived -- the
+ * NVLink transfer of pair p overlaps the row pass of p + 1 and the column pass
+ * of p - 1. comm may be NULL for a 1-rank slab. dev_send == dev_recv is allowed
+ * for 1 rank. */
+OCN_API int ocn_slab_frame(ocn_slab* s, ocn_comm* comm, double t, double choppiness,
+                           void* dev_send, void* dev_recv);
+
 /* ================= composed surface and ABHF heightfields ================== */
 /* Simulation::compose_height (sim.cpp:44-51) in bulk: height_at over the maps
  * plus FdmZone::sample of each listed zone (pass every body's zone except the

@@ -162,6 +162,12 @@ SIGNATURES = {
     "ocn_slab_rows": (ci, [vp, cd, cd, vp]),
     "ocn_slab_cols": (ci, [vp, vp]),
     "ocn_slab_download": (ci, [vp, ci, d]),
+    "ocn_comm_unique_id": (ci, [C.c_char_p]),
+    "ocn_comm_create": (ci, [vp, C.c_char_p, ci, ci, pvp]),
+    "ocn_comm_destroy": (ci, [vp]),
+    "ocn_comm_info": (ci, [vp, C.POINTER(ci), C.POINTER(ci)]),
+    "ocn_slab_exchange": (ci, [vp, vp, ci, vp, vp]),
+    "ocn_slab_frame": (ci, [vp, vp, cd, cd, vp, vp]),
     "ocn_compose_height": (ci, [vp, ci, pvp, i64, d, d]),
     "ocn_compose_grid": (ci, [vp, ci, pvp, ci, cd, d]),
     "ocn_heightfield_write_field": (ci, [vp, ci, ci, C.c_float, C.c_char_p]),

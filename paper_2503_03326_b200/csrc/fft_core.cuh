@@ -221,12 +221,15 @@ struct NoHook {
 //              and n >= N - T (r = 0 and r = E - 1 of every thread) may be
 //              nonzero: pass 0 is then the 2-term DFT x_0 + x_{E-1} w^{-m}
 //              (a band-limited column: rows [0, R) and (N - R, N), R <= T)
+//   on_mid   : (optional, P > 1) called by every thread right after the
+//              barrier that follows pass 0 (every thread's pass-0 loads and
+//              exchange stores are done)
 template <int N, bool WARP = false, bool LOAD_SM = false, bool STORE_SM = false, bool TW_SM = false,
           int BAR = 0, int BAR_THREADS = 0, bool SPARSE = false, class Load, class Store,
-          class Free = NoHook>
+          class Free = NoHook, class Mid = NoHook>
 __device__ __forceinline__ void cta_fft(int t, float2* sm, const float2* __restrict__ tw,
                                         Load&& load, Store&& store, Free&& on_free = Free{},
-                                        bool edge_only = false) {
+                                        bool edge_only = false, Mid&& on_mid = Mid{}) {
   using PL = Plan<N>;
   constexpr int E = PL::E, T = PL::T, P = PL::P;
   static_assert(!WARP || T <= 32, "warp-synchronous FFT needs T <= 32");
@@ -264,6 +267,7 @@ __device__ __forceinline__ void cta_fft(int t, float2* sm, const float2* __restr
         sm[pad32(t * E + r)] = v[bitrev(r, PL::LOGE)];
       });
     fft_sync<WARP, BAR, BAR_THREADS>();
+    on_mid();
     static_for<1, P>([&](auto pi) {
       constexpr int p = decltype(pi)::value;
       constexpr int R = PL::radix(p);

@@ -105,6 +105,7 @@ struct SlabRowArgs {
   const float2* spec;
   float2* send;  // [dest][4][rows][cols]
   const float2* tw;
+  int p0, np;    // packed pairs [p0, p0 + np) of this launch
 };
 
 // packed surface pair p at mode (i, j): h~ M_p (surface.cpp:77-80)
@@ -126,8 +127,8 @@ __global__ void __launch_bounds__(SlabLaunch<N>::THREADS) k_slab_rows(const Slab
   extern __shared__ float2 smem[];
   const int local = threadIdx.x / L::T, t = threadIdx.x - local * L::T;
   const int item = blockIdx.x * L::PER_CTA + local;  // (row, pair)
-  const bool valid = item < a.rows * 4;
-  const int li = valid ? item >> 2 : 0, p = item & 3;
+  const bool valid = item < a.rows * a.np;
+  const int li = valid ? item / a.np : 0, p = a.p0 + item % a.np;
   const float kx = a.dk * (float)(a.row0 + li - N / 2);
   const float2* srow = a.spec + (size_t)li * N;
   // surface_pair as one branch-free form with per-pair constants (as k_rows_w):
@@ -164,6 +165,7 @@ struct SlabColArgs {
   const float2* recv;  // [src][4][rows][cols]
   float* fields;       // [8][N][cols]
   const float2* tw;
+  int p0;              // first packed pair of this launch (grid y / z = pairs)
 };
 
 template <int N>
@@ -171,7 +173,7 @@ __global__ void __launch_bounds__(SlabLaunch<N>::THREADS) k_slab_cols(const Slab
   using L = SlabLaunch<N>;
   extern __shared__ float2 smem[];
   const int c = threadIdx.x % L::PER_CTA, t = threadIdx.x / L::PER_CTA;
-  const int p = blockIdx.y;
+  const int p = a.p0 + blockIdx.y;
   const int kc = blockIdx.x * L::PER_CTA + c;
   const bool valid = kc < a.cols;
   const int col = a.col0 + (valid ? kc : 0);
@@ -212,7 +214,7 @@ __global__ void __launch_bounds__(kFsB * kFsPC * (N / kFsN2) / 32) k_slab_colsA(
   using PL = fft::Plan<N1>;
   constexpr int T = PL::T, TPW = 32 / T, S = PL::SMEM;
   extern __shared__ float2 smem[];  // [NT][S]
-  const int p = blockIdx.z, kc0 = blockIdx.x * kFsPC, i20 = blockIdx.y * kFsB;
+  const int p = a.p0 + blockIdx.z, kc0 = blockIdx.x * kFsPC, i20 = blockIdx.y * kFsB;
   for (int e = threadIdx.x; e < N1 * NT; e += blockDim.x) {
     const int c = e % kFsPC, i2l = (e / kFsPC) % kFsB, i1 = e / NT;
     smem[(i2l * kFsPC + c) * S + fft::pad32(i1)] =
@@ -243,7 +245,7 @@ __global__ void __launch_bounds__(kFsB * kFsPC * kFsN2 / 32) k_slab_colsB(const 
   using PL = fft::Plan<kFsN2>;
   constexpr int T = PL::T, TPW = 32 / T, S = PL::SMEM;
   extern __shared__ float2 smem[];  // [NT][S]
-  const int p = blockIdx.z, kc0 = blockIdx.x * kFsPC, k10 = blockIdx.y * kFsB;
+  const int p = a.p0 + blockIdx.z, kc0 = blockIdx.x * kFsPC, k10 = blockIdx.y * kFsB;
   for (int e = threadIdx.x; e < kFsN2 * NT; e += blockDim.x) {
     const int c = e % kFsPC, k1l = (e / kFsPC) % kFsB, i2 = e / NT;
     smem[(k1l * kFsPC + c) * S + fft::pad32(i2)] =
@@ -270,7 +272,7 @@ __global__ void __launch_bounds__(kFsB * kFsPC * kFsN2 / 32) k_slab_colsB(const 
 }
 
 template <int N>
-bool slab_fourstep(ocn_slab* sl, const SlabColArgs& a, float2* recv) {
+bool slab_fourstep(ocn_slab* sl, const SlabColArgs& a, float2* recv, int np) {
   if constexpr (N >= 4096) {
     if (a.cols % kFsPC) return false;
     constexpr int N1 = N / kFsN2;
@@ -282,20 +284,20 @@ bool slab_fourstep(ocn_slab* sl, const SlabColArgs& a, float2* recv) {
       OCN_CUDA(cudaFuncSetAttribute(k_slab_colsB<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemB));
       attr = true;
     }
-    const dim3 ga(a.cols / kFsPC, kFsN2 / kFsB, 4), gb(a.cols / kFsPC, N1 / kFsB, 4);
+    const dim3 ga(a.cols / kFsPC, kFsN2 / kFsB, np), gb(a.cols / kFsPC, N1 / kFsB, np);
     k_slab_colsA<N><<<ga, kFsB * kFsPC * N1 / 32, smemA, sl->ctx->stream>>>(a, recv, sl->tw1.p, sl->wn.p);
     OCN_LAUNCHED(sl->ctx);
     k_slab_colsB<N><<<gb, kFsB * kFsPC * kFsN2 / 32, smemB, sl->ctx->stream>>>(a, recv, sl->tw2.p);
     OCN_LAUNCHED(sl->ctx);
     return true;
   } else {
-    (void)sl, (void)a, (void)recv;
+    (void)sl, (void)a, (void)recv, (void)np;
     return false;
   }
 }
 
 template <int N>
-void slab_rows_launch(ocn_slab* sl, const SlabRowArgs& a) {
+void slab_rows_launch(ocn_slab* sl, const SlabRowArgs& a) {  // pairs [a.p0, a.p0 + a.np)
   using L = SlabLaunch<N>;
   static bool attr = false;
   if (!attr && L::SMEM_BYTES > 48 * 1024) {
@@ -305,14 +307,14 @@ void slab_rows_launch(ocn_slab* sl, const SlabRowArgs& a) {
                                   (int)L::SMEM_BYTES));
   }
   attr = true;
-  const int blocks = (a.rows * 4 + L::PER_CTA - 1) / L::PER_CTA;
+  const int blocks = (a.rows * a.np + L::PER_CTA - 1) / L::PER_CTA;
   k_slab_rows<N><<<blocks, L::THREADS, L::SMEM_BYTES, sl->ctx->stream>>>(a);
   OCN_LAUNCHED(sl->ctx);
 }
 
 template <int N>
-void slab_cols_launch(ocn_slab* sl, const SlabColArgs& a, float2* recv) {
-  if (slab_fourstep<N>(sl, a, recv)) return;
+void slab_cols_launch(ocn_slab* sl, const SlabColArgs& a, float2* recv, int np) {
+  if (slab_fourstep<N>(sl, a, recv, np)) return;
   using L = SlabLaunch<N>;
   static bool attr = false;
   if (!attr && L::SMEM_BYTES > 48 * 1024) {
@@ -322,7 +324,7 @@ void slab_cols_launch(ocn_slab* sl, const SlabColArgs& a, float2* recv) {
                                   (int)L::SMEM_BYTES));
   }
   attr = true;
-  dim3 grid((a.cols + L::PER_CTA - 1) / L::PER_CTA, 4);
+  dim3 grid((a.cols + L::PER_CTA - 1) / L::PER_CTA, np);
   k_slab_cols<N><<<grid, L::THREADS, L::SMEM_BYTES, sl->ctx->stream>>>(a);
   OCN_LAUNCHED(sl->ctx);
 }
@@ -356,6 +358,46 @@ __global__ void k_f32_f64_slab(size_t n, const float* in, double* out) {
 }  // namespace
 
 std::vector<float2> make_twiddles(int n);  // spectral.cu
+
+// Row pass of packed pairs [p0, p0 + np) (evolve: also advance h~ to t first).
+void slab_rows_pairs(ocn_slab* sl, double t, double choppiness, void* dev_send, int p0, int np,
+                     bool evolve) {
+  ocn_ctx* ctx = sl->ctx;
+  ProfWindow pw(ctx, OCN_PROF_ROWS);
+  if (evolve) {
+    k_set_time_slab<<<1, 1, 0, ctx->stream>>>(sl->d_time.p, t);
+    OCN_LAUNCHED(ctx);
+    const size_t slab = (size_t)sl->rows * sl->n;
+    k_slab_evolve<<<grid_cap(ctx, slab), 256, 0, ctx->stream>>>(
+        sl->n, sl->rank * sl->rows, sl->rows, sl->gc, sl->d_time.p, sl->h0.p, sl->h0m.p, sl->spec.p);
+    OCN_LAUNCHED(ctx);
+  }
+  SlabRowArgs a{sl->rank * sl->rows, sl->rows, sl->cols, (float)sl->gc.dk, (float)choppiness,
+                sl->spec.p, (float2*)dev_send, sl->twiddle.p, p0, np};
+#define OCN_SR(NN) slab_rows_launch<NN>(sl, a)
+  OCN_SLAB_DISPATCH(sl->n, OCN_SR)
+#undef OCN_SR
+}
+
+// Column pass of packed pairs [p0, p0 + np) from the receive layout.
+void slab_cols_pairs(ocn_slab* sl, void* dev_recv, int p0, int np) {
+  ProfWindow pw(sl->ctx, OCN_PROF_COLS);
+  int lg = 0;
+  while ((1 << lg) < sl->rows) ++lg;
+  SlabColArgs a{sl->rows, sl->cols, sl->rank * sl->cols, lg, (const float2*)dev_recv, sl->fields.p,
+                sl->twiddle.p, p0};
+#define OCN_SC(NN) slab_cols_launch<NN>(sl, a, (float2*)dev_recv, np)
+  OCN_SLAB_DISPATCH(sl->n, OCN_SC)
+#undef OCN_SC
+}
+
+void slab_geometry(const ocn_slab* sl, ocn_ctx** ctx, int* n, int* ranks, int* rank, int* rows) {
+  *ctx = sl->ctx;
+  *n = sl->n;
+  *ranks = sl->ranks;
+  *rank = sl->rank;
+  *rows = sl->rows;
+}
 
 }  // namespace ocn
 
@@ -445,20 +487,8 @@ int ocn_slab_info(const ocn_slab* sl, int* rows, int* cols, size_t* exchange_byt
 int ocn_slab_rows(ocn_slab* sl, double t, double choppiness, void* dev_send) {
   return api_call(sl ? sl->ctx : nullptr, [&] {
     OCN_REQUIRE(sl && dev_send, "null argument");
-    ocn_ctx* ctx = sl->ctx;
-    DeviceScope ds(ctx);
-    ProfWindow pw(ctx, OCN_PROF_ROWS);
-    k_set_time_slab<<<1, 1, 0, ctx->stream>>>(sl->d_time.p, t);
-    OCN_LAUNCHED(ctx);
-    const size_t slab = (size_t)sl->rows * sl->n;
-    k_slab_evolve<<<grid_cap(ctx, slab), 256, 0, ctx->stream>>>(
-        sl->n, sl->rank * sl->rows, sl->rows, sl->gc, sl->d_time.p, sl->h0.p, sl->h0m.p, sl->spec.p);
-    OCN_LAUNCHED(ctx);
-    SlabRowArgs a{sl->rank * sl->rows, sl->rows, sl->cols, (float)sl->gc.dk, (float)choppiness,
-                  sl->spec.p, (float2*)dev_send, sl->twiddle.p};
-#define OCN_SR(NN) slab_rows_launch<NN>(sl, a)
-    OCN_SLAB_DISPATCH(sl->n, OCN_SR)
-#undef OCN_SR
+    DeviceScope ds(sl->ctx);
+    slab_rows_pairs(sl, t, choppiness, dev_send, 0, 4, true);
   });
 }
 
@@ -466,14 +496,7 @@ int ocn_slab_cols(ocn_slab* sl, void* dev_recv) {
   return api_call(sl ? sl->ctx : nullptr, [&] {
     OCN_REQUIRE(sl && dev_recv, "null argument");
     DeviceScope ds(sl->ctx);
-    ProfWindow pw(sl->ctx, OCN_PROF_COLS);
-    int lg = 0;
-    while ((1 << lg) < sl->rows) ++lg;
-    SlabColArgs a{sl->rows, sl->cols, sl->rank * sl->cols, lg, (const float2*)dev_recv, sl->fields.p,
-                  sl->twiddle.p};
-#define OCN_SC(NN) slab_cols_launch<NN>(sl, a, (float2*)dev_recv)
-    OCN_SLAB_DISPATCH(sl->n, OCN_SC)
-#undef OCN_SC
+    slab_cols_pairs(sl, dev_recv, 0, 4);
   });
 }
 

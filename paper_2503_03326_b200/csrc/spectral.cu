@@ -131,6 +131,20 @@ void set_smem_attrs() {
   done = true;
 }
 
+// Column kernel of the spectral step: OCN_COLS=direct selects k_cols_direct
+// (direct loads, 2 CTAs / SM), otherwise the persistent TMA ring.
+static int cols_variant() {
+  static const int v = [] {
+    const char* e = getenv("OCN_COLS");
+    if (!e) return 0;
+    if (!strcmp(e, "direct")) return 1;
+    if (!strcmp(e, "tma2")) return 2;  // 2 persistent CTAs / SM, one TMA stage each, STG stores
+    if (!strcmp(e, "ring")) return 3;  // compact chunk ring + double-buffered exchange / staging
+    return 0;
+  }();
+  return v;
+}
+
 template <int N>
 constexpr bool use_warp_kernels() {
   return N >= 128 && N <= 1024;
@@ -143,23 +157,32 @@ void launch_rows(ocn_ctx* ctx, const RowArgs& a, bool plain, cudaStream_t st, in
     using W = WarpLaunch<N>;
     const int slots = (max_seg + W::TPW - 1) / W::TPW;
     const int cap = 8;
-    // surface grids have 4 transforms: two rows per CTA keep 8 warps busy
-    static const int max_rpc = [] {  // experiment override: OCN_ROWS_RPC=1|2|4
+    // surface rows per CTA: a grid has only 4 surface transforms, so several
+    // rows keep the CTA's 8 warps busy and amortise its twiddle / staging set-up
+    static constexpr int kMaxRpc = N >= 1024 ? 4 : 2;  // 8 at N = 256 measured slower (config 1: 1.15 vs 1.10 ms)
+    static const int max_rpc = [] {  // experiment override: OCN_ROWS_RPC=1|2|4|8
       const char* e = getenv("OCN_ROWS_RPC");
-      return e && atoi(e) > 0 ? std::min(atoi(e), N >= 1024 ? 4 : 2) : (N >= 1024 ? 4 : 2);
+      return e && atoi(e) > 0 ? std::min(atoi(e), kMaxRpc) : kMaxRpc;
     }();
-    int rpc = 1;  // staging holds 4 rows of h~ (2 N float4 = 4 N float2)
+    int rpc = 1;
     if (!plain && family == 0)
       while (2 * rpc <= max_rpc && 2 * rpc * slots <= 2 * cap) rpc *= 2;
     const int warps = slots * rpc < cap ? slots * rpc : cap;
     RowArgs ar = a;
     ar.rpc = rpc;
-    const size_t smem = (plain ? 0 : 2 * N * sizeof(float4)) + W::TWN * sizeof(float2) +
+    // staging: velocity (V0, W0, |k|) 20 B per mode of one row; surface h~ (8 B)
+    // plus 1/|k| (4 B, N < 1024) per mode of each of the rpc rows
+    auto stage_f4 = [](int r) {
+      const size_t surf = (size_t)r * N * (N >= 1024 ? 8 : 12);
+      return (int)((std::max<size_t>(surf, (size_t)N * 20) + 15) / 16);
+    };
+    ar.stage_f4 = plain ? 0 : stage_f4(family == 0 ? rpc : 1);
+    const size_t smem = (size_t)ar.stage_f4 * sizeof(float4) + W::TWN * sizeof(float2) +
                         (size_t)warps * W::TPW * W::STRIDE * sizeof(float2);
     static bool attr = false;
     if (!attr) {
-      const int smax = 2 * N * sizeof(float4) + W::TWN * sizeof(float2) +
-                       8 * W::TPW * W::STRIDE * sizeof(float2);
+      const int smax = stage_f4(kMaxRpc) * (int)sizeof(float4) + W::TWN * (int)sizeof(float2) +
+                       8 * W::TPW * W::STRIDE * (int)sizeof(float2);
       OCN_CUDA(cudaFuncSetAttribute(k_rows_w<N, kRowPlain>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
       OCN_CUDA(cudaFuncSetAttribute(k_rows_w<N, kRowSurface>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
       OCN_CUDA(cudaFuncSetAttribute(k_rows_w<N, kRowVelocity>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
@@ -185,19 +208,6 @@ void launch_rows(ocn_ctx* ctx, const RowArgs& a, bool plain, cudaStream_t st, in
   OCN_LAUNCHED(ctx);
 }
 
-// Column kernel of the spectral step: OCN_COLS=direct selects k_cols_direct
-// (direct loads, 2 CTAs / SM), otherwise the persistent TMA ring.
-static int cols_variant() {
-  static const int v = [] {
-    const char* e = getenv("OCN_COLS");
-    if (!e) return 0;
-    if (!strcmp(e, "direct")) return 1;
-    if (!strcmp(e, "tma2")) return 2;  // 2 persistent CTAs / SM, one TMA stage each, STG stores
-    return 0;
-  }();
-  return v;
-}
-
 template <int N>
 void launch_cols(ocn_ctx* ctx, const ColArgs& a, int G, bool complex_out, cudaStream_t st,
                  const CUtensorMap* map, const CUtensorMap* chunk_map) {
@@ -213,6 +223,22 @@ void launch_cols(ocn_ctx* ctx, const ColArgs& a, int G, bool complex_out, cudaSt
       }
       const int tiles_x = N / L::PER_CTA;
       k_cols_direct<N><<<tiles_x * G, L::THREADS, smem, st>>>(a, tiles_x);
+      OCN_LAUNCHED(ctx);
+      return;
+    }
+  }
+  if constexpr (ColRing<N>::OK) {
+    if (map && chunk_map && !complex_out && a.out_maps && cols_variant() == 3) {
+      using RG = ColRing<N>;
+      static bool attr3 = false;
+      if (!attr3) {
+        OCN_CUDA(cudaFuncSetAttribute(k_cols_ring<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)RG::SMEM));
+        attr3 = true;
+      }
+      const int tiles_x = N / RG::PC, ntiles = tiles_x * G;
+      const int grid = std::min(ntiles, ctx->sm_count);
+      k_cols_ring<N><<<grid, RG::THREADS, RG::SMEM, st>>>(*chunk_map, a, tiles_x, ntiles);
       OCN_LAUNCHED(ctx);
       return;
     }
@@ -365,11 +391,25 @@ static bool cols_tma_store() {
   return on;
 }
 
+// Store map of one fp32 output plane for the ring column kernel's per-warp
+// boxes: the plane viewed as [N / T][T][N] (row = t + T r'), box {PC, 32 / PC, 32}.
+static void plane_warp_map_for(int n, float* plane, CUtensorMap* map) {
+  const int pc = cols_tma_pc(n), T = n / 32;
+  const uint64_t dims[3] = {(uint64_t)n, (uint64_t)T, 32};
+  const uint64_t strides[2] = {(uint64_t)n * 4, (uint64_t)T * n * 4};
+  const uint32_t box[3] = {(uint32_t)pc, (uint32_t)(32 / pc), 32};
+  *map = CUtensorMap{};
+  if (plane && !tma::encode_f32(map, 3, plane, dims, strides, box))
+    fail(OCN_ERR_CUDA, "cuTensorMapEncodeTiled failed for an output plane (N=%d)", n);
+}
+
 static void build_out_maps(int n, const XformDesc* desc, int count, DevBuf<CUtensorMap>& out) {
+  const bool warp_boxes = cols_variant() == 3 && n >= 256 && n <= 1024;
   std::vector<CUtensorMap> h((size_t)2 * count);
   for (int i = 0; i < count; ++i) {
-    plane_map_for(n, desc[i].out_re, &h[2 * i]);
-    plane_map_for(n, desc[i].out_im, &h[2 * i + 1]);
+    auto mk = warp_boxes ? plane_warp_map_for : plane_map_for;
+    mk(n, desc[i].out_re, &h[2 * i]);
+    mk(n, desc[i].out_im, &h[2 * i + 1]);
   }
   out.alloc(h.size());
   OCN_CUDA(cudaMemcpy(out.p, h.data(), h.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
@@ -573,15 +613,15 @@ static void enqueue_spectral(ocn_cascades* cas, SpectralPlan* plan, ocn_maps* ma
     ProfWindow pw(ctx, OCN_PROF_EVOLVE);  // every grid in one launch
     // skip never-read rows only where every reader is a band-aware warp row kernel
     const int skip = n >= 128 && n <= 1024 && cas->cols_map_ok && band_skip_enabled() ? 1 : 0;
-    const size_t total = nn * cas->count;
+    const size_t total = nn * cas->base;  // table modes; each evolved for every frame
     if (plan->need_velocity)
-      k_evolve<true><<<grid_for(ctx, total), 256, 0, A>>>(total, ilog2(n), cas->d_time.p,
-                                                          cas->h0p.p, cas->omega.p, cas->spec_h.p,
-                                                          cas->spec_g.p, cas->gconst.p, skip);
+      k_evolve<true><<<grid_for(ctx, total), 256, 0, A>>>(
+          total, ilog2(n), cas->base, cas->frames, cas->d_time.p, cas->h0p.p, cas->omega.p,
+          cas->spec_h.p, cas->spec_g.p, cas->gconst.p, skip);
     else
-      k_evolve<false><<<grid_for(ctx, total), 256, 0, A>>>(total, ilog2(n), cas->d_time.p,
-                                                           cas->h0p.p, cas->omega.p, cas->spec_h.p,
-                                                           nullptr, cas->gconst.p, skip);
+      k_evolve<false><<<grid_for(ctx, total), 256, 0, A>>>(
+          total, ilog2(n), cas->base, cas->frames, cas->d_time.p, cas->h0p.p, cas->omega.p,
+          cas->spec_h.p, nullptr, cas->gconst.p, skip);
     OCN_LAUNCHED(ctx);
   }
   for (size_t gidx = 0; gidx < plan->groups.size(); ++gidx) {

@@ -66,6 +66,40 @@ class SlabSurface:
             pass
 
 
+class Comm:
+    """The library's own NCCL communicator (ocn_comm): rank 0 makes the unique
+    id, `share` distributes it (e.g. torch.distributed.broadcast_object_list),
+    every rank joins on its context's device."""
+
+    def __init__(self, ctx, nranks: int, rank: int, share=None):
+        uid = C.create_string_buffer(128)
+        if rank == 0:
+            check(lib().ocn_comm_unique_id(uid), None, "comm id")
+        raw = bytes(uid.raw)
+        if share is not None:
+            raw = share(raw)
+        self.ctx = ctx
+        h = C.c_void_p()
+        check(lib().ocn_comm_create(ctx.h, C.c_char_p(raw), nranks, rank, C.byref(h)), ctx.h,
+              "comm")
+        self.h = h
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().ocn_comm_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+def frame(slab: "SlabSurface", comm, t: float, send_ptr: int, recv_ptr: int,
+          choppiness: float = 1.0):
+    """ocn_slab_frame: rows, per-pair exchange over NVLink, columns (async)."""
+    check(lib().ocn_slab_frame(slab.h, comm.h if comm else None, t, choppiness,
+                               C.c_void_p(send_ptr), C.c_void_p(recv_ptr)), slab.ctx.h, "frame")
+
+
 def exchange(send, recv, group=None):
     """All-to-all of the equal R x R tile blocks (send[peer] -> rank peer)."""
     import torch.distributed as dist
