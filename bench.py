@@ -368,15 +368,20 @@ class Frame4(_SingleStream):
 # ---------------------------------------------------------------- config 5
 C5_N, C5_L = 16384, 4096.0
 C5_WORKLOAD = ("config5: single 16384^2 surface (8 fields, 4 packed transforms), row slabs per "
-               "rank, NCCL all-to-all tile transpose between the row and column passes")
+               "rank, tile all-to-all over NVLink (grouped ncclSend/ncclRecv on the library's "
+               "communicator) pipelined per packed pair between the row and column passes")
 
 
 class Frame5(_SingleStream):
-    """This rank's slab of the 16384^2 grid; the transpose is an NCCL all-to-all."""
+    """This rank's slab of the 16384^2 grid. A step is ocn_slab_frame: per packed
+    pair the row pass, the tile all-to-all over NVLink (grouped ncclSend / ncclRecv
+    on the library's own communicator, ocn_comm) and the column pass, pipelined
+    per pair. Profiling passes (serialize) run rows, the whole exchange and the
+    columns one after the other, the exchange timed with CUDA events."""
 
     def __init__(self, device: int, rank: int, world: int, dist):
         from paper_2503_03326_b200 import ocean as oc
-        from paper_2503_03326_b200.slab import SlabSurface, tile_layout
+        from paper_2503_03326_b200.slab import Comm, SlabSurface, tile_layout
         import torch
         self.oc, self.L, self.dist = oc, oc.lib(), dist
         self.ctx = oc.Context(device)
@@ -386,30 +391,42 @@ class Frame5(_SingleStream):
         _, total = tile_layout(self.slab.rows, world)
         self.send = torch.empty(2 * total, dtype=torch.float32, device=f"cuda:{device}")
         self.recv = self.send if world == 1 else torch.empty_like(self.send)
+        self.comm = None
+        if world > 1:
+            def share(raw):
+                obj = [raw]
+                dist.broadcast_object_list(obj, src=0)
+                return obj[0]
+            self.comm = Comm(self.ctx, world, rank, share)
         self.stream = torch.cuda.ExternalStream(self.ctx.stream, device=f"cuda:{device}")
         self.world = world
         self.t = 0.0
         self.points = C5_N * C5_N // world
         self.a2a_ms = []
-        self._col = np.zeros(C5_N, np.float64)
         self.timing = False
+        self.serialize = False
 
     def step(self, read_report: bool = False):
         import torch
         self.t += DT
-        self.slab.rows_pass(self.t, self.send.data_ptr())
-        if self.world > 1:
-            with torch.cuda.stream(self.stream):
+        L, h = self.L, self.slab.h
+        comm = self.comm.h if self.comm else None
+        sp, rp = C.c_void_p(self.send.data_ptr()), C.c_void_p(self.recv.data_ptr())
+        if not self.serialize:
+            self.oc.check(L.ocn_slab_frame(h, comm, self.t, 1.0, sp, rp), self.ctx.h, "frame")
+        else:
+            self.slab.rows_pass(self.t, self.send.data_ptr())
+            if self.world > 1:
                 if self.timing:
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     e0.record(self.stream)
-                self.dist.all_to_all_single(self.recv, self.send)
+                self.oc.check(L.ocn_slab_exchange(h, comm, -1, sp, rp), self.ctx.h, "exchange")
                 if self.timing:
                     e1.record(self.stream)
                     self.a2a_ms.append((e0, e1))
-        self.slab.cols_pass(self.recv.data_ptr())
-        if read_report:  # the frame's result probe: one column of the height field -> host
-            self.oc.check(self.L.ocn_ctx_synchronize(self.ctx.h), self.ctx.h, "sync")
+            self.slab.cols_pass(self.recv.data_ptr())
+        if read_report:  # the frame's result probe: synchronize (fields stay on the device)
+            self.oc.check(L.ocn_ctx_synchronize(self.ctx.h), self.ctx.h, "sync")
 
 
 def _dist():
