@@ -139,7 +139,8 @@ static int cols_variant() {
     if (!e) return 0;
     if (!strcmp(e, "direct")) return 1;
     if (!strcmp(e, "tma2")) return 2;  // 2 persistent CTAs / SM, one TMA stage each, STG stores
-    if (!strcmp(e, "ring")) return 3;  // compact chunk ring + double-buffered exchange / staging
+    if (!strcmp(e, "ring")) return 3;  // compact chunk ring + per-warp TMA stores
+    if (!strcmp(e, "tmaw")) return 4;  // TMA ring, per-warp TMA stores (no epilogue barrier)
     return 0;
   }();
   return v;
@@ -267,6 +268,21 @@ void launch_cols(ocn_ctx* ctx, const ColArgs& a, int G, bool complex_out, cudaSt
           }
           const int grid2 = std::min(ntiles, 2 * ctx->sm_count);
           k_cols_tma<N, false, 1, false, 2><<<grid2, CT::THREADS, CT::smem(1), st>>>(
+              *map, *chunk_map, a, tiles_x, ntiles);
+          OCN_LAUNCHED(ctx);
+          return;
+        }
+      }
+      if constexpr (N >= 256 && N <= 1024 && CT::smem(2, true) <= 227 * 1024) {
+        if (!complex_out && a.out_maps && cols_variant() == 4) {
+          static bool attr4 = false;
+          if (!attr4) {
+            OCN_CUDA(cudaFuncSetAttribute(k_cols_tma<N, false, 2, true, 1, true>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)CT::smem(2, true)));
+            attr4 = true;
+          }
+          k_cols_tma<N, false, 2, true, 1, true><<<grid, CT::THREADS, CT::smem(2, true), st>>>(
               *map, *chunk_map, a, tiles_x, ntiles);
           OCN_LAUNCHED(ctx);
           return;
@@ -404,7 +420,7 @@ static void plane_warp_map_for(int n, float* plane, CUtensorMap* map) {
 }
 
 static void build_out_maps(int n, const XformDesc* desc, int count, DevBuf<CUtensorMap>& out) {
-  const bool warp_boxes = cols_variant() == 3 && n >= 256 && n <= 1024;
+  const bool warp_boxes = (cols_variant() == 3 || cols_variant() == 4) && n >= 256 && n <= 1024;
   std::vector<CUtensorMap> h((size_t)2 * count);
   for (int i = 0; i < count; ++i) {
     auto mk = warp_boxes ? plane_warp_map_for : plane_map_for;

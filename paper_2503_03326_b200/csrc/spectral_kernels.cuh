@@ -691,7 +691,13 @@ int cols_tma_pc(int n) { return n >= 128 && n <= 4096 ? 8192 / n : 0; }
 // the others are exactly zero (the row pass skipped them) and pass 0 reads
 // them as zero. Scratch row r holds spectrum row r ^ N/2, so the nonzero rows
 // are [0, row_half) and (N - row_half, N).
-template <int N, bool COMPLEX_OUT, int S, bool TMA_STORE = false, int MINB = 1>
+// WARP_STORE (with TMA_STORE): every warp stores its own outputs -- thread t
+// of column c ends with rows t + T r', so a warp's outputs are one 3-D box
+// {PC, 32 / PC, 32} of the plane viewed as [N / T][T][N] (plane_warp_map_for)
+// -- from its own 8 KB of the staging, after a per-thread fence and a
+// __syncwarp: no CTA barrier and no CTA-wide fence in the epilogue.
+template <int N, bool COMPLEX_OUT, int S, bool TMA_STORE = false, int MINB = 1,
+          bool WARP_STORE = false>
 __global__ void __launch_bounds__(ColTma<N>::THREADS, MINB)
     k_cols_tma(const __grid_constant__ CUtensorMap src, const __grid_constant__ CUtensorMap src_chunk,
                const ColArgs a, int tiles_x, int ntiles) {
@@ -744,7 +750,8 @@ __global__ void __launch_bounds__(ColTma<N>::THREADS, MINB)
     float2* buf = smem + s * CT::STAGE;
     tma::mbar_wait(bar0 + 8 * s, phase);
     auto refill = [&] {
-      if (TMA_STORE && threadIdx.x == 0) tma::bulk_wait_read();  // staging free again
+      if (TMA_STORE && (WARP_STORE ? (threadIdx.x & 31) == 0 : threadIdx.x == 0))
+        tma::bulk_wait_read();  // staging free again
       __syncthreads();  // every thread's shared reads of this buffer are done
       if (threadIdx.x == 0) {
         const int next = tile + S * gridDim.x;
@@ -769,6 +776,26 @@ __global__ void __launch_bounds__(ColTma<N>::THREADS, MINB)
             out[(size_t)r * N + col] = x;
           },
           refill, edge_only);
+    } else if constexpr (TMA_STORE && WARP_STORE) {
+      constexpr int T = CT::T;
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      float* my_re = sre + warp * 1024;  // 32 r' x 32 lanes
+      float* my_im = sim + warp * 1024;
+      fft::cta_fft<N, false, true, false, true, 0, 0, true>(
+          t, buf + c * CT::STRIDE, stw, load_band,
+          [&](int r, float2 x) {
+            my_re[(r / T) * 32 + lane] = x.x;  // box order {c, t, r'}; fft.cpp:93-99 split
+            my_im[(r / T) * 32 + lane] = x.y;
+          },
+          refill, edge_only);
+      tma::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        const int col0 = col - c, t0 = (warp * 32) / PC;
+        tma::store_3d(a.out_maps + 2 * xf, tma::smem_u32(my_re), col0, t0, 0);
+        if (a.desc[xf].out_im) tma::store_3d(a.out_maps + 2 * xf + 1, tma::smem_u32(my_im), col0, t0, 0);
+        tma::bulk_commit();
+      }
     } else if constexpr (TMA_STORE) {
       fft::cta_fft<N, false, true, false, true, 0, 0, true>(
           t, buf + c * CT::STRIDE, stw, load_band,
@@ -797,7 +824,7 @@ __global__ void __launch_bounds__(ColTma<N>::THREADS, MINB)
     }
     if (++s == S) s = 0, phase ^= 1;
   }
-  if (TMA_STORE && threadIdx.x == 0) tma::bulk_wait();
+  if (TMA_STORE && (WARP_STORE ? (threadIdx.x & 31) == 0 : threadIdx.x == 0)) tma::bulk_wait();
 }
 
 // Column pass with a compact load ring and per-warp TMA stores (256 <= N <=

@@ -44,7 +44,7 @@ def test_reference_simulation_runs_on_dropin():
     assert rc_g == 0, out_g
     g, hg = _parse(out_g)
     c, hc = _parse(out_c)
-    assert g.shape == c.shape == (48, 24)
+    assert g.shape == c.shape == (48, 23)
     assert np.array_equal(g[:, :3], c[:, :3])  # step, body, time
     pos, vel, quat = slice(3, 6), slice(6, 9), slice(9, 13)
     assert np.abs(g[:, pos] - c[:, pos]).max() <= 1e-5  # metres
