@@ -131,17 +131,16 @@ void set_smem_attrs() {
   done = true;
 }
 
-// Column kernel of the spectral step: OCN_COLS=direct selects k_cols_direct
-// (direct loads, 2 CTAs / SM), otherwise the persistent TMA ring.
+// Column kernel epilogue of the spectral step: per-warp TMA stores (default;
+// 0.507 vs 0.518 ms config-3 spectral) or, with OCN_COLS=tma, one CTA-wide
+// TMA store per tile behind a fence and a CTA barrier. Measured and removed
+// (config 3 spectral, ms): direct loads with 2 CTAs / SM 0.572; 2 persistent
+// CTAs / SM with one TMA stage each and warp stores 0.538; a compact chunk
+// ring with double-buffered exchange 0.661.
 static int cols_variant() {
   static const int v = [] {
     const char* e = getenv("OCN_COLS");
-    if (!e) return 0;
-    if (!strcmp(e, "direct")) return 1;
-    if (!strcmp(e, "tma2")) return 2;  // 2 persistent CTAs / SM, one TMA stage each, STG stores
-    if (!strcmp(e, "ring")) return 3;  // compact chunk ring + per-warp TMA stores
-    if (!strcmp(e, "tmaw")) return 4;  // TMA ring, per-warp TMA stores (no epilogue barrier)
-    return 0;
+    return e && !strcmp(e, "tma") ? 0 : 4;
   }();
   return v;
 }
@@ -212,38 +211,6 @@ void launch_rows(ocn_ctx* ctx, const RowArgs& a, bool plain, cudaStream_t st, in
 template <int N>
 void launch_cols(ocn_ctx* ctx, const ColArgs& a, int G, bool complex_out, cudaStream_t st,
                  const CUtensorMap* map, const CUtensorMap* chunk_map) {
-  if constexpr (N >= 128 && N <= 1024) {
-    if (!complex_out && cols_variant() == 1) {
-      using L = Launch<N>;
-      const size_t smem = ((size_t)L::PER_CTA * L::COL_STRIDE + fft::Plan<N>::tw_size()) * 8;
-      static bool attr = false;
-      if (!attr) {
-        OCN_CUDA(cudaFuncSetAttribute(k_cols_direct<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
-        attr = true;
-      }
-      const int tiles_x = N / L::PER_CTA;
-      k_cols_direct<N><<<tiles_x * G, L::THREADS, smem, st>>>(a, tiles_x);
-      OCN_LAUNCHED(ctx);
-      return;
-    }
-  }
-  if constexpr (ColRing<N>::OK) {
-    if (map && chunk_map && !complex_out && a.out_maps && cols_variant() == 3) {
-      using RG = ColRing<N>;
-      static bool attr3 = false;
-      if (!attr3) {
-        OCN_CUDA(cudaFuncSetAttribute(k_cols_ring<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)RG::SMEM));
-        attr3 = true;
-      }
-      const int tiles_x = N / RG::PC, ntiles = tiles_x * G;
-      const int grid = std::min(ntiles, ctx->sm_count);
-      k_cols_ring<N><<<grid, RG::THREADS, RG::SMEM, st>>>(*chunk_map, a, tiles_x, ntiles);
-      OCN_LAUNCHED(ctx);
-      return;
-    }
-  }
   if constexpr (ColTma<N>::OK) {
     if (map) {
       using CT = ColTma<N>;
@@ -257,32 +224,16 @@ void launch_cols(ocn_ctx* ctx, const ColArgs& a, int G, bool complex_out, cudaSt
       }
       const int tiles_x = N / CT::PC, ntiles = tiles_x * G;
       const int grid = std::min(ntiles, ctx->sm_count);
-      if constexpr (CT::smem(1) * 2 <= 227 * 1024) {
-        if (!complex_out && cols_variant() == 2) {
-          static bool attr2 = false;
-          if (!attr2) {
-            OCN_CUDA(cudaFuncSetAttribute(k_cols_tma<N, false, 1, false, 2>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)CT::smem(1)));
-            attr2 = true;
-          }
-          const int grid2 = std::min(ntiles, 2 * ctx->sm_count);
-          k_cols_tma<N, false, 1, false, 2><<<grid2, CT::THREADS, CT::smem(1), st>>>(
-              *map, *chunk_map, a, tiles_x, ntiles);
-          OCN_LAUNCHED(ctx);
-          return;
-        }
-      }
       if constexpr (N >= 256 && N <= 1024 && CT::smem(2, true) <= 227 * 1024) {
         if (!complex_out && a.out_maps && cols_variant() == 4) {
           static bool attr4 = false;
           if (!attr4) {
-            OCN_CUDA(cudaFuncSetAttribute(k_cols_tma<N, false, 2, true, 1, true>,
+            OCN_CUDA(cudaFuncSetAttribute(k_cols_tma<N, false, 2, true, true>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)CT::smem(2, true)));
             attr4 = true;
           }
-          k_cols_tma<N, false, 2, true, 1, true><<<grid, CT::THREADS, CT::smem(2, true), st>>>(
+          k_cols_tma<N, false, 2, true, true><<<grid, CT::THREADS, CT::smem(2, true), st>>>(
               *map, *chunk_map, a, tiles_x, ntiles);
           OCN_LAUNCHED(ctx);
           return;
@@ -420,7 +371,7 @@ static void plane_warp_map_for(int n, float* plane, CUtensorMap* map) {
 }
 
 static void build_out_maps(int n, const XformDesc* desc, int count, DevBuf<CUtensorMap>& out) {
-  const bool warp_boxes = (cols_variant() == 3 || cols_variant() == 4) && n >= 256 && n <= 1024;
+  const bool warp_boxes = cols_variant() == 4 && n >= 256 && n <= 1024;
   std::vector<CUtensorMap> h((size_t)2 * count);
   for (int i = 0; i < count; ++i) {
     auto mk = warp_boxes ? plane_warp_map_for : plane_map_for;

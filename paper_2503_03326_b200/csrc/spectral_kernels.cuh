@@ -607,45 +607,6 @@ __global__ void __launch_bounds__(Launch<N>::THREADS) k_cols(const ColArgs a) {
   }
 }
 
-// Column pass with direct loads, one column tile (PC columns x N rows) per
-// CTA, two CTAs per SM: the scratch is read straight into registers (only the
-// band rows of band-limited transforms: the others were never written by the
-// row pass and are exactly zero), shared memory holds only the inter-pass
-// exchange and the twiddles, and Re / Im go out as evict-first stores. Per
-// element that moves 16 B through the shared-memory crossbar instead of the
-// TMA ring's 48 (tile landing, pass-0 read, exchange, staging, TMA-store read).
-template <int N>
-__global__ void __launch_bounds__(Launch<N>::THREADS, 2) k_cols_direct(const ColArgs a, int tiles_x) {
-  using L = Launch<N>;
-  using PL = fft::Plan<N>;
-  constexpr int PC = L::PER_CTA, H = N / 2;
-  extern __shared__ __align__(16) float2 smem[];
-  float2* stw = smem + PC * L::COL_STRIDE;
-  for (int i = threadIdx.x; i < PL::tw_size(); i += blockDim.x) stw[i] = __ldg(a.tw + i);
-  const int c = threadIdx.x % PC, t = threadIdx.x / PC;
-  const int xf = blockIdx.x / tiles_x;
-  const int col = (blockIdx.x - xf * tiles_x) * PC + c;
-  const XformDesc* dp = a.desc + xf;
-  const int rh0 = a.gc ? __ldg(&dp->row_half) : 0;
-  const int rh = rh0 > 0 ? rh0 : H + 1;
-  const bool edge_only = rh <= PL::T;  // band within the first / last T rows of the column
-  const float2* in = a.scratch + (size_t)xf * N * N + col;
-  float* out_re = reinterpret_cast<float*>(__ldg(reinterpret_cast<const unsigned long long*>(&dp->out_re)));
-  float* out_im = reinterpret_cast<float*>(__ldg(reinterpret_cast<const unsigned long long*>(&dp->out_im)));
-  __syncthreads();  // twiddles staged
-  fft::cta_fft<N, false, false, false, true, 0, 0, (PL::P > 1)>(
-      t, smem + c * L::COL_STRIDE, stw,
-      [&](int i) {
-        // scratch row i holds spectrum row i ^ N/2: nonzero only for |(i ^ H) - H| < rh
-        return abs((i ^ H) - H) < rh ? __ldcs(in + (size_t)i * N) : make_float2(0.f, 0.f);
-      },
-      [&](int r, float2 x) {
-        __stcs(out_re + (size_t)r * N + col, x.x);  // fft.cpp:93-99 split
-        if (out_im) __stcs(out_im + (size_t)r * N + col, x.y);
-      },
-      fft::NoHook{}, edge_only);
-}
-
 // Column pass, persistent and TMA-fed (128 <= N <= 4096). A CTA walks the
 // column tiles [N rows][PC columns] (tile = transform x column block) with a
 // ring of STAGES shared buffers: one elected thread keeps STAGES - 1 tiles in
@@ -696,9 +657,8 @@ int cols_tma_pc(int n) { return n >= 128 && n <= 4096 ? 8192 / n : 0; }
 // {PC, 32 / PC, 32} of the plane viewed as [N / T][T][N] (plane_warp_map_for)
 // -- from its own 8 KB of the staging, after a per-thread fence and a
 // __syncwarp: no CTA barrier and no CTA-wide fence in the epilogue.
-template <int N, bool COMPLEX_OUT, int S, bool TMA_STORE = false, int MINB = 1,
-          bool WARP_STORE = false>
-__global__ void __launch_bounds__(ColTma<N>::THREADS, MINB)
+template <int N, bool COMPLEX_OUT, int S, bool TMA_STORE = false, bool WARP_STORE = false>
+__global__ void __launch_bounds__(ColTma<N>::THREADS, 1)
     k_cols_tma(const __grid_constant__ CUtensorMap src, const __grid_constant__ CUtensorMap src_chunk,
                const ColArgs a, int tiles_x, int ntiles) {
   using CT = ColTma<N>;
@@ -825,151 +785,6 @@ __global__ void __launch_bounds__(ColTma<N>::THREADS, MINB)
     if (++s == S) s = 0, phase ^= 1;
   }
   if (TMA_STORE && (WARP_STORE ? (threadIdx.x & 31) == 0 : threadIdx.x == 0)) tma::bulk_wait();
-}
-
-// Column pass with a compact load ring and per-warp TMA stores (256 <= N <=
-// 1024, the spectral step's split outputs). Persistent, one 8-warp CTA per SM:
-//  * a ring of 32-row chunks (32 x PC float2 each) filled by TMA: a tile loads
-//    only the chunks that hold its band rows (2 of 32 for the R <= 32 grids and
-//    depths), so many band-limited tiles are in flight at once and the next
-//    tiles' load latency hides behind the current one;
-//  * one exchange buffer X (padded per column) between pass 0 (reads the ring)
-//    and pass 1;
-//  * per-warp staging: thread t of column c ends with rows t + T r' (r' < 32),
-//    so a warp's outputs form one 3-D box {PC columns, 32 / PC t-values, 32 r'}
-//    of the plane viewed as [N / T][T][N]; each warp writes its Re / Im box to
-//    its own staging, fences and issues its own two TMA stores -- no CTA
-//    barrier and no CTA-wide fence per tile for the epilogue;
-//  * the twiddles.
-// Two CTA barriers per tile: A after pass 0 (the tile's ring chunks are free:
-// thread 0 releases them and tops the ring up), B after pass 1's exchange
-// reads (X may be overwritten by the next tile's pass 0).
-template <int N>
-struct ColRing {
-  using CT = ColTma<N>;
-  static constexpr int PC = CT::PC, STRIDE = CT::STRIDE, T = CT::T, THREADS = CT::THREADS;
-  static constexpr int XB = (PC * STRIDE + 15) / 16 * 16;  // float2 per exchange buffer
-  static constexpr int CH = 32, NCH = N / CH;                // rows per chunk
-  static constexpr int CHUNK = CH * PC;                      // float2 per chunk
-  static constexpr int TW = CT::TW;
-  static constexpr int TPWARP = 32 / PC;                     // t-values per warp
-  static constexpr int WSTAGE = 32 * 32;                     // floats per warp and plane
-  static constexpr int TB = 16;                              // tiles in flight (mbarriers)
-  static constexpr size_t FIXED =
-      ((size_t)XB + TW) * 8 + (size_t)(THREADS / 32) * 2 * WSTAGE * 4 + TB * 8;
-  static constexpr int RING = (int)((227 * 1024 - FIXED) / (CHUNK * 8));
-  static constexpr size_t SMEM = FIXED + (size_t)RING * CHUNK * 8;
-  static constexpr bool OK = N >= 256 && N <= 1024 && RING >= NCH && PC <= 32 &&
-                             N / T == 32 && THREADS == 256;
-};
-
-template <int N>
-__global__ void __launch_bounds__(ColRing<N>::THREADS, 1)
-    k_cols_ring(const __grid_constant__ CUtensorMap src_chunk, const ColArgs a, int tiles_x,
-                int ntiles) {
-  using R = ColRing<N>;
-  constexpr int PC = R::PC, T = R::T, H = N / 2, CH = R::CH, NCH = R::NCH, RING = R::RING;
-  constexpr int TB = R::TB;
-  extern __shared__ __align__(128) float2 smem[];
-  float2* X = smem;                           // exchange
-  float2* stw = smem + R::XB;                 // twiddles
-  float* wst = reinterpret_cast<float*>(stw + R::TW);  // per-warp staging [warp][2][WSTAGE]
-  float2* ring = reinterpret_cast<float2*>(wst + (R::THREADS / 32) * 2 * R::WSTAGE);
-  const uint32_t bar0 = tma::smem_u32(ring + (size_t)RING * R::CHUNK);
-  const int c = threadIdx.x % PC, t = threadIdx.x / PC;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float* my_re = wst + warp * 2 * R::WSTAGE;
-  float* my_im = my_re + R::WSTAGE;
-  // band chunks of a tile: [0, lo) and [hi, NCH); full tiles: lo = NCH, hi = NCH
-  struct Band {
-    int rh, lo, hi;
-  };
-  auto band_of = [&](int tile) {
-    const int xf = tile / tiles_x;
-    const int r0 = a.gc ? __ldg(&a.desc[xf].row_half) : 0;
-    Band b{r0 > 0 ? r0 : H + 1, NCH, NCH};
-    if (b.rh <= H) {
-      const int lo = (b.rh + CH - 1) / CH, hi = (N - b.rh + 1) / CH;
-      if (lo < hi) b.lo = lo, b.hi = hi;
-    }
-    return b;
-  };
-  // producer state (thread 0): next tile to load, chunks issued / released
-  int p_tile = blockIdx.x, p_seq = 0, head = 0, tail = 0;
-  auto top_up = [&](int c_seq) {
-    while (p_tile < ntiles && p_seq < c_seq + TB) {
-      const Band b = band_of(p_tile);
-      const int nch = b.lo + (NCH - b.hi);
-      if (head + nch - tail > RING) break;
-      const int xf = p_tile / tiles_x, col0 = (p_tile - xf * tiles_x) * PC;
-      const uint32_t bar = bar0 + 8 * (p_seq % TB);
-      tma::mbar_arrive_expect_tx(bar, (uint32_t)nch * R::CHUNK * 8);
-      for (int k = 0; k < NCH; ++k) {
-        if (k >= b.lo && k < b.hi) continue;
-        const int slot = head % RING;
-        tma::load_4d(tma::smem_u32(ring + (size_t)slot * R::CHUNK), &src_chunk, 2 * col0, 0, k, xf,
-                     bar);
-        ++head;
-      }
-      ++p_seq;
-      p_tile += gridDim.x;
-    }
-  };
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < TB; ++i) tma::mbar_init(bar0 + 8 * i, 1);
-    tma::fence_mbar_init();
-    top_up(0);
-  }
-  for (int i = threadIdx.x; i < R::TW; i += R::THREADS) stw[i] = __ldg(a.tw + i);
-  __syncthreads();
-  int base = 0;  // ring position of the current tile's first chunk (all threads)
-  int seq = 0;
-  const int tl = t % R::TPWARP;  // this thread's t within its warp's box
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++seq) {
-    const int xf = tile / tiles_x, col0 = (tile - xf * tiles_x) * PC;
-    const Band b = band_of(tile);
-    const int nch = b.lo + (NCH - b.hi);
-    const bool edge_only = b.rh <= N / 32;
-    tma::mbar_wait(bar0 + 8 * (seq % TB), (uint32_t)(seq / TB) & 1);
-    const float2* rg = ring;
-    auto load = [&](int i) {
-      if (!(abs((i ^ H) - H) < b.rh)) return make_float2(0.f, 0.f);  // never-written rows
-      const int k = i / CH;
-      int slot = base + (k < b.lo ? k : b.lo + (k - b.hi));
-      if (slot >= RING) slot -= RING;
-      return rg[(size_t)slot * R::CHUNK + (i % CH) * PC + c];
-    };
-    auto mid = [&] {  // barrier A: every thread is past pass 0 of this tile
-      if (threadIdx.x == 0) {
-        tail += nch;
-        top_up(seq + 1);
-      }
-    };
-    auto free_hook = [&] {  // X fully read: barrier B, then this warp's staging is free?
-      __syncthreads();
-      if (lane == 0) tma::bulk_wait_read();  // this warp's previous stores read its staging
-      __syncwarp();
-    };
-    fft::cta_fft<N, false, false, false, true, 0, 0, true>(
-        t, X + c * R::STRIDE, stw, load,
-        [&](int k, float2 x) {
-          const int o = (k / T) * 32 + tl * PC + c;  // box order {c, tl, r'}
-          my_re[o] = x.x;                            // fft.cpp:93-99 split
-          my_im[o] = x.y;
-        },
-        free_hook, edge_only, mid);
-    tma::fence_proxy_async_smem();  // this thread's staging writes -> the async proxy
-    __syncwarp();
-    if (lane == 0) {
-      const int t0 = (warp * 32) / PC;  // first t of this warp
-      tma::store_3d(a.out_maps + 2 * xf, tma::smem_u32(my_re), col0, t0, 0);
-      if (a.desc[xf].out_im) tma::store_3d(a.out_maps + 2 * xf + 1, tma::smem_u32(my_im), col0, t0, 0);
-      tma::bulk_commit();
-    }
-    base += nch;
-    if (base >= RING) base -= RING;
-  }
-  if (lane == 0) tma::bulk_wait();
 }
 
 // fp64 interleaved pair -> fp32 X + iY (fft.cpp:88-91)
