@@ -98,6 +98,17 @@ struct PinnedBuf {
   }
 };
 
+
+// Opt a kernel into `bytes` of dynamic shared memory on the current device,
+// once per (device, kernel, size): the attribute lives in the device context,
+// so a process-wide flag would leave a second device's context without it.
+// Thread-safe (spectral.cu).
+void smem_opt_in(const void* func, int bytes);
+template <class F>
+inline void smem_opt_in(F* func, size_t bytes) {
+  smem_opt_in(reinterpret_cast<const void*>(func), (int)bytes);
+}
+
 }  // namespace ocn
 
 // The context: one device, one stream, reusable scratch.

@@ -413,12 +413,7 @@ void mask_launch(ocn_zone* z, MaskArgs A, const int* nloops_dev, int nloops_host
                                      z->bin_edges.p, bin_cap);
   OCN_LAUNCHED(ctx);
   const size_t smem = kMaskEdgesSmem * 2 * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    OCN_CUDA(cudaFuncSetAttribute(k_mask_cells, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
-    attr = true;
-  }
+  smem_opt_in(k_mask_cells, smem);
   k_mask_cells<<<ctx->sm_count * 4, 256, smem, st>>>(A, z->mask_box.p, z->loop_bbox.p,
                                                      z->loops_off.p, z->loops_xz.p, (int)box_cap,
                                                      z->mask_h.p, z->mask_f.p, z->curr(), apply,

@@ -889,12 +889,7 @@ void hydro_evaluate(ocn_mesh* m, const ocn_pose* pose, const ocn_fluid* fluid,
   OCN_LAUNCHED(ctx);
   const size_t chain_smem = std::max(9 * kChainPar * sizeof(int),
                                      2 * kChainSeq * sizeof(int) + kChainSeq);
-  static bool attr = false;
-  if (!attr) {
-    OCN_CUDA(cudaFuncSetAttribute(k_chain, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)chain_smem));
-    attr = true;
-  }
+  smem_opt_in(k_chain, chain_smem);
   k_chain<<<1, kChainThreads, chain_smem, st>>>(m->total.p, m->partner.p, m->used.p, m->loop_off.p,
                                                 m->point_ref.p, m->loop_counts.p);
   OCN_LAUNCHED(ctx);

@@ -37,6 +37,7 @@ struct ocn_slab {
   ocn::DevBuf<float2> spec;      // [rows][N]: h~ (the slab builds surface fields only)
   ocn::DevBuf<float2> twiddle;
   ocn::DevBuf<float2> tw1, tw2, wn;  // four-step column pass: inner tables, w_N^m
+  ocn::DevBuf<float2> tw128, w_hi, w_lo;  // four-step row pass (N = 16384): w_N^(128 h), w_N^l
   ocn::DevBuf<double> d_time;
   ocn::DevBuf<float> fields;     // [8][N][cols]
 };
@@ -159,6 +160,73 @@ __global__ void __launch_bounds__(SlabLaunch<N>::THREADS) k_slab_rows(const Slab
       });
 }
 
+// Row pass for N = 16384 = 128 x 128: one 512-thread CTA per (row, pair), the
+// row's FFT as a four-step inside shared memory with warp-synchronous
+// 128-point FFTs (4 threads each) -- two CTA barriers per row instead of the
+// generic 3-pass CTA FFT's four, and every twiddle from shared memory:
+//   step 1 (group g = i2): Y[k1] = sum_i1 x[128 i1 + i2] w_128^(i1 k1), times
+//          w_N^(i2 k1) (= hi[m >> 7] lo[m & 127], m = i2 k1), written
+//          transposed to X[k1][i2];
+//   step 2 (group g = k1, in place): out[k1 + 128 k2] = sum_i2 X[k1][i2] w_128^(i2 k2).
+// x[j] is the packed coefficient of the pair at mode (row, j) (surface.cpp:77-80),
+// generated in step 1's loads from h~ (as k_slab_rows).
+constexpr int kRow4sThreads = 512;
+template <int N>
+__global__ void __launch_bounds__(kRow4sThreads, 1)
+    k_slab_rows_4s(const SlabRowArgs a, const float2* __restrict__ tw128,
+                   const float2* __restrict__ w_hi, const float2* __restrict__ w_lo) {
+  constexpr int M = 128;
+  static_assert(N == M * M, "four-step row pass is for N = 16384");
+  using PL = fft::Plan<M>;
+  constexpr int T = PL::T, S = PL::SMEM;
+  extern __shared__ float2 smem[];
+  float2* X = smem;              // [128][S]
+  float2* stw = X + M * S;       // Plan<128> twiddles
+  float2* hi = stw + PL::tw_size();
+  float2* lo = hi + M;
+  for (int i = threadIdx.x; i < PL::tw_size(); i += kRow4sThreads) stw[i] = __ldg(tw128 + i);
+  for (int i = threadIdx.x; i < M; i += kRow4sThreads) hi[i] = __ldg(w_hi + i), lo[i] = __ldg(w_lo + i);
+  const int li = blockIdx.x / a.np, p = a.p0 + blockIdx.x % a.np;
+  const int g = threadIdx.x / T, t = threadIdx.x % T;
+  const float kx = a.dk * (float)(a.row0 + li - N / 2);
+  const float2* srow = a.spec + (size_t)li * N;
+  const float chop = a.chop, kx2 = kx * kx;
+  float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f, c4 = 0.f, c5 = 0.f, c6 = 0.f;
+  if (p == 0) c0 = 1.f, c1 = -chop;
+  else if (p == 1) c5 = chop;
+  else if (p == 2) c2 = chop, c6 = chop;
+  else c3 = -1.f, c4 = kx;
+  __syncthreads();  // tables staged
+  // step 1: the 128 DFTs over i1 (stride-128 elements), group g = i2
+  fft::cta_fft<M, true, false, false, true>(
+      t, X + g * S, stw,
+      [&](int i1) {
+        const int j = M * i1 + g;
+        const float2 h = __ldg(srow + j);
+        const float kz = a.dk * (float)(j - N / 2);
+        const float k2 = fmaf(kz, kz, kx2);
+        const float inv = k2 > 0.f ? rsqrtf(k2) : 0.f;
+        const float mr = fmaf(inv * kx, fmaf(c2, kz, c1), fmaf(c3, kz, c0));
+        const float mi = fmaf(inv, fmaf(c6 * kz, kz, c5 * (kz + kx2)), c4);
+        return make_float2(h.x * mr - h.y * mi, h.x * mi + h.y * mr);
+      },
+      [&](int k1, float2 y) {
+        const int m = g * k1;
+        X[k1 * S + g] = fft::cmul(y, fft::cmul(hi[m >> 7], lo[m & (M - 1)]));
+      },
+      [] { __syncthreads(); });  // every group's exchange reads done: X may be overwritten
+  __syncthreads();
+  // step 2: the 128 DFTs over i2 (rows of X), group g = k1, in place
+  const int cols_log2 = __ffs(a.cols) - 1;
+  fft::cta_fft<M, true, true, false, true>(
+      t, X + g * S, stw, [&](int i2) { return X[g * S + i2]; },
+      [&](int k2, float2 x) {
+        const int k = g + M * k2;
+        const int dest = k >> cols_log2, kc = k & (a.cols - 1);
+        a.send[(((size_t)dest * 4 + p) * a.rows + li) * a.cols + kc] = x;
+      });
+}
+
 struct SlabColArgs {
   int rows, cols, col0;
   int rows_log2;  // rows = N / ranks is a power of two
@@ -199,9 +267,11 @@ constexpr int kFsN2 = 128;  // inner length of the second step
 constexpr int kFsPC = 32;   // columns per tile (256-byte row segments: DRAM page locality)
 constexpr int kFsB = 2;     // i2 (step A) or k1 (step B) values per CTA (64 transforms)
 
+// element (row i, column kc) of pair p in the receive layout [src][4][R][R]:
+// ((src 4 + p) R + li) cols + kc = (i + 3 R src) cols + (p R cols + kc)
 __device__ __forceinline__ size_t recv_index(const SlabColArgs& a, int p, int i, int kc) {
-  const int src = i >> a.rows_log2, li = i & (a.rows - 1);
-  return (((size_t)src * 4 + p) * a.rows + li) * a.cols + kc;
+  const int src = i >> a.rows_log2;
+  return (size_t)(i + 3 * a.rows * src) * a.cols + ((size_t)p * a.rows * a.cols + kc);
 }
 
 // step A: for each i2 of the tile, Y[k1] = sum_i1 x[128 i1 + i2] w_N1^(i1 k1),
@@ -215,11 +285,13 @@ __global__ void __launch_bounds__(kFsB * kFsPC * (N / kFsN2) / 32) k_slab_colsA(
   constexpr int T = PL::T, TPW = 32 / T, S = PL::SMEM;
   extern __shared__ float2 smem[];  // [NT][S]
   const int p = a.p0 + blockIdx.z, kc0 = blockIdx.x * kFsPC, i20 = blockIdx.y * kFsB;
-  for (int e = threadIdx.x; e < N1 * NT; e += blockDim.x) {
-    const int c = e % kFsPC, i2l = (e / kFsPC) % kFsB, i1 = e / NT;
-    smem[(i2l * kFsPC + c) * S + fft::pad32(i1)] =
-        __ldg(recv + recv_index(a, p, kFsN2 * i1 + i20 + i2l, kc0 + c));
-  }
+  // each thread moves one (column, i2) lane: fixed across the rows it visits
+  constexpr int STEP = kFsB * kFsPC * N1 / 32 / NT;  // i1 per iteration (blockDim / NT)
+  const int c = threadIdx.x % kFsPC, i2l = (threadIdx.x / kFsPC) % kFsB, i10 = threadIdx.x / NT;
+  float2* lane_sm = smem + (i2l * kFsPC + c) * S;
+#pragma unroll 8
+  for (int i1 = i10; i1 < N1; i1 += STEP)
+    lane_sm[fft::pad32(i1)] = __ldg(recv + recv_index(a, p, kFsN2 * i1 + i20 + i2l, kc0 + c));
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tr = warp * TPW + lane / T, t = lane % T;
@@ -229,11 +301,9 @@ __global__ void __launch_bounds__(kFsB * kFsPC * (N / kFsN2) / 32) k_slab_colsA(
       t, buf, tw1, [&](int n) { return buf[fft::pad32(n)]; },
       [&](int k1, float2 x) { buf[fft::pad32(k1)] = fft::cmul(x, __ldg(wn + i2 * k1)); });
   __syncthreads();
-  for (int e = threadIdx.x; e < N1 * NT; e += blockDim.x) {
-    const int c = e % kFsPC, i2l = (e / kFsPC) % kFsB, k1 = e / NT;
-    recv[recv_index(a, p, kFsN2 * k1 + i20 + i2l, kc0 + c)] =
-        smem[(i2l * kFsPC + c) * S + fft::pad32(k1)];
-  }
+#pragma unroll 8
+  for (int k1 = i10; k1 < N1; k1 += STEP)
+    recv[recv_index(a, p, kFsN2 * k1 + i20 + i2l, kc0 + c)] = lane_sm[fft::pad32(k1)];
 }
 
 // step B: for each k1 of the tile, X[k1 + N1 k2] = sum_i2 Y[128 k1 + i2] w_128^(i2 k2);
@@ -246,11 +316,13 @@ __global__ void __launch_bounds__(kFsB * kFsPC * kFsN2 / 32) k_slab_colsB(const 
   constexpr int T = PL::T, TPW = 32 / T, S = PL::SMEM;
   extern __shared__ float2 smem[];  // [NT][S]
   const int p = a.p0 + blockIdx.z, kc0 = blockIdx.x * kFsPC, k10 = blockIdx.y * kFsB;
-  for (int e = threadIdx.x; e < kFsN2 * NT; e += blockDim.x) {
-    const int c = e % kFsPC, k1l = (e / kFsPC) % kFsB, i2 = e / NT;
-    smem[(k1l * kFsPC + c) * S + fft::pad32(i2)] =
-        __ldg(recv + recv_index(a, p, kFsN2 * (k10 + k1l) + i2, kc0 + c));
-  }
+  constexpr int STEP = kFsB * kFsPC * kFsN2 / 32 / NT;
+  const int c = threadIdx.x % kFsPC, k1l = (threadIdx.x / kFsPC) % kFsB, i20 = threadIdx.x / NT;
+  float2* lane_sm = smem + (k1l * kFsPC + c) * S;
+  const float2* lane_src = recv + recv_index(a, p, kFsN2 * (k10 + k1l), kc0 + c);
+  // rows 128 (k10 + k1l) + i2 stay inside one source block (R >= 128)
+#pragma unroll 8
+  for (int i2 = i20; i2 < kFsN2; i2 += STEP) lane_sm[fft::pad32(i2)] = __ldg(lane_src + (size_t)i2 * a.cols);
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tr = warp * TPW + lane / T, t = lane % T;
@@ -261,10 +333,11 @@ __global__ void __launch_bounds__(kFsB * kFsPC * kFsN2 / 32) k_slab_colsB(const 
   __syncthreads();
   float* re = a.fields + (size_t)(2 * p) * N * a.cols;
   float* im = a.fields + (size_t)(2 * p + 1) * N * a.cols;
-  for (int e = threadIdx.x; e < kFsN2 * NT; e += blockDim.x) {
-    const int c = e % kFsPC, k1l = (e / kFsPC) % kFsB, k2 = e / NT;
-    const int k = k10 + k1l + N1 * k2, kc = kc0 + c;
-    const float2 x = smem[(k1l * kFsPC + c) * S + fft::pad32(k2)];
+  const int kc = kc0 + c;
+#pragma unroll 8
+  for (int k2 = i20; k2 < kFsN2; k2 += STEP) {
+    const int k = k10 + k1l + N1 * k2;
+    const float2 x = lane_sm[fft::pad32(k2)];
     const float sg = ((k + a.col0 + kc) & 1) ? -1.f : 1.f;  // fft.cpp:73-75
     __stcs(re + (size_t)k * a.cols + kc, sg * x.x);          // fft.cpp:93-99
     __stcs(im + (size_t)k * a.cols + kc, sg * x.y);
@@ -278,12 +351,8 @@ bool slab_fourstep(ocn_slab* sl, const SlabColArgs& a, float2* recv, int np) {
     constexpr int N1 = N / kFsN2;
     const size_t smemA = (size_t)kFsB * kFsPC * fft::Plan<N1>::SMEM * sizeof(float2);
     const size_t smemB = (size_t)kFsB * kFsPC * fft::Plan<kFsN2>::SMEM * sizeof(float2);
-    static bool attr = false;
-    if (!attr) {
-      OCN_CUDA(cudaFuncSetAttribute(k_slab_colsA<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemA));
-      OCN_CUDA(cudaFuncSetAttribute(k_slab_colsB<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemB));
-      attr = true;
-    }
+    smem_opt_in(k_slab_colsA<N>, smemA);
+    smem_opt_in(k_slab_colsB<N>, smemB);
     const dim3 ga(a.cols / kFsPC, kFsN2 / kFsB, np), gb(a.cols / kFsPC, N1 / kFsB, np);
     k_slab_colsA<N><<<ga, kFsB * kFsPC * N1 / 32, smemA, sl->ctx->stream>>>(a, recv, sl->tw1.p, sl->wn.p);
     OCN_LAUNCHED(sl->ctx);
@@ -298,15 +367,20 @@ bool slab_fourstep(ocn_slab* sl, const SlabColArgs& a, float2* recv, int np) {
 
 template <int N>
 void slab_rows_launch(ocn_slab* sl, const SlabRowArgs& a) {  // pairs [a.p0, a.p0 + a.np)
-  using L = SlabLaunch<N>;
-  static bool attr = false;
-  if (!attr && L::SMEM_BYTES > 48 * 1024) {
-    OCN_CUDA(cudaFuncSetAttribute(k_slab_rows<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)L::SMEM_BYTES));
-    OCN_CUDA(cudaFuncSetAttribute(k_slab_cols<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)L::SMEM_BYTES));
+  if constexpr (N == 16384) {
+    using PL = fft::Plan<128>;
+    const size_t smem = ((size_t)128 * PL::SMEM + PL::tw_size() + 2 * 128) * sizeof(float2);
+    smem_opt_in(k_slab_rows_4s<N>, smem);
+    k_slab_rows_4s<N><<<a.rows * a.np, kRow4sThreads, smem, sl->ctx->stream>>>(
+        a, sl->tw128.p, sl->w_hi.p, sl->w_lo.p);
+    OCN_LAUNCHED(sl->ctx);
+    return;
   }
-  attr = true;
+  using L = SlabLaunch<N>;
+  if (L::SMEM_BYTES > 48 * 1024) {
+    smem_opt_in(k_slab_rows<N>, L::SMEM_BYTES);
+    smem_opt_in(k_slab_cols<N>, L::SMEM_BYTES);
+  }
   const int blocks = (a.rows * a.np + L::PER_CTA - 1) / L::PER_CTA;
   k_slab_rows<N><<<blocks, L::THREADS, L::SMEM_BYTES, sl->ctx->stream>>>(a);
   OCN_LAUNCHED(sl->ctx);
@@ -316,14 +390,10 @@ template <int N>
 void slab_cols_launch(ocn_slab* sl, const SlabColArgs& a, float2* recv, int np) {
   if (slab_fourstep<N>(sl, a, recv, np)) return;
   using L = SlabLaunch<N>;
-  static bool attr = false;
-  if (!attr && L::SMEM_BYTES > 48 * 1024) {
-    OCN_CUDA(cudaFuncSetAttribute(k_slab_rows<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)L::SMEM_BYTES));
-    OCN_CUDA(cudaFuncSetAttribute(k_slab_cols<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)L::SMEM_BYTES));
+  if (L::SMEM_BYTES > 48 * 1024) {
+    smem_opt_in(k_slab_rows<N>, L::SMEM_BYTES);
+    smem_opt_in(k_slab_cols<N>, L::SMEM_BYTES);
   }
-  attr = true;
   dim3 grid((a.cols + L::PER_CTA - 1) / L::PER_CTA, np);
   k_slab_cols<N><<<grid, L::THREADS, L::SMEM_BYTES, sl->ctx->stream>>>(a);
   OCN_LAUNCHED(sl->ctx);
@@ -457,6 +527,17 @@ int ocn_slab_create(ocn_ctx* ctx, int n, int ranks, int rank, double length, dou
         w[m] = make_float2((float)std::cos(ang), (float)std::sin(ang));
       }
       up(sl->wn, w);
+      if (n == 16384) {  // w_N^m = w_hi[m >> 7] w_lo[m & 127] for m < N
+        std::vector<float2> hi(128), lo(128);
+        for (int m = 0; m < 128; ++m) {
+          const double ah = 2.0 * kPi * (128.0 * m) / n, al = 2.0 * kPi * m / n;
+          hi[m] = make_float2((float)std::cos(ah), (float)std::sin(ah));
+          lo[m] = make_float2((float)std::cos(al), (float)std::sin(al));
+        }
+        up(sl->tw128, make_twiddles(128));
+        up(sl->w_hi, hi);
+        up(sl->w_lo, lo);
+      }
     }
     OCN_CUDA(cudaStreamSynchronize(ctx->stream));
     ctx_retain(ctx);

@@ -24,6 +24,9 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <mutex>
+#include <set>
+#include <tuple>
 
 #include "fft_core.cuh"
 #include "objects.cuh"
@@ -66,6 +69,16 @@ bool tma::encode_f32(CUtensorMap* map, int rank, void* base, const uint64_t* dim
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank, base, dims, strides, box, elem,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+void smem_opt_in(const void* func, int bytes) {
+  static std::mutex mu;
+  static std::set<std::tuple<int, const void*, int>> done;
+  int dev = 0;
+  OCN_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  if (!done.insert({dev, func, bytes}).second) return;
+  OCN_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
 }
 
 static void cascades_release(ocn_cascades* c) {
@@ -115,20 +128,13 @@ int grid_for(ocn_ctx* ctx, size_t n, int threads = 256) {
 
 template <int N>
 void set_smem_attrs() {
-  static bool done = false;  // per process; attributes are per-function
-  if (done) return;
   using L = Launch<N>;
   if (L::SMEM_BYTES > 48 * 1024) {
-    OCN_CUDA(cudaFuncSetAttribute(k_rows<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)L::SMEM_BYTES));
-    OCN_CUDA(cudaFuncSetAttribute(k_rows<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)L::SMEM_BYTES));
-    OCN_CUDA(cudaFuncSetAttribute(k_cols<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)L::SMEM_BYTES));
-    OCN_CUDA(cudaFuncSetAttribute(k_cols<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)L::SMEM_BYTES));
+    smem_opt_in(k_rows<N, false>, L::SMEM_BYTES);
+    smem_opt_in(k_rows<N, true>, L::SMEM_BYTES);
+    smem_opt_in(k_cols<N, false>, L::SMEM_BYTES);
+    smem_opt_in(k_cols<N, true>, L::SMEM_BYTES);
   }
-  done = true;
 }
 
 // Column kernel epilogue of the spectral step: per-warp TMA stores (default;
@@ -179,14 +185,12 @@ void launch_rows(ocn_ctx* ctx, const RowArgs& a, bool plain, cudaStream_t st, in
     ar.stage_f4 = plain ? 0 : stage_f4(family == 0 ? rpc : 1);
     const size_t smem = (size_t)ar.stage_f4 * sizeof(float4) + W::TWN * sizeof(float2) +
                         (size_t)warps * W::TPW * W::STRIDE * sizeof(float2);
-    static bool attr = false;
-    if (!attr) {
-      const int smax = stage_f4(kMaxRpc) * (int)sizeof(float4) + W::TWN * (int)sizeof(float2) +
-                       8 * W::TPW * W::STRIDE * (int)sizeof(float2);
-      OCN_CUDA(cudaFuncSetAttribute(k_rows_w<N, kRowPlain>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
-      OCN_CUDA(cudaFuncSetAttribute(k_rows_w<N, kRowSurface>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
-      OCN_CUDA(cudaFuncSetAttribute(k_rows_w<N, kRowVelocity>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
-      attr = true;
+    {
+      const size_t smax = (size_t)stage_f4(kMaxRpc) * sizeof(float4) + W::TWN * sizeof(float2) +
+                          (size_t)8 * W::TPW * W::STRIDE * sizeof(float2);
+      smem_opt_in(k_rows_w<N, kRowPlain>, smax);
+      smem_opt_in(k_rows_w<N, kRowSurface>, smax);
+      smem_opt_in(k_rows_w<N, kRowVelocity>, smax);
     }
     const dim3 grid(N / rpc, plain ? 1 : nseg);
     if (plain)
@@ -214,25 +218,14 @@ void launch_cols(ocn_ctx* ctx, const ColArgs& a, int G, bool complex_out, cudaSt
   if constexpr (ColTma<N>::OK) {
     if (map) {
       using CT = ColTma<N>;
-      static bool attr = false;
-      if (!attr) {
-        OCN_CUDA(cudaFuncSetAttribute(k_cols_tma<N, false, CT::STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CT::SMEM));
-        OCN_CUDA(cudaFuncSetAttribute(k_cols_tma<N, true, CT::STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CT::SMEM));
-        if (CT::smem(2, true) <= 227 * 1024)
-          OCN_CUDA(cudaFuncSetAttribute(k_cols_tma<N, false, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CT::smem(2, true)));
-        attr = true;
-      }
+      smem_opt_in(k_cols_tma<N, false, CT::STAGES>, CT::SMEM);
+      smem_opt_in(k_cols_tma<N, true, CT::STAGES>, CT::SMEM);
+      if (CT::smem(2, true) <= 227 * 1024) smem_opt_in(k_cols_tma<N, false, 2, true>, CT::smem(2, true));
       const int tiles_x = N / CT::PC, ntiles = tiles_x * G;
       const int grid = std::min(ntiles, ctx->sm_count);
       if constexpr (N >= 256 && N <= 1024 && CT::smem(2, true) <= 227 * 1024) {
         if (!complex_out && a.out_maps && cols_variant() == 4) {
-          static bool attr4 = false;
-          if (!attr4) {
-            OCN_CUDA(cudaFuncSetAttribute(k_cols_tma<N, false, 2, true, true>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)CT::smem(2, true)));
-            attr4 = true;
-          }
+          smem_opt_in(k_cols_tma<N, false, 2, true, true>, CT::smem(2, true));
           k_cols_tma<N, false, 2, true, true><<<grid, CT::THREADS, CT::smem(2, true), st>>>(
               *map, *chunk_map, a, tiles_x, ntiles);
           OCN_LAUNCHED(ctx);

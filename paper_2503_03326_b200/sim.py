@@ -222,6 +222,8 @@ class Simulation:
             self._bctx = [oc.Context(device, priority=1) for _ in bodies]
             self._B = [torch.cuda.ExternalStream(c.stream, device=f"cuda:{device}") for c in self._bctx]
             self._agg = [torch.cuda.Event() for _ in bodies]
+            # per map / slice buffer: the aggregates of the step that last read it
+            self._aggb = [[torch.cuda.Event() for _ in bodies] for _ in range(nbuf)]
             self._zdone = [torch.cuda.Event() for _ in bodies]
             self.bodies: List[_Body] = [_Body(b, dt, c) for b, c in zip(bodies, self._bctx)]
         else:
@@ -318,6 +320,8 @@ class Simulation:
                                                       C.byref(frame), C.byref(body.config.mask)),
                   body.zone.ctx.h, "mask")
             self._agg[i].record(B)
+            if self.pipelined:
+                self._aggb[self._cur][i].record(B)
         for k, body in enumerate(self.bodies):
             B = self._B[k]
             for i in range(nb):
@@ -351,14 +355,15 @@ class Simulation:
             self._bodies_calls(speeds, dt)
         if self.pipelined:
             # the bodies' stages are enqueued; the next step's spectral step (a function of
-            # time only) goes into the other buffer once this step's map readers are done
+            # time only) goes into the other buffer, whose last readers were the PREVIOUS
+            # step's bodies -- so it runs while this step's bodies run
+            k = 1 - self._cur
             if self.concurrent:
-                for ev in self._agg:
+                for ev in self._aggb[k]:
                     self._S.wait_event(ev)
             else:
                 self._consumed[self._cur].record(self._H)
-                self._S.wait_event(self._consumed[self._cur])
-            k = 1 - self._cur
+                self._S.wait_event(self._consumed[k])
             self._spectral(k, t_next + dt, True)
             self._ready[k].record(self._S)
             self._prefetched = True

@@ -18,8 +18,10 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.fixture(scope="module", params=[(False, False, False), (False, True, False),
-                                        (True, True, False), (True, False, True)],
-                ids=["serial-calls", "serial-native", "pipelined-native", "concurrent"])
+                                        (True, False, False), (True, True, False),
+                                        (True, False, True)],
+                ids=["serial-calls", "serial-native", "pipelined", "pipelined-native",
+                     "concurrent"])
 def run(request):
     from paper_2503_03326_b200 import ocean as oc
     from paper_2503_03326_b200.sim import BodyConfig, Simulation

@@ -1,7 +1,7 @@
 """Time one configuration's spectral step alone under kernel-variant switches
 (env vars read by libocean_b200): prints ms per step (device events).
 
-    python tools/spectral_bench.py LABEL [CONFIG]   (CONFIG 3 default, 4 or 1)
+    python tools/spectral_bench.py LABEL [CONFIG]   (CONFIG 3 default, 4, 1 or 5)
 """
 import os
 import sys
@@ -14,6 +14,9 @@ cfg = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 if cfg == 4:
     fr = bench.Frame4(0, 0, 1)
     step = lambda k: fr.L.ocn_surface_generate(fr.maps.h, 0.1 + k / 60, 1.0)  # noqa: E731
+elif cfg == 5:
+    fr = bench.Frame5(0, 0, 1, None)
+    step = lambda k: fr.step()  # noqa: E731
 elif cfg == 1:
     fr = bench.Frame1(0, 0, 1)
     step = lambda k: fr.L.ocn_surface_generate_batch(fr.maps.h, 0.1 + k * 10, 1 / 60, 1.0)  # noqa: E731
