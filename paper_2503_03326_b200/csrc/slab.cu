@@ -277,6 +277,15 @@ __global__ void __launch_bounds__(SlabLaunch<N>::THREADS) k_slab_cols(const Slab
 }
 
 // ---------------------------------------------------------------- four-step columns
+// Stride between the 64 transform buffers of a four-step CTA. The cooperative
+// tile loads / stores walk the 32 columns of a row (c fastest): with the FFT's
+// own stride (132 = 4 mod 16 float2) they hit 4 bank pairs per half-warp; an
+// odd stride spreads them (OCN_FS_ODD=1 at build time).
+#ifndef OCN_FS_ODD
+#define OCN_FS_ODD 0
+#endif
+template <int SMEM>
+constexpr int kFsStride = OCN_FS_ODD ? (SMEM | 1) : SMEM;
 constexpr int kFsN2 = 128;  // inner length of the second step
 constexpr int kFsPC = 32;   // columns per tile (256-byte row segments: DRAM page locality)
 constexpr int kFsB = 2;     // i2 (step A) or k1 (step B) values per CTA (64 transforms)
@@ -296,14 +305,14 @@ __global__ void __launch_bounds__(kFsB * kFsPC * (N / kFsN2) / 32) k_slab_colsA(
                                                              const float2* __restrict__ wn) {
   constexpr int N1 = N / kFsN2, NT = kFsB * kFsPC;
   using PL = fft::Plan<N1>;
-  constexpr int T = PL::T, TPW = 32 / T, S = PL::SMEM;
+  constexpr int T = PL::T, TPW = 32 / T, S = kFsStride<PL::SMEM>;
   extern __shared__ float2 smem[];  // [NT][S]
   const int p = a.p0 + blockIdx.z, kc0 = blockIdx.x * kFsPC, i20 = blockIdx.y * kFsB;
   // each thread moves one (column, i2) lane: fixed across the rows it visits
   constexpr int STEP = kFsB * kFsPC * N1 / 32 / NT;  // i1 per iteration (blockDim / NT)
   const int c = threadIdx.x % kFsPC, i2l = (threadIdx.x / kFsPC) % kFsB, i10 = threadIdx.x / NT;
   float2* lane_sm = smem + (i2l * kFsPC + c) * S;
-#pragma unroll 8
+#pragma unroll
   for (int i1 = i10; i1 < N1; i1 += STEP)
     lane_sm[fft::pad32(i1)] = __ldg(recv + recv_index(a, p, kFsN2 * i1 + i20 + i2l, kc0 + c));
   __syncthreads();
@@ -315,7 +324,7 @@ __global__ void __launch_bounds__(kFsB * kFsPC * (N / kFsN2) / 32) k_slab_colsA(
       t, buf, tw1, [&](int n) { return buf[fft::pad32(n)]; },
       [&](int k1, float2 x) { buf[fft::pad32(k1)] = fft::cmul(x, __ldg(wn + i2 * k1)); });
   __syncthreads();
-#pragma unroll 8
+#pragma unroll
   for (int k1 = i10; k1 < N1; k1 += STEP)
     recv[recv_index(a, p, kFsN2 * k1 + i20 + i2l, kc0 + c)] = lane_sm[fft::pad32(k1)];
 }
@@ -327,7 +336,7 @@ __global__ void __launch_bounds__(kFsB * kFsPC * kFsN2 / 32) k_slab_colsB(const 
                                                         const float2* __restrict__ tw2) {
   constexpr int N1 = N / kFsN2, NT = kFsB * kFsPC;
   using PL = fft::Plan<kFsN2>;
-  constexpr int T = PL::T, TPW = 32 / T, S = PL::SMEM;
+  constexpr int T = PL::T, TPW = 32 / T, S = kFsStride<PL::SMEM>;
   extern __shared__ float2 smem[];  // [NT][S]
   const int p = a.p0 + blockIdx.z, kc0 = blockIdx.x * kFsPC, k10 = blockIdx.y * kFsB;
   constexpr int STEP = kFsB * kFsPC * kFsN2 / 32 / NT;
@@ -335,7 +344,7 @@ __global__ void __launch_bounds__(kFsB * kFsPC * kFsN2 / 32) k_slab_colsB(const 
   float2* lane_sm = smem + (k1l * kFsPC + c) * S;
   const float2* lane_src = recv + recv_index(a, p, kFsN2 * (k10 + k1l), kc0 + c);
   // rows 128 (k10 + k1l) + i2 stay inside one source block (R >= 128)
-#pragma unroll 8
+#pragma unroll
   for (int i2 = i20; i2 < kFsN2; i2 += STEP) lane_sm[fft::pad32(i2)] = __ldg(lane_src + (size_t)i2 * a.cols);
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -348,7 +357,7 @@ __global__ void __launch_bounds__(kFsB * kFsPC * kFsN2 / 32) k_slab_colsB(const 
   float* re = a.fields + (size_t)(2 * p) * N * a.cols;
   float* im = a.fields + (size_t)(2 * p + 1) * N * a.cols;
   const int kc = kc0 + c;
-#pragma unroll 8
+#pragma unroll
   for (int k2 = i20; k2 < kFsN2; k2 += STEP) {
     const int k = k10 + k1l + N1 * k2;
     const float2 x = lane_sm[fft::pad32(k2)];

@@ -8,7 +8,7 @@ out=paper_2503_03326_b200/lib/variants; mkdir -p $out /tmp/ocn_var_$name
 objs=""
 for f in paper_2503_03326_b200/csrc/*.cu; do
   o=/tmp/ocn_var_$name/$(basename $f .cu).o
-  if [ "$(basename $f)" = "spectral.cu" ]; then
+  if [ "$(basename $f)" = "${VARIANT_SRC:-spectral.cu}" ]; then
     nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr -Xcompiler -fPIC -Xcompiler -fvisibility=hidden -Iinclude "$@" -c $f -o $o
   else
     o=paper_2503_03326_b200/build/$(basename $f .cu).o
