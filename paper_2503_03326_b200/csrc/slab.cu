@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(kFsB * kFsPC * (N / kFsN2) / 32) k_slab_colsA(
   constexpr int STEP = kFsB * kFsPC * N1 / 32 / NT;  // i1 per iteration (blockDim / NT)
   const int c = threadIdx.x % kFsPC, i2l = (threadIdx.x / kFsPC) % kFsB, i10 = threadIdx.x / NT;
   float2* lane_sm = smem + (i2l * kFsPC + c) * S;
-#pragma unroll
+#pragma unroll 8
   for (int i1 = i10; i1 < N1; i1 += STEP)
     lane_sm[fft::pad32(i1)] = __ldg(recv + recv_index(a, p, kFsN2 * i1 + i20 + i2l, kc0 + c));
   __syncthreads();
@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(kFsB * kFsPC * (N / kFsN2) / 32) k_slab_colsA(
       t, buf, tw1, [&](int n) { return buf[fft::pad32(n)]; },
       [&](int k1, float2 x) { buf[fft::pad32(k1)] = fft::cmul(x, __ldg(wn + i2 * k1)); });
   __syncthreads();
-#pragma unroll
+#pragma unroll 8
   for (int k1 = i10; k1 < N1; k1 += STEP)
     recv[recv_index(a, p, kFsN2 * k1 + i20 + i2l, kc0 + c)] = lane_sm[fft::pad32(k1)];
 }
@@ -344,7 +344,7 @@ __global__ void __launch_bounds__(kFsB * kFsPC * kFsN2 / 32) k_slab_colsB(const 
   float2* lane_sm = smem + (k1l * kFsPC + c) * S;
   const float2* lane_src = recv + recv_index(a, p, kFsN2 * (k10 + k1l), kc0 + c);
   // rows 128 (k10 + k1l) + i2 stay inside one source block (R >= 128)
-#pragma unroll
+#pragma unroll 8
   for (int i2 = i20; i2 < kFsN2; i2 += STEP) lane_sm[fft::pad32(i2)] = __ldg(lane_src + (size_t)i2 * a.cols);
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(kFsB * kFsPC * kFsN2 / 32) k_slab_colsB(const 
   float* re = a.fields + (size_t)(2 * p) * N * a.cols;
   float* im = a.fields + (size_t)(2 * p + 1) * N * a.cols;
   const int kc = kc0 + c;
-#pragma unroll
+#pragma unroll 8
   for (int k2 = i20; k2 < kFsN2; k2 += STEP) {
     const int k = k10 + k1l + N1 * k2;
     const float2 x = lane_sm[fft::pad32(k2)];
@@ -372,8 +372,8 @@ bool slab_fourstep(ocn_slab* sl, const SlabColArgs& a, float2* recv, int np) {
   if constexpr (N >= 4096) {
     if (a.cols % kFsPC) return false;
     constexpr int N1 = N / kFsN2;
-    const size_t smemA = (size_t)kFsB * kFsPC * fft::Plan<N1>::SMEM * sizeof(float2);
-    const size_t smemB = (size_t)kFsB * kFsPC * fft::Plan<kFsN2>::SMEM * sizeof(float2);
+    const size_t smemA = (size_t)kFsB * kFsPC * kFsStride<fft::Plan<N1>::SMEM> * sizeof(float2);
+    const size_t smemB = (size_t)kFsB * kFsPC * kFsStride<fft::Plan<kFsN2>::SMEM> * sizeof(float2);
     smem_opt_in(k_slab_colsA<N>, smemA);
     smem_opt_in(k_slab_colsB<N>, smemB);
     const dim3 ga(a.cols / kFsPC, kFsN2 / kFsB, np), gb(a.cols / kFsPC, N1 / kFsB, np);
