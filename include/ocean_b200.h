@@ -432,6 +432,12 @@ OCN_API int ocn_mesh_destroy(ocn_mesh* mesh);
  * and the report is fetched with ocn_hydro_report_get. */
 OCN_API int ocn_hydro_aggregate(ocn_mesh* mesh, const ocn_pose* pose, const ocn_fluid* fluid,
                         const double* host_vertex_depth, ocn_hydro_report* report);
+/* aggregate for n <= 16 bodies as ONE launch set (Simulation::step's body loop,
+ * sim.cpp:74-83): meshes[i] at poses[i] against fluids[i] -- each with its own
+ * zone list and drag coefficients; all fluids share maps / slices and all meshes
+ * one context. reports may be NULL (async; ocn_hydro_report_get per mesh). */
+OCN_API int ocn_hydro_aggregate_batch(int n, ocn_mesh* const* meshes, const ocn_pose* poses,
+                                      const ocn_fluid* fluids, ocn_hydro_report* reports);
 OCN_API int ocn_hydro_report_get(ocn_mesh* mesh, ocn_hydro_report* report);
 /* Per-vertex world positions (3 doubles) and signed depths of the last evaluation. */
 OCN_API int ocn_hydro_vertices(ocn_mesh* mesh, double* host_world, double* host_depth);

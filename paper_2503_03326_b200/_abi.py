@@ -138,6 +138,8 @@ SIGNATURES = {
     "ocn_mesh_create": (ci, [vp, ci, d, ci, i32, d, d, cd, pvp]),
     "ocn_mesh_destroy": (ci, [vp]),
     "ocn_hydro_aggregate": (ci, [vp, C.POINTER(Pose), C.POINTER(Fluid), d, C.POINTER(HydroReport)]),
+    "ocn_hydro_aggregate_batch": (ci, [ci, pvp, C.POINTER(Pose), C.POINTER(Fluid),
+                                       C.POINTER(HydroReport)]),
     "ocn_hydro_report_get": (ci, [vp, C.POINTER(HydroReport)]),
     "ocn_hydro_vertices": (ci, [vp, d, d]),
     "ocn_hydro_states": (ci, [vp, ci, C.POINTER(TriangleState), C.POINTER(ci)]),

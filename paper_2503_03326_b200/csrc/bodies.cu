@@ -1,15 +1,24 @@
 // bodies.cu — the per-body part of Simulation::step (sim.cpp:73-109) for all
-// bodies in one C-ABI call: host orchestration of the device stages, so a
-// multi-body step costs one library call instead of five per body.
+// bodies in one C-ABI call, with every body's hull evaluated by ONE batched
+// launch set (hydro.cu: HydroBatch, blockIdx.y = body).
 //
-// Order is sim.cpp's: per body i, aggregate against height_at plus every other
-// body's zone (compose_height, sim.cpp:44-51), update_stability (spacing
-// changes at once, so body i+1 sees it), and the mask computed but not applied;
-// then per body apply_mask + FdmZone::step at the pre-integration position;
-// then the reports are read (one stream synchronisation).
+// Order is sim.cpp's: body i's hull senses every other body's zone with the
+// spacing that zone has at body i's turn -- zones j < i are past their
+// update_stability (sim.cpp:74-99). update_stability is host scalar bookkeeping
+// (the zone's field is untouched), so the jobs are built in body order with
+// the stabilities updated in between, each job capturing its zone views as
+// they stand, and the whole batch then runs at once. The masks are computed
+// (not applied) per body, then per body apply_mask + FdmZone::step at the
+// pre-integration position, then the reports are read (one synchronisation).
 #include <vector>
 
-#include "objects.cuh"
+#include "hydro_internal.cuh"
+
+namespace ocn {
+HydroJob make_job(ocn_mesh* m, const ocn_pose* pose, const ocn_fluid* fluid, const double* host_depth);
+void fill_samplers_batch(HydroBatch<kMaxBatch>& B, const ocn_fluid* fluid);
+void hydro_evaluate_jobs(int n, ocn_mesh* const* meshes, const HydroBatch<kMaxBatch>& B);
+}  // namespace ocn
 
 using namespace ocn;
 
@@ -17,42 +26,52 @@ extern "C" {
 
 int ocn_bodies_step(int n_bodies, const ocn_body_frame* bodies, const ocn_fluid* fluid, double dt,
                     ocn_hydro_report* reports) {
-  if (n_bodies < 0 || (n_bodies > 0 && (!bodies || !fluid))) return OCN_ERR_ARG;
-  if (n_bodies == 0) return OCN_OK;
-  std::vector<void*> others;
-  others.reserve(n_bodies);
-  for (int i = 0; i < n_bodies; ++i) {
-    const ocn_body_frame& b = bodies[i];
-    others.clear();
-    for (int k = 0; k < n_bodies; ++k)
-      if (k != i) others.push_back(bodies[k].zone);
-    ocn_fluid f = *fluid;
-    f.n_zones = (int32_t)others.size();
-    f.zones = others.empty() ? nullptr : others.data();
-    f.cd_water = b.cd_water;
-    f.cd_air = b.cd_air;
-    int st = ocn_hydro_aggregate((ocn_mesh*)b.mesh, &b.pose, &f, nullptr, nullptr);
-    if (st != OCN_OK) return st;
-    st = ocn_zone_update_stability((ocn_zone*)b.zone, b.speed, dt);
-    if (st != OCN_OK) return st;
-    st = ocn_zone_mask_from_hydro_deferred((ocn_zone*)b.zone, (ocn_mesh*)b.mesh, b.yaw,
-                                           b.pose.position[0], b.pose.position[2], b.speed,
-                                           &b.frame, &b.mask);
-    if (st != OCN_OK) return st;
-  }
-  for (int i = 0; i < n_bodies; ++i) {
-    int st = ocn_zone_apply_last_mask((ocn_zone*)bodies[i].zone);
-    if (st != OCN_OK) return st;
-    st = ocn_zone_step((ocn_zone*)bodies[i].zone, dt, bodies[i].pose.position[0],
-                       bodies[i].pose.position[2]);
-    if (st != OCN_OK) return st;
-  }
-  if (!reports) return OCN_OK;  // asynchronous: reports via ocn_hydro_report_get
-  for (int i = 0; i < n_bodies; ++i) {
-    const int st = ocn_hydro_report_get((ocn_mesh*)bodies[i].mesh, &reports[i]);
-    if (st != OCN_OK) return st;
-  }
-  return OCN_OK;
+  ocn_mesh* m0 = n_bodies > 0 && bodies ? (ocn_mesh*)bodies[0].mesh : nullptr;
+  return api_call(m0 ? m0->ctx : nullptr, [&] {
+    OCN_REQUIRE(n_bodies >= 0 && n_bodies <= kMaxBatch, "ocn_bodies_step: %d bodies (0..%d)",
+                n_bodies, kMaxBatch);
+    if (n_bodies == 0) return;
+    OCN_REQUIRE(bodies && fluid, "null argument");
+    auto check = [](int st) {
+      if (st != OCN_OK) fail(st, "%s", global_error().c_str());
+    };
+    std::vector<ocn_mesh*> meshes(n_bodies);
+    HydroBatch<kMaxBatch> B{};
+    B.n = n_bodies;
+    std::vector<void*> others;
+    for (int i = 0; i < n_bodies; ++i) {
+      const ocn_body_frame& b = bodies[i];
+      OCN_REQUIRE(b.mesh && b.zone, "body %d: null mesh / zone", i);
+      meshes[i] = (ocn_mesh*)b.mesh;
+      OCN_REQUIRE(meshes[i]->ctx == m0->ctx, "bodies must share one context");
+      others.clear();
+      for (int k = 0; k < n_bodies; ++k)
+        if (k != i) others.push_back(bodies[k].zone);
+      ocn_fluid f = *fluid;
+      f.n_zones = (int32_t)others.size();
+      f.zones = others.empty() ? nullptr : others.data();
+      f.cd_water = b.cd_water;
+      f.cd_air = b.cd_air;
+      f.host_velocity = nullptr;
+      if (i == 0) fill_samplers_batch(B, &f);
+      B.job[i] = make_job(meshes[i], &b.pose, &f, nullptr);
+      check(ocn_zone_update_stability((ocn_zone*)b.zone, b.speed, dt));
+    }
+    hydro_evaluate_jobs(n_bodies, meshes.data(), B);
+    for (int i = 0; i < n_bodies; ++i) {
+      const ocn_body_frame& b = bodies[i];
+      check(ocn_zone_mask_from_hydro_deferred((ocn_zone*)b.zone, meshes[i], b.yaw,
+                                              b.pose.position[0], b.pose.position[2], b.speed,
+                                              &b.frame, &b.mask));
+    }
+    for (int i = 0; i < n_bodies; ++i) {
+      check(ocn_zone_apply_last_mask((ocn_zone*)bodies[i].zone));
+      check(ocn_zone_step((ocn_zone*)bodies[i].zone, dt, bodies[i].pose.position[0],
+                          bodies[i].pose.position[2]));
+    }
+    if (!reports) return;  // asynchronous: reports via ocn_hydro_report_get
+    for (int i = 0; i < n_bodies; ++i) check(ocn_hydro_report_get(meshes[i], &reports[i]));
+  });
 }
 
 }  // extern "C"

@@ -23,6 +23,7 @@
 // report is bit-identical run to run.
 #include <algorithm>
 #include <cstring>
+#include <vector>
 
 #include "hydro_internal.cuh"
 #include "samplers.cuh"
@@ -54,10 +55,18 @@ __device__ __forceinline__ double3 qrot(const PoseDev& P, double3 v) {
 // Algorithm-1 iteration (surface.cpp:141-151, 4 iterations) and the four
 // partials are combined by a fixed xor tree, so the 48 taps of an iteration
 // are in flight together and 4x more threads hide the gather latency.
-__global__ void __launch_bounds__(128) k_vertices(int nv, const double* __restrict__ verts,
-                                                  PoseDev P, SurfView surf, int have_surf,
-                                                  ZoneList zones, const double* override_depth,
-                                                  double* wpos, double* depth) {
+template <int NB>
+__global__ void __launch_bounds__(128) k_vertices(const __grid_constant__ HydroBatch<NB> B) {
+  const HydroJob& J = B.job[blockIdx.y];
+  const int nv = J.nv;
+  const double* __restrict__ verts = J.verts;
+  const PoseDev& P = J.P;
+  const SurfView& surf = B.surf;
+  const int have_surf = B.have_surf;
+  const ZoneList& zones = J.zones;
+  const double* override_depth = J.override_depth;
+  double* wpos = J.wpos;
+  double* depth = J.depth;
   const int lane = threadIdx.x & 31, q = lane & 3;
   const int per_warp = 8;  // vertices per warp pass
   const int warp_g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -143,11 +152,17 @@ __device__ int2 block_exclusive_scan(int2 v, int2* warp_tot, int2* total) {
   return make_int2(base.x + incl.x - v.x, base.y + incl.y - v.y);
 }
 
-__global__ void __launch_bounds__(kScanBlock) k_classify_scan(int nt, const int3* __restrict__ tris,
-                                                             const double* __restrict__ areas,
-                                                             const double* __restrict__ depth,
-                                                             int2* counts, int2* offsets,
-                                                             int2* block_sums) {
+template <int NB>
+__global__ void __launch_bounds__(kScanBlock) k_classify_scan(const __grid_constant__ HydroBatch<NB> B) {
+  const HydroJob& J = B.job[blockIdx.y];
+  const int nt = J.nt;
+  if ((int)blockIdx.x * kScanBlock >= nt) return;  // this job's blocks end earlier (uniform)
+  const int3* __restrict__ tris = J.tris;
+  const double* __restrict__ areas = J.areas;
+  const double* __restrict__ depth = J.depth;
+  int2* counts = J.counts;
+  int2* offsets = J.offsets;
+  int2* block_sums = J.block_sums;
   __shared__ int2 warp_tot[32];
   __shared__ int2 tot;
   const int t = blockIdx.x * kScanBlock + threadIdx.x;
@@ -172,7 +187,12 @@ __global__ void __launch_bounds__(kScanBlock) k_classify_scan(int nt, const int3
 }
 
 // exclusive scan of the per-block totals in one block (any count), total out
-__global__ void __launch_bounds__(kScanBlock) k_scan_blocks(int nb, int2* block_sums, int2* total) {
+template <int NB>
+__global__ void __launch_bounds__(kScanBlock) k_scan_blocks(const __grid_constant__ HydroBatch<NB> B) {
+  const HydroJob& J = B.job[blockIdx.y];
+  const int nb = (J.nt + kScanBlock - 1) / kScanBlock;
+  int2* block_sums = J.block_sums;
+  int2* total = J.total;
   __shared__ int2 warp_tot[32];
   __shared__ int2 tot;
   int2 carry = make_int2(0, 0);
@@ -202,14 +222,20 @@ __device__ __forceinline__ void emit_state(StateDev* s, int parent, int status, 
   *s = r;
 }
 
-__global__ void __launch_bounds__(256) k_emit(int nt, const int3* __restrict__ tris,
-                                              const double* __restrict__ normals,
-                                              const double* __restrict__ wpos,
-                                              const double* __restrict__ depth, PoseDev P,
-                                              const int2* __restrict__ counts,
-                                              const int2* __restrict__ offsets,
-                                              const int2* __restrict__ block_sums, StateDev* states,
-                                              SegDev* segs) {
+template <int NB>
+__global__ void __launch_bounds__(256) k_emit(const __grid_constant__ HydroBatch<NB> B) {
+  const HydroJob& J = B.job[blockIdx.y];
+  const int nt = J.nt;
+  const int3* __restrict__ tris = J.tris;
+  const double* __restrict__ normals = J.normals;
+  const double* __restrict__ wpos = J.wpos;
+  const double* __restrict__ depth = J.depth;
+  const PoseDev& P = J.P;
+  const int2* __restrict__ counts = J.counts;
+  const int2* __restrict__ offsets = J.offsets;
+  const int2* __restrict__ block_sums = J.block_sums;
+  StateDev* states = J.states;
+  SegDev* segs = J.segs;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
     const int2 c = counts[t];
     if (c.x == 0) continue;
@@ -285,14 +311,22 @@ __device__ void finalize_report(int nblocks, const double* block_out, PoseDev P,
 // Per-state loads (hydro.cpp:215-306) reduced per block in a fixed tree; the
 // last block to finish (ticket counter) reduces the block partials in a fixed
 // order and writes the report, so no separate finalize launch is needed.
-__global__ void __launch_bounds__(kForceThreads) k_forces(const StateDev* __restrict__ states,
-                                                          const int2* total, PoseDev P,
-                                                          SliceView vel, int have_vel, int clamp,
-                                                          FluidDev F, double* block_out,
-                                                          int* domain_err, int* ticket,
-                                                          double mesh_volume, int degenerate,
-                                                          ReportDev* rep,
-                                                          const double* __restrict__ ext_vel) {
+template <int NB>
+__global__ void __launch_bounds__(kForceThreads) k_forces(const __grid_constant__ HydroBatch<NB> B) {
+  const HydroJob& J = B.job[blockIdx.y];
+  const StateDev* __restrict__ states = J.states;
+  const int2* total = J.total;
+  const PoseDev& P = J.P;
+  const SliceView& vel = B.vel;
+  const int have_vel = B.have_vel, clamp = J.clamp;
+  const FluidDev& F = J.F;
+  double* block_out = J.block_out;
+  int* domain_err = J.flags;
+  int* ticket = J.ticket;
+  const double mesh_volume = J.volume;
+  const int degenerate = J.degenerate;
+  ReportDev* rep = J.report;
+  const double* __restrict__ ext_vel = J.ext_vel;
   __shared__ double wsum[kForceThreads / 32][kTerms];
   const int ns = total->x;
   double acc[kTerms];
@@ -463,8 +497,15 @@ __device__ __forceinline__ unsigned hash64(unsigned long long k) {
 
 // Inserts every (segment, side) under its edge key; a key on a closed mesh
 // has exactly two entries (the two triangles sharing the crossed edge).
-__global__ void k_chain_hash(const SegDev* segs, const int2* total, int hcap,
-                             unsigned long long* hkeys, int* hvals, int* err) {
+template <int NB>
+__global__ void k_chain_hash(const __grid_constant__ HydroBatch<NB> B) {
+  const HydroJob& J = B.job[blockIdx.y];
+  const SegDev* segs = J.segs;
+  const int2* total = J.total;
+  const int hcap = J.hcap;
+  unsigned long long* hkeys = J.hkeys;
+  int* hvals = J.hvals;
+  int* err = J.flags + 1;
   const int nseg = total->y;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < 2 * nseg; e += gridDim.x * blockDim.x) {
     const int s = e >> 1, side = e & 1;
@@ -486,8 +527,15 @@ __global__ void k_chain_hash(const SegDev* segs, const int2* total, int hcap,
 }
 
 // partner[e] = the other (segment, side) with the same key, or -1
-__global__ void k_chain_partner(const SegDev* segs, const int2* total, int hcap,
-                                const unsigned long long* hkeys, const int* hvals, int* partner) {
+template <int NB>
+__global__ void k_chain_partner(const __grid_constant__ HydroBatch<NB> B) {
+  const HydroJob& J = B.job[blockIdx.y];
+  const SegDev* segs = J.segs;
+  const int2* total = J.total;
+  const int hcap = J.hcap;
+  const unsigned long long* hkeys = J.hkeys;
+  const int* hvals = J.hvals;
+  int* partner = J.partner;
   const int nseg = total->y;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < 2 * nseg; e += gridDim.x * blockDim.x) {
     const int s = e >> 1, side = e & 1;
@@ -566,9 +614,15 @@ __device__ void chain_walk_seq(int nseg, const int* partner, unsigned char* used
 // loop; loops are numbered by increasing s0 exactly as the reference emits
 // them. Open topology (a crossed edge with one segment) or huge waterlines
 // take the sequential walk.
-__global__ void __launch_bounds__(kChainThreads) k_chain(const int2* total, const int* partner_g,
-                                                         unsigned char* used_g, int* loop_off,
-                                                         int* point_ref, int* counts_out) {
+template <int NB>
+__global__ void __launch_bounds__(kChainThreads) k_chain(const __grid_constant__ HydroBatch<NB> B) {
+  const HydroJob& J = B.job[blockIdx.y];
+  const int2* total = J.total;
+  const int* partner_g = J.partner;
+  unsigned char* used_g = J.used;
+  int* loop_off = J.loop_off;
+  int* point_ref = J.point_ref;
+  int* counts_out = J.loop_counts;
   extern __shared__ int sm_chain[];
   __shared__ int s_open;
   __shared__ int s_wsum[kChainThreads / 32];
@@ -749,8 +803,13 @@ __global__ void __launch_bounds__(kChainThreads) k_chain(const int2* total, cons
   }
 }
 
-__global__ void k_chain_points(const SegDev* segs, const int* counts, const int* point_ref,
-                               double* points) {
+template <int NB>
+__global__ void k_chain_points(const __grid_constant__ HydroBatch<NB> B) {
+  const HydroJob& J = B.job[blockIdx.y];
+  const SegDev* segs = J.segs;
+  const int* counts = J.loop_counts;
+  const int* point_ref = J.point_ref;
+  double* points = J.loop_points;
   const int np = counts[1];
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < np; q += gridDim.x * blockDim.x) {
     const int e = point_ref[q];
@@ -760,9 +819,21 @@ __global__ void k_chain_points(const SegDev* segs, const int* counts, const int*
   }
 }
 
-__global__ void k_report_loops(ReportDev* rep, const int* counts) {
-  rep->r.waterline_loops = counts[0];
-  rep->r.waterline_points = counts[1];
+template <int NB>
+__global__ void k_report_loops(const __grid_constant__ HydroBatch<NB> B) {
+  const HydroJob& J = B.job[blockIdx.y];
+  J.report->r.waterline_loops = J.loop_counts[0];
+  J.report->r.waterline_points = J.loop_counts[1];
+}
+
+// the per-evaluation resets of every job: flags and the waterline hash table
+template <int NB>
+__global__ void k_hydro_clear(const __grid_constant__ HydroBatch<NB> B) {
+  const HydroJob& J = B.job[blockIdx.y];
+  const int i0 = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+  if (i0 < 4) J.flags[i0] = 0;
+  for (int i = i0; i < J.hcap; i += stride) J.hkeys[i] = 0ull;
+  for (int i = i0; i < 3 * J.hcap; i += stride) J.hvals[i] = 0;
 }
 
 int grid_of(ocn_ctx* ctx, int n, int threads) {
@@ -774,76 +845,133 @@ int grid_of(ocn_ctx* ctx, int n, int threads) {
 }  // namespace
 
 // ---------------------------------------------------------------- host pipeline
-void hydro_evaluate(ocn_mesh* m, const ocn_pose* pose, const ocn_fluid* fluid,
-                    const double* host_depth) {
-  ocn_ctx* ctx = m->ctx;
-  DeviceScope ds(ctx);
-  cudaStream_t st = ctx->stream;
-  PoseDev P;
+// The job of one mesh: pose, medium, zones and (optional) host-sampled depths;
+// uploads what the evaluation reads from host memory onto the mesh's buffers.
+HydroJob make_job(ocn_mesh* m, const ocn_pose* pose, const ocn_fluid* fluid,
+                  const double* host_depth) {
+  cudaStream_t st = m->ctx->stream;
+  HydroJob J{};
+  J.verts = m->verts.p, J.tris = m->tris.p, J.normals = m->normals.p, J.areas = m->areas.p;
+  J.nv = m->nv, J.nt = m->nt, J.degenerate = m->degenerate, J.hcap = m->hcap;
+  J.volume = m->volume;
   for (int k = 0; k < 3; ++k) {
-    P.p[k] = pose->position[k];
-    P.v[k] = pose->linear_velocity[k];
-    P.w[k] = pose->angular_velocity[k];
-    P.com[k] = pose->com_body[k];
+    J.P.p[k] = pose->position[k];
+    J.P.v[k] = pose->linear_velocity[k];
+    J.P.w[k] = pose->angular_velocity[k];
+    J.P.com[k] = pose->com_body[k];
   }
-  for (int k = 0; k < 4; ++k) P.q[k] = pose->orientation[k];
-  ocn_maps* maps = fluid ? (ocn_maps*)fluid->maps : nullptr;
-  ocn_slices* slices = fluid ? (ocn_slices*)fluid->slices : nullptr;
-  // maps == NULL: still water (FluidQuery::still_water, hydro.cpp:25-30) plus any zones
-  SurfView sv{};
-  if (maps) sv = make_surf_view(maps);
-  SliceView vv{};
-  if (slices) vv = make_slice_view(slices);
-  ZoneList zl{};
+  for (int k = 0; k < 4; ++k) J.P.q[k] = pose->orientation[k];
   if (fluid && fluid->n_zones) {
     OCN_REQUIRE(fluid->n_zones <= kMaxZones, "too many zones (%d)", fluid->n_zones);
-    zl.count = fluid->n_zones;
-    for (int z = 0; z < zl.count; ++z) zl.z[z] = zone_view((ocn_zone*)fluid->zones[z]);
+    J.zones.count = fluid->n_zones;
+    for (int z = 0; z < J.zones.count; ++z) J.zones.z[z] = zone_view((ocn_zone*)fluid->zones[z]);
   }
-  FluidDev F{};
   if (fluid) {
-    for (int k = 0; k < 3; ++k) F.wind[k] = fluid->wind[k];
-    F.water_density = fluid->water_density;
-    F.air_density = fluid->air_density;
-    F.cd_water = fluid->cd_water;
-    F.cd_air = fluid->cd_air;
-    F.n_profile = fluid->n_profile;
+    for (int k = 0; k < 3; ++k) J.F.wind[k] = fluid->wind[k];
+    J.F.water_density = fluid->water_density;
+    J.F.air_density = fluid->air_density;
+    J.F.cd_water = fluid->cd_water;
+    J.F.cd_air = fluid->cd_air;
+    J.F.n_profile = fluid->n_profile;
     if (fluid->n_profile > 0) {
       m->d_profile.ensure(2 * (size_t)fluid->n_profile);
       OCN_CUDA(cudaMemcpyAsync(m->d_profile.p, fluid->host_profile,
                                2 * (size_t)fluid->n_profile * sizeof(double),
                                cudaMemcpyHostToDevice, st));
-      F.profile = m->d_profile.p;
+      J.F.profile = m->d_profile.p;
     }
+    J.clamp = fluid->velocity_clamp;
   } else {
-    F.water_density = 1025.0;
-    F.air_density = 1.204;
-    F.cd_water = F.cd_air = 1.0;
+    J.F.water_density = 1025.0;
+    J.F.air_density = 1.204;
+    J.F.cd_water = J.F.cd_air = 1.0;
+    J.clamp = 1;
   }
-  const int nv = m->nv, nt = m->nt;
-  const double* d_override = nullptr;
   if (host_depth) {
-    OCN_CUDA(cudaMemcpyAsync(m->override_depth.p, host_depth, nv * sizeof(double),
+    OCN_CUDA(cudaMemcpyAsync(m->override_depth.p, host_depth, m->nv * sizeof(double),
                              cudaMemcpyHostToDevice, st));
-    d_override = m->override_depth.p;
+    J.override_depth = m->override_depth.p;
   }
+  J.wpos = m->wpos.p, J.depth = m->depth.p;
+  J.counts = m->counts.p, J.offsets = m->offsets.p, J.block_sums = m->block_sums.p;
+  J.total = m->total.p;
+  J.states = m->states.p, J.segs = m->segs.p;
+  J.block_out = m->block_out.p, J.report = m->report.p, J.flags = m->flags.p;
+  J.ticket = m->ticket.p;
+  J.hkeys = m->hkeys.p, J.hvals = m->hvals.p, J.partner = m->partner.p, J.used = m->used.p;
+  J.loop_off = m->loop_off.p, J.point_ref = m->point_ref.p, J.loop_counts = m->loop_counts.p;
+  J.loop_points = m->loop_points.p;
+  return J;
+}
+
+// Clip stage of every job: vertices, classification + scan, emission.
+template <int NB>
+void launch_clip(ocn_ctx* ctx, const HydroBatch<NB>& B, int max_nv, int max_nt) {
+  cudaStream_t st = ctx->stream;
+  const unsigned nb = (unsigned)B.n;
+  int max_hcap = 0;
+  for (int i = 0; i < B.n; ++i) max_hcap = std::max(max_hcap, B.job[i].hcap);
+  k_hydro_clear<NB><<<dim3(std::max(1, grid_of(ctx, 3 * max_hcap, 256) / (int)nb), nb), 256, 0, st>>>(B);
+  OCN_LAUNCHED(ctx);
+  k_vertices<NB><<<dim3(std::max(1, grid_of(ctx, 4 * max_nv, 128) / (int)nb), nb), 128, 0, st>>>(B);
+  OCN_LAUNCHED(ctx);
+  const int sb = (max_nt + kScanBlock - 1) / kScanBlock;
+  k_classify_scan<NB><<<dim3(sb, nb), kScanBlock, 0, st>>>(B);
+  OCN_LAUNCHED(ctx);
+  k_scan_blocks<NB><<<dim3(1, nb), kScanBlock, 0, st>>>(B);
+  OCN_LAUNCHED(ctx);
+  k_emit<NB><<<dim3(std::max(1, grid_of(ctx, max_nt, 256) / (int)nb), nb), 256, 0, st>>>(B);
+  OCN_LAUNCHED(ctx);
+}
+
+// Reduction and waterline stages of every job.
+template <int NB>
+void launch_reduce(ocn_ctx* ctx, const HydroBatch<NB>& B, int max_nt) {
+  cudaStream_t st = ctx->stream;
+  const unsigned nb = (unsigned)B.n;
+  // the per-job partial count is fixed (block_out holds 2 sm_count partials)
+  const int fblocks = std::max(8, ctx->sm_count * 2 / B.n);
+  k_forces<NB><<<dim3(fblocks, nb), kForceThreads, 0, st>>>(B);
+  OCN_LAUNCHED(ctx);
+  const int cb = std::max(1, grid_of(ctx, 2 * max_nt, 256) / (int)nb);
+  k_chain_hash<NB><<<dim3(cb, nb), 256, 0, st>>>(B);
+  OCN_LAUNCHED(ctx);
+  k_chain_partner<NB><<<dim3(cb, nb), 256, 0, st>>>(B);
+  OCN_LAUNCHED(ctx);
+  const size_t chain_smem = std::max(9 * kChainPar * sizeof(int),
+                                     2 * kChainSeq * sizeof(int) + kChainSeq);
+  smem_opt_in(k_chain<NB>, chain_smem);
+  k_chain<NB><<<dim3(1, nb), kChainThreads, chain_smem, st>>>(B);
+  OCN_LAUNCHED(ctx);
+  k_chain_points<NB><<<dim3(std::max(1, grid_of(ctx, max_nt, 256) / (int)nb), nb), 256, 0, st>>>(B);
+  OCN_LAUNCHED(ctx);
+  k_report_loops<NB><<<dim3(1, nb), 1, 0, st>>>(B);
+  OCN_LAUNCHED(ctx);
+}
+
+template <int NB>
+void fill_samplers(HydroBatch<NB>& B, const ocn_fluid* fluid) {
+  ocn_maps* maps = fluid ? (ocn_maps*)fluid->maps : nullptr;
+  ocn_slices* slices = fluid ? (ocn_slices*)fluid->slices : nullptr;
+  // maps == NULL: still water (FluidQuery::still_water, hydro.cpp:25-30) plus any zones
+  B.have_surf = maps != nullptr;
+  if (maps) B.surf = make_surf_view(maps);
+  B.have_vel = slices != nullptr;
+  if (slices) B.vel = make_slice_view(slices);
+}
+
+void hydro_evaluate(ocn_mesh* m, const ocn_pose* pose, const ocn_fluid* fluid,
+                    const double* host_depth) {
+  ocn_ctx* ctx = m->ctx;
+  DeviceScope ds(ctx);
+  cudaStream_t st = ctx->stream;
+  HydroBatch<1> B{};
+  B.n = 1;
+  fill_samplers(B, fluid);
+  B.job[0] = make_job(m, pose, fluid, host_depth);
   ProfWindow pw(ctx, OCN_PROF_HYDRO);
-  OCN_CUDA(cudaMemsetAsync(m->flags.p, 0, 4 * sizeof(int), st));
-  k_vertices<<<grid_of(ctx, 4 * (size_t)nv, 128), 128, 0, st>>>(nv, m->verts.p, P, sv, maps != nullptr, zl,
-                                                   d_override, m->wpos.p, m->depth.p);
-  OCN_LAUNCHED(ctx);
-  const int nb = (nt + kScanBlock - 1) / kScanBlock;
-  k_classify_scan<<<nb, kScanBlock, 0, st>>>(nt, m->tris.p, m->areas.p, m->depth.p, m->counts.p,
-                                             m->offsets.p, m->block_sums.p);
-  OCN_LAUNCHED(ctx);
-  k_scan_blocks<<<1, kScanBlock, 0, st>>>(nb, m->block_sums.p, m->total.p);
-  OCN_LAUNCHED(ctx);
-  k_emit<<<grid_of(ctx, nt, 256), 256, 0, st>>>(nt, m->tris.p, m->normals.p, m->wpos.p, m->depth.p,
-                                               P, m->counts.p, m->offsets.p, m->block_sums.p,
-                                               m->states.p, m->segs.p);
-  OCN_LAUNCHED(ctx);
-  const double* ext_vel = nullptr;
-  if (fluid && fluid->host_velocity && !slices) {
+  launch_clip(ctx, B, m->nv, m->nt);
+  if (fluid && fluid->host_velocity && !fluid->slices) {
     // host water_velocity sampler (hydro.cpp:276-282): the submerged states'
     // centroids go to the host once, the callback fills their medium
     // velocities, which the force pass reads instead of velocity_at
@@ -870,35 +998,50 @@ void hydro_evaluate(ocn_mesh* m, const ocn_pose* pose, const ocn_fluid* fluid,
     m->ext_vel.ensure(m->ext_vel_host.size());
     OCN_CUDA(cudaMemcpyAsync(m->ext_vel.p, m->ext_vel_host.data(),
                              m->ext_vel_host.size() * sizeof(double), cudaMemcpyHostToDevice, st));
-    ext_vel = m->ext_vel.p;
+    B.job[0].ext_vel = m->ext_vel.p;
   }
-  const int fblocks = ctx->sm_count * 2;
-  k_forces<<<fblocks, kForceThreads, 0, st>>>(m->states.p, m->total.p, P, vv, slices != nullptr,
-                                             fluid ? fluid->velocity_clamp : 1, F,
-                                             m->block_out.p, m->flags.p, m->ticket.p, m->volume,
-                                             m->degenerate, m->report.p, ext_vel);
-  OCN_LAUNCHED(ctx);
-  // waterline
-  OCN_CUDA(cudaMemsetAsync(m->hkeys.p, 0, m->hkeys.bytes(), st));
-  OCN_CUDA(cudaMemsetAsync(m->hvals.p, 0, m->hvals.bytes(), st));
-  k_chain_hash<<<grid_of(ctx, 2 * nt, 256), 256, 0, st>>>(m->segs.p, m->total.p, m->hcap,
-                                                          m->hkeys.p, m->hvals.p, m->flags.p + 1);
-  OCN_LAUNCHED(ctx);
-  k_chain_partner<<<grid_of(ctx, 2 * nt, 256), 256, 0, st>>>(m->segs.p, m->total.p, m->hcap,
-                                                             m->hkeys.p, m->hvals.p, m->partner.p);
-  OCN_LAUNCHED(ctx);
-  const size_t chain_smem = std::max(9 * kChainPar * sizeof(int),
-                                     2 * kChainSeq * sizeof(int) + kChainSeq);
-  smem_opt_in(k_chain, chain_smem);
-  k_chain<<<1, kChainThreads, chain_smem, st>>>(m->total.p, m->partner.p, m->used.p, m->loop_off.p,
-                                                m->point_ref.p, m->loop_counts.p);
-  OCN_LAUNCHED(ctx);
-  k_chain_points<<<grid_of(ctx, nt, 256), 256, 0, st>>>(m->segs.p, m->loop_counts.p,
-                                                        m->point_ref.p, m->loop_points.p);
-  OCN_LAUNCHED(ctx);
-  k_report_loops<<<1, 1, 0, st>>>(m->report.p, m->loop_counts.p);
-  OCN_LAUNCHED(ctx);
+  launch_reduce(ctx, B, m->nt);
   m->evaluated = true;
+}
+
+void fill_samplers_batch(HydroBatch<kMaxBatch>& B, const ocn_fluid* fluid) {
+  fill_samplers(B, fluid);
+}
+
+// Runs prepared jobs (make_job per mesh) as one launch set.
+void hydro_evaluate_jobs(int n, ocn_mesh* const* meshes, const HydroBatch<kMaxBatch>& B) {
+  ocn_ctx* ctx = meshes[0]->ctx;
+  DeviceScope ds(ctx);
+  int max_nv = 0, max_nt = 0;
+  for (int i = 0; i < n; ++i) {
+    max_nv = std::max(max_nv, meshes[i]->nv);
+    max_nt = std::max(max_nt, meshes[i]->nt);
+  }
+  ProfWindow pw(ctx, OCN_PROF_HYDRO);
+  launch_clip(ctx, B, max_nv, max_nt);
+  launch_reduce(ctx, B, max_nt);
+  for (int i = 0; i < n; ++i) meshes[i]->evaluated = true;
+}
+
+// Simulation::step's body loop (sim.cpp:74-83) as one launch set: job i is
+// meshes[i] at poses[i] against fluids[i] (its own zones / drag constants, zone
+// views taken now); every fluid shares the maps and slices.
+void hydro_evaluate_batch(int n, ocn_mesh* const* meshes, const ocn_pose* poses,
+                          const ocn_fluid* fluids) {
+  ocn_ctx* ctx = meshes[0]->ctx;
+  DeviceScope ds(ctx);
+  HydroBatch<kMaxBatch> B{};
+  B.n = n;
+  fill_samplers(B, &fluids[0]);
+  for (int i = 0; i < n; ++i) {
+    OCN_REQUIRE(meshes[i] && meshes[i]->ctx == ctx, "batched meshes must share one context");
+    OCN_REQUIRE(fluids[i].maps == fluids[0].maps && fluids[i].slices == fluids[0].slices,
+                "batched evaluations must share the surface and velocity samplers");
+    OCN_REQUIRE(!fluids[i].host_velocity || fluids[i].slices,
+                "host velocity samplers are not batched (use ocn_hydro_aggregate)");
+    B.job[i] = make_job(meshes[i], &poses[i], &fluids[i], nullptr);
+  }
+  hydro_evaluate_jobs(n, meshes, B);
 }
 
 void hydro_check_flags(ocn_mesh* m) {
@@ -994,6 +1137,29 @@ int ocn_hydro_aggregate(ocn_mesh* m, const ocn_pose* pose, const ocn_fluid* flui
       OCN_CUDA(cudaStreamSynchronize(m->ctx->stream));
       hydro_check_flags(m);
       *report = r.r;
+    }
+  });
+}
+
+int ocn_hydro_aggregate_batch(int n, ocn_mesh* const* meshes, const ocn_pose* poses,
+                              const ocn_fluid* fluids, ocn_hydro_report* reports) {
+  ocn_ctx* ctx = n > 0 && meshes && meshes[0] ? meshes[0]->ctx : nullptr;
+  return api_call(ctx, [&] {
+    OCN_REQUIRE(n >= 0 && n <= kMaxBatch, "batch of %d meshes (1..%d)", n, kMaxBatch);
+    if (n == 0) return;
+    OCN_REQUIRE(meshes && poses && fluids, "null argument");
+    hydro_evaluate_batch(n, meshes, poses, fluids);
+    if (reports) {
+      DeviceScope ds(ctx);
+      std::vector<ReportDev> r(n);
+      for (int i = 0; i < n; ++i)
+        OCN_CUDA(cudaMemcpyAsync(&r[i], meshes[i]->report.p, sizeof(ReportDev),
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+      OCN_CUDA(cudaStreamSynchronize(ctx->stream));
+      for (int i = 0; i < n; ++i) {
+        hydro_check_flags(meshes[i]);
+        reports[i] = r[i].r;
+      }
     }
   });
 }

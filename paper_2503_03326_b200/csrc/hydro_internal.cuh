@@ -37,6 +37,48 @@ struct ReportDev {
   ocn_hydro_report r;
 };
 
+// One hull evaluation of a (possibly batched) aggregate launch set: the mesh,
+// this evaluation's pose / medium / zones / samplers, and the mesh's buffers.
+struct HydroJob {
+  const double* verts;
+  const int3* tris;
+  const double* normals;
+  const double* areas;
+  int nv, nt, degenerate, hcap;
+  double volume;
+  PoseDev P;
+  FluidDev F;
+  int clamp;                      // velocity_at clamps y into [y_min, y_max]
+  const double* override_depth;   // host-sampled vertex depths, or nullptr
+  const double* ext_vel;          // host-sampled medium velocity per state, or nullptr
+  ZoneList zones;                 // FdmZone::sample terms (sim.cpp:44-51)
+  double *wpos, *depth;
+  int2 *counts, *offsets, *block_sums, *total;
+  StateDev* states;
+  SegDev* segs;
+  double* block_out;
+  ReportDev* report;
+  int* flags;
+  int* ticket;
+  unsigned long long* hkeys;
+  int *hvals, *partner;
+  unsigned char* used;
+  int *loop_off, *point_ref, *loop_counts;
+  double* loop_points;
+};
+
+// NB jobs sharing the surface / velocity samplers, passed by value (one
+// kernel-parameter block per launch: no upload); blockIdx.y = job.
+constexpr int kMaxBatch = 16;
+template <int NB>
+struct HydroBatch {
+  int n;
+  int have_surf, have_vel;
+  SurfView surf;
+  SliceView vel;
+  HydroJob job[NB];
+};
+
 }  // namespace ocn
 
 struct ocn_mesh {
