@@ -498,6 +498,63 @@ typedef struct ocn_body_frame {
  * enqueued (async); read them with ocn_hydro_report_get. */
 OCN_API int ocn_bodies_step(int n_bodies, const ocn_body_frame* bodies, const ocn_fluid* fluid,
                             double dt, ocn_hydro_report* reports);
+/* ================= Simulation on device-resident state ====================
+ * Simulation (sim.hpp:16-60, sim.cpp:15-131) in C++ behind the C-ABI: the spectral
+ * surface and slices, every body's hull in one batched launch set with sim.cpp's
+ * zone order (ocn_bodies_step), deferred masks, zone steps, and the rigid-body
+ * integration (rigid_body.cpp:6-61) on the host. pipelined != 0 (with
+ * rebuild_stride 1) prefetches step f+1's spectral step into a second map /
+ * slice buffer on a low-priority context while step f's bodies run. */
+typedef struct ocn_sim_config {
+  int32_t resolution;
+  int32_t count;         /* cascades (<= 16) */
+  double lengths[16];    /* CascadeConfig (surface.hpp:18-25) */
+  double cutoffs[16];    /* count - 1 band edges */
+  ocn_spectrum_params spectrum;
+  ocn_slice_config slices;
+  double choppiness;
+  double dt;
+  double wind[3];
+  int32_t rebuild_stride; /* VelocityScenarioConfig::rebuild_stride */
+  int32_t pipelined;
+} ocn_sim_config;
+/* BodyConfig (scenario.hpp:30-47) with the hull's TriMesh properties (the mesh is
+ * built and validated by the caller: ocn_mesh_create on the sim's context). */
+typedef struct ocn_sim_body {
+  ocn_mesh* mesh;
+  double volume;
+  double centroid[3];
+  double bbox_min[3];
+  double bbox_max[3];
+  double unit_inertia[9]; /* TriMesh::unit_inertia, row-major */
+  double density;         /* kg / m^3, or mass when has_mass */
+  double mass;
+  int32_t has_mass;
+  int32_t box_inertia;
+  double position[3];
+  double yaw;
+  double initial_velocity[3];
+  double cd_water, cd_air, angular_damping;
+  int32_t n_thrust;
+  int32_t reserved0;
+  const double* thrust;   /* n_thrust x (until, fx, fy, fz), body frame (sim.cpp:53-57) */
+  ocn_fdm_config fdm;
+  ocn_mask_params mask;
+} ocn_sim_body;
+typedef struct ocn_sim ocn_sim;
+OCN_API int ocn_sim_create(ocn_ctx* ctx, const ocn_sim_config* cfg, int n_bodies,
+                           const ocn_sim_body* bodies, ocn_sim** out);
+OCN_API int ocn_sim_destroy(ocn_sim* sim);
+/* Simulation::step, `steps` times (synchronous: each step reads the reports). */
+OCN_API int ocn_sim_step(ocn_sim* sim, int steps);
+/* Body state: position, orientation (w x y z), linear and angular velocity (13
+ * doubles) and its last hydro report; either pointer may be NULL. */
+OCN_API int ocn_sim_body_state(const ocn_sim* sim, int body, double* host_state13,
+                               ocn_hydro_report* report);
+/* time, step index, the current maps / slices and the bodies' zones (any may be NULL). */
+OCN_API int ocn_sim_info(const ocn_sim* sim, double* time, int* step_index, ocn_maps** maps,
+                         ocn_slices** slices, ocn_zone** zones);
+
 /* Cells of the last mask in row-major order (MaskCell, interactive.hpp:56-59). */
 OCN_API int ocn_zone_mask_download(ocn_zone* z, int capacity, int32_t* host_ij, double* host_h,
                            int* n_cells);

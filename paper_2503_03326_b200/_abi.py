@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 from ._types import (Fluid, FdmConfig, HydroReport, MaskFrame, MaskParams, Pose, SliceConfig,
-                     SpectrumParams, TriangleState, ZoneState, BodyFrame, XformInfo)
+                     SpectrumParams, TriangleState, ZoneState, BodyFrame, XformInfo, SimConfig,
+                     SimBody)
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 # OCN_LIB: an alternative build of the same library (kernel-variant experiments)
@@ -177,6 +178,11 @@ SIGNATURES = {
     "ocn_zone_mask_from_hydro_deferred": (ci, [vp, vp, cd, cd, cd, cd, C.POINTER(MaskFrame), C.POINTER(MaskParams)]),
     "ocn_zone_apply_last_mask": (ci, [vp]),
     "ocn_bodies_step": (ci, [ci, C.POINTER(BodyFrame), C.POINTER(Fluid), cd, C.POINTER(HydroReport)]),
+    "ocn_sim_create": (ci, [vp, C.POINTER(SimConfig), ci, C.POINTER(SimBody), pvp]),
+    "ocn_sim_destroy": (ci, [vp]),
+    "ocn_sim_step": (ci, [vp, ci]),
+    "ocn_sim_body_state": (ci, [vp, ci, d, C.POINTER(HydroReport)]),
+    "ocn_sim_info": (ci, [vp, d, C.POINTER(ci), pvp, pvp, pvp]),
     "ocn_direct_create": (ci, [vp, cd, pvp]),
     "ocn_direct_destroy": (ci, [vp]),
     "ocn_direct_modes": (ci, [vp, C.POINTER(C.c_int64)]),

@@ -253,3 +253,49 @@ class XformInfo(C.Structure):
         ("y0", C.c_double),
         ("y1", C.c_double),
     ]
+
+
+class SimConfig(C.Structure):
+    """ocn_sim_config — the scenario part of Simulation (sim.hpp:16-60)."""
+
+    _fields_ = [
+        ("resolution", C.c_int32),
+        ("count", C.c_int32),
+        ("lengths", C.c_double * 16),
+        ("cutoffs", C.c_double * 16),
+        ("spectrum", SpectrumParams),
+        ("slices", SliceConfig),
+        ("choppiness", C.c_double),
+        ("dt", C.c_double),
+        ("wind", C.c_double * 3),
+        ("rebuild_stride", C.c_int32),
+        ("pipelined", C.c_int32),
+    ]
+
+
+class SimBody(C.Structure):
+    """ocn_sim_body — BodyConfig (scenario.hpp:30-47) + the hull's TriMesh properties."""
+
+    _fields_ = [
+        ("mesh", C.c_void_p),
+        ("volume", C.c_double),
+        ("centroid", C.c_double * 3),
+        ("bbox_min", C.c_double * 3),
+        ("bbox_max", C.c_double * 3),
+        ("unit_inertia", C.c_double * 9),
+        ("density", C.c_double),
+        ("mass", C.c_double),
+        ("has_mass", C.c_int32),
+        ("box_inertia", C.c_int32),
+        ("position", C.c_double * 3),
+        ("yaw", C.c_double),
+        ("initial_velocity", C.c_double * 3),
+        ("cd_water", C.c_double),
+        ("cd_air", C.c_double),
+        ("angular_damping", C.c_double),
+        ("n_thrust", C.c_int32),
+        ("reserved0", C.c_int32),
+        ("thrust", C.POINTER(C.c_double)),
+        ("fdm", FdmConfig),
+        ("mask", MaskParams),
+    ]

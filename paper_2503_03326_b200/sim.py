@@ -395,3 +395,85 @@ class Simulation:
         """(bodies, 13): position, orientation (w x y z), linear, angular velocity."""
         return np.array([np.concatenate([b.rigid.position, b.rigid.orientation, b.rigid.linear_velocity,
                                          b.rigid.angular_velocity]) for b in self.bodies])
+
+
+class DeviceSimulation:
+    """Simulation::step (sim.cpp:15-131) run entirely by the C++ library over
+    device-resident state (ocn_sim): spectral step, every body's hull in one
+    batched launch set, deferred masks, zone steps and the rigid-body
+    integration in C++ -- one C-ABI call per step. Same scene description as
+    Simulation; poses() / submerged volumes / reports read back per step."""
+
+    def __init__(self, cascade_config: "oc.CascadeConfig", spectrum: SpectrumParams,
+                 slices: SliceConfig, bodies: Sequence[BodyConfig], dt: float = 1.0 / 60.0,
+                 wind=(0.0, 0.0, 0.0), choppiness: float = 1.0, rebuild_stride: int = 1,
+                 pipelined: bool = True, device: int = 0):
+        from ._types import SimBody, SimConfig
+        cascade_config.validate()
+        self.ctx = oc.Context(device, priority=1 if pipelined else 0)
+        cfg = SimConfig()
+        cfg.resolution = cascade_config.resolution
+        cfg.count = len(cascade_config.lengths)
+        for c, L in enumerate(cascade_config.lengths):
+            cfg.lengths[c] = L
+        for c, x in enumerate(cascade_config.cutoffs):
+            cfg.cutoffs[c] = x
+        cfg.spectrum = spectrum
+        cfg.slices = slices
+        cfg.choppiness, cfg.dt = choppiness, dt
+        cfg.wind[:] = tuple(float(w) for w in wind)
+        cfg.rebuild_stride, cfg.pipelined = int(rebuild_stride), int(pipelined)
+        self.meshes = [oc.TriMesh(b.vertices, b.triangles, ctx=self.ctx) for b in bodies]
+        arr = (SimBody * max(len(bodies), 1))()
+        self._thrust = []
+        for i, (b, m) in enumerate(zip(bodies, self.meshes)):
+            sb = arr[i]
+            sb.mesh = m.h
+            sb.volume = m.volume
+            sb.centroid[:] = tuple(m.centroid)
+            sb.bbox_min[:] = tuple(m.bbox_min)
+            sb.bbox_max[:] = tuple(m.bbox_max)
+            sb.unit_inertia[:] = tuple(np.asarray(m.unit_inertia, np.float64).ravel())
+            sb.density = b.density
+            sb.box_inertia = int(b.box_inertia)
+            sb.position[:] = tuple(b.position)
+            sb.yaw = b.yaw
+            sb.initial_velocity[:] = tuple(b.initial_velocity)
+            sb.cd_water, sb.cd_air, sb.angular_damping = b.cd_water, b.cd_air, b.angular_damping
+            th = np.ascontiguousarray([[u, *f] for u, f in b.thrust], np.float64).reshape(-1)
+            self._thrust.append(th)
+            sb.n_thrust = len(b.thrust)
+            sb.thrust = th.ctypes.data_as(C.POINTER(C.c_double)) if len(b.thrust) else None
+            sb.fdm, sb.mask = b.fdm, b.mask
+        h = C.c_void_p()
+        check(lib().ocn_sim_create(self.ctx.h, C.byref(cfg), len(bodies), arr, C.byref(h)),
+              self.ctx.h, "sim_create")
+        self.h = h
+        self.n_bodies = len(bodies)
+
+    def step(self, steps: int = 1):
+        check(lib().ocn_sim_step(self.h, steps), self.ctx.h, "sim_step")
+
+    def poses(self) -> np.ndarray:
+        """(bodies, 13): position, orientation (w x y z), linear, angular velocity."""
+        out = np.zeros((self.n_bodies, 13))
+        for i in range(self.n_bodies):
+            check(lib().ocn_sim_body_state(self.h, i, out[i].ctypes.data_as(C.POINTER(C.c_double)),
+                                           None), self.ctx.h, "body_state")
+        return out
+
+    def reports(self) -> List[HydroReport]:
+        reps = []
+        for i in range(self.n_bodies):
+            r = HydroReport()
+            check(lib().ocn_sim_body_state(self.h, i, None, C.byref(r)), self.ctx.h, "body_state")
+            reps.append(r)
+        return reps
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().ocn_sim_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass

@@ -105,7 +105,8 @@ def test_struct_layouts_match_header():
              "ocn_triangle_state": T.TriangleState, "ocn_fdm_config": T.FdmConfig,
              "ocn_mask_params": T.MaskParams, "ocn_mask_frame": T.MaskFrame,
              "ocn_zone_state": T.ZoneState, "ocn_body_frame": T.BodyFrame,
-             "ocn_xform_info": T.XformInfo}
+             "ocn_xform_info": T.XformInfo, "ocn_sim_config": T.SimConfig,
+             "ocn_sim_body": T.SimBody}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "ocean_b200.h"', 'int main(void){']
     for cname, py in pairs.items():
         lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')

@@ -12,10 +12,11 @@ sys.path.insert(0, ".")
 from paper_2503_03326_b200 import ocean as oc  # noqa: E402
 from paper_2503_03326_b200._types import FdmConfig, SliceConfig, SpectrumParams  # noqa: E402
 from paper_2503_03326_b200.meshgen import uv_ellipsoid  # noqa: E402
-from paper_2503_03326_b200.sim import BodyConfig, Simulation  # noqa: E402
+from paper_2503_03326_b200.sim import BodyConfig, DeviceSimulation, Simulation  # noqa: E402
 
 
-def main(n_bodies=10, steps=60, n=1024, pipelined=False, native=False, concurrent=False):
+def main(n_bodies=10, steps=60, n=1024, pipelined=False, native=False, concurrent=False,
+         device=False):
     p = SpectrumParams.make(wind_speed=20.0, fetch=1e5, wind_direction=0.4, swell=0.5,
                             direction_mix=0.5, rng_seed=42)
     p.has_peak_omega_override = 1
@@ -24,10 +25,13 @@ def main(n_bodies=10, steps=60, n=1024, pipelined=False, native=False, concurren
     bodies = [BodyConfig(vertices=v, triangles=t, position=(15.0 * (b % 5), -0.3, 20.0 * (b // 5)),
                          yaw=0.1 * b, initial_velocity=(0.0, 0.0, 2.0), density=500.0,
                          fdm=FdmConfig.make(grid_size=256, margin=16)) for b in range(n_bodies)]
-    sim = Simulation(oc.CascadeConfig(n, [1024.0, 256.0, 16.0, 4.0],
-                                      [12 * math.pi / 256, 12 * math.pi / 16, 12 * math.pi / 4]), p,
-                     SliceConfig.make(count=32), bodies, pipelined=pipelined, native=native,
-                     concurrent=concurrent)
+    cc = oc.CascadeConfig(n, [1024.0, 256.0, 16.0, 4.0],
+                          [12 * math.pi / 256, 12 * math.pi / 16, 12 * math.pi / 4])
+    if device:
+        sim = DeviceSimulation(cc, p, SliceConfig.make(count=32), bodies, pipelined=pipelined)
+    else:
+        sim = Simulation(cc, p, SliceConfig.make(count=32), bodies, pipelined=pipelined,
+                         native=native, concurrent=concurrent)
     for _ in range(5):
         sim.step()
     t0 = time.perf_counter()
@@ -36,7 +40,7 @@ def main(n_bodies=10, steps=60, n=1024, pipelined=False, native=False, concurren
     ms = (time.perf_counter() - t0) * 1e3 / steps
     print(f"simulation: {n_bodies} bodies x {len(t)} triangles, {n}^2 x 4 cascades + 32 slices: "
           f"{ms:.3f} ms/step (host wall, {steps} steps, {'concurrent bodies' if concurrent else 'pipelined' if pipelined else 'serial'}, "
-          f"{'ocn_bodies_step' if native and not concurrent else 'per-body calls'})")
+          f"{'ocn_sim (C++ step)' if device else 'ocn_bodies_step' if native and not concurrent else 'per-body calls'})")
 
 
 if __name__ == "__main__":
@@ -45,3 +49,7 @@ if __name__ == "__main__":
     main(pipelined=True)
     main(pipelined=True, native=True)
     main(concurrent=True)
+    main(device=True)
+    main(device=True, pipelined=True)
+    for nb in (1, 2, 5):
+        main(n_bodies=nb, device=True, pipelined=True)
