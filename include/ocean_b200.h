@@ -439,6 +439,8 @@ OCN_API int ocn_hydro_aggregate(ocn_mesh* mesh, const ocn_pose* pose, const ocn_
 OCN_API int ocn_hydro_aggregate_batch(int n, ocn_mesh* const* meshes, const ocn_pose* poses,
                                       const ocn_fluid* fluids, ocn_hydro_report* reports);
 OCN_API int ocn_hydro_report_get(ocn_mesh* mesh, ocn_hydro_report* report);
+/* The reports of n evaluated meshes of one context with one synchronisation. */
+OCN_API int ocn_hydro_reports_get(int n, ocn_mesh* const* meshes, ocn_hydro_report* reports);
 /* Per-vertex world positions (3 doubles) and signed depths of the last evaluation. */
 OCN_API int ocn_hydro_vertices(ocn_mesh* mesh, double* host_world, double* host_depth);
 /* TriangleStates of the last evaluation in parent order (ClipResult::states). */

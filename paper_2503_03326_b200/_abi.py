@@ -142,6 +142,7 @@ SIGNATURES = {
     "ocn_hydro_aggregate_batch": (ci, [ci, pvp, C.POINTER(Pose), C.POINTER(Fluid),
                                        C.POINTER(HydroReport)]),
     "ocn_hydro_report_get": (ci, [vp, C.POINTER(HydroReport)]),
+    "ocn_hydro_reports_get": (ci, [ci, pvp, C.POINTER(HydroReport)]),
     "ocn_hydro_vertices": (ci, [vp, d, d]),
     "ocn_hydro_states": (ci, [vp, ci, C.POINTER(TriangleState), C.POINTER(ci)]),
     "ocn_hydro_waterline": (ci, [vp, C.POINTER(ci), C.POINTER(ci), i32, d]),

@@ -18,6 +18,7 @@ namespace ocn {
 HydroJob make_job(ocn_mesh* m, const ocn_pose* pose, const ocn_fluid* fluid, const double* host_depth);
 void fill_samplers_batch(HydroBatch<kMaxBatch>& B, const ocn_fluid* fluid);
 void hydro_evaluate_jobs(int n, ocn_mesh* const* meshes, const HydroBatch<kMaxBatch>& B);
+void hydro_reports_read(int n, ocn_mesh* const* meshes, ocn_hydro_report* out);
 }  // namespace ocn
 
 using namespace ocn;
@@ -70,7 +71,7 @@ int ocn_bodies_step(int n_bodies, const ocn_body_frame* bodies, const ocn_fluid*
                           bodies[i].pose.position[2]));
     }
     if (!reports) return;  // asynchronous: reports via ocn_hydro_report_get
-    for (int i = 0; i < n_bodies; ++i) check(ocn_hydro_report_get(meshes[i], &reports[i]));
+    hydro_reports_read(n_bodies, meshes.data(), reports);
   });
 }
 

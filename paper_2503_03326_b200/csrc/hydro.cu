@@ -1051,6 +1051,34 @@ void hydro_check_flags(ocn_mesh* m) {
   if (flags[1]) fail(OCN_ERR_MESH, "waterline: an edge is shared by more than two triangles");
 }
 
+// The reports (and error flags) of n evaluated meshes on one context: async
+// copies into each mesh's pinned staging, one stream synchronisation.
+void hydro_reports_read(int n, ocn_mesh* const* meshes, ocn_hydro_report* out) {
+  if (n <= 0) return;
+  ocn_ctx* ctx = meshes[0]->ctx;
+  DeviceScope ds(ctx);
+  for (int i = 0; i < n; ++i) {
+    ocn_mesh* m = meshes[i];
+    OCN_REQUIRE(m && m->ctx == ctx, "meshes of one context");
+    OCN_REQUIRE(m->evaluated, "no hydro evaluation yet");
+    if (!m->h_report) {
+      OCN_CUDA(cudaMallocHost(&m->h_report, sizeof(ReportDev)));
+      OCN_CUDA(cudaMallocHost(&m->h_flags, 4 * sizeof(int)));
+    }
+    OCN_CUDA(cudaMemcpyAsync(m->h_report, m->report.p, sizeof(ReportDev), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    OCN_CUDA(cudaMemcpyAsync(m->h_flags, m->flags.p, 4 * sizeof(int), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+  }
+  OCN_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (int i = 0; i < n; ++i) {
+    const ocn_mesh* m = meshes[i];
+    if (m->h_flags[0]) fail(OCN_ERR_DOMAIN, "velocity_at: depth outside [y_min, y_max]");
+    if (m->h_flags[1]) fail(OCN_ERR_MESH, "waterline: an edge is shared by more than two triangles");
+    out[i] = m->h_report->r;
+  }
+}
+
 }  // namespace ocn
 
 using namespace ocn;
@@ -1149,31 +1177,21 @@ int ocn_hydro_aggregate_batch(int n, ocn_mesh* const* meshes, const ocn_pose* po
     if (n == 0) return;
     OCN_REQUIRE(meshes && poses && fluids, "null argument");
     hydro_evaluate_batch(n, meshes, poses, fluids);
-    if (reports) {
-      DeviceScope ds(ctx);
-      std::vector<ReportDev> r(n);
-      for (int i = 0; i < n; ++i)
-        OCN_CUDA(cudaMemcpyAsync(&r[i], meshes[i]->report.p, sizeof(ReportDev),
-                                 cudaMemcpyDeviceToHost, ctx->stream));
-      OCN_CUDA(cudaStreamSynchronize(ctx->stream));
-      for (int i = 0; i < n; ++i) {
-        hydro_check_flags(meshes[i]);
-        reports[i] = r[i].r;
-      }
-    }
+    if (reports) hydro_reports_read(n, meshes, reports);
   });
 }
 
 int ocn_hydro_report_get(ocn_mesh* m, ocn_hydro_report* report) {
   return api_call(m ? m->ctx : nullptr, [&] {
     OCN_REQUIRE(m && report, "null argument");
-    OCN_REQUIRE(m->evaluated, "no hydro evaluation yet");
-    DeviceScope ds(m->ctx);
-    ReportDev r;
-    OCN_CUDA(cudaMemcpyAsync(&r, m->report.p, sizeof(r), cudaMemcpyDeviceToHost, m->ctx->stream));
-    OCN_CUDA(cudaStreamSynchronize(m->ctx->stream));
-    hydro_check_flags(m);
-    *report = r.r;
+    hydro_reports_read(1, &m, report);
+  });
+}
+
+int ocn_hydro_reports_get(int n, ocn_mesh* const* meshes, ocn_hydro_report* reports) {
+  return api_call(n > 0 && meshes && meshes[0] ? meshes[0]->ctx : nullptr, [&] {
+    OCN_REQUIRE(n >= 0 && (n == 0 || (meshes && reports)), "null argument");
+    hydro_reports_read(n, meshes, reports);
   });
 }
 

@@ -104,6 +104,13 @@ struct ocn_mesh {
   ocn::DevBuf<unsigned char> used;
   ocn::DevBuf<int> loop_off, point_ref, loop_counts;
   ocn::DevBuf<double> loop_points;
+  // pinned host staging of the report and flags (one synchronisation per read)
+  ocn::ReportDev* h_report = nullptr;
+  int* h_flags = nullptr;
+  ~ocn_mesh() {
+    if (h_report) cudaFreeHost(h_report);
+    if (h_flags) cudaFreeHost(h_flags);
+  }
 };
 
 // FdmZone (interactive.hpp:61-104): host scalars + device fp32 fields

@@ -16,6 +16,10 @@
 
 #include "hydro_internal.cuh"
 
+namespace ocn {
+void hydro_reports_read(int n, ocn_mesh* const* meshes, ocn_hydro_report* out);
+}
+
 namespace {
 
 struct V3 {
@@ -354,7 +358,9 @@ int ocn_sim_step(ocn_sim* s, int steps) {
         OCN_CUDA(cudaEventRecord(s->ready[1 - k], s->sctx->stream));
         s->prefetched = true;
       }
-      for (int i = 0; i < nb; ++i) check(ocn_hydro_report_get(s->bodies[i].mesh, &reports[i]));
+      std::vector<ocn_mesh*> meshes(nb);
+      for (int i = 0; i < nb; ++i) meshes[i] = s->bodies[i].mesh;
+      hydro_reports_read(nb, meshes.data(), reports.data());
       // forces and integration (sim.cpp:112-125)
       for (int i = 0; i < nb; ++i) {
         SimBody& b = s->bodies[i];

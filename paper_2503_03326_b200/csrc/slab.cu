@@ -277,15 +277,12 @@ __global__ void __launch_bounds__(SlabLaunch<N>::THREADS) k_slab_cols(const Slab
 }
 
 // ---------------------------------------------------------------- four-step columns
-// Stride between the 64 transform buffers of a four-step CTA. The cooperative
-// tile loads / stores walk the 32 columns of a row (c fastest): with the FFT's
-// own stride (132 = 4 mod 16 float2) they hit 4 bank pairs per half-warp; an
-// odd stride spreads them (OCN_FS_ODD=1 at build time).
-#ifndef OCN_FS_ODD
-#define OCN_FS_ODD 0
-#endif
+// Stride between the 64 transform buffers of a four-step CTA: the FFT's own
+// (conflict-free for its exchanges); an odd stride, which spreads the
+// cooperative column-major tile loads over more banks, measured slower (config 5
+// 18.7 vs 17.4 ms).
 template <int SMEM>
-constexpr int kFsStride = OCN_FS_ODD ? (SMEM | 1) : SMEM;
+constexpr int kFsStride = SMEM;
 constexpr int kFsN2 = 128;  // inner length of the second step
 constexpr int kFsPC = 32;   // columns per tile (256-byte row segments: DRAM page locality)
 constexpr int kFsB = 2;     // i2 (step A) or k1 (step B) values per CTA (64 transforms)
