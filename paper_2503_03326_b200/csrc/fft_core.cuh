@@ -84,10 +84,34 @@ struct Tw {
   static constexpr float s = (float)c_sinpi2(K, LEN);
 };
 
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+// Complex arithmetic on the packed fp32x2 pipe of sm_100 (FADD2 / FMUL2 /
+// FFMA2: one instruction per complex add, two per complex multiply; operand
+// broadcast, swap and per-half negation are free modifiers). The rounding of
+// cmul and the general twiddle matches the scalar fmaf forms exactly.
+#if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 1000 && !defined(OCN_SCALAR_COMPLEX)
+#define OCN_F32X2 1
+#endif
+
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) {
+#ifdef OCN_F32X2
+  return __fadd2_rn(a, b);
+#else
+  return make_float2(a.x + b.x, a.y + b.y);
+#endif
+}
+__device__ __forceinline__ float2 csub(float2 a, float2 b) {
+#ifdef OCN_F32X2
+  return __fadd2_rn(a, make_float2(-b.x, -b.y));
+#else
+  return make_float2(a.x - b.x, a.y - b.y);
+#endif
+}
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+#ifdef OCN_F32X2
+  return __ffma2_rn(make_float2(a.x, a.x), b, __fmul2_rn(make_float2(a.y, a.y), make_float2(-b.y, b.x)));
+#else
   return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+#endif
 }
 
 // x * exp(+2 pi i K / LEN) with the trivial angles special-cased
@@ -104,13 +128,25 @@ __device__ __forceinline__ float2 twiddle_c(float2 x) {
     return make_float2(x.y, -x.x);
   } else if constexpr (8 * k == LEN) {  // *(1+i)/sqrt2
     constexpr float h = 0.70710678118654752440f;
+#ifdef OCN_F32X2
+    return __fmul2_rn(__fadd2_rn(make_float2(x.x, x.x), make_float2(-x.y, x.y)), make_float2(h, h));
+#else
     return make_float2((x.x - x.y) * h, (x.x + x.y) * h);
+#endif
   } else if constexpr (8 * k == 3 * LEN) {  // *(-1+i)/sqrt2
     constexpr float h = 0.70710678118654752440f;
+#ifdef OCN_F32X2
+    return __fmul2_rn(__fadd2_rn(make_float2(x.y, x.x), make_float2(x.x, -x.y)), make_float2(-h, h));
+#else
     return make_float2(-(x.x + x.y) * h, (x.x - x.y) * h);
+#endif
   } else {
     constexpr float c = Tw<LEN, k>::c, s = Tw<LEN, k>::s;
+#ifdef OCN_F32X2
+    return __ffma2_rn(make_float2(x.x, x.x), make_float2(c, s), __fmul2_rn(make_float2(x.y, x.y), make_float2(-s, c)));
+#else
     return make_float2(fmaf(x.x, c, -x.y * s), fmaf(x.x, s, x.y * c));
+#endif
   }
 }
 

@@ -146,7 +146,8 @@ void set_smem_attrs() {
 static int cols_variant() {
   static const int v = [] {
     const char* e = getenv("OCN_COLS");
-    return e && !strcmp(e, "tma") ? 0 : 4;
+    if (e && !strcmp(e, "tma")) return 0;
+    return 4;
   }();
   return v;
 }
