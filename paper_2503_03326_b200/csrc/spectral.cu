@@ -192,12 +192,19 @@ void launch_rows(ocn_ctx* ctx, const RowArgs& a, bool plain, cudaStream_t st, in
       smem_opt_in(k_rows_w<N, kRowPlain>, smax);
       smem_opt_in(k_rows_w<N, kRowSurface>, smax);
       smem_opt_in(k_rows_w<N, kRowVelocity>, smax);
+      smem_opt_in(k_rows_w<N, kRowSurface, true>, smax);
+      smem_opt_in(k_rows_w<N, kRowVelocity, true>, smax);
     }
     const dim3 grid(N / rpc, plain ? 1 : nseg);
+    const bool fused = a.h0p != nullptr;
     if (plain)
       k_rows_w<N, kRowPlain><<<grid, 32 * warps, smem, st>>>(ar);
+    else if (family == 0 && fused)
+      k_rows_w<N, kRowSurface, true><<<grid, 32 * warps, smem, st>>>(ar);
     else if (family == 0)
       k_rows_w<N, kRowSurface><<<grid, 32 * warps, smem, st>>>(ar);
+    else if (fused)
+      k_rows_w<N, kRowVelocity, true><<<grid, 32 * warps, smem, st>>>(ar);
     else
       k_rows_w<N, kRowVelocity><<<grid, 32 * warps, smem, st>>>(ar);
     OCN_LAUNCHED(ctx);
@@ -379,6 +386,14 @@ static void build_out_maps(int n, const XformDesc* desc, int count, DevBuf<CUten
 static bool band_skip_enabled() {
   static const bool on = [] {
     const char* e = getenv("OCN_NO_BAND_SKIP");
+    return !(e && *e && *e != '0');
+  }();
+  return on;
+}
+
+bool fused_evolve_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("OCN_NO_FUSED_EVOLVE");
     return !(e && *e && *e != '0');
   }();
   return on;
@@ -570,7 +585,14 @@ static void enqueue_spectral(ocn_cascades* cas, SpectralPlan* plan, ocn_maps* ma
   const size_t nn = (size_t)n * n;
   cudaStream_t A = ctx->stream;
   ProfWindow whole(ctx, OCN_PROF_SPECTRAL);
-  {
+  // Time-batched frame sets with N in the warp row kernel's range: the row pass
+  // evaluates h~ / G itself (no spectrum round trip through memory, no evolve
+  // launch). Measured on B200: config 1 0.998 -> 0.953 ms per 10 frames; for
+  // single-frame sets the extra per-row table loads cost more than the evolve
+  // pass saves (config 3 0.491 -> 0.514, config 4 0.947 -> 0.971), so those keep
+  // k_evolve. OCN_NO_FUSED_EVOLVE=1 keeps it everywhere.
+  const bool fused = n >= 128 && n <= 1024 && cas->frames > 1 && fused_evolve_enabled();
+  if (!fused) {
     ProfWindow pw(ctx, OCN_PROF_EVOLVE);  // every grid in one launch
     // skip never-read rows only where every reader is a band-aware warp row kernel
     const int skip = n >= 128 && n <= 1024 && cas->cols_map_ok && band_skip_enabled() ? 1 : 0;
@@ -603,6 +625,11 @@ static void enqueue_spectral(ocn_cascades* cas, SpectralPlan* plan, ocn_maps* ma
     // TMA column pass reads only the band rows (off with OCN_NO_BAND_SKIP=1)
     const bool band = cas->cols_map_ok && band_skip_enabled();
     ra.skip_zero_rows = band ? 1 : 0;
+    if (fused) {
+      ra.h0p = cas->h0p.p;
+      ra.omega = cas->omega.p;
+      ra.d_time = cas->d_time.p;
+    }
     {
       ProfWindow pw(ctx, OCN_PROF_ROWS);
       rows_dispatch(ctx, n, ra, false, A, gr.nseg, gr.max_seg, gr.family);

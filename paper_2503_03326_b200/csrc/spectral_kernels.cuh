@@ -234,7 +234,26 @@ struct RowArgs {
   // them (set only when the column pass treats them as zero without reading)
   int skip_zero_rows;
   int stage_f4;  // warp row kernel: float4 slots of the per-row staging area
+  // fused evolve (warp row kernel): h~ / G of the staged rows are evaluated
+  // from the h0p / omega tables at d_time (k_evolve's arithmetic) instead of
+  // being read from spec_h / spec_g
+  const float4* h0p;
+  const double* omega;
+  const double* d_time;
 };
+
+// h~ (surface, A + B) or G (velocity, A - B) of one mode at time t from its
+// (h0(k), conj h0(-k)) pair and w(k) -- k_evolve's arithmetic, bit for bit
+template <bool G_FORM>
+__device__ __forceinline__ float2 evolve_mode(float4 hp, double w, double t) {
+  double ph = w * t;
+  ph -= 6.283185307179586476925 * rint(ph * 0.15915494309189533577);
+  float s, cs;
+  sincosf((float)ph, &s, &cs);
+  const float ar = hp.x * cs - hp.y * s, ai = hp.x * s + hp.y * cs;
+  const float br = hp.z * cs + hp.w * s, bi = hp.w * cs - hp.z * s;
+  return G_FORM ? make_float2(ar - br, ai - bi) : make_float2(ar + br, ai + bi);
+}
 
 // packed coefficient X + iY of transform `d` at mode (i, j)
 __device__ __forceinline__ float2 packed_coef(const XformDesc& d, float2 s, int i, int j, int n,
@@ -377,7 +396,7 @@ enum RowMode : int { kRowPlain = 0, kRowSurface = 1, kRowVelocity = 2 };
 #ifndef OCN_ROWS_MINB_SMALL
 #define OCN_ROWS_MINB_SMALL 2
 #endif
-template <int N, int MODE>
+template <int N, int MODE, bool FUSED = false>
 __global__ void __launch_bounds__(256, N >= 1024 ? 2 : OCN_ROWS_MINB_SMALL) k_rows_w(const RowArgs a) {
   constexpr bool PLAIN = MODE == kRowPlain;
   using W = WarpLaunch<N>;
@@ -428,11 +447,18 @@ __global__ void __launch_bounds__(256, N >= 1024 ? 2 : OCN_ROWS_MINB_SMALL) k_ro
     const float2* srow =
         (MODE == kRowSurface ? a.spec_h : a.spec_g) + ((size_t)grid * N + row0) * N;
     const float g = (float)a.gc[grid].p.gravity;
+    const size_t tab = FUSED ? ((size_t)a.gc[grid].src * N + row0) * N : 0;
+    const double tt = FUSED ? a.d_time[0] + (double)a.gc[grid].frame * a.d_time[1] : 0.0;
     // MUFU reciprocal square roots (no IEEE slow-path calls, so the row's
     // loads issue back to back); only the arrays this family reads
 #pragma unroll 4
     for (int j = threadIdx.x; j < rpc * N; j += blockDim.x) {
-      const float2 sp = __ldg(srow + j);  // h~ (surface) or G (velocity)
+      // h~ (surface) or G (velocity)
+      float2 sp;
+      if constexpr (FUSED)
+        sp = evolve_mode<MODE == kRowVelocity>(__ldg(a.h0p + tab + j), __ldg(a.omega + tab + j), tt);
+      else
+        sp = __ldg(srow + j);
       const float kx = dkf * (float)(row0 + j / N - N / 2);
       const float kz = dkf * (float)((j & (N - 1)) - N / 2);
       const float k2 = kx * kx + kz * kz;
