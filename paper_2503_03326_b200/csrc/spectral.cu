@@ -399,17 +399,29 @@ bool fused_evolve_enabled() {
   return on;
 }
 
+bool merged_cols_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("OCN_NO_MERGED_COLS");
+    return !(e && *e && *e != '0');
+  }();
+  return on;
+}
+
 size_t group_for(int n, int total) {
   // Scratch budget of the transform groups. Larger groups amortise the row
   // kernel's per-row staging over more transforms and keep the persistent
   // column kernel's tile ring full: measured on B200 at N = 1024 (config 3,
   // spectral ms / frame, first TMA column kernel) 64 MB 1.75, 256 MB 1.46,
   // 512 MB 1.39, 1 GB 1.36, 2 GB 1.33; with balanced family groups (get_plan)
-  // 384 MB 1.100, 512 MB 1.123, 768 MB 1.095, 1 GB 1.124 -> 768 MB default
-  // (96-transform groups at N = 1024). OCN_SCRATCH_MB overrides.
+  // 384 MB 1.100, 512 MB 1.123, 768 MB 1.095, 1 GB 1.124. With the current
+  // kernels (f32x2 FFT, per-warp TMA stores) 768 MB 0.492 / 0.949 (configs 3 /
+  // 4), 1200 MB 0.473 / 0.949, 1536 MB 0.473 / 0.937: every config's
+  // transforms fit in one scratch at 1536 MB (config 3: 164 x 8 MB; config 4:
+  // 768 x 2 MB; config 1: 2400 x 512 KB), which also lets the column pass run
+  // as one launch (enqueue_spectral). OCN_SCRATCH_MB overrides.
   static const size_t budget = [] {
     const char* e = getenv("OCN_SCRATCH_MB");
-    return (size_t)(e && atoi(e) > 0 ? atoi(e) : 768) << 20;
+    return (size_t)(e && atoi(e) > 0 ? atoi(e) : 1536) << 20;
   }();
   size_t per = (size_t)n * n * sizeof(float2);
   size_t g = budget / per;
@@ -607,9 +619,31 @@ static void enqueue_spectral(ocn_cascades* cas, SpectralPlan* plan, ocn_maps* ma
           cas->spec_h.p, nullptr, cas->gconst.p, skip);
     OCN_LAUNCHED(ctx);
   }
+  // When every transform of the step fits in the scratch at once, the family
+  // groups' row passes write disjoint scratch ranges and ONE column launch
+  // covers all of them (config 3: 7 -> 4 launches, no per-group column-pass
+  // tail; measured 0.473 -> see DESIGN.md). OCN_NO_MERGED_COLS=1 keeps one
+  // column launch per group.
+  int all = 0;
+  for (const auto& gr : plan->groups) all += gr.count;
+  const bool merged = plan->groups.size() > 1 && all <= cas->group && merged_cols_enabled();
+  const bool band = cas->cols_map_ok && band_skip_enabled();
+  auto run_cols = [&](int first, int count) {
+    ColArgs ca{};
+    ca.scratch = cas->scratch.p;
+    ca.desc = plan->desc.p + first;
+    ca.tw = cas->twiddle.p;
+    ca.out_maps = plan->out_maps.p ? plan->out_maps.p + 2 * first : nullptr;
+    ca.gc = band ? cas->gconst.p : nullptr;
+    ProfWindow pw(ctx, OCN_PROF_COLS);
+    cols_dispatch(ctx, n, ca, count, false, A, cas->cols_map_ok ? &cas->cols_map : nullptr,
+                  cas->cols_map_ok ? &cas->cols_chunk_map : nullptr);
+  };
+  size_t off = 0;  // merged: this group's first scratch slot
   for (size_t gidx = 0; gidx < plan->groups.size(); ++gidx) {
     const SpectralPlan::Group& gr = plan->groups[gidx];
-    float2* scratch = cas->scratch.p;
+    float2* scratch = cas->scratch.p + (merged ? off * nn : 0);
+    off += gr.count;
     RowArgs ra{};
     ra.items = n * gr.count;
     ra.G = gr.count;
@@ -623,7 +657,6 @@ static void enqueue_spectral(ocn_cascades* cas, SpectralPlan* plan, ocn_maps* ma
     ra.tw = cas->twiddle.p;
     // band-limited grids: the row pass skips the exactly-zero rows and the
     // TMA column pass reads only the band rows (off with OCN_NO_BAND_SKIP=1)
-    const bool band = cas->cols_map_ok && band_skip_enabled();
     ra.skip_zero_rows = band ? 1 : 0;
     if (fused) {
       ra.h0p = cas->h0p.p;
@@ -634,18 +667,9 @@ static void enqueue_spectral(ocn_cascades* cas, SpectralPlan* plan, ocn_maps* ma
       ProfWindow pw(ctx, OCN_PROF_ROWS);
       rows_dispatch(ctx, n, ra, false, A, gr.nseg, gr.max_seg, gr.family);
     }
-    ColArgs ca{};
-    ca.scratch = scratch;
-    ca.desc = plan->desc.p + gr.first;
-    ca.tw = cas->twiddle.p;
-    ca.out_maps = plan->out_maps.p ? plan->out_maps.p + 2 * gr.first : nullptr;
-    ca.gc = band ? cas->gconst.p : nullptr;
-    {
-      ProfWindow pw(ctx, OCN_PROF_COLS);
-      cols_dispatch(ctx, n, ca, gr.count, false, A, cas->cols_map_ok ? &cas->cols_map : nullptr,
-                    cas->cols_map_ok ? &cas->cols_chunk_map : nullptr);
-    }
+    if (!merged) run_cols(gr.first, gr.count);
   }
+  if (merged) run_cols(plan->groups[0].first, all);
   if (plan->assembly && maps) assemble_grids(maps, A);
 }
 
