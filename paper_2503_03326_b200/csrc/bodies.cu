@@ -19,6 +19,12 @@ HydroJob make_job(ocn_mesh* m, const ocn_pose* pose, const ocn_fluid* fluid, con
 void fill_samplers_batch(HydroBatch<kMaxBatch>& B, const ocn_fluid* fluid);
 void hydro_evaluate_jobs(int n, ocn_mesh* const* meshes, const HydroBatch<kMaxBatch>& B);
 void hydro_reports_read(int n, ocn_mesh* const* meshes, ocn_hydro_report* out);
+void zones_step_batch(int nz, ocn_zone* const* zones, double dt, const double* bx, const double* bz);
+void zones_apply_last_mask_batch(int nz, ocn_zone* const* zones);
+void zones_mask_from_hydro_batch(int nz, ocn_zone* const* zones, ocn_mesh* const* meshes,
+                                 const double* yaw, const double* bx, const double* bz,
+                                 const double* speed, const ocn_mask_frame* frames,
+                                 const ocn_mask_params* params);
 }  // namespace ocn
 
 using namespace ocn;
@@ -59,17 +65,26 @@ int ocn_bodies_step(int n_bodies, const ocn_body_frame* bodies, const ocn_fluid*
       check(ocn_zone_update_stability((ocn_zone*)b.zone, b.speed, dt));
     }
     hydro_evaluate_jobs(n_bodies, meshes.data(), B);
+    // every body's mask, apply and FDM step as one launch each (zones are
+    // independent: batching keeps sim.cpp's per-body results)
+    std::vector<ocn_zone*> zones(n_bodies);
+    std::vector<double> yaw(n_bodies), bx(n_bodies), bz(n_bodies), speed(n_bodies);
+    std::vector<ocn_mask_frame> frames(n_bodies);
+    std::vector<ocn_mask_params> params(n_bodies);
     for (int i = 0; i < n_bodies; ++i) {
       const ocn_body_frame& b = bodies[i];
-      check(ocn_zone_mask_from_hydro_deferred((ocn_zone*)b.zone, meshes[i], b.yaw,
-                                              b.pose.position[0], b.pose.position[2], b.speed,
-                                              &b.frame, &b.mask));
+      zones[i] = (ocn_zone*)b.zone;
+      yaw[i] = b.yaw;
+      bx[i] = b.pose.position[0];
+      bz[i] = b.pose.position[2];
+      speed[i] = b.speed;
+      frames[i] = b.frame;
+      params[i] = b.mask;
     }
-    for (int i = 0; i < n_bodies; ++i) {
-      check(ocn_zone_apply_last_mask((ocn_zone*)bodies[i].zone));
-      check(ocn_zone_step((ocn_zone*)bodies[i].zone, dt, bodies[i].pose.position[0],
-                          bodies[i].pose.position[2]));
-    }
+    zones_mask_from_hydro_batch(n_bodies, zones.data(), meshes.data(), yaw.data(), bx.data(),
+                                bz.data(), speed.data(), frames.data(), params.data());
+    zones_apply_last_mask_batch(n_bodies, zones.data());
+    zones_step_batch(n_bodies, zones.data(), dt, bx.data(), bz.data());
     if (!reports) return;  // asynchronous: reports via ocn_hydro_report_get
     hydro_reports_read(n_bodies, meshes.data(), reports);
   });

@@ -37,12 +37,28 @@ namespace {
 // Each thread computes 4 consecutive cells of one row; interior threads (every
 // read in range, the common case) take one branch-free path, the rest the
 // bounds-checked one. Same arithmetic order in both.
-__global__ void __launch_bounds__(256) k_fdm_step(int n, int m, int wx, int wz, int ox, int oz,
-                                                  float a, float d, const float* __restrict__ curr,
-                                                  const float* __restrict__ prev, float* next) {
+struct FdmJob {
+  int n, m, wx, wz, ox, oz;
+  float a, d;
+  const float* curr;
+  const float* prev;
+  float* next;
+};
+struct FdmBatch {
+  int count;
+  FdmJob j[kMaxBatch];
+};
+
+// zone blockIdx.z of the batch (every zone of a Simulation step in one launch)
+__global__ void __launch_bounds__(256) k_fdm_step(const __grid_constant__ FdmBatch B) {
+  const FdmJob& J = B.j[blockIdx.z];
+  const int n = J.n, m = J.m, wx = J.wx, wz = J.wz, ox = J.ox, oz = J.oz;
+  const float a = J.a, d = J.d;
+  const float* __restrict__ curr = J.curr;
+  const float* __restrict__ prev = J.prev;
   const int j0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
   const int i = blockIdx.y;
-  if (j0 >= n) return;
+  if (j0 >= n || i >= n) return;
   const int k = i + wx;
   const bool row_in = i >= m && i < n - m;
   const bool fast = row_in && k >= 1 && k + 1 < n && j0 >= m && j0 + 3 < n - m &&
@@ -79,7 +95,7 @@ __global__ void __launch_bounds__(256) k_fdm_step(int n, int m, int wx, int wz, 
       }
     }
   }
-  float* dst = next + (size_t)i * n + j0;
+  float* dst = J.next + (size_t)i * n + j0;
   if ((n & 3) == 0) {  // rows start 16-byte aligned: one vector store
     *reinterpret_cast<float4*>(dst) = make_float4(out[0], out[1], out[2], out[3]);
   } else {
@@ -98,20 +114,33 @@ __global__ void k_apply_cells(int n, int m, int count, const int* ij, const doub
 }
 
 // apply_mask (interactive.cpp:113-118) of the cell set the last mask pass
-// left on the device (box [i0, i1) x [j0, j1), flags, heights).
-__global__ void k_apply_box(const int* box, const unsigned char* mask_f, const double* mask_h,
-                            size_t cap, int n, int m, float* curr) {
+// left on the device (box [i0, i1) x [j0, j1), flags, heights); zone blockIdx.y
+struct ApplyJob {
+  const int* box;
+  const unsigned char* mask_f;
+  const double* mask_h;
+  size_t cap;
+  int n, m;
+  float* curr;
+};
+struct ApplyBatch {
+  int count;
+  ApplyJob j[kMaxBatch];
+};
+__global__ void k_apply_box(const __grid_constant__ ApplyBatch B) {
+  const ApplyJob& J = B.j[blockIdx.y];
+  const int* box = J.box;
   const int i0 = box[0], i1 = box[1], j0 = box[2], j1 = box[3];
   if (box[4] <= 0 || i1 <= i0 || j1 <= j0) return;
-  const int bw = j1 - j0;
+  const int bw = j1 - j0, n = J.n, m = J.m;
   size_t cells = (size_t)(i1 - i0) * bw;
-  if (cells > cap) cells = cap;
+  if (cells > J.cap) cells = J.cap;
   for (size_t c = blockIdx.x * (size_t)blockDim.x + threadIdx.x; c < cells;
        c += (size_t)gridDim.x * blockDim.x) {
-    if (!mask_f[c]) continue;
+    if (!J.mask_f[c]) continue;
     const int i = i0 + (int)(c / bw), j = j0 + (int)(c % bw);
     if (i < m || j < m || i >= n - m || j >= n - m) continue;
-    curr[(size_t)i * n + j] = (float)mask_h[c];
+    J.curr[(size_t)i * n + j] = (float)J.mask_h[c];
   }
 }
 
@@ -145,6 +174,32 @@ struct MaskArgs {
   double mesh_volume;
 };
 
+// One zone's mask pass (k_mask_prepare block / k_mask_cells grid row)
+struct MaskJob {
+  MaskArgs A;
+  const int* nloops_dev;  // loop count on the device (mask_from_hydro) or null
+  int nloops_host;
+  const int* off;
+  const double* pts;
+  double* out_xz;
+  int* out_off;
+  double* bbox;
+  int* box;
+  int* bin_off;
+  int* bin_edges;
+  int bin_cap;
+  int box_w_cap;
+  double* mask_h;
+  unsigned char* mask_f;
+  float* curr;
+  int apply;
+  int* count;
+};
+struct MaskBatch {
+  int count;
+  MaskJob j[kMaxBatch];
+};
+
 __device__ __forceinline__ void derotate(const MaskArgs& A, double px, double pz, double* lx,
                                          double* lz) {
   const double qx = __dsub_rn(px, A.bx), qz = __dsub_rn(pz, A.bz);
@@ -166,18 +221,26 @@ __device__ __forceinline__ int mask_bin(double x, double lo, double w) {
 // ray parity of p when min(ax, bx) <= p.x < max(ax, bx)), so a cell tests the
 // few edges of its bin; the per-edge test is untouched, so the parity (and the
 // cell set) is exactly the reference's.
-__global__ void __launch_bounds__(1024) k_mask_prepare(MaskArgs A, const int* nloops_dev,
-                                                       int nloops_host, const int* off,
-                                                       const double* pts, double* out_xz,
-                                                       int* out_off, double* bbox, int* box,
-                                                       int* bin_off, int* bin_edges,
-                                                       int bin_cap) {
+// zone blockIdx.x of the batch: one block per zone
+__global__ void __launch_bounds__(1024) k_mask_prepare(const __grid_constant__ MaskBatch B) {
+  const MaskJob& J = B.j[blockIdx.x];
+  const MaskArgs& A = J.A;
+  const int* off = J.off;
+  const double* pts = J.pts;
+  double* out_xz = J.out_xz;
+  int* out_off = J.out_off;
+  double* bbox = J.bbox;
+  int* box = J.box;
+  int* bin_off = J.bin_off;
+  int* bin_edges = J.bin_edges;
+  const int bin_cap = J.bin_cap;
   __shared__ int s_cnt[kMaskBins + 1];
   __shared__ int s_kept;
   __shared__ double s_lo[2][32], s_hi[2][32];
   __shared__ int s_wsum[32];
-  const int nl = nloops_dev ? nloops_dev[0] : nloops_host;
+  const int nl = J.nloops_dev ? J.nloops_dev[0] : J.nloops_host;
   if (threadIdx.x == 0) {
+    *J.count = 0;  // k_mask_cells accumulates into it
     int kept = 0, np = 0;
     out_off[0] = 0;
     for (int l = 0; l < nl; ++l) {
@@ -313,12 +376,22 @@ constexpr int kMaskEdgesSmem = 4096;  // loop points cached in shared memory
 
 // Per candidate cell: bbox cull, +z ray-crossing parity, V-shaped height;
 // optionally writes the height into curr (apply_mask, interactive.cpp:113-118).
-__global__ void __launch_bounds__(256) k_mask_cells(MaskArgs A, const int* box,
-                                                    const double* bbox, const int* loop_off,
-                                                    const double* loops_xz, int box_w_cap,
-                                                    double* mask_h, unsigned char* mask_f,
-                                                    float* curr, int apply, int* count,
-                                                    const int* bin_off, const int* bin_edges) {
+// zone blockIdx.y of the batch
+__global__ void __launch_bounds__(256) k_mask_cells(const __grid_constant__ MaskBatch B) {
+  const MaskJob& J = B.j[blockIdx.y];
+  const MaskArgs& A = J.A;
+  const int* box = J.box;
+  const double* bbox = J.bbox;
+  const int* loop_off = J.out_off;
+  const double* loops_xz = J.out_xz;
+  const int box_w_cap = J.box_w_cap;
+  double* mask_h = J.mask_h;
+  unsigned char* mask_f = J.mask_f;
+  float* curr = J.curr;
+  const int apply = J.apply;
+  int* count = J.count;
+  const int* bin_off = J.bin_off;
+  const int* bin_edges = J.bin_edges;
   extern __shared__ double sm_pts[];
   const int i0 = box[0], i1 = box[1], j0 = box[2], j1 = box[3], kept = box[4];
   if (kept == 0 || i1 <= i0 || j1 <= j0) return;
@@ -393,32 +466,59 @@ void check_mask_frame(const ocn_mask_frame* f) {
     fail(OCN_ERR_DOMAIN, "mask_height: degenerate body frame");
 }
 
-// shared by the explicit-loops and from-hydro entry points
-void mask_launch(ocn_zone* z, MaskArgs A, const int* nloops_dev, int nloops_host,
+// One zone's mask job (device buffers sized on the host first)
+MaskJob mask_job(ocn_zone* z, const MaskArgs& A, const int* nloops_dev, int nloops_host,
                  const int* d_off, const double* d_pts, int max_points, int apply) {
-  ocn_ctx* ctx = z->ctx;
-  cudaStream_t st = ctx->stream;
   z->loops_xz.ensure(2 * (size_t)std::max(max_points, 1));
   z->loops_off.ensure((size_t)max_points / 4 + 2);
   const size_t box_cap = (size_t)(z->n - 2 * z->margin) * (z->n - 2 * z->margin);
   z->mask_h.ensure(box_cap);
   z->mask_f.ensure(box_cap);
-  ProfWindow pw(ctx, OCN_PROF_MASK);
-  OCN_CUDA(cudaMemsetAsync(z->mask_count.p, 0, sizeof(int), st));
   const int bin_cap = 8 * std::max(max_points, 1) + 16 * kMaskBins;
   z->bin_off.ensure(kMaskBins + 1);
   z->bin_edges.ensure(bin_cap);
-  k_mask_prepare<<<1, 1024, 0, st>>>(A, nloops_dev, nloops_host, d_off, d_pts, z->loops_xz.p,
-                                     z->loops_off.p, z->loop_bbox.p, z->mask_box.p, z->bin_off.p,
-                                     z->bin_edges.p, bin_cap);
+  MaskJob J{};
+  J.A = A;
+  J.nloops_dev = nloops_dev;
+  J.nloops_host = nloops_host;
+  J.off = d_off;
+  J.pts = d_pts;
+  J.out_xz = z->loops_xz.p;
+  J.out_off = z->loops_off.p;
+  J.bbox = z->loop_bbox.p;
+  J.box = z->mask_box.p;
+  J.bin_off = z->bin_off.p;
+  J.bin_edges = z->bin_edges.p;
+  J.bin_cap = bin_cap;
+  J.box_w_cap = (int)box_cap;
+  J.mask_h = z->mask_h.p;
+  J.mask_f = z->mask_f.p;
+  J.curr = z->curr();
+  J.apply = apply;
+  J.count = z->mask_count.p;
+  return J;
+}
+
+// the mask passes of B.count zones: two launches whatever the count
+void mask_launch_batch(ocn_ctx* ctx, const MaskBatch& B) {
+  cudaStream_t st = ctx->stream;
+  ProfWindow pw(ctx, OCN_PROF_MASK);
+  k_mask_prepare<<<B.count, 1024, 0, st>>>(B);
   OCN_LAUNCHED(ctx);
   const size_t smem = kMaskEdgesSmem * 2 * sizeof(double);
   smem_opt_in(k_mask_cells, smem);
-  k_mask_cells<<<ctx->sm_count * 4, 256, smem, st>>>(A, z->mask_box.p, z->loop_bbox.p,
-                                                     z->loops_off.p, z->loops_xz.p, (int)box_cap,
-                                                     z->mask_h.p, z->mask_f.p, z->curr(), apply,
-                                                     z->mask_count.p, z->bin_off.p, z->bin_edges.p);
+  const int per = std::max(1, ctx->sm_count * 4 / B.count);
+  k_mask_cells<<<dim3(per, B.count), 256, smem, st>>>(B);
   OCN_LAUNCHED(ctx);
+}
+
+// shared by the explicit-loops and from-hydro entry points
+void mask_launch(ocn_zone* z, MaskArgs A, const int* nloops_dev, int nloops_host,
+                 const int* d_off, const double* d_pts, int max_points, int apply) {
+  MaskBatch B{};
+  B.count = 1;
+  B.j[0] = mask_job(z, A, nloops_dev, nloops_host, d_off, d_pts, max_points, apply);
+  mask_launch_batch(z->ctx, B);
 }
 
 MaskArgs mask_args(ocn_zone* z, double yaw, double bx, double bz, double speed,
@@ -436,6 +536,98 @@ MaskArgs mask_args(ocn_zone* z, double yaw, double bx, double bz, double speed,
 }
 
 }  // namespace
+
+// FdmZone::step (interactive.cpp:67-111) of n zones: the scalar bookkeeping per
+// zone on the host, the stencils as ONE launch (zone = blockIdx.z)
+void zones_step_batch(int nz, ocn_zone* const* zones, double dt, const double* bx, const double* bz) {
+  if (nz <= 0) return;
+  OCN_REQUIRE(nz <= kMaxBatch, "%d zones in one step batch (max %d)", nz, kMaxBatch);
+  ocn_ctx* ctx = zones[0]->ctx;
+  FdmBatch B{};
+  B.count = nz;
+  int max_n = 0;
+  for (int q = 0; q < nz; ++q) {
+    ocn_zone* z = zones[q];
+    OCN_REQUIRE(z && z->ctx == ctx, "zones must share one context");
+    const double mx = bx[q] - z->pos_curr[0], mz = bz[q] - z->pos_curr[1];
+    const double rx = mx / z->delta + z->carry[0];
+    const double rz = mz / z->delta + z->carry[1];
+    int wx = (int)std::floor(rx), wz = (int)std::floor(rz);
+    z->carry[0] = rx - wx;
+    z->carry[1] = rz - wz;
+    const int max_shift = z->margin - 1;
+    const size_t nn = (size_t)z->n * z->n;
+    if (std::abs(wx) > max_shift || std::abs(wz) > max_shift) {
+      wx = std::clamp(wx, -max_shift, max_shift);
+      wz = std::clamp(wz, -max_shift, max_shift);
+      OCN_CUDA(cudaMemsetAsync(z->curr(), 0, nn * sizeof(float), ctx->stream));
+      OCN_CUDA(cudaMemsetAsync(z->prev(), 0, nn * sizeof(float), ctx->stream));
+      ++z->dropped_wake;
+    }
+    const int ox = wx + z->last_shift[0], oz = wz + z->last_shift[1];
+    const double a = z->c * z->c * dt * dt / (z->delta * z->delta);
+    const int inext = 3 - z->icurr - z->iprev;
+    B.j[q] = FdmJob{z->n, z->margin, wx, wz, ox, oz, (float)a, (float)z->damping,
+                    z->curr(), z->prev(), z->buf[inext].p};
+    max_n = std::max(max_n, z->n);
+    z->iprev = z->icurr;
+    z->icurr = inext;
+    z->origin[0] += wx * z->delta;
+    z->origin[1] += wz * z->delta;
+    z->last_shift[0] = wx;
+    z->last_shift[1] = wz;
+    z->pos_curr[0] = bx[q];
+    z->pos_curr[1] = bz[q];
+  }
+  const dim3 grid(((max_n + 3) / 4 + 255) / 256, max_n, nz);
+  ProfWindow pw(ctx, OCN_PROF_FDM);
+  k_fdm_step<<<grid, 256, 0, ctx->stream>>>(B);
+  OCN_LAUNCHED(ctx);
+}
+
+// apply_mask (interactive.cpp:113-118) of each zone's last deferred mask, one launch
+void zones_apply_last_mask_batch(int nz, ocn_zone* const* zones) {
+  if (nz <= 0) return;
+  OCN_REQUIRE(nz <= kMaxBatch, "%d zones in one mask batch (max %d)", nz, kMaxBatch);
+  ocn_ctx* ctx = zones[0]->ctx;
+  ApplyBatch B{};
+  B.count = nz;
+  for (int q = 0; q < nz; ++q) {
+    ocn_zone* z = zones[q];
+    OCN_REQUIRE(z && z->ctx == ctx, "zones must share one context");
+    B.j[q] = ApplyJob{z->mask_box.p, z->mask_f.p, z->mask_h.p, z->mask_f.n, z->n, z->margin,
+                      z->curr()};
+  }
+  k_apply_box<<<dim3(std::max(1, ctx->sm_count * 2 / nz), nz), 256, 0, ctx->stream>>>(B);
+  OCN_LAUNCHED(ctx);
+}
+
+// Simulation's per-body masks (sim.cpp:86-99) from each mesh's last hydro
+// evaluation, computed (not applied) for n zones in two launches
+void zones_mask_from_hydro_batch(int nz, ocn_zone* const* zones, ocn_mesh* const* meshes,
+                                 const double* yaw, const double* bx, const double* bz,
+                                 const double* speed, const ocn_mask_frame* frames,
+                                 const ocn_mask_params* params) {
+  if (nz <= 0) return;
+  OCN_REQUIRE(nz <= kMaxBatch, "%d zones in one mask batch (max %d)", nz, kMaxBatch);
+  MaskBatch B{};
+  B.count = nz;
+  for (int q = 0; q < nz; ++q) {
+    ocn_zone* z = zones[q];
+    ocn_mesh* mesh = meshes[q];
+    OCN_REQUIRE(z && mesh && frames && params, "bad arguments");
+    OCN_REQUIRE(mesh->evaluated, "mesh has no hydro evaluation");
+    OCN_REQUIRE(mesh->ctx == z->ctx && z->ctx == zones[0]->ctx, "meshes and zones must share one context");
+    check_mask_frame(&frames[q]);
+    MaskArgs A = mask_args(z, yaw[q], bx[q], bz[q], speed[q], &frames[q], &params[q]);
+    A.vw = &mesh->report.p->r.submerged_volume;
+    A.mesh_volume = mesh->volume;
+    B.j[q] = mask_job(z, A, mesh->loop_counts.p, 0, mesh->loop_off.p, mesh->loop_points.p,
+                      2 * mesh->nt + 2, 0);
+  }
+  mask_launch_batch(zones[0]->ctx, B);
+}
+
 }  // namespace ocn
 
 using namespace ocn;
@@ -531,40 +723,8 @@ int ocn_zone_update_stability(ocn_zone* z, double speed, double dt) {
 int ocn_zone_step(ocn_zone* z, double dt, double bx, double bz) {
   return api_call(z ? z->ctx : nullptr, [&] {
     OCN_REQUIRE(z, "null zone");
-    ocn_ctx* ctx = z->ctx;
-    DeviceScope ds(ctx);
-    const double mx = bx - z->pos_curr[0], mz = bz - z->pos_curr[1];
-    const double rx = mx / z->delta + z->carry[0];
-    const double rz = mz / z->delta + z->carry[1];
-    int wx = (int)std::floor(rx), wz = (int)std::floor(rz);
-    z->carry[0] = rx - wx;
-    z->carry[1] = rz - wz;
-    const int max_shift = z->margin - 1;
-    const size_t nn = (size_t)z->n * z->n;
-    if (std::abs(wx) > max_shift || std::abs(wz) > max_shift) {
-      wx = std::clamp(wx, -max_shift, max_shift);
-      wz = std::clamp(wz, -max_shift, max_shift);
-      OCN_CUDA(cudaMemsetAsync(z->curr(), 0, nn * sizeof(float), ctx->stream));
-      OCN_CUDA(cudaMemsetAsync(z->prev(), 0, nn * sizeof(float), ctx->stream));
-      ++z->dropped_wake;
-    }
-    const int ox = wx + z->last_shift[0], oz = wz + z->last_shift[1];
-    const double a = z->c * z->c * dt * dt / (z->delta * z->delta);
-    const int inext = 3 - z->icurr - z->iprev;
-    dim3 grid(((z->n + 3) / 4 + 255) / 256, z->n);
-    ProfWindow pw(ctx, OCN_PROF_FDM);
-    k_fdm_step<<<grid, 256, 0, ctx->stream>>>(z->n, z->margin, wx, wz, ox, oz, (float)a,
-                                              (float)z->damping, z->curr(), z->prev(),
-                                              z->buf[inext].p);
-    OCN_LAUNCHED(ctx);
-    z->iprev = z->icurr;
-    z->icurr = inext;
-    z->origin[0] += wx * z->delta;
-    z->origin[1] += wz * z->delta;
-    z->last_shift[0] = wx;
-    z->last_shift[1] = wz;
-    z->pos_curr[0] = bx;
-    z->pos_curr[1] = bz;
+    DeviceScope ds(z->ctx);
+    zones_step_batch(1, &z, dt, &bx, &bz);
   });
 }
 
@@ -653,11 +813,8 @@ int ocn_zone_mask_from_hydro_deferred(ocn_zone* z, ocn_mesh* mesh, double yaw, d
 int ocn_zone_apply_last_mask(ocn_zone* z) {
   return api_call(z ? z->ctx : nullptr, [&] {
     OCN_REQUIRE(z, "null zone");
-    ocn_ctx* ctx = z->ctx;
-    DeviceScope ds(ctx);
-    k_apply_box<<<ctx->sm_count * 2, 256, 0, ctx->stream>>>(z->mask_box.p, z->mask_f.p, z->mask_h.p,
-                                                           z->mask_f.n, z->n, z->margin, z->curr());
-    OCN_LAUNCHED(ctx);
+    DeviceScope ds(z->ctx);
+    zones_apply_last_mask_batch(1, &z);
   });
 }
 
