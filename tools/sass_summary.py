@@ -2,7 +2,7 @@
 needed): total instructions and the counts of the mnemonics that prove the
 Blackwell data paths (TMA: UTMALDG / UTMASTG / UBLKCP; mbarrier: SYNCS), the
 shared-memory exchange (LDS / STS), global traffic (LDG / STG) and FP32 / FP64
-arithmetic, written to profiles/sass_summary_<tag>.txt.
+arithmetic (scalar and packed fp32x2), written to profiles/sass_summary_<tag>.txt.
 
     python tools/sass_summary.py r02
 """
@@ -15,7 +15,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(ROOT, "paper_2503_03326_b200", "lib", "libocean_b200.so")
 KEYS = ["UTMALDG", "UTMASTG", "UBLKCP", "SYNCS", "LDS", "STS", "LDG", "STG", "BAR", "SHFL",
-        "FFMA", "FADD", "FMUL", "DFMA", "DADD", "DMUL", "MUFU"]
+        "FFMA", "FADD", "FMUL", "FFMA2", "FADD2", "FMUL2", "DFMA", "DADD", "DMUL", "MUFU"]
 
 
 def main(tag):
