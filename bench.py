@@ -701,6 +701,9 @@ def _config_line(args, cfgno, dist, rank, world, local, steps, warmup, peak, pea
     return line
 
 
+EXTRA_CONFIG_BUDGET_S = 300
+
+
 def run_ours(args):
     dist, rank, world, local = _dist()
     peak, peak_kind = _peaks()
@@ -710,15 +713,34 @@ def run_ours(args):
         import gc
         import torch
         extra = {}
+        if line is not None:
+            line["configs"] = extra
         for cfgno in (1, 4, 5):
             gc.collect()
             torch.cuda.empty_cache()
-            sub = _config_line(args, cfgno, dist, rank, world, local, min(args.steps, 10),
-                               args.warmup, peak, peak_kind, headline=False)
+            # the headline line must survive a failing or hung secondary config
+            # (e.g. a multi-rank exchange that never completes): each runs under
+            # a watchdog that prints what was measured so far and exits
+            done = threading.Event()
+
+            def watchdog(cfgno=cfgno, done=done):
+                if done.wait(EXTRA_CONFIG_BUDGET_S):
+                    return
+                if line is not None:
+                    extra[str(cfgno)] = {"unavailable": f"timed out after {EXTRA_CONFIG_BUDGET_S} s"}
+                    print(json.dumps(line), flush=True)
+                os._exit(0)
+
+            threading.Thread(target=watchdog, daemon=True).start()
+            try:
+                sub = _config_line(args, cfgno, dist, rank, world, local, min(args.steps, 10),
+                                   args.warmup, peak, peak_kind, headline=False)
+            except Exception as e:  # noqa: BLE001 -- reported in the line, headline kept
+                sub = {"unavailable": f"{type(e).__name__}: {str(e)[:300]}"}
+            finally:
+                done.set()
             if sub is not None:
                 extra[str(cfgno)] = sub
-        if line is not None:
-            line["configs"] = extra
     if line is not None:
         print(json.dumps(line), flush=True)
     if dist:
