@@ -40,6 +40,8 @@ struct ocn_slab {
   ocn::DevBuf<float2> tw128, w_hi, w_lo;  // four-step row pass (N = 16384): w_N^(128 h), w_N^l
   ocn::DevBuf<double> d_time;
   ocn::DevBuf<float> fields;     // [8][N][cols]
+  ocn::DevBuf<float2> ring;      // fused four-step columns: step A results, kFsRing column blocks
+  ocn::DevBuf<int> fs_sync;      // fused four-step columns: dispatch counter, per-block A / B counts
 };
 
 namespace ocn {
@@ -364,6 +366,147 @@ __global__ void __launch_bounds__(kFsB * kFsPC * kFsN2 / 32) k_slab_colsB(const 
   }
 }
 
+// ---------------------------------------------------------------- fused four-step columns
+// Steps A and B of the four-step column pass in ONE persistent kernel over a
+// work list ordered by 32-column block: the block's N1 / kFsB... A items (pairs
+// of i2, as k_slab_colsA) then its B items (pairs of k1, as k_slab_colsB). A
+// writes its results to a ring of kFsRing block slots instead of back into
+// `recv`; B reads them from there. A block's intermediate (N x 32 x 8 B, 4 MB at
+// N = 16384) is consumed while it is still in L2 and the ring slot is
+// overwritten before its lines are evicted: the column pass moves recv once and
+// the fields once instead of recv three times and the fields once.
+//   B items of block b wait until A_done[b] = nA (A never waits for B of its
+//   own block); A items of block b >= kFsRing wait, before writing, until
+//   B_done[b - kFsRing] = nB (that slot's readers are done). Items are taken
+//   in list order (one atomic per item), so every item waits only on items
+//   taken earlier: no deadlock whatever the residency.
+constexpr int kFsRing = 8;
+constexpr int kFsLag = 3;  // B items of a block run this many blocks after its A items
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void spin_until(const int* p, int target) {
+  while (ld_acquire(p) < target) __nanosleep(64);
+}
+
+template <int N>
+__global__ void __launch_bounds__(kFsB * kFsPC * kFsN2 / 32) k_slab_cols_fused(
+    const SlabColArgs a, const float2* __restrict__ recv, float2* ring, int* sync, int nblocks,
+    const float2* __restrict__ tw1, const float2* __restrict__ wn, const float2* __restrict__ tw2) {
+  constexpr int N1 = N / kFsN2, NT = kFsB * kFsPC;
+  constexpr int nA = kFsN2 / kFsB, nB = N1 / kFsB, PER = nA + nB;
+  static_assert(kFsB * kFsPC * N1 / 32 == kFsB * kFsPC * kFsN2 / 32 || N1 <= kFsN2,
+                "step A uses at most the CTA's threads");
+  constexpr int THREADS = kFsB * kFsPC * kFsN2 / 32;
+  constexpr int THREADS_A = kFsB * kFsPC * N1 / 32;
+  constexpr size_t SLOT = (size_t)N * kFsPC;  // float2 per ring slot
+  extern __shared__ float2 smem[];
+  __shared__ int s_item;
+  int* dispatch = sync;
+  int* a_done = sync + 1;
+  int* b_done = sync + 1 + nblocks;
+  const int ncb = a.cols / kFsPC;
+  // work list by step st: A items of block st, then B items of block st - kFsLag
+  // (B of a block is taken kFsLag blocks after its A items, which are then long
+  // done: no spinning on a block still being produced)
+  const int total = (nblocks + kFsLag) * PER;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(dispatch, 1);
+    __syncthreads();
+    const int item = s_item;
+    if (item >= total) return;
+    const int st = item / PER, r = item - st * PER;
+    const int blk = r < nA ? st : st - kFsLag;
+    if (blk < 0 || blk >= nblocks) {
+      __syncthreads();  // s_item is rewritten by the next iteration
+      continue;
+    }
+    const int p = a.p0 + blk / ncb, kc0 = (blk % ncb) * kFsPC;
+    float2* slot = ring + (size_t)(blk % kFsRing) * SLOT;
+    if (r < nA) {
+      // ---- step A (k_slab_colsA): i2 = 2 r, 2 r + 1
+      using PL = fft::Plan<N1>;
+      constexpr int T = PL::T, TPW = 32 / T, S = kFsStride<PL::SMEM>;
+      constexpr int STEP = THREADS_A / NT;
+      const int i20 = r * kFsB;
+      if (threadIdx.x < THREADS_A) {
+        const int c = threadIdx.x % kFsPC, i2l = (threadIdx.x / kFsPC) % kFsB, i10 = threadIdx.x / NT;
+        float2* lane_sm = smem + (i2l * kFsPC + c) * S;
+#pragma unroll 8
+        for (int i1 = i10; i1 < N1; i1 += STEP)
+          lane_sm[fft::pad32(i1)] = __ldg(recv + recv_index(a, p, kFsN2 * i1 + i20 + i2l, kc0 + c));
+      }
+      __syncthreads();
+      if (threadIdx.x < THREADS_A) {
+        const int tr = warp * TPW + lane / T, t = lane % T;
+        float2* buf = smem + tr * S;
+        const int i2 = i20 + tr / kFsPC;
+        fft::cta_fft<N1, true, true, true>(
+            t, buf, tw1, [&](int n) { return buf[fft::pad32(n)]; },
+            [&](int k1, float2 x) { buf[fft::pad32(k1)] = fft::cmul(x, __ldg(wn + i2 * k1)); });
+      }
+      if (blk >= kFsRing && threadIdx.x == 0) spin_until(b_done + blk - kFsRing, nB);
+      __syncthreads();
+      if (threadIdx.x < THREADS_A) {
+        const int c = threadIdx.x % kFsPC, i2l = (threadIdx.x / kFsPC) % kFsB, i10 = threadIdx.x / NT;
+        const float2* lane_sm = smem + (i2l * kFsPC + c) * S;
+#pragma unroll 8
+        for (int k1 = i10; k1 < N1; k1 += STEP)
+          __stcg(slot + (size_t)(kFsN2 * k1 + i20 + i2l) * kFsPC + c, lane_sm[fft::pad32(k1)]);
+      }
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) atomicAdd(a_done + blk, 1);
+    } else {
+      // ---- step B (k_slab_colsB): k1 = 2 (r - nA), + 1
+      using PL = fft::Plan<kFsN2>;
+      constexpr int T = PL::T, TPW = 32 / T, S = kFsStride<PL::SMEM>;
+      constexpr int STEP = THREADS / NT;
+      const int k10 = (r - nA) * kFsB;
+      const int c = threadIdx.x % kFsPC, k1l = (threadIdx.x / kFsPC) % kFsB, i20 = threadIdx.x / NT;
+      float2* lane_sm = smem + (k1l * kFsPC + c) * S;
+      if (threadIdx.x == 0) spin_until(a_done + blk, nA);
+      __syncthreads();
+      const float2* lane_src = slot + (size_t)(kFsN2 * (k10 + k1l)) * kFsPC + c;
+#pragma unroll 8
+      for (int i2 = i20; i2 < kFsN2; i2 += STEP)
+        lane_sm[fft::pad32(i2)] = __ldcg(lane_src + (size_t)i2 * kFsPC);
+      __syncthreads();
+      if (threadIdx.x == 0) atomicAdd(b_done + blk, 1);  // the slot's reads of this item are done
+      const int tr = warp * TPW + lane / T, t = lane % T;
+      float2* buf = smem + tr * S;
+      fft::cta_fft<kFsN2, true, true, true>(
+          t, buf, tw2, [&](int n) { return buf[fft::pad32(n)]; },
+          [&](int k2, float2 x) { buf[fft::pad32(k2)] = x; });
+      __syncthreads();
+      float* re = a.fields + (size_t)(2 * p) * N * a.cols;
+      float* im = a.fields + (size_t)(2 * p + 1) * N * a.cols;
+      const int kc = kc0 + c;
+#pragma unroll 8
+      for (int k2 = i20; k2 < kFsN2; k2 += STEP) {
+        const int k = k10 + k1l + N1 * k2;
+        const float2 x = lane_sm[fft::pad32(k2)];
+        const float sg = ((k + a.col0 + kc) & 1) ? -1.f : 1.f;  // fft.cpp:73-75
+        __stcs(re + (size_t)k * a.cols + kc, sg * x.x);          // fft.cpp:93-99
+        __stcs(im + (size_t)k * a.cols + kc, sg * x.y);
+      }
+    }
+    __syncthreads();  // shared memory is reused by the next item
+  }
+}
+
+static bool fused_cols_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("OCN_SLAB_NO_FUSED_COLS");
+    return !(e && *e && *e != '0');
+  }();
+  return on;
+}
+
 template <int N>
 bool slab_fourstep(ocn_slab* sl, const SlabColArgs& a, float2* recv, int np) {
   if constexpr (N >= 4096) {
@@ -373,6 +516,23 @@ bool slab_fourstep(ocn_slab* sl, const SlabColArgs& a, float2* recv, int np) {
     const size_t smemB = (size_t)kFsB * kFsPC * kFsStride<fft::Plan<kFsN2>::SMEM> * sizeof(float2);
     smem_opt_in(k_slab_colsA<N>, smemA);
     smem_opt_in(k_slab_colsB<N>, smemB);
+    if (fused_cols_enabled() && N1 <= kFsN2) {
+      const int nblocks = np * (a.cols / kFsPC);
+      sl->ring.ensure((size_t)kFsRing * N * kFsPC);
+      sl->fs_sync.ensure(1 + 2 * (size_t)nblocks);
+      OCN_CUDA(cudaMemsetAsync(sl->fs_sync.p, 0, (1 + 2 * (size_t)nblocks) * sizeof(int),
+                               sl->ctx->stream));
+      const size_t smemF = std::max(smemA, smemB);
+      smem_opt_in(k_slab_cols_fused<N>, smemF);
+      int per_sm = 0;
+      OCN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &per_sm, k_slab_cols_fused<N>, kFsB * kFsPC * kFsN2 / 32, smemF));
+      const int grid = std::max(1, per_sm) * sl->ctx->sm_count;
+      k_slab_cols_fused<N><<<grid, kFsB * kFsPC * kFsN2 / 32, smemF, sl->ctx->stream>>>(
+          a, recv, sl->ring.p, sl->fs_sync.p, nblocks, sl->tw1.p, sl->wn.p, sl->tw2.p);
+      OCN_LAUNCHED(sl->ctx);
+      return true;
+    }
     const dim3 ga(a.cols / kFsPC, kFsN2 / kFsB, np), gb(a.cols / kFsPC, N1 / kFsB, np);
     k_slab_colsA<N><<<ga, kFsB * kFsPC * N1 / 32, smemA, sl->ctx->stream>>>(a, recv, sl->tw1.p, sl->wn.p);
     OCN_LAUNCHED(sl->ctx);
