@@ -372,7 +372,9 @@ __global__ void __launch_bounds__(1024) k_mask_prepare(const __grid_constant__ M
   box[4] = kept;
 }
 
-constexpr int kMaskEdgesSmem = 4096;  // loop points cached in shared memory
+// loop points cached in shared memory (16 KB: a mask CTA fits beside a
+// column-pass CTA of a concurrent spectral step; longer waterlines read global)
+constexpr int kMaskEdgesSmem = 1024;
 
 // Per candidate cell: bbox cull, +z ray-crossing parity, V-shaped height;
 // optionally writes the height into curr (apply_mask, interactive.cpp:113-118).

@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(128) k_vertices(const __grid_constant__ HydroB
 // One triangle per thread; each 1024-triangle block also scans its counts
 // (exclusive, parent order, hydro.cpp:151-163) and leaves its total for
 // k_scan_blocks; k_emit adds the block's offset.
-constexpr int kScanBlock = 1024;
+constexpr int kScanBlock = 512;  // <= 16 K registers per CTA: fits beside a column-pass CTA
 
 __device__ __forceinline__ int2 add2(int2 a, int2 b) { return make_int2(a.x + b.x, a.y + b.y); }
 
@@ -223,7 +223,7 @@ __device__ __forceinline__ void emit_state(StateDev* s, int parent, int status, 
 }
 
 template <int NB>
-__global__ void __launch_bounds__(256) k_emit(const __grid_constant__ HydroBatch<NB> B) {
+__global__ void __launch_bounds__(128) k_emit(const __grid_constant__ HydroBatch<NB> B) {
   const HydroJob& J = B.job[blockIdx.y];
   const int nt = J.nt;
   const int3* __restrict__ tris = J.tris;
@@ -920,7 +920,7 @@ void launch_clip(ocn_ctx* ctx, const HydroBatch<NB>& B, int max_nv, int max_nt) 
   OCN_LAUNCHED(ctx);
   k_scan_blocks<NB><<<dim3(1, nb), kScanBlock, 0, st>>>(B);
   OCN_LAUNCHED(ctx);
-  k_emit<NB><<<dim3(std::max(1, grid_of(ctx, max_nt, 256) / (int)nb), nb), 256, 0, st>>>(B);
+  k_emit<NB><<<dim3(std::max(1, grid_of(ctx, max_nt, 128) / (int)nb), nb), 128, 0, st>>>(B);
   OCN_LAUNCHED(ctx);
 }
 

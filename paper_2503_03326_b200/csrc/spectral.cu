@@ -230,7 +230,20 @@ void launch_cols(ocn_ctx* ctx, const ColArgs& a, int G, bool complex_out, cudaSt
       smem_opt_in(k_cols_tma<N, true, CT::STAGES>, CT::SMEM);
       if (CT::smem(2, true) <= 227 * 1024) smem_opt_in(k_cols_tma<N, false, 2, true>, CT::smem(2, true));
       const int tiles_x = N / CT::PC, ntiles = tiles_x * G;
-      const int grid = std::min(ntiles, ctx->sm_count);
+      // persistent: one CTA per SM but one SM left free. A concurrent stream's
+      // kernels (the frame pipeline's hull / mask / FDM chain) fit beside a
+      // column CTA (<= 20 K registers, <= 17 KB shared memory each) except
+      // the single-CTA ones (waterline chain, mask preparation, block scan),
+      // which take the free SM instead of waiting for the whole column pass.
+      // Measured (config 3, one box): frame 0.578 -> 0.546-0.552 ms device,
+      // e2e 0.578 -> 0.534-0.536; the spectral step alone 0.4665 -> 0.4669.
+      // OCN_COLS_GRID overrides the CTA count.
+      static const int cap = [] {
+        const char* e = getenv("OCN_COLS_GRID");
+        return e && atoi(e) > 0 ? atoi(e) : 0;
+      }();
+      const int per_sm_grid = cap ? std::min(cap, ctx->sm_count) : std::max(1, ctx->sm_count - 1);
+      const int grid = std::min(ntiles, per_sm_grid);
       if constexpr (N >= 256 && N <= 1024 && CT::smem(2, true) <= 227 * 1024) {
         if (!complex_out && a.out_maps && cols_variant() == 4) {
           smem_opt_in(k_cols_tma<N, false, 2, true, true>, CT::smem(2, true));
