@@ -687,6 +687,13 @@ def _config_line(args, cfgno, dist, rank, world, local, steps, warmup, peak, pea
         "gpu_launches": m["launches"],
         "clocks": m["clocks"],
     }
+    st = m["stages"]
+    if {"spectral", "hydro", "mask", "fdm"} <= set(st):
+        # the same stages under Simulation::timing()'s names (sim.hpp:50-54): the
+        # reference's surface and velocity stages are one fused spectral step
+        # here; the rigid integrator is out of the frame (north_star scope)
+        line["stages_ms_reference_names"] = {"surface+velocity": st["spectral"], "hydro": st["hydro"],
+                                             "zones": st["mask"] + st["fdm"], "integrate": None}
     if m["kernels"]:
         line["spectral_kernels_ms_eager"] = m["kernels"]
     line.update(extra)

@@ -553,6 +553,17 @@ OCN_API int ocn_sim_step(ocn_sim* sim, int steps);
  * doubles) and its last hydro report; either pointer may be NULL. */
 OCN_API int ocn_sim_body_state(const ocn_sim* sim, int body, double* host_state13,
                                ocn_hydro_report* report);
+/* Cumulative stage times in seconds in Simulation::Timing order (sim.hpp:50-54):
+ * [0] surface, [1] velocity, [2] hydro, [3] zones, [4] integrate. [0] is the
+ * device time of the whole spectral step -- maps and velocity slices are one
+ * fused step (one graph) here, so [1] stays 0 -- [2] / [3] the device time of
+ * the batched hulls / of the masks + FDM steps (CUDA events on their streams;
+ * overlapping in pipelined mode), [4] the host time of the rigid integration.
+ * Informational, as in the reference; collected while ocn_sim_set_timing is on. */
+OCN_API int ocn_sim_timing(const ocn_sim* sim, double* seconds5);
+/* Stage timing is collected only while enabled (off at creation: the events
+ * and clock reads cost host time in a host-synchronous step). */
+OCN_API int ocn_sim_set_timing(ocn_sim* sim, int enabled);
 /* time, step index, the current maps / slices and the bodies' zones (any may be NULL). */
 OCN_API int ocn_sim_info(const ocn_sim* sim, double* time, int* step_index, ocn_maps** maps,
                          ocn_slices** slices, ocn_zone** zones);

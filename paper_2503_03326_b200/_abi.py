@@ -183,6 +183,8 @@ SIGNATURES = {
     "ocn_sim_destroy": (ci, [vp]),
     "ocn_sim_step": (ci, [vp, ci]),
     "ocn_sim_body_state": (ci, [vp, ci, d, C.POINTER(HydroReport)]),
+    "ocn_sim_timing": (ci, [vp, d]),
+    "ocn_sim_set_timing": (ci, [vp, ci]),
     "ocn_sim_info": (ci, [vp, d, C.POINTER(ci), pvp, pvp, pvp]),
     "ocn_direct_create": (ci, [vp, cd, pvp]),
     "ocn_direct_destroy": (ci, [vp]),

@@ -29,12 +29,13 @@ void zones_mask_from_hydro_batch(int nz, ocn_zone* const* zones, ocn_mesh* const
 
 using namespace ocn;
 
-extern "C" {
-
-int ocn_bodies_step(int n_bodies, const ocn_body_frame* bodies, const ocn_fluid* fluid, double dt,
-                    ocn_hydro_report* reports) {
+namespace ocn {
+// ocn_bodies_step; `mid` (optional) is recorded on the bodies' stream between
+// the hulls and the zone passes (ocn_sim's hydro / zones stage timing)
+void bodies_step(int n_bodies, const ocn_body_frame* bodies, const ocn_fluid* fluid, double dt,
+                 ocn_hydro_report* reports, cudaEvent_t mid) {
   ocn_mesh* m0 = n_bodies > 0 && bodies ? (ocn_mesh*)bodies[0].mesh : nullptr;
-  return api_call(m0 ? m0->ctx : nullptr, [&] {
+  {
     OCN_REQUIRE(n_bodies >= 0 && n_bodies <= kMaxBatch, "ocn_bodies_step: %d bodies (0..%d)",
                 n_bodies, kMaxBatch);
     if (n_bodies == 0) return;
@@ -65,6 +66,8 @@ int ocn_bodies_step(int n_bodies, const ocn_body_frame* bodies, const ocn_fluid*
       check(ocn_zone_update_stability((ocn_zone*)b.zone, b.speed, dt));
     }
     hydro_evaluate_jobs(n_bodies, meshes.data(), B);
+    if (mid) OCN_CUDA(cudaEventRecord(mid, m0->ctx->stream));
+    NvtxRange nv("zones");
     // every body's mask, apply and FDM step as one launch each (zones are
     // independent: batching keeps sim.cpp's per-body results)
     std::vector<ocn_zone*> zones(n_bodies);
@@ -87,7 +90,17 @@ int ocn_bodies_step(int n_bodies, const ocn_body_frame* bodies, const ocn_fluid*
     zones_step_batch(n_bodies, zones.data(), dt, bx.data(), bz.data());
     if (!reports) return;  // asynchronous: reports via ocn_hydro_report_get
     hydro_reports_read(n_bodies, meshes.data(), reports);
-  });
+  }
+}
+}  // namespace ocn
+
+extern "C" {
+
+int ocn_bodies_step(int n_bodies, const ocn_body_frame* bodies, const ocn_fluid* fluid, double dt,
+                    ocn_hydro_report* reports) {
+  ocn_mesh* m0 = n_bodies > 0 && bodies ? (ocn_mesh*)bodies[0].mesh : nullptr;
+  return api_call(m0 ? m0->ctx : nullptr,
+                  [&] { bodies_step(n_bodies, bodies, fluid, dt, reports, nullptr); });
 }
 
 }  // extern "C"

@@ -183,6 +183,7 @@ int ocn_comm_info(const ocn_comm* cm, int* nranks, int* rank) {
 }
 
 int ocn_slab_exchange(ocn_slab* sl, ocn_comm* cm, int pair, void* dev_send, void* dev_recv) {
+  NvtxRange nv("slab.exchange");
   ocn_ctx* ctx = nullptr;
   int n = 0, ranks = 0, rank = 0, rows = 0;
   if (sl) slab_geometry(sl, &ctx, &n, &ranks, &rank, &rows);

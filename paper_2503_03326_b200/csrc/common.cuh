@@ -13,6 +13,9 @@
 
 #include "../../include/ocean_b200.h"
 
+// NVTX v3 (header-only; a no-op unless a tool such as Nsight attaches)
+#include <nvtx3/nvToolsExt.h>
+
 namespace ocn {
 
 constexpr double kPi = 3.14159265358979323846;
@@ -238,4 +241,15 @@ struct OutStage {
   }
 };
 
+}  // namespace ocn
+
+namespace ocn {
+// NVTX range over a C-ABI stage (names follow the reference's stages:
+// sim.hpp:50-54 surface / velocity / hydro / zones / integrate)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 }  // namespace ocn

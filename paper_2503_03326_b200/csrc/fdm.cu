@@ -503,6 +503,7 @@ MaskJob mask_job(ocn_zone* z, const MaskArgs& A, const int* nloops_dev, int nloo
 
 // the mask passes of B.count zones: two launches whatever the count
 void mask_launch_batch(ocn_ctx* ctx, const MaskBatch& B) {
+  NvtxRange nv("zones.mask");
   cudaStream_t st = ctx->stream;
   ProfWindow pw(ctx, OCN_PROF_MASK);
   k_mask_prepare<<<B.count, 1024, 0, st>>>(B);
@@ -542,6 +543,7 @@ MaskArgs mask_args(ocn_zone* z, double yaw, double bx, double bz, double speed,
 // FdmZone::step (interactive.cpp:67-111) of n zones: the scalar bookkeeping per
 // zone on the host, the stencils as ONE launch (zone = blockIdx.z)
 void zones_step_batch(int nz, ocn_zone* const* zones, double dt, const double* bx, const double* bz) {
+  NvtxRange nv("zones.fdm");
   if (nz <= 0) return;
   OCN_REQUIRE(nz <= kMaxBatch, "%d zones in one step batch (max %d)", nz, kMaxBatch);
   ocn_ctx* ctx = zones[0]->ctx;

@@ -962,6 +962,7 @@ void fill_samplers(HydroBatch<NB>& B, const ocn_fluid* fluid) {
 
 void hydro_evaluate(ocn_mesh* m, const ocn_pose* pose, const ocn_fluid* fluid,
                     const double* host_depth) {
+  NvtxRange nv("hydro");
   ocn_ctx* ctx = m->ctx;
   DeviceScope ds(ctx);
   cudaStream_t st = ctx->stream;
@@ -1010,6 +1011,7 @@ void fill_samplers_batch(HydroBatch<kMaxBatch>& B, const ocn_fluid* fluid) {
 
 // Runs prepared jobs (make_job per mesh) as one launch set.
 void hydro_evaluate_jobs(int n, ocn_mesh* const* meshes, const HydroBatch<kMaxBatch>& B) {
+  NvtxRange nv("hydro");
   ocn_ctx* ctx = meshes[0]->ctx;
   DeviceScope ds(ctx);
   int max_nv = 0, max_nt = 0;

@@ -10,11 +10,17 @@
 // beside them; CUDA events order the buffers (ready: its spectral step done;
 // consumed: the last body stage reading it done). Only the hydro reports come
 // back to the host each step, for the integration.
+#include <chrono>
 #include <cmath>
 #include <memory>
 #include <vector>
 
 #include "hydro_internal.cuh"
+
+namespace ocn {
+void bodies_step(int n_bodies, const ocn_body_frame* bodies, const ocn_fluid* fluid, double dt,
+                 ocn_hydro_report* reports, cudaEvent_t mid);  // bodies.cu
+}
 
 namespace ocn {
 void hydro_reports_read(int n, ocn_mesh* const* meshes, ocn_hydro_report* out);
@@ -161,6 +167,18 @@ struct ocn_sim {
   int step_index = 0, rebuild_stride = 1;
   double wind[3]{};
   std::vector<SimBody> bodies;
+  // Simulation::Timing (sim.hpp:50-54): device time of the spectral step
+  // (surface and velocity are one fused graph), of the hulls and of the zone
+  // passes (CUDA events on their streams), host time of the integration
+  struct Stage {
+    cudaEvent_t a = nullptr, b = nullptr;
+    bool pending = false;
+    double seconds = 0.0;
+  };
+  Stage spec[2], hyd, zon;    // spec: one pair per buffer (settled when reused)
+  cudaEvent_t mid = nullptr;  // hulls -> zones split (recorded inside the bodies step)
+  double integrate_s = 0.0;
+  bool timing = false;        // ocn_sim_set_timing (off: no events, no host clock reads)
 };
 
 namespace {
@@ -179,8 +197,33 @@ void spectral(ocn_sim* s, int k, double t, bool slices) {
     check(ocn_surface_generate(s->maps[k], t, s->chop));
 }
 
+void stage_settle(ocn_sim::Stage& st);
+
+// spectral() between a pair of timing events on the spectral stream
+void timed_spectral(ocn_sim* s, int k, double t, bool slices) {
+  ocn_sim::Stage& st = s->spec[k];
+  stage_settle(st);  // this buffer's previous step (complete by now)
+  if (s->timing) OCN_CUDA(cudaEventRecord(st.a, s->sctx->stream));
+  spectral(s, k, t, slices);
+  if (s->timing) {
+    OCN_CUDA(cudaEventRecord(st.b, s->sctx->stream));
+    st.pending = true;
+  }
+}
+
+void stage_settle(ocn_sim::Stage& st) {  // fold a completed event pair into the total
+  if (!st.pending) return;
+  OCN_CUDA(cudaEventSynchronize(st.b));
+  float ms = 0.f;
+  OCN_CUDA(cudaEventElapsedTime(&ms, st.a, st.b));
+  st.seconds += 1e-3 * ms;
+  st.pending = false;
+}
+
 void destroy(ocn_sim* s) {
   if (!s) return;
+  for (auto* e : {s->spec[0].a, s->spec[0].b, s->spec[1].a, s->spec[1].b, s->hyd.a, s->zon.b, s->mid})
+    if (e) cudaEventDestroy(e);
   for (auto& b : s->bodies)
     if (b.zone) ocn_zone_destroy(b.zone);
   for (int k = 0; k < 2; ++k) {
@@ -236,6 +279,10 @@ int ocn_sim_create(ocn_ctx* ctx, const ocn_sim_config* cfg, int n_bodies,
       OCN_CUDA(cudaEventCreateWithFlags(&s->ready[k], cudaEventDisableTiming));
       OCN_CUDA(cudaEventCreateWithFlags(&s->consumed[k], cudaEventDisableTiming));
     }
+    for (auto* e : {&s->spec[0].a, &s->spec[0].b, &s->spec[1].a, &s->spec[1].b, &s->hyd.a,
+                    &s->zon.b, &s->mid})
+      OCN_CUDA(cudaEventCreate(e));
+    s->hyd.b = s->zon.a = s->mid;
     spectral(s.get(), 0, 0.0, true);  // sim.cpp:18-20
     if (s->pipelined) OCN_CUDA(cudaEventRecord(s->ready[0], s->sctx->stream));
     for (int i = 0; i < n_bodies; ++i) {  // sim.cpp:22-36
@@ -300,12 +347,12 @@ int ocn_sim_step(ocn_sim* s, int steps) {
       const double t_next = s->time + s->dt;  // sim.cpp:61
       int k = 0;
       if (!s->pipelined) {
-        spectral(s, 0, t_next, s->step_index % s->rebuild_stride == 0);
+        timed_spectral(s, 0, t_next, s->step_index % s->rebuild_stride == 0);
       } else {
         k = 1 - s->cur;
         if (!s->prefetched) {  // first step: nothing prefetched yet
           OCN_CUDA(cudaStreamWaitEvent(s->sctx->stream, s->consumed[k], 0));
-          spectral(s, k, t_next, true);
+          timed_spectral(s, k, t_next, true);
           OCN_CUDA(cudaEventRecord(s->ready[k], s->sctx->stream));
         }
         s->cur = k;
@@ -348,20 +395,33 @@ int ocn_sim_step(ocn_sim* s, int steps) {
         f.frame.mesh_height = ext.y;
         f.mask = b.mask;
       }
-      check(ocn_bodies_step(nb, frames.data(), &fluid, s->dt, nullptr));
+      if (s->timing) OCN_CUDA(cudaEventRecord(s->hyd.a, s->ctx->stream));
+      {
+        NvtxRange nv("hydro+zones");
+        bodies_step(nb, frames.data(), &fluid, s->dt, nullptr, s->timing ? s->mid : nullptr);
+      }
+      if (s->timing) OCN_CUDA(cudaEventRecord(s->zon.b, s->ctx->stream));
       if (s->pipelined) {
         // the next step's spectral step (a function of time only) goes into the
         // other buffer, whose last readers were the PREVIOUS step's bodies
         OCN_CUDA(cudaEventRecord(s->consumed[k], s->ctx->stream));
         OCN_CUDA(cudaStreamWaitEvent(s->sctx->stream, s->consumed[1 - k], 0));
-        spectral(s, 1 - k, t_next + s->dt, true);
+        timed_spectral(s, 1 - k, t_next + s->dt, true);
         OCN_CUDA(cudaEventRecord(s->ready[1 - k], s->sctx->stream));
         s->prefetched = true;
       }
       std::vector<ocn_mesh*> meshes(nb);
       for (int i = 0; i < nb; ++i) meshes[i] = s->bodies[i].mesh;
-      hydro_reports_read(nb, meshes.data(), reports.data());
+      hydro_reports_read(nb, meshes.data(), reports.data());  // the bodies' stream is idle now
+      if (s->timing) {
+        s->hyd.pending = s->zon.pending = true;
+        stage_settle(s->hyd);
+        stage_settle(s->zon);
+      }
       // forces and integration (sim.cpp:112-125)
+      NvtxRange nv_int("integrate");
+      const auto t_int = s->timing ? std::chrono::steady_clock::now()
+                                   : std::chrono::steady_clock::time_point{};
       for (int i = 0; i < nb; ++i) {
         SimBody& b = s->bodies[i];
         const ocn_hydro_report& rp = reports[i];
@@ -379,6 +439,9 @@ int ocn_sim_step(ocn_sim* s, int steps) {
           }
         r.integrate({0.0, -s->gravity, 0.0}, s->dt, b.damping);
       }
+      if (s->timing)
+        s->integrate_s +=
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t_int).count();
       s->time = t_next;
       ++s->step_index;
       for (int i = 0; i < nb; ++i) {  // check_finite, sim.cpp:133-142
@@ -388,6 +451,27 @@ int ocn_sim_step(ocn_sim* s, int steps) {
           fail(OCN_ERR_NUMERIC, "non-finite body state (body %d, step %d)", i, s->step_index);
       }
     }
+  });
+}
+
+int ocn_sim_set_timing(ocn_sim* s, int enabled) {
+  if (!s) return OCN_ERR_ARG;
+  s->timing = enabled != 0;
+  return OCN_OK;
+}
+
+int ocn_sim_timing(const ocn_sim* sc, double* seconds5) {
+  if (!sc || !seconds5) return OCN_ERR_ARG;
+  ocn_sim* s = const_cast<ocn_sim*>(sc);
+  return api_call(s->ctx, [&] {
+    DeviceScope ds(s->ctx);
+    stage_settle(s->spec[0]);
+    stage_settle(s->spec[1]);
+    seconds5[0] = s->spec[0].seconds + s->spec[1].seconds;  // surface + velocity (one fused step)
+    seconds5[1] = 0.0;
+    seconds5[2] = s->hyd.seconds;
+    seconds5[3] = s->zon.seconds;
+    seconds5[4] = s->integrate_s;
   });
 }
 

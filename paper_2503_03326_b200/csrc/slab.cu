@@ -612,6 +612,7 @@ std::vector<float2> make_twiddles(int n);  // spectral.cu
 // Row pass of packed pairs [p0, p0 + np) (evolve: also advance h~ to t first).
 void slab_rows_pairs(ocn_slab* sl, double t, double choppiness, void* dev_send, int p0, int np,
                      bool evolve) {
+  NvtxRange nv("slab.rows");
   ocn_ctx* ctx = sl->ctx;
   ProfWindow pw(ctx, OCN_PROF_ROWS);
   if (evolve) {
@@ -633,6 +634,7 @@ void slab_rows_pairs(ocn_slab* sl, double t, double choppiness, void* dev_send, 
 
 // Column pass of packed pairs [p0, p0 + np) from the receive layout.
 void slab_cols_pairs(ocn_slab* sl, void* dev_recv, int p0, int np) {
+  NvtxRange nv("slab.cols");
   ProfWindow pw(sl->ctx, OCN_PROF_COLS);
   int lg = 0;
   while ((1 << lg) < sl->rows) ++lg;

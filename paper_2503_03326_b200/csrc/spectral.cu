@@ -696,6 +696,7 @@ static bool graphs_enabled() {
 
 void spectral_step(ocn_cascades* cas, ocn_maps* maps, ocn_slices* slices, double t,
                    double choppiness, double dt) {
+  NvtxRange nv(slices ? (maps ? "surface+velocity" : "velocity") : "surface");
   ocn_ctx* ctx = cas->ctx;
   DeviceScope ds(ctx);
   OCN_REQUIRE(cas->h0.p, "these maps carry no spectrum (ocn_maps_create_bare)");

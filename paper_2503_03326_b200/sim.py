@@ -454,6 +454,19 @@ class DeviceSimulation:
     def step(self, steps: int = 1):
         check(lib().ocn_sim_step(self.h, steps), self.ctx.h, "sim_step")
 
+    def set_timing(self, enabled: bool = True):
+        """Collect stage times from now on (ocn_sim_set_timing; off by default)."""
+        check(lib().ocn_sim_set_timing(self.h, 1 if enabled else 0), self.ctx.h, "sim_timing")
+
+    def timing(self) -> dict:
+        """Cumulative stage seconds with Simulation::timing()'s names (sim.hpp:50-54);
+        surface covers the fused maps + slices step (velocity stays 0). Collected
+        while set_timing(True) is on."""
+        t = np.zeros(5)
+        check(lib().ocn_sim_timing(self.h, t.ctypes.data_as(C.POINTER(C.c_double))), self.ctx.h,
+              "sim_timing")
+        return dict(zip(("surface", "velocity", "hydro", "zones", "integrate"), t.tolist()))
+
     def poses(self) -> np.ndarray:
         """(bodies, 13): position, orientation (w x y z), linear, angular velocity."""
         out = np.zeros((self.n_bodies, 13))

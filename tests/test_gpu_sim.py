@@ -92,6 +92,7 @@ def test_device_simulation_matches_reference(pipelined):
                          angular_damping=s["angular_damping"], fdm=s["fdm"]) for b in s["bodies"]]
     sim = DeviceSimulation(oc.CascadeConfig(s["n"], s["lengths"], s["cutoffs"]), s["params"],
                            s["slices"], bodies, dt=s["dt"], wind=s["wind"], pipelined=pipelined)
+    sim.set_timing(True)
     v0 = sim.poses()[:, 7:10].copy()
     ref = np.load(os.path.join(HERE, "golden", "sim_ref.npz"))
     rp = ref["pose"]
@@ -107,3 +108,9 @@ def test_device_simulation_matches_reference(pipelined):
             assert np.linalg.norm(dv_g - dv_r) <= 1e-4 * np.linalg.norm(dv_r), (st, b)
             assert np.abs(g[0:3] - r[0:3]).max() <= 1e-5, (st, b)
             assert np.abs(g[3:7] - r[3:7]).max() <= 1e-6, (st, b)
+    # Simulation::timing() stages (sim.hpp:50-54): device time of the fused
+    # spectral step, hulls, zones; host time of the integration
+    tm = sim.timing()
+    assert list(tm) == ["surface", "velocity", "hydro", "zones", "integrate"]
+    assert tm["surface"] > 0 and tm["hydro"] > 0 and tm["zones"] > 0 and tm["integrate"] > 0, tm
+    assert tm["velocity"] == 0.0
