@@ -130,6 +130,7 @@ struct ocn_ctx {
   std::atomic<int> refs{1};  // owner + every handle created on it (freed at zero)
   int sm_count = 148;
   cudaStream_t stream = nullptr;
+  int priority = 0;  // ocn_ctx_create_priority: -1 low (work beside a higher-priority stream), 0, 1
   std::string last_error;
   std::atomic<uint64_t> launches{0};
   ocn::PinnedBuf pinned;

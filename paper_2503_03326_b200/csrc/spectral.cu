@@ -230,8 +230,9 @@ void launch_cols(ocn_ctx* ctx, const ColArgs& a, int G, bool complex_out, cudaSt
       smem_opt_in(k_cols_tma<N, true, CT::STAGES>, CT::SMEM);
       if (CT::smem(2, true) <= 227 * 1024) smem_opt_in(k_cols_tma<N, false, 2, true>, CT::smem(2, true));
       const int tiles_x = N / CT::PC, ntiles = tiles_x * G;
-      // persistent: one CTA per SM but one SM left free. A concurrent stream's
-      // kernels (the frame pipeline's hull / mask / FDM chain) fit beside a
+      // persistent: one CTA per SM; on a low-priority context (the spectral
+      // side of a frame pipeline) one SM is left free. The concurrent
+      // high-priority stream's kernels (hull / mask / FDM chain) fit beside a
       // column CTA (<= 20 K registers, <= 17 KB shared memory each) except
       // the single-CTA ones (waterline chain, mask preparation, block scan),
       // which take the free SM instead of waiting for the whole column pass.
@@ -242,7 +243,8 @@ void launch_cols(ocn_ctx* ctx, const ColArgs& a, int G, bool complex_out, cudaSt
         const char* e = getenv("OCN_COLS_GRID");
         return e && atoi(e) > 0 ? atoi(e) : 0;
       }();
-      const int per_sm_grid = cap ? std::min(cap, ctx->sm_count) : std::max(1, ctx->sm_count - 1);
+      const int per_sm_grid = cap ? std::min(cap, ctx->sm_count)
+                                  : std::max(1, ctx->sm_count - (ctx->priority < 0 ? 1 : 0));
       const int grid = std::min(ntiles, per_sm_grid);
       if constexpr (N >= 256 && N <= 1024 && CT::smem(2, true) <= 227 * 1024) {
         if (!complex_out && a.out_maps && cols_variant() == 4) {
@@ -801,6 +803,7 @@ int ocn_ctx_create_priority(int device, int priority, ocn_ctx** out) {
     int lo = 0, hi = 0;  // CUDA: lower numbers are higher priorities
     OCN_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     const int prio = priority > 0 ? hi : (priority < 0 ? lo : 0);
+    ctx->priority = priority;
     OCN_CUDA(cudaStreamCreateWithPriority(&ctx->stream, cudaStreamNonBlocking, prio));
     *out = ctx.release();
   });
