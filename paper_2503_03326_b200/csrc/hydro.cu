@@ -67,6 +67,12 @@ __global__ void __launch_bounds__(128) k_vertices(const __grid_constant__ HydroB
   const double* override_depth = J.override_depth;
   double* wpos = J.wpos;
   double* depth = J.depth;
+  {  // the evaluation's resets (read only by later kernels): flags, waterline hash table
+    const int i0 = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+    if (i0 < 4) J.flags[i0] = 0;
+    for (int i = i0; i < J.hcap; i += stride) J.hkeys[i] = 0ull;
+    for (int i = i0; i < 3 * J.hcap; i += stride) J.hvals[i] = 0;
+  }
   const int lane = threadIdx.x & 31, q = lane & 3;
   const int per_warp = 8;  // vertices per warp pass
   const int warp_g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -644,7 +650,11 @@ __global__ void __launch_bounds__(kChainThreads) k_chain(const __grid_constant__
       for (int e = tid; e < nodes; e += blockDim.x) sm_chain[e] = partner_g[e];
     for (int q = tid; q < nseg; q += blockDim.x) used[q] = 0;
     __syncthreads();
-    if (tid == 0) chain_walk_seq(nseg, partner, used, loop_off, point_ref, counts_out);
+    if (tid == 0) {
+      chain_walk_seq(nseg, partner, used, loop_off, point_ref, counts_out);
+      J.report->r.waterline_loops = counts_out[0];
+      J.report->r.waterline_points = counts_out[1];
+    }
     return;
   }
   int* prt = sm_chain;                 // [nodes] partner
@@ -784,6 +794,8 @@ __global__ void __launch_bounds__(kChainThreads) k_chain(const __grid_constant__
     counts_out[0] = s_csum[kChainThreads / 32 - 1];
     counts_out[1] = s_wsum[kChainThreads / 32 - 1];
     loop_off[0] = 0;
+    J.report->r.waterline_loops = counts_out[0];  // (was k_report_loops)
+    J.report->r.waterline_points = counts_out[1];
   }
   __syncthreads();
   // ---- scatter point references: position = (L - dist) mod L, closing point at L
@@ -819,22 +831,7 @@ __global__ void k_chain_points(const __grid_constant__ HydroBatch<NB> B) {
   }
 }
 
-template <int NB>
-__global__ void k_report_loops(const __grid_constant__ HydroBatch<NB> B) {
-  const HydroJob& J = B.job[blockIdx.y];
-  J.report->r.waterline_loops = J.loop_counts[0];
-  J.report->r.waterline_points = J.loop_counts[1];
-}
 
-// the per-evaluation resets of every job: flags and the waterline hash table
-template <int NB>
-__global__ void k_hydro_clear(const __grid_constant__ HydroBatch<NB> B) {
-  const HydroJob& J = B.job[blockIdx.y];
-  const int i0 = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
-  if (i0 < 4) J.flags[i0] = 0;
-  for (int i = i0; i < J.hcap; i += stride) J.hkeys[i] = 0ull;
-  for (int i = i0; i < 3 * J.hcap; i += stride) J.hvals[i] = 0;
-}
 
 int grid_of(ocn_ctx* ctx, int n, int threads) {
   int b = (n + threads - 1) / threads;
@@ -909,10 +906,6 @@ template <int NB>
 void launch_clip(ocn_ctx* ctx, const HydroBatch<NB>& B, int max_nv, int max_nt) {
   cudaStream_t st = ctx->stream;
   const unsigned nb = (unsigned)B.n;
-  int max_hcap = 0;
-  for (int i = 0; i < B.n; ++i) max_hcap = std::max(max_hcap, B.job[i].hcap);
-  k_hydro_clear<NB><<<dim3(std::max(1, grid_of(ctx, 3 * max_hcap, 256) / (int)nb), nb), 256, 0, st>>>(B);
-  OCN_LAUNCHED(ctx);
   k_vertices<NB><<<dim3(std::max(1, grid_of(ctx, 4 * max_nv, 128) / (int)nb), nb), 128, 0, st>>>(B);
   OCN_LAUNCHED(ctx);
   const int sb = (max_nt + kScanBlock - 1) / kScanBlock;
@@ -944,8 +937,6 @@ void launch_reduce(ocn_ctx* ctx, const HydroBatch<NB>& B, int max_nt) {
   k_chain<NB><<<dim3(1, nb), kChainThreads, chain_smem, st>>>(B);
   OCN_LAUNCHED(ctx);
   k_chain_points<NB><<<dim3(std::max(1, grid_of(ctx, max_nt, 256) / (int)nb), nb), 256, 0, st>>>(B);
-  OCN_LAUNCHED(ctx);
-  k_report_loops<NB><<<dim3(1, nb), 1, 0, st>>>(B);
   OCN_LAUNCHED(ctx);
 }
 
