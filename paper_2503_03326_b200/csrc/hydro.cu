@@ -655,6 +655,13 @@ __global__ void __launch_bounds__(kChainThreads) k_chain(const __grid_constant__
       J.report->r.waterline_loops = counts_out[0];
       J.report->r.waterline_points = counts_out[1];
     }
+    __syncthreads();
+    const int np = counts_out[1];  // loop points (was k_chain_points)
+    for (int q = tid; q < np; q += blockDim.x) {
+      const int e = point_ref[q];
+      const SegDev& sg = J.segs[e >> 1];
+      st3(J.loop_points + 3 * q, (e & 1) ? sg.pb : sg.pa);
+    }
     return;
   }
   int* prt = sm_chain;                 // [nodes] partner
@@ -810,26 +817,18 @@ __global__ void __launch_bounds__(kChainThreads) k_chain(const __grid_constant__
     if (off < 0) continue;  // loop shorter than 3 points
     const int L = dist[prt[st ^ 1]] + 1;
     const int pos = (L - dist[e]) % L;
-    point_ref[off + pos] = canon(e);
-    if (e == st) point_ref[off + L] = canon(e);
+    const int ce = canon(e);
+    const SegDev& sg = J.segs[ce >> 1];  // the point itself (was k_chain_points)
+    const double3 p = (ce & 1) ? sg.pb : sg.pa;
+    point_ref[off + pos] = ce;
+    st3(J.loop_points + 3 * (off + pos), p);
+    if (e == st) {
+      point_ref[off + L] = ce;
+      st3(J.loop_points + 3 * (off + L), p);
+    }
   }
 }
 
-template <int NB>
-__global__ void k_chain_points(const __grid_constant__ HydroBatch<NB> B) {
-  const HydroJob& J = B.job[blockIdx.y];
-  const SegDev* segs = J.segs;
-  const int* counts = J.loop_counts;
-  const int* point_ref = J.point_ref;
-  double* points = J.loop_points;
-  const int np = counts[1];
-  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < np; q += gridDim.x * blockDim.x) {
-    const int e = point_ref[q];
-    const SegDev& s = segs[e >> 1];
-    const double3 p = (e & 1) ? s.pb : s.pa;
-    st3(points + 3 * q, p);
-  }
-}
 
 
 
@@ -935,8 +934,6 @@ void launch_reduce(ocn_ctx* ctx, const HydroBatch<NB>& B, int max_nt) {
                                      2 * kChainSeq * sizeof(int) + kChainSeq);
   smem_opt_in(k_chain<NB>, chain_smem);
   k_chain<NB><<<dim3(1, nb), kChainThreads, chain_smem, st>>>(B);
-  OCN_LAUNCHED(ctx);
-  k_chain_points<NB><<<dim3(std::max(1, grid_of(ctx, max_nt, 256) / (int)nb), nb), 256, 0, st>>>(B);
   OCN_LAUNCHED(ctx);
 }
 
