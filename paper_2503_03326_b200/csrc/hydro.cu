@@ -8,7 +8,7 @@
 //   k_vertices   world transform + Algorithm-1 height (+ other zones) -> depth
 //   k_classify_scan  per triangle: 0 / 1 / 3 states, 0 / 1 waterline segment,
 //                and the block-local exclusive scan of those counts
-//   k_scan_blocks    the block totals -> order-preserving offsets (parent
+//   (last classify block) the block totals -> order-preserving offsets (parent
 //                order, hydro.cpp:151-163)
 //   k_emit       TriangleStates and crossing segments at their offsets
 //   k_forces     per state: prism volume, immersion moment, drag (velocity_at
@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(128) k_vertices(const __grid_constant__ HydroB
 // counts.x = states emitted (0 degenerate, 1 whole, 3 split), counts.y = segment.
 // One triangle per thread; each 1024-triangle block also scans its counts
 // (exclusive, parent order, hydro.cpp:151-163) and leaves its total for
-// k_scan_blocks; k_emit adds the block's offset.
+// the last classify block; k_emit adds the block's offset.
 constexpr int kScanBlock = 512;  // <= 16 K registers per CTA: fits beside a column-pass CTA
 
 __device__ __forceinline__ int2 add2(int2 a, int2 b) { return make_int2(a.x + b.x, a.y + b.y); }
@@ -190,29 +190,32 @@ __global__ void __launch_bounds__(kScanBlock) k_classify_scan(const __grid_const
   }
   __syncthreads();
   if (threadIdx.x == 0) block_sums[blockIdx.x] = tot;
-}
-
-// exclusive scan of the per-block totals in one block (any count), total out
-template <int NB>
-__global__ void __launch_bounds__(kScanBlock) k_scan_blocks(const __grid_constant__ HydroBatch<NB> B) {
-  const HydroJob& J = B.job[blockIdx.y];
-  const int nb = (J.nt + kScanBlock - 1) / kScanBlock;
-  int2* block_sums = J.block_sums;
-  int2* total = J.total;
-  __shared__ int2 warp_tot[32];
-  __shared__ int2 tot;
+  // the last of this job's blocks scans the block totals (was k_scan_blocks);
+  // the ticket is k_forces' too, each resetting it when done
+  const int nb = (nt + kScanBlock - 1) / kScanBlock;
+  __threadfence();
+  __syncthreads();
+  __shared__ bool last;
+  if (threadIdx.x == 0) last = atomicAdd(J.ticket, 1) == nb - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
   int2 carry = make_int2(0, 0);
   for (int base = 0; base < nb; base += kScanBlock) {
     const int i = base + threadIdx.x;
-    const int2 v = i < nb ? block_sums[i] : make_int2(0, 0);
-    const int2 ex = block_exclusive_scan(v, warp_tot, &tot);
-    if (i < nb) block_sums[i] = add2(carry, ex);
+    const int2 v = i < nb ? __ldcg(block_sums + i) : make_int2(0, 0);
+    const int2 bex = block_exclusive_scan(v, warp_tot, &tot);
+    if (i < nb) block_sums[i] = add2(carry, bex);
     __syncthreads();
     carry = add2(carry, tot);
     __syncthreads();
   }
-  if (threadIdx.x == 0) *total = carry;
+  if (threadIdx.x == 0) {
+    *J.total = carry;
+    *J.ticket = 0;
+  }
 }
+
 
 // ---------------------------------------------------------------- K7: emit
 __device__ __forceinline__ void emit_state(StateDev* s, int parent, int status, double3 a, double3 b,
@@ -909,8 +912,6 @@ void launch_clip(ocn_ctx* ctx, const HydroBatch<NB>& B, int max_nv, int max_nt) 
   OCN_LAUNCHED(ctx);
   const int sb = (max_nt + kScanBlock - 1) / kScanBlock;
   k_classify_scan<NB><<<dim3(sb, nb), kScanBlock, 0, st>>>(B);
-  OCN_LAUNCHED(ctx);
-  k_scan_blocks<NB><<<dim3(1, nb), kScanBlock, 0, st>>>(B);
   OCN_LAUNCHED(ctx);
   k_emit<NB><<<dim3(std::max(1, grid_of(ctx, max_nt, 128) / (int)nb), nb), 128, 0, st>>>(B);
   OCN_LAUNCHED(ctx);
