@@ -536,33 +536,22 @@ __global__ void k_chain_hash(const __grid_constant__ HydroBatch<NB> B) {
 }
 
 // partner[e] = the other (segment, side) with the same key, or -1
-template <int NB>
-__global__ void k_chain_partner(const __grid_constant__ HydroBatch<NB> B) {
-  const HydroJob& J = B.job[blockIdx.y];
-  const SegDev* segs = J.segs;
-  const int2* total = J.total;
-  const int hcap = J.hcap;
-  const unsigned long long* hkeys = J.hkeys;
-  const int* hvals = J.hvals;
-  int* partner = J.partner;
-  const int nseg = total->y;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < 2 * nseg; e += gridDim.x * blockDim.x) {
-    const int s = e >> 1, side = e & 1;
-    const int2 k = side ? segs[s].kb : segs[s].ka;
-    const unsigned long long key = key64(k) + 1ull;
-    unsigned h = hash64(key) & (hcap - 1);
-    int p = -1;
-    for (int probe = 0; probe < hcap; ++probe) {
-      if (hkeys[h] == key) {
-        const int cnt = min(hvals[3 * h + 2], 2);
-        for (int q = 0; q < cnt; ++q)
-          if (hvals[3 * h + q] != e) p = hvals[3 * h + q];
-        break;
-      }
-      h = (h + 1) & (hcap - 1);
+__device__ __forceinline__ int chain_partner_of(const HydroJob& J, int e) {
+  const int s = e >> 1, side = e & 1;
+  const int2 k = side ? J.segs[s].kb : J.segs[s].ka;
+  const unsigned long long key = key64(k) + 1ull;
+  unsigned h = hash64(key) & (J.hcap - 1);
+  int p = -1;
+  for (int probe = 0; probe < J.hcap; ++probe) {
+    if (J.hkeys[h] == key) {
+      const int cnt = min(J.hvals[3 * h + 2], 2);
+      for (int q = 0; q < cnt; ++q)
+        if (J.hvals[3 * h + q] != e) p = J.hvals[3 * h + q];
+      break;
     }
-    partner[e] = p;
+    h = (h + 1) & (J.hcap - 1);
   }
+  return p;
 }
 
 // Sequential walk with the reference's visiting order (hydro.cpp:167-213) in
@@ -640,8 +629,11 @@ __global__ void __launch_bounds__(kChainThreads) k_chain(const __grid_constant__
   if (tid == 0) s_open = 0;
   __syncthreads();
   const int nodes = 2 * nseg;
-  for (int e = tid; e < nodes; e += blockDim.x)
-    if (partner_g[e] < 0) s_open = 1;
+  for (int e = tid; e < nodes; e += blockDim.x) {  // partners from the hash table (was k_chain_partner)
+    const int p = chain_partner_of(J, e);
+    J.partner[e] = p;
+    if (p < 0) s_open = 1;
+  }
   __syncthreads();
   if (s_open || nseg > kChainPar) {
     // sequential fallback
@@ -928,8 +920,6 @@ void launch_reduce(ocn_ctx* ctx, const HydroBatch<NB>& B, int max_nt) {
   OCN_LAUNCHED(ctx);
   const int cb = std::max(1, grid_of(ctx, 2 * max_nt, 256) / (int)nb);
   k_chain_hash<NB><<<dim3(cb, nb), 256, 0, st>>>(B);
-  OCN_LAUNCHED(ctx);
-  k_chain_partner<NB><<<dim3(cb, nb), 256, 0, st>>>(B);
   OCN_LAUNCHED(ctx);
   const size_t chain_smem = std::max(9 * kChainPar * sizeof(int),
                                      2 * kChainSeq * sizeof(int) + kChainSeq);
